@@ -1,0 +1,205 @@
+/*
+ * qdpb.h -- C ABI of the B200-native QDP hot path (arXiv:1408.5925, "A Framework for
+ * Lattice QCD Calculations on GPUs").
+ *
+ * The library (paper_1408_5925_b200/libqdpb.so) implements, in hand-written sm_100a
+ * CUDA kernels, the data-parallel operations the paper's QDP-JIT/PTX layer accelerates:
+ * lattice fields in a coalesced structure-of-arrays layout (section
+ * III-B), the circular shift (section II-C), the Wilson hopping term
+ * (section VIII-C), the clover term (eq. (1)), the
+ * lattice BLAS (norm2 / innerProduct / axpy) and an even-odd CG solve of the Wilson(-clover)
+ * operator, with the sub-grid decomposition and inner/face overlap of
+ * section V.
+ *
+ * Conventions:
+ *  - mu = 0,1,2,3 <-> x,y,z,t (R2); gamma matrices in the DeGrand-Rossi chiral basis (R1).
+ *  - All global and local extents are even and >= 2 (R6).  Local site order is
+ *    lexicographic s = x + Lx(y + Ly(z + Lz t)) (R7); parity = (X+Y+Z+T) mod 2 of the
+ *    GLOBAL coordinates, which equals the local parity (local origins are even); the
+ *    checkerboard index of a site of parity p is cb = s >> 1 (R7).
+ *  - Boundary conditions are periodic in every direction (R5).
+ *  - Rank r has processor coordinates r = p0 + P0(p1 + P1(p2 + P2 p3)) in the grid P.
+ *
+ * Host canonical layouts (the contract of import/export; the device layout is opaque):
+ *  - QDP_FERMION: REAL[sites][4 spin][3 colour][2 re/im]; subset QDP_ALL: all local sites
+ *    in lexicographic order; subset QDP_EVEN/QDP_ODD: the sites of that parity in cb order.
+ *  - QDP_GAUGE:   REAL[local sites][4 mu][3 row][3 col][2]   (always subset QDP_ALL; U_mu(x)).
+ *  - QDP_CLOVER:  REAL[sites][12][12][2] dense, index i = 3*spin + colour; sites as for
+ *    fermions.  Only the two chiral 6x6 blocks (spins {0,1}, {2,3}) are stored on the
+ *    device, as 6 real diagonal + 15 complex lower-triangle numbers each (PAPER.md:228-230,
+ *    Table I lower part); import reads the diagonal and the strictly-lower triangle of each
+ *    block and ignores the rest.
+ *  REAL is double for QDP_F64 fields and float for QDP_F32 fields.
+ *
+ * Ownership: fields from qdp_field_alloc own their device memory (released by
+ * qdp_field_free); fields from qdp_field_wrap borrow caller memory (never freed by the
+ * library; >= 256-byte aligned, at least qdp_field_bytes() device bytes).
+ *
+ * Streams: every call enqueues its kernels on the context stream (qdp_init / qdp_set_stream)
+ * and returns without synchronising, EXCEPT calls that return host values (import, export,
+ * norm2, inner_product, cg_solve, clover_build), which synchronise the stream before
+ * returning.
+ *
+ * Errors: every entry point returns a status; 0 = QDP_OK, > 0 = warning, < 0 = error.
+ * On error nothing has been enqueued and the outputs are unchanged, except QDP_ECUDA /
+ * QDP_ENCCL (a device or communication failure after launch; the context should be
+ * finalised).  qdp_last_error(ctx) returns a human-readable message for the last error.
+ * One host thread per context.
+ */
+#ifndef QDPB_H
+#define QDPB_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct qdp_ctx_s *qdp_ctx;     /* one per process = one GPU: geometry, streams, comm, scratch */
+typedef struct qdp_field_s *qdp_field; /* a lattice field on one context */
+
+enum { QDP_F64 = 0, QDP_F32 = 1 };                             /* precision */
+enum { QDP_FERMION = 0, QDP_GAUGE = 1, QDP_CLOVER = 2 };      /* kind */
+enum { QDP_ALL = -1, QDP_EVEN = 0, QDP_ODD = 1 };             /* subset / parity */
+enum { QDP_FORWARD = +1, QDP_BACKWARD = -1 };                 /* shift direction */
+
+enum {
+  QDP_OK = 0,
+  QDP_NOT_CONVERGED = 1, /* cg_solve hit maxit; x holds the last iterate */
+  QDP_EINVAL = -1,       /* bad argument (NULL handle, bad enum, bad mu/sign, wrong kind/subset) */
+  QDP_ESHAPE = -2,       /* odd / non-divisible dims, byte-count mismatch, fields on different contexts */
+  QDP_EPREC = -3,        /* precision mismatch between fields */
+  QDP_EALIAS = -4,       /* an output aliases an input where that is not allowed */
+  QDP_ENOMEM = -5,       /* device or host allocation failed */
+  QDP_ECUDA = -6,        /* CUDA error */
+  QDP_ENCCL = -7,        /* NCCL error or NCCL unavailable for nranks > 1 */
+  QDP_ESINGULAR = -8,    /* a clover block has a zero pivot */
+  QDP_EUNSUPPORTED = -9  /* valid request this build does not implement */
+};
+
+/* ---- context ---------------------------------------------------------------------- */
+
+/* NCCL unique id (rank 0 only; the caller broadcasts the 128 bytes to all ranks). */
+int qdp_get_unique_id(unsigned char id[128]);
+
+/* Create a context for this rank.  global_dims: the global lattice; proc_grid: ranks per
+ * dimension (product == nranks); local dims = global/proc, all even (else QDP_ESHAPE).
+ * id: NCCL id from qdp_get_unique_id (ignored, may be NULL, when nranks == 1).
+ * cuda_stream: cudaStream_t to enqueue on (NULL: the context creates its own).
+ * The current CUDA device at the time of the call is the context's device. */
+int qdp_init(const int global_dims[4], const int proc_grid[4], int rank, int nranks,
+             const unsigned char *id, void *cuda_stream, qdp_ctx *out);
+int qdp_finalize(qdp_ctx ctx);
+int qdp_set_stream(qdp_ctx ctx, void *cuda_stream);
+int qdp_synchronize(qdp_ctx ctx);
+/* local_dims[4], proc_coords[4] of this rank */
+int qdp_get_geometry(qdp_ctx ctx, int local_dims[4], int proc_coords[4]);
+
+/* Options (qdp_set_option / qdp_get_option):
+ *  QDP_OPT_OVERLAP    1 (default): overlap face exchange with the interior kernel
+ *                     (PAPER.md:212); 0: exchange first, then compute (Fig. 6 "off").
+ *  QDP_OPT_SELF_HALO  bitmask of dims with one rank that are nevertheless treated as
+ *                     partitioned: faces are packed and the halo path runs, the peer being
+ *                     this rank (single-GPU test mode of the multi-GPU code).
+ *  QDP_OPT_PROFILE    1: bracket every launch with CUDA events (see qdp_profile_query).
+ *  QDP_OPT_BLOCK      threads per block of the dslash kernels (0 = auto-tuned default).
+ *  QDP_OPT_DET_REDUCE 1 (default): cross-rank sums by allgather + rank-ordered sum
+ *                     (deterministic); 0: ncclAllReduce. */
+enum { QDP_OPT_OVERLAP = 0, QDP_OPT_SELF_HALO = 1, QDP_OPT_PROFILE = 2, QDP_OPT_BLOCK = 3,
+       QDP_OPT_DET_REDUCE = 4 };
+int qdp_set_option(qdp_ctx ctx, int option, long value);
+int qdp_get_option(qdp_ctx ctx, int option, long *value);
+
+/* ---- fields (section II-B; Table I) ---------------------------------- */
+
+int qdp_field_alloc(qdp_ctx ctx, int kind, int prec, int subset, qdp_field *out);
+int qdp_field_wrap(qdp_ctx ctx, int kind, int prec, int subset, void *dev_ptr, size_t bytes,
+                   qdp_field *out);
+int qdp_field_free(qdp_field f);
+/* host_bytes: size of the host canonical array; device_bytes: device footprint */
+int qdp_field_bytes(qdp_ctx ctx, int kind, int prec, int subset, size_t *host_bytes,
+                    size_t *device_bytes);
+int qdp_field_info(const qdp_field f, int *kind, int *prec, int *subset, void **dev_ptr);
+/* copy host canonical data (bytes must equal host_bytes) into the field, converting the
+ * layout on the device; export is the inverse.  Host memory may be pageable or pinned. */
+int qdp_field_import(qdp_field f, const void *host, size_t bytes);
+int qdp_field_export(const qdp_field f, void *host, size_t bytes);
+int qdp_field_zero(qdp_field f);
+/* dst <- src (same kind/precision; subsets equal, or dst ALL and src a parity, or
+ * src ALL and dst a parity: the matching parity is copied). */
+int qdp_field_copy(qdp_field dst, const qdp_field src);
+
+/* ---- data-parallel operations ---------------------------------------------------------- */
+
+/* Circular shift (section II-C, Fig. 1; reading R4):
+ *   out(x) = in(x + sign * mu^),  sign = QDP_FORWARD (+1) or QDP_BACKWARD (-1).
+ * Fermion fields: in ALL -> out ALL; in parity p -> out parity 1-p.  Gauge fields: ALL.
+ * Faces crossing ranks are exchanged (packed, sent, received) by the library.
+ * out == in -> QDP_EALIAS. */
+int qdp_shift(qdp_field out, const qdp_field in, int mu, int sign);
+
+/* Wilson hopping term H of PAPER.md:282 (reading R3: no kappa, no 1/2):
+ *   (H psi)(x) = sum_mu [(1 - gamma_mu) U_mu(x) psi(x+mu) + (1 + gamma_mu) U_mu(x-mu)^dag psi(x-mu)]
+ * on the output sites of parity out_parity (QDP_EVEN / QDP_ODD), reading psi on the other
+ * parity; out_parity = QDP_ALL applies H on all sites (both parity blocks; out and psi ALL).
+ * out: fermion of subset out_parity or ALL (then only out_parity's block is written);
+ * psi: fermion of subset 1-out_parity or ALL.  U: gauge.  Same precision (QDP_EPREC).
+ * out == psi -> QDP_EALIAS. */
+int qdp_dslash(qdp_field out, const qdp_field U, const qdp_field psi, int out_parity);
+
+/* Global sums over the field's subset and all ranks (fp64 accumulation for both precisions;
+ * deterministic for a fixed launch configuration and rank count):
+ *   norm2(a) = sum_x |a(x)|^2 ; inner_product(a, b) = sum_x conj(a(x)) . b(x) (out[0]=re, out[1]=im). */
+int qdp_norm2(const qdp_field a, double *out);
+int qdp_inner_product(const qdp_field a, const qdp_field b, double out[2]);
+/* y <- a x + y (complex a) on y's subset; x == y allowed. */
+int qdp_axpy(double a_re, double a_im, const qdp_field x, qdp_field y);
+
+/* Clover term (eq. (1); reading R10), the Wilson mass folded in:
+ *   A(x) = (4 + mass) + 1/4 c_SW sum_{mu,nu} sigma_mu,nu F_mu,nu(x),
+ *   sigma_mu,nu = [gamma_mu, gamma_nu] / (2i),  F = traceless part of (Q - Q^dag)/(8i),
+ * Q the four clover leaves.  A (nullable) receives A on its subset's sites, Ainv (nullable)
+ * A^{-1} on its subset's sites.  Both QDP_CLOVER fields of U's precision.  Computed in fp64
+ * internally.  Returns QDP_ESINGULAR if a 6x6 block has a zero pivot. */
+int qdp_clover_build(qdp_field A, qdp_field Ainv, const qdp_field U, double mass, double csw);
+/* out(x) = A(x) in(x) on the sites of `parity` (QDP_ALL: all); out may equal in. */
+int qdp_clover_apply(qdp_field out, const qdp_field A, const qdp_field in, int parity);
+
+/* Even-odd preconditioned CGNR for M x = b, M = A - H/2 (readings R3, R12-R14):
+ *   Mhat = A_oo - 1/4 H_oe A_ee^-1 H_eo ; bhat_o = b_o + 1/2 H_oe A_ee^-1 b_e ;
+ *   CG on Mhat^dag Mhat x_o = Mhat^dag bhat_o from x_o = 0 ; x_e = A_ee^-1 (b_e + 1/2 H_eo x_o).
+ * x, b: full (QDP_ALL) fermions; U: gauge.  A / Ainv: clover fields from qdp_clover_build
+ * (A covering the odd sites, Ainv the even sites), or both NULL for Wilson (A = 4 + mass).
+ * Stops when |r_k|^2 <= tol^2 |r_0|^2 (r the CGNR residual) or after maxit iterations.
+ * iters (nullable): iterations done; resid_hist (nullable): resid_hist[k] = |r_k|/|r_0|
+ * for k = 0..min(iters, hist_cap-1); true_resid (nullable): |b - M x| / |b|.
+ * Returns QDP_OK, QDP_NOT_CONVERGED, or an error. */
+int qdp_cg_solve(qdp_field x, const qdp_field b, const qdp_field U, const qdp_field A,
+                 const qdp_field Ainv, double mass, double tol, int maxit, int *iters,
+                 double *resid_hist, int hist_cap, double *true_resid);
+
+/* ---- diagnostics ---------------------------------------------------------------------- */
+
+const char *qdp_strerror(int status);
+const char *qdp_last_error(qdp_ctx ctx);
+
+/* Kernel classes for profiling and launch counting. */
+enum { QDP_PK_DSLASH = 0,  /* interior / whole-lattice dslash */
+       QDP_PK_DSLASH_EXT,  /* exterior (face) dslash */
+       QDP_PK_PACK,        /* face packing */
+       QDP_PK_BLAS,        /* axpy / xpay / fused CG updates */
+       QDP_PK_REDUCE,      /* norm2 / inner product (both passes) */
+       QDP_PK_CLOVER,      /* clover apply / build */
+       QDP_PK_SHIFT,       /* shift */
+       QDP_PK_LAYOUT,      /* import / export / copy / zero */
+       QDP_PK_COUNT };
+/* launches: kernels launched in this class since the last reset (always counted);
+ * total_ms: sum of their CUDA-event durations (only while QDP_OPT_PROFILE = 1; resolving
+ * the events synchronises the stream).  kernel_class = -1: totals over all classes. */
+int qdp_profile_query(qdp_ctx ctx, int kernel_class, long *launches, double *total_ms);
+int qdp_profile_reset(qdp_ctx ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QDPB_H */

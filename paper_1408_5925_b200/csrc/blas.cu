@@ -1,0 +1,340 @@
+// blas.cu -- lattice BLAS on fermion parity blocks: norm2 / innerProduct reductions
+// (warp shuffle -> block partials -> one fixed-order final pass; fp64 accumulation for
+// both precisions, deterministic for a fixed launch configuration), axpy, and the fused
+// CG updates (north star).
+//
+// Every kernel runs one thread per checkerboard site (grid-stride), looping over the
+// site's planes (12 double2 or 6 float4) and over nblk consecutive parity blocks, so the
+// padded tail of each plane (cb >= Vh) is never read or written.
+#include "internal.h"
+
+namespace qdpb {
+
+template <typename R> struct E;  // one plane element
+template <> struct E<double> {
+  using T = double2;
+  static constexpr int NP = 12;  // planes per parity block
+  static constexpr int NR = 2;   // reals per element
+  static __device__ __forceinline__ void get(const T &v, double r[2]) { r[0] = v.x; r[1] = v.y; }
+  static __device__ __forceinline__ T put(const double r[2]) { return make_double2(r[0], r[1]); }
+};
+template <> struct E<float> {
+  using T = float4;
+  static constexpr int NP = 6;
+  static constexpr int NR = 4;
+  static __device__ __forceinline__ void get(const T &v, float r[4]) { r[0] = v.x; r[1] = v.y; r[2] = v.z; r[3] = v.w; }
+  static __device__ __forceinline__ T put(const float r[4]) { return make_float4(r[0], r[1], r[2], r[3]); }
+};
+
+constexpr int RB = 256;  // reduction block
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+// block sum of (v0, v1); thread 0 writes partials[2*blockIdx.x + {0,1}]
+__device__ __forceinline__ void block_partial(double v0, double v1, double *partials) {
+  __shared__ double s0[RB / 32], s1[RB / 32];
+  v0 = warp_sum(v0);
+  v1 = warp_sum(v1);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) { s0[w] = v0; s1[w] = v1; }
+  __syncthreads();
+  if (w == 0) {
+    v0 = l < RB / 32 ? s0[l] : 0.0;
+    v1 = l < RB / 32 ? s1[l] : 0.0;
+    v0 = warp_sum(v0);
+    v1 = warp_sum(v1);
+    if (l == 0) { partials[2 * blockIdx.x] = v0; partials[2 * blockIdx.x + 1] = v1; }
+  }
+}
+
+// Final pass: one block sums n partial pairs in a fixed order -> res[slot], res[slot+1].
+__global__ void __launch_bounds__(1024) final_kernel(const double *partials, int n, double *res, int slot) {
+  __shared__ double s0[32], s1[32];
+  double v0 = 0.0, v1 = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) { v0 += partials[2 * i]; v1 += partials[2 * i + 1]; }
+  v0 = warp_sum(v0);
+  v1 = warp_sum(v1);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) { s0[w] = v0; s1[w] = v1; }
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x >> 5;
+    v0 = l < nw ? s0[l] : 0.0;
+    v1 = l < nw ? s1[l] : 0.0;
+    v0 = warp_sum(v0);
+    v1 = warp_sum(v1);
+    if (l == 0) { res[slot] = v0; res[slot + 1] = v1; }
+  }
+}
+
+// rank-ordered sum of gathered per-rank values: res[slot+k] = sum_r g[r*n + k]
+__global__ void rank_sum_kernel(const double *g, int nranks, int n, double *res, int slot) {
+  const int k = threadIdx.x;
+  if (k >= n) return;
+  double s = 0.0;
+  for (int r = 0; r < nranks; r++) s += g[r * n + k];
+  res[slot + k] = s;
+}
+
+template <typename R>
+__global__ void __launch_bounds__(RB) norm2_kernel(const Geom g, const typename E<R>::T *a, int nblk, double *partials) {
+  double acc = 0.0;
+  const size_t bs = (size_t)E<R>::NP * g.stride;
+  for (int cb = blockIdx.x * blockDim.x + threadIdx.x; cb < g.Vh; cb += gridDim.x * blockDim.x)
+    for (int b = 0; b < nblk; b++)
+#pragma unroll
+      for (int k = 0; k < E<R>::NP; k++) {
+        R v[E<R>::NR];
+        E<R>::get(a[b * bs + (size_t)k * g.stride + cb], v);
+#pragma unroll
+        for (int j = 0; j < E<R>::NR; j++) acc += (double)v[j] * (double)v[j];
+      }
+  block_partial(acc, 0.0, partials);
+}
+
+template <typename R>
+__global__ void __launch_bounds__(RB) inner_kernel(const Geom g, const typename E<R>::T *a, const typename E<R>::T *b_,
+                                                   int nblk, double *partials) {
+  double re = 0.0, im = 0.0;
+  const size_t bs = (size_t)E<R>::NP * g.stride;
+  for (int cb = blockIdx.x * blockDim.x + threadIdx.x; cb < g.Vh; cb += gridDim.x * blockDim.x)
+    for (int b = 0; b < nblk; b++)
+#pragma unroll
+      for (int k = 0; k < E<R>::NP; k++) {
+        const size_t i = b * bs + (size_t)k * g.stride + cb;
+        R u[E<R>::NR], v[E<R>::NR];
+        E<R>::get(a[i], u);
+        E<R>::get(b_[i], v);
+#pragma unroll
+        for (int j = 0; j < E<R>::NR; j += 2) {
+          re += (double)u[j] * v[j] + (double)u[j + 1] * v[j + 1];
+          im += (double)u[j] * v[j + 1] - (double)u[j + 1] * v[j];
+        }
+      }
+  block_partial(re, im, partials);
+}
+
+template <typename R>
+__global__ void __launch_bounds__(RB) axpy_kernel(const Geom g, R ar, R ai, const typename E<R>::T *x,
+                                                  typename E<R>::T *y, int nblk) {
+  const size_t bs = (size_t)E<R>::NP * g.stride;
+  for (int cb = blockIdx.x * blockDim.x + threadIdx.x; cb < g.Vh; cb += gridDim.x * blockDim.x)
+    for (int b = 0; b < nblk; b++)
+#pragma unroll
+      for (int k = 0; k < E<R>::NP; k++) {
+        const size_t i = b * bs + (size_t)k * g.stride + cb;
+        R u[E<R>::NR], v[E<R>::NR];
+        E<R>::get(x[i], u);
+        E<R>::get(y[i], v);
+#pragma unroll
+        for (int j = 0; j < E<R>::NR; j += 2) {
+          const R re = ar * u[j] - ai * u[j + 1] + v[j];
+          const R im = ar * u[j + 1] + ai * u[j] + v[j + 1];
+          v[j] = re;
+          v[j + 1] = im;
+        }
+        y[i] = E<R>::put(v);
+      }
+}
+
+// y = x + a y
+template <typename R>
+__global__ void __launch_bounds__(RB) xpay_kernel(const Geom g, const typename E<R>::T *x, R a, typename E<R>::T *y, int nblk) {
+  const size_t bs = (size_t)E<R>::NP * g.stride;
+  for (int cb = blockIdx.x * blockDim.x + threadIdx.x; cb < g.Vh; cb += gridDim.x * blockDim.x)
+    for (int b = 0; b < nblk; b++)
+#pragma unroll
+      for (int k = 0; k < E<R>::NP; k++) {
+        const size_t i = b * bs + (size_t)k * g.stride + cb;
+        R u[E<R>::NR], v[E<R>::NR];
+        E<R>::get(x[i], u);
+        E<R>::get(y[i], v);
+#pragma unroll
+        for (int j = 0; j < E<R>::NR; j++) v[j] = u[j] + a * v[j];
+        y[i] = E<R>::put(v);
+      }
+}
+
+template <typename R>
+__global__ void __launch_bounds__(RB) scale_copy_kernel(const Geom g, typename E<R>::T *d, const typename E<R>::T *s, R a, int nblk) {
+  const size_t bs = (size_t)E<R>::NP * g.stride;
+  for (int cb = blockIdx.x * blockDim.x + threadIdx.x; cb < g.Vh; cb += gridDim.x * blockDim.x)
+    for (int b = 0; b < nblk; b++)
+#pragma unroll
+      for (int k = 0; k < E<R>::NP; k++) {
+        const size_t i = b * bs + (size_t)k * g.stride + cb;
+        R u[E<R>::NR];
+        E<R>::get(s[i], u);
+#pragma unroll
+        for (int j = 0; j < E<R>::NR; j++) u[j] *= a;
+        d[i] = E<R>::put(u);
+      }
+}
+
+// x += alpha p ; r -= alpha q ; partial |r|^2   with alpha = res[rho] / res[pq]  (CG step 5)
+template <typename R>
+__global__ void __launch_bounds__(RB) cg_xr_kernel(const Geom g, typename E<R>::T *x, typename E<R>::T *r,
+                                                   const typename E<R>::T *p, const typename E<R>::T *q,
+                                                   const double *res, int rho_slot, int pq_slot, double *partials) {
+  const R alpha = (R)(res[rho_slot] / res[pq_slot]);
+  double acc = 0.0;
+  for (int cb = blockIdx.x * blockDim.x + threadIdx.x; cb < g.Vh; cb += gridDim.x * blockDim.x)
+#pragma unroll
+    for (int k = 0; k < E<R>::NP; k++) {
+      const size_t i = (size_t)k * g.stride + cb;
+      R xv[E<R>::NR], rv[E<R>::NR], pv[E<R>::NR], qv[E<R>::NR];
+      E<R>::get(x[i], xv);
+      E<R>::get(r[i], rv);
+      E<R>::get(p[i], pv);
+      E<R>::get(q[i], qv);
+#pragma unroll
+      for (int j = 0; j < E<R>::NR; j++) {
+        xv[j] = xv[j] + alpha * pv[j];
+        rv[j] = rv[j] - alpha * qv[j];
+        acc += (double)rv[j] * (double)rv[j];
+      }
+      x[i] = E<R>::put(xv);
+      r[i] = E<R>::put(rv);
+    }
+  block_partial(acc, 0.0, partials);
+}
+
+// p = r + beta p, beta = res[rn] / res[ro]
+template <typename R>
+__global__ void __launch_bounds__(RB) cg_p_kernel(const Geom g, typename E<R>::T *p, const typename E<R>::T *r,
+                                                  const double *res, int rn, int ro) {
+  const R beta = (R)(res[rn] / res[ro]);
+  for (int cb = blockIdx.x * blockDim.x + threadIdx.x; cb < g.Vh; cb += gridDim.x * blockDim.x)
+#pragma unroll
+    for (int k = 0; k < E<R>::NP; k++) {
+      const size_t i = (size_t)k * g.stride + cb;
+      R pv[E<R>::NR], rv[E<R>::NR];
+      E<R>::get(p[i], pv);
+      E<R>::get(r[i], rv);
+#pragma unroll
+      for (int j = 0; j < E<R>::NR; j++) pv[j] = rv[j] + beta * pv[j];
+      p[i] = E<R>::put(pv);
+    }
+}
+
+// ------------------------------------------------------------------ host wrappers
+static int red_grid(const Geom &g) {
+  int n = grid_for(g.Vh, RB);
+  return n < 148 * 8 ? n : 148 * 8;
+}
+
+template <typename R> using T_ = typename E<R>::T;
+
+static int finish(qdp_ctx ctx, int nparts, int slot) {
+  ProfEvent ev;
+  prof_begin(ctx, QDP_PK_REDUCE, &ev);
+  final_kernel<<<1, 1024, 0, ctx->stream>>>(ctx->red_partials, nparts, ctx->red_result, slot);
+  return prof_end(ctx, &ev);
+}
+
+int blas_norm2(qdp_ctx ctx, int prec, const void *a, int nblk, int slot) {
+  const Geom &g = ctx->geom;
+  const int nb = red_grid(g);
+  int rc;
+  if ((rc = ensure_reduce(ctx, nb))) return rc;
+  ProfEvent ev;
+  prof_begin(ctx, QDP_PK_REDUCE, &ev);
+  if (prec == QDP_F64) norm2_kernel<double><<<nb, RB, 0, ctx->stream>>>(g, (const T_<double> *)a, nblk, ctx->red_partials);
+  else norm2_kernel<float><<<nb, RB, 0, ctx->stream>>>(g, (const T_<float> *)a, nblk, ctx->red_partials);
+  if ((rc = prof_end(ctx, &ev))) return rc;
+  return finish(ctx, nb, slot);
+}
+
+int blas_inner(qdp_ctx ctx, int prec, const void *a, const void *b, int nblk, int slot) {
+  const Geom &g = ctx->geom;
+  const int nb = red_grid(g);
+  int rc;
+  if ((rc = ensure_reduce(ctx, nb))) return rc;
+  ProfEvent ev;
+  prof_begin(ctx, QDP_PK_REDUCE, &ev);
+  if (prec == QDP_F64)
+    inner_kernel<double><<<nb, RB, 0, ctx->stream>>>(g, (const T_<double> *)a, (const T_<double> *)b, nblk, ctx->red_partials);
+  else
+    inner_kernel<float><<<nb, RB, 0, ctx->stream>>>(g, (const T_<float> *)a, (const T_<float> *)b, nblk, ctx->red_partials);
+  if ((rc = prof_end(ctx, &ev))) return rc;
+  return finish(ctx, nb, slot);
+}
+
+int reduce_global(qdp_ctx ctx, int slot, int n) {
+  if (ctx->nranks == 1) return QDP_OK;
+  int rc;
+  if (ctx->det_reduce) {
+    if ((rc = comm_allgather_f64(ctx, ctx->red_result + slot, ctx->red_gather, n, ctx->stream))) return rc;
+    ProfEvent ev;
+    prof_begin(ctx, QDP_PK_REDUCE, &ev);
+    rank_sum_kernel<<<1, 32, 0, ctx->stream>>>(ctx->red_gather, ctx->nranks, n, ctx->red_result, slot);
+    return prof_end(ctx, &ev);
+  }
+  return comm_allreduce_f64(ctx, ctx->red_result + slot, n, ctx->stream);
+}
+
+int blas_axpy(qdp_ctx ctx, int prec, double ar, double ai, const void *x, void *y, int nblk) {
+  const Geom &g = ctx->geom;
+  ProfEvent ev;
+  prof_begin(ctx, QDP_PK_BLAS, &ev);
+  const int nb = grid_for(g.Vh, RB);
+  if (prec == QDP_F64) axpy_kernel<double><<<nb, RB, 0, ctx->stream>>>(g, ar, ai, (const T_<double> *)x, (T_<double> *)y, nblk);
+  else axpy_kernel<float><<<nb, RB, 0, ctx->stream>>>(g, (float)ar, (float)ai, (const T_<float> *)x, (T_<float> *)y, nblk);
+  return prof_end(ctx, &ev);
+}
+
+int blas_xpay(qdp_ctx ctx, int prec, const void *x, double a, void *y, int nblk) {
+  const Geom &g = ctx->geom;
+  ProfEvent ev;
+  prof_begin(ctx, QDP_PK_BLAS, &ev);
+  const int nb = grid_for(g.Vh, RB);
+  if (prec == QDP_F64) xpay_kernel<double><<<nb, RB, 0, ctx->stream>>>(g, (const T_<double> *)x, a, (T_<double> *)y, nblk);
+  else xpay_kernel<float><<<nb, RB, 0, ctx->stream>>>(g, (const T_<float> *)x, (float)a, (T_<float> *)y, nblk);
+  return prof_end(ctx, &ev);
+}
+
+int blas_scale_copy(qdp_ctx ctx, int prec, void *dst, const void *src, double a, int nblk) {
+  const Geom &g = ctx->geom;
+  ProfEvent ev;
+  prof_begin(ctx, QDP_PK_BLAS, &ev);
+  const int nb = grid_for(g.Vh, RB);
+  if (prec == QDP_F64) scale_copy_kernel<double><<<nb, RB, 0, ctx->stream>>>(g, (T_<double> *)dst, (const T_<double> *)src, a, nblk);
+  else scale_copy_kernel<float><<<nb, RB, 0, ctx->stream>>>(g, (T_<float> *)dst, (const T_<float> *)src, (float)a, nblk);
+  return prof_end(ctx, &ev);
+}
+
+int blas_cg_update_xr(qdp_ctx ctx, int prec, void *x, void *r, const void *p, const void *q, int rho_slot,
+                      int pq_slot, int rr_slot) {
+  const Geom &g = ctx->geom;
+  const int nb = red_grid(g);
+  int rc;
+  if ((rc = ensure_reduce(ctx, nb))) return rc;
+  ProfEvent ev;
+  prof_begin(ctx, QDP_PK_BLAS, &ev);
+  if (prec == QDP_F64)
+    cg_xr_kernel<double><<<nb, RB, 0, ctx->stream>>>(g, (T_<double> *)x, (T_<double> *)r, (const T_<double> *)p,
+                                                      (const T_<double> *)q, ctx->red_result, rho_slot, pq_slot, ctx->red_partials);
+  else
+    cg_xr_kernel<float><<<nb, RB, 0, ctx->stream>>>(g, (T_<float> *)x, (T_<float> *)r, (const T_<float> *)p,
+                                                     (const T_<float> *)q, ctx->red_result, rho_slot, pq_slot, ctx->red_partials);
+  if ((rc = prof_end(ctx, &ev))) return rc;
+  if ((rc = finish(ctx, nb, rr_slot))) return rc;
+  return reduce_global(ctx, rr_slot, 1);
+}
+
+int blas_cg_update_p(qdp_ctx ctx, int prec, void *p, const void *r, int rn, int ro) {
+  const Geom &g = ctx->geom;
+  ProfEvent ev;
+  prof_begin(ctx, QDP_PK_BLAS, &ev);
+  const int nb = grid_for(g.Vh, RB);
+  if (prec == QDP_F64)
+    cg_p_kernel<double><<<nb, RB, 0, ctx->stream>>>(g, (T_<double> *)p, (const T_<double> *)r, ctx->red_result, rn, ro);
+  else
+    cg_p_kernel<float><<<nb, RB, 0, ctx->stream>>>(g, (T_<float> *)p, (const T_<float> *)r, ctx->red_result, rn, ro);
+  return prof_end(ctx, &ev);
+}
+
+}  // namespace qdpb

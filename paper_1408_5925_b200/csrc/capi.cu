@@ -1,0 +1,650 @@
+// capi.cu -- the extern "C" entry points of include/qdpb.h: argument validation, field
+// objects, geometry, scratch management, launch bookkeeping, dispatch to the kernels.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "internal.h"
+
+using namespace qdpb;
+
+namespace qdpb {
+
+int set_error(qdp_ctx ctx, int status, const char *fmt, ...) {
+  if (ctx) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    ctx->last_error = buf;
+  }
+  return status;
+}
+
+int cuda_check(qdp_ctx ctx, cudaError_t e, const char *what) {
+  return set_error(ctx, QDP_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+static cudaEvent_t pool_event(qdp_ctx ctx) {
+  if (!ctx->event_pool.empty()) {
+    cudaEvent_t e = ctx->event_pool.back();
+    ctx->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+void prof_begin(qdp_ctx ctx, int cls, ProfEvent *ev) {
+  ev->cls = cls;
+  ev->a = ev->b = nullptr;
+  ctx->launches[cls]++;
+  if (ctx->profiling) {
+    ev->a = pool_event(ctx);
+    ev->b = pool_event(ctx);
+    cudaEventRecord(ev->a, ctx->stream);
+  }
+}
+
+int prof_end(qdp_ctx ctx, ProfEvent *ev) {
+  cudaError_t e = cudaGetLastError();
+  if (ev->a) {
+    cudaEventRecord(ev->b, ctx->stream);
+    ctx->pending.push_back(*ev);
+  }
+  if (e != cudaSuccess) return cuda_check(ctx, e, "kernel launch");
+  return QDP_OK;
+}
+
+static int resolve_profile(qdp_ctx ctx) {
+  if (ctx->pending.empty()) return QDP_OK;
+  QDP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  for (auto &p : ctx->pending) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) ctx->prof_ms[p.cls] += ms;
+    ctx->event_pool.push_back(p.a);
+    ctx->event_pool.push_back(p.b);
+  }
+  ctx->pending.clear();
+  return QDP_OK;
+}
+
+int ensure_staging(qdp_ctx ctx, size_t bytes) {
+  if (ctx->staging_bytes >= bytes) return QDP_OK;
+  if (ctx->staging) {
+    QDP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    cudaFree(ctx->staging);
+    ctx->staging = nullptr;
+    ctx->staging_bytes = 0;
+  }
+  if (cudaMalloc(&ctx->staging, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return set_error(ctx, QDP_ENOMEM, "staging buffer of %zu bytes", bytes);
+  }
+  ctx->staging_bytes = bytes;
+  return QDP_OK;
+}
+
+int ensure_reduce(qdp_ctx ctx, int blocks) {
+  if (ctx->red_capacity >= blocks) return QDP_OK;
+  if (ctx->red_partials) {
+    QDP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    cudaFree(ctx->red_partials);
+  }
+  ctx->red_partials = nullptr;
+  ctx->red_capacity = 0;
+  if (cudaMalloc((void **)&ctx->red_partials, sizeof(double) * 2 * blocks) != cudaSuccess) {
+    cudaGetLastError();
+    return set_error(ctx, QDP_ENOMEM, "reduction partials");
+  }
+  ctx->red_capacity = blocks;
+  return QDP_OK;
+}
+
+int ensure_halo(qdp_ctx ctx, int prec) {
+  const Geom &g = ctx->geom;
+  size_t need = 0;
+  for (int mu = 0; mu < 4; mu++)
+    if ((g.part >> mu) & 1) {
+      size_t b = (size_t)g.faceVh[mu] * 12 * (prec == QDP_F64 ? 8 : 4);
+      if (b > need) need = b;
+    }
+  if (ctx->halo_bytes[prec] >= need) return QDP_OK;
+  QDP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  for (int mu = 0; mu < 4; mu++)
+    for (int d = 0; d < 2; d++) {
+      if (ctx->halo_send[prec][mu][d]) cudaFree(ctx->halo_send[prec][mu][d]);
+      if (ctx->halo_recv[prec][mu][d]) cudaFree(ctx->halo_recv[prec][mu][d]);
+      ctx->halo_send[prec][mu][d] = ctx->halo_recv[prec][mu][d] = nullptr;
+    }
+  ctx->halo_bytes[prec] = 0;
+  for (int mu = 0; mu < 4; mu++)
+    for (int d = 0; d < 2; d++) {
+      if (cudaMalloc(&ctx->halo_send[prec][mu][d], need) != cudaSuccess ||
+          cudaMalloc(&ctx->halo_recv[prec][mu][d], need) != cudaSuccess) {
+        cudaGetLastError();
+        return set_error(ctx, QDP_ENOMEM, "halo buffers");
+      }
+    }
+  ctx->halo_bytes[prec] = need;
+  return QDP_OK;
+}
+
+static void update_partition(qdp_ctx ctx) {
+  int part = 0;
+  for (int mu = 0; mu < 4; mu++)
+    if (ctx->pgrid[mu] > 1 || ((ctx->self_halo >> mu) & 1)) part |= 1 << mu;
+  ctx->geom.part = part;
+}
+
+static size_t field_device_bytes(qdp_ctx ctx, int kind, int prec, int subset) {
+  const size_t blk = parity_block_bytes(kind, prec, ctx->geom.stride);
+  return (kind == KIND_GAUGE || subset == QDP_ALL) ? 2 * blk : blk;
+}
+static size_t field_host_bytes(qdp_ctx ctx, int kind, int prec, int subset) {
+  const long sites = (kind == KIND_GAUGE || subset == QDP_ALL) ? ctx->V : ctx->geom.Vh;
+  return (size_t)sites * host_site_reals(kind) * (prec == QDP_F64 ? 8 : 4);
+}
+
+}  // namespace qdpb
+
+static bool valid_kind(int k) { return k == QDP_FERMION || k == QDP_GAUGE || k == QDP_CLOVER; }
+static bool valid_prec(int p) { return p == QDP_F64 || p == QDP_F32; }
+static bool valid_subset(int s) { return s == QDP_ALL || s == QDP_EVEN || s == QDP_ODD; }
+
+// ---------------------------------------------------------------------------- context
+extern "C" int qdp_get_unique_id(unsigned char id[128]) {
+  if (!id) return QDP_EINVAL;
+  return comm_get_unique_id(id);
+}
+
+extern "C" int qdp_init(const int global_dims[4], const int proc_grid[4], int rank, int nranks, const unsigned char *id,
+                        void *cuda_stream, qdp_ctx *out) {
+  if (!global_dims || !proc_grid || !out) return QDP_EINVAL;
+  *out = nullptr;
+  if (nranks < 1 || rank < 0 || rank >= nranks) return QDP_EINVAL;
+  long prod = 1;
+  for (int mu = 0; mu < 4; mu++) {
+    if (proc_grid[mu] < 1 || global_dims[mu] < 2) return QDP_ESHAPE;
+    if (global_dims[mu] % proc_grid[mu]) return QDP_ESHAPE;
+    const int l = global_dims[mu] / proc_grid[mu];
+    if (l < 2 || (l & 1)) return QDP_ESHAPE;  // reading R6: every local extent even
+    prod *= proc_grid[mu];
+  }
+  if (prod != nranks) return QDP_ESHAPE;
+  long V = 1;
+  for (int mu = 0; mu < 4; mu++) V *= global_dims[mu] / proc_grid[mu];
+  if (V / 2 > (1L << 30)) return QDP_ESHAPE;
+
+  qdp_ctx c = new qdp_ctx_s();
+  memcpy(c->gdims, global_dims, sizeof(c->gdims));
+  memcpy(c->pgrid, proc_grid, sizeof(c->pgrid));
+  c->rank = rank;
+  c->nranks = nranks;
+  int r = rank;
+  for (int mu = 0; mu < 4; mu++) {
+    c->pcoord[mu] = r % proc_grid[mu];
+    r /= proc_grid[mu];
+  }
+  for (int mu = 0; mu < 4; mu++)
+    for (int d = 0; d < 2; d++) {
+      int pc[4];
+      memcpy(pc, c->pcoord, sizeof(pc));
+      pc[mu] = (pc[mu] + (d ? 1 : -1) + proc_grid[mu]) % proc_grid[mu];
+      c->neighbour[mu][d] = pc[0] + proc_grid[0] * (pc[1] + proc_grid[1] * (pc[2] + proc_grid[2] * pc[3]));
+    }
+  Geom &g = c->geom;
+  for (int mu = 0; mu < 4; mu++) g.L[mu] = global_dims[mu] / proc_grid[mu];
+  g.Lh0 = g.L[0] / 2;
+  c->V = V;
+  g.Vh = (int)(V / 2);
+  g.stride = (g.Vh + 63) / 64 * 64;
+  for (int mu = 0; mu < 4; mu++) g.faceVh[mu] = (int)(V / g.L[mu] / 2);
+  update_partition(c);
+
+  int rc = QDP_OK;
+  cudaError_t e = cudaGetDevice(&c->device);
+  if (e != cudaSuccess) rc = cuda_check(c, e, "cudaGetDevice");
+  if (!rc) {
+    if (cuda_stream) {
+      c->stream = (cudaStream_t)cuda_stream;
+    } else {
+      e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+      c->own_stream = true;
+      if (e != cudaSuccess) rc = cuda_check(c, e, "cudaStreamCreate");
+    }
+  }
+  if (!rc && (e = cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking)) != cudaSuccess)
+    rc = cuda_check(c, e, "comm stream");
+  if (!rc && ((e = cudaEventCreateWithFlags(&c->ev_packed, cudaEventDisableTiming)) != cudaSuccess ||
+              (e = cudaEventCreateWithFlags(&c->ev_comm, cudaEventDisableTiming)) != cudaSuccess))
+    rc = cuda_check(c, e, "events");
+  if (!rc && (e = cudaMalloc((void **)&c->red_result, 64 * sizeof(double))) != cudaSuccess) rc = cuda_check(c, e, "scalars");
+  if (!rc && (e = cudaMemset(c->red_result, 0, 64 * sizeof(double))) != cudaSuccess) rc = cuda_check(c, e, "scalars");
+  if (!rc && (e = cudaMalloc((void **)&c->red_gather, 8 * sizeof(double) * nranks)) != cudaSuccess) rc = cuda_check(c, e, "gather");
+  if (!rc && (e = cudaMallocHost((void **)&c->host_pinned, 64 * sizeof(double))) != cudaSuccess) rc = cuda_check(c, e, "pinned");
+  if (!rc) rc = comm_init(c, id);
+  if (rc) {
+    qdp_finalize(c);
+    return rc;
+  }
+  *out = c;
+  return QDP_OK;
+}
+
+extern "C" int qdp_finalize(qdp_ctx c) {
+  if (!c) return QDP_EINVAL;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  resolve_profile(c);
+  comm_destroy(c);
+  for (auto e : c->event_pool) cudaEventDestroy(e);
+  if (c->ev_packed) cudaEventDestroy(c->ev_packed);
+  if (c->ev_comm) cudaEventDestroy(c->ev_comm);
+  for (int p = 0; p < 2; p++)
+    for (int mu = 0; mu < 4; mu++)
+      for (int d = 0; d < 2; d++) {
+        if (c->halo_send[p][mu][d]) cudaFree(c->halo_send[p][mu][d]);
+        if (c->halo_recv[p][mu][d]) cudaFree(c->halo_recv[p][mu][d]);
+      }
+  if (c->staging) cudaFree(c->staging);
+  if (c->red_partials) cudaFree(c->red_partials);
+  if (c->red_result) cudaFree(c->red_result);
+  if (c->red_gather) cudaFree(c->red_gather);
+  if (c->host_pinned) cudaFreeHost(c->host_pinned);
+  if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return QDP_OK;
+}
+
+extern "C" int qdp_set_stream(qdp_ctx c, void *s) {
+  if (!c) return QDP_EINVAL;
+  if (c->own_stream) {
+    cudaStreamSynchronize(c->stream);
+    cudaStreamDestroy(c->stream);
+    c->own_stream = false;
+  }
+  if (!s) {
+    QDP_CUDA(c, cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->own_stream = true;
+  } else {
+    c->stream = (cudaStream_t)s;
+  }
+  return QDP_OK;
+}
+
+extern "C" int qdp_synchronize(qdp_ctx c) {
+  if (!c) return QDP_EINVAL;
+  QDP_CUDA(c, cudaStreamSynchronize(c->stream));
+  return QDP_OK;
+}
+
+extern "C" int qdp_get_geometry(qdp_ctx c, int local_dims[4], int proc_coords[4]) {
+  if (!c) return QDP_EINVAL;
+  if (local_dims) memcpy(local_dims, c->geom.L, 4 * sizeof(int));
+  if (proc_coords) memcpy(proc_coords, c->pcoord, 4 * sizeof(int));
+  return QDP_OK;
+}
+
+extern "C" int qdp_set_option(qdp_ctx c, int opt, long v) {
+  if (!c) return QDP_EINVAL;
+  switch (opt) {
+    case QDP_OPT_OVERLAP: c->overlap = v ? 1 : 0; return QDP_OK;
+    case QDP_OPT_SELF_HALO:
+      if (v < 0 || v > 15) return set_error(c, QDP_EINVAL, "self-halo mask must be in [0, 15]");
+      c->self_halo = (int)v;
+      update_partition(c);
+      return QDP_OK;
+    case QDP_OPT_PROFILE:
+      if (!v) resolve_profile(c);
+      c->profiling = v ? 1 : 0;
+      return QDP_OK;
+    case QDP_OPT_BLOCK:
+      if (v < 0 || v > 1024 || (v % 32)) return set_error(c, QDP_EINVAL, "block must be a multiple of 32 <= 1024");
+      c->block = (int)v;
+      return QDP_OK;
+    case QDP_OPT_DET_REDUCE: c->det_reduce = v ? 1 : 0; return QDP_OK;
+  }
+  return set_error(c, QDP_EINVAL, "unknown option %d", opt);
+}
+
+extern "C" int qdp_get_option(qdp_ctx c, int opt, long *v) {
+  if (!c || !v) return QDP_EINVAL;
+  switch (opt) {
+    case QDP_OPT_OVERLAP: *v = c->overlap; return QDP_OK;
+    case QDP_OPT_SELF_HALO: *v = c->self_halo; return QDP_OK;
+    case QDP_OPT_PROFILE: *v = c->profiling; return QDP_OK;
+    case QDP_OPT_BLOCK: *v = c->block; return QDP_OK;
+    case QDP_OPT_DET_REDUCE: *v = c->det_reduce; return QDP_OK;
+  }
+  return set_error(c, QDP_EINVAL, "unknown option %d", opt);
+}
+
+// ---------------------------------------------------------------------------- fields
+extern "C" int qdp_field_bytes(qdp_ctx c, int kind, int prec, int subset, size_t *hb, size_t *db) {
+  if (!c || !valid_kind(kind) || !valid_prec(prec) || !valid_subset(subset)) return QDP_EINVAL;
+  if (kind == QDP_GAUGE && subset != QDP_ALL) return set_error(c, QDP_EINVAL, "gauge fields are QDP_ALL");
+  if (hb) *hb = field_host_bytes(c, kind, prec, subset);
+  if (db) *db = field_device_bytes(c, kind, prec, subset);
+  return QDP_OK;
+}
+
+static int make_field(qdp_ctx c, int kind, int prec, int subset, void *ptr, size_t bytes, bool owned, qdp_field *out) {
+  qdp_field f = new qdp_field_s();
+  f->ctx = c;
+  f->kind = kind;
+  f->prec = prec;
+  f->subset = subset;
+  f->data = ptr;
+  f->bytes = bytes;
+  f->owned = owned;
+  *out = f;
+  return QDP_OK;
+}
+
+extern "C" int qdp_field_alloc(qdp_ctx c, int kind, int prec, int subset, qdp_field *out) {
+  if (!c || !out) return QDP_EINVAL;
+  *out = nullptr;
+  int rc = qdp_field_bytes(c, kind, prec, subset, nullptr, nullptr);
+  if (rc) return rc;
+  const size_t bytes = field_device_bytes(c, kind, prec, subset);
+  void *p = nullptr;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return set_error(c, QDP_ENOMEM, "field of %zu bytes", bytes);
+  }
+  QDP_CUDA(c, cudaMemsetAsync(p, 0, bytes, c->stream));
+  return make_field(c, kind, prec, subset, p, bytes, true, out);
+}
+
+extern "C" int qdp_field_wrap(qdp_ctx c, int kind, int prec, int subset, void *ptr, size_t bytes, qdp_field *out) {
+  if (!c || !out || !ptr) return QDP_EINVAL;
+  *out = nullptr;
+  int rc = qdp_field_bytes(c, kind, prec, subset, nullptr, nullptr);
+  if (rc) return rc;
+  if (bytes < field_device_bytes(c, kind, prec, subset))
+    return set_error(c, QDP_ESHAPE, "wrap: %zu bytes < required %zu", bytes, field_device_bytes(c, kind, prec, subset));
+  if ((uintptr_t)ptr % 256) return set_error(c, QDP_EINVAL, "wrap: pointer not 256-byte aligned");
+  return make_field(c, kind, prec, subset, ptr, bytes, false, out);
+}
+
+extern "C" int qdp_field_free(qdp_field f) {
+  if (!f) return QDP_EINVAL;
+  if (f->owned && f->data) {
+    cudaStreamSynchronize(f->ctx->stream);
+    cudaFree(f->data);
+  }
+  delete f;
+  return QDP_OK;
+}
+
+extern "C" int qdp_field_info(const qdp_field f, int *kind, int *prec, int *subset, void **ptr) {
+  if (!f) return QDP_EINVAL;
+  if (kind) *kind = f->kind;
+  if (prec) *prec = f->prec;
+  if (subset) *subset = f->subset;
+  if (ptr) *ptr = f->data;
+  return QDP_OK;
+}
+
+extern "C" int qdp_field_import(qdp_field f, const void *host, size_t bytes) {
+  if (!f || !host) return QDP_EINVAL;
+  qdp_ctx c = f->ctx;
+  const size_t hb = field_host_bytes(c, f->kind, f->prec, f->subset);
+  if (bytes != hb) return set_error(c, QDP_ESHAPE, "import: %zu bytes, expected %zu", bytes, hb);
+  int rc;
+  if ((rc = ensure_staging(c, hb))) return rc;
+  QDP_CUDA(c, cudaMemcpyAsync(c->staging, host, hb, cudaMemcpyHostToDevice, c->stream));
+  if ((rc = layout_import(f, c->staging))) return rc;
+  QDP_CUDA(c, cudaStreamSynchronize(c->stream));
+  return QDP_OK;
+}
+
+extern "C" int qdp_field_export(const qdp_field f, void *host, size_t bytes) {
+  if (!f || !host) return QDP_EINVAL;
+  qdp_ctx c = f->ctx;
+  const size_t hb = field_host_bytes(c, f->kind, f->prec, f->subset);
+  if (bytes != hb) return set_error(c, QDP_ESHAPE, "export: %zu bytes, expected %zu", bytes, hb);
+  int rc;
+  if ((rc = ensure_staging(c, hb))) return rc;
+  if ((rc = layout_export(f, c->staging))) return rc;
+  QDP_CUDA(c, cudaMemcpyAsync(host, c->staging, hb, cudaMemcpyDeviceToHost, c->stream));
+  QDP_CUDA(c, cudaStreamSynchronize(c->stream));
+  return QDP_OK;
+}
+
+extern "C" int qdp_field_zero(qdp_field f) {
+  if (!f) return QDP_EINVAL;
+  qdp_ctx c = f->ctx;
+  QDP_CUDA(c, cudaMemsetAsync(f->data, 0, field_device_bytes(c, f->kind, f->prec, f->subset), c->stream));
+  return QDP_OK;
+}
+
+// parity block `par` of field f (nullptr if absent)
+static char *block_of(const qdp_field f, int par) {
+  if (f->kind == QDP_GAUGE) return nullptr;
+  const size_t blk = parity_block_bytes(f->kind, f->prec, f->ctx->geom.stride);
+  if (f->subset == QDP_ALL) return (char *)f->data + par * blk;
+  return f->subset == par ? (char *)f->data : nullptr;
+}
+
+static int check_pair(const qdp_field a, const qdp_field b) {
+  if (a->ctx != b->ctx) return set_error(a->ctx, QDP_ESHAPE, "fields on different contexts");
+  if (a->prec != b->prec) return set_error(a->ctx, QDP_EPREC, "precision mismatch");
+  return QDP_OK;
+}
+
+extern "C" int qdp_field_copy(qdp_field dst, const qdp_field src) {
+  if (!dst || !src) return QDP_EINVAL;
+  int rc;
+  if ((rc = check_pair(dst, src))) return rc;
+  qdp_ctx c = dst->ctx;
+  if (dst->kind != src->kind) return set_error(c, QDP_EINVAL, "copy: kind mismatch");
+  if (dst == src || dst->data == src->data) return QDP_OK;
+  if (dst->kind == QDP_GAUGE || dst->subset == src->subset) {
+    QDP_CUDA(c, cudaMemcpyAsync(dst->data, src->data, field_device_bytes(c, dst->kind, dst->prec, dst->subset),
+                                cudaMemcpyDeviceToDevice, c->stream));
+    return QDP_OK;
+  }
+  const int par = dst->subset == QDP_ALL ? src->subset : dst->subset;
+  char *d = block_of(dst, par), *s = block_of(src, par);
+  if (!d || !s) return set_error(c, QDP_EINVAL, "copy: incompatible subsets");
+  QDP_CUDA(c, cudaMemcpyAsync(d, s, parity_block_bytes(dst->kind, dst->prec, c->geom.stride), cudaMemcpyDeviceToDevice,
+                              c->stream));
+  return QDP_OK;
+}
+
+// ---------------------------------------------------------------------------- operations
+extern "C" int qdp_shift(qdp_field out, const qdp_field in, int mu, int sign) {
+  if (!out || !in) return QDP_EINVAL;
+  int rc;
+  if ((rc = check_pair(out, in))) return rc;
+  qdp_ctx c = out->ctx;
+  if (mu < 0 || mu > 3 || (sign != 1 && sign != -1)) return set_error(c, QDP_EINVAL, "shift: bad mu/sign");
+  if (out->kind != in->kind || in->kind == QDP_CLOVER) return set_error(c, QDP_EINVAL, "shift: fermion or gauge fields");
+  if (out == in || out->data == in->data) return set_error(c, QDP_EALIAS, "shift: out aliases in");
+  if (in->kind == QDP_FERMION) {
+    const bool ok = (in->subset == QDP_ALL && out->subset == QDP_ALL) ||
+                    (in->subset != QDP_ALL && out->subset == 1 - in->subset);
+    if (!ok) return set_error(c, QDP_EINVAL, "shift: parity p input needs a parity 1-p output");
+  }
+  return shift_field(c, out, in, mu, sign);
+}
+
+extern "C" int qdp_dslash(qdp_field out, const qdp_field U, const qdp_field psi, int out_parity) {
+  if (!out || !U || !psi) return QDP_EINVAL;
+  int rc;
+  if ((rc = check_pair(out, psi)) || (rc = check_pair(out, U))) return rc;
+  qdp_ctx c = out->ctx;
+  if (out->kind != QDP_FERMION || psi->kind != QDP_FERMION || U->kind != QDP_GAUGE)
+    return set_error(c, QDP_EINVAL, "dslash: kinds (fermion, gauge, fermion)");
+  if (!valid_subset(out_parity)) return set_error(c, QDP_EINVAL, "dslash: bad parity");
+  if (out == psi || out->data == psi->data) return set_error(c, QDP_EALIAS, "dslash: out aliases psi");
+  const int first = out_parity == QDP_ALL ? 0 : out_parity, last = out_parity == QDP_ALL ? 1 : out_parity;
+  if (out_parity == QDP_ALL && (out->subset != QDP_ALL || psi->subset != QDP_ALL))
+    return set_error(c, QDP_EINVAL, "dslash: out_parity ALL needs ALL fields");
+  for (int p = first; p <= last; p++)
+    if (!block_of(out, p) || !block_of(psi, 1 - p)) return set_error(c, QDP_EINVAL, "dslash: subset mismatch");
+  for (int p = first; p <= last; p++) {
+    DslashArgs a = {};
+    a.out = block_of(out, p);
+    a.psi = block_of(psi, 1 - p);
+    a.U = U->data;
+    a.parity = p;
+    a.epi = EPI_PLAIN;
+    a.b = 1.0;
+    if ((rc = dslash(c, out->prec, a))) return rc;
+  }
+  return QDP_OK;
+}
+
+static int read_result(qdp_ctx c, int slot, int n, double *out) {
+  QDP_CUDA(c, cudaMemcpyAsync(c->host_pinned, c->red_result + slot, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  QDP_CUDA(c, cudaStreamSynchronize(c->stream));
+  memcpy(out, c->host_pinned, n * sizeof(double));
+  return QDP_OK;
+}
+
+extern "C" int qdp_norm2(const qdp_field a, double *out) {
+  if (!a || !out) return QDP_EINVAL;
+  qdp_ctx c = a->ctx;
+  if (a->kind != QDP_FERMION) return set_error(c, QDP_EINVAL, "norm2: fermion fields");
+  int rc;
+  if ((rc = blas_norm2(c, a->prec, a->data, a->subset == QDP_ALL ? 2 : 1, 8))) return rc;
+  if ((rc = reduce_global(c, 8, 1))) return rc;
+  return read_result(c, 8, 1, out);
+}
+
+extern "C" int qdp_inner_product(const qdp_field a, const qdp_field b, double out[2]) {
+  if (!a || !b || !out) return QDP_EINVAL;
+  int rc;
+  if ((rc = check_pair(a, b))) return rc;
+  qdp_ctx c = a->ctx;
+  if (a->kind != QDP_FERMION || b->kind != QDP_FERMION) return set_error(c, QDP_EINVAL, "inner: fermion fields");
+  if (a->subset != b->subset) return set_error(c, QDP_EINVAL, "inner: subsets differ");
+  if ((rc = blas_inner(c, a->prec, a->data, b->data, a->subset == QDP_ALL ? 2 : 1, 10))) return rc;
+  if ((rc = reduce_global(c, 10, 2))) return rc;
+  return read_result(c, 10, 2, out);
+}
+
+extern "C" int qdp_axpy(double ar, double ai, const qdp_field x, qdp_field y) {
+  if (!x || !y) return QDP_EINVAL;
+  int rc;
+  if ((rc = check_pair(x, y))) return rc;
+  qdp_ctx c = y->ctx;
+  if (x->kind != QDP_FERMION || y->kind != QDP_FERMION) return set_error(c, QDP_EINVAL, "axpy: fermion fields");
+  if (x->subset == y->subset) return blas_axpy(c, y->prec, ar, ai, x->data, y->data, y->subset == QDP_ALL ? 2 : 1);
+  if (x->subset == QDP_ALL) return blas_axpy(c, y->prec, ar, ai, block_of(x, y->subset), y->data, 1);
+  return set_error(c, QDP_EINVAL, "axpy: x must cover y's subset");
+}
+
+extern "C" int qdp_clover_build(qdp_field A, qdp_field Ainv, const qdp_field U, double mass, double csw) {
+  if (!U || (!A && !Ainv)) return QDP_EINVAL;
+  qdp_ctx c = U->ctx;
+  int rc;
+  if (U->kind != QDP_GAUGE) return set_error(c, QDP_EINVAL, "clover_build: U must be a gauge field");
+  for (qdp_field f : {A, Ainv}) {
+    if (!f) continue;
+    if ((rc = check_pair(f, U))) return rc;
+    if (f->kind != QDP_CLOVER) return set_error(c, QDP_EINVAL, "clover_build: outputs must be clover fields");
+  }
+  if (A && Ainv && A->data == Ainv->data) return set_error(c, QDP_EALIAS, "clover_build: A aliases Ainv");
+  for (int mu = 0; mu < 4; mu++)
+    if (c->pgrid[mu] > 1)
+      return set_error(c, QDP_EUNSUPPORTED, "clover_build: partitioned lattices need the extended gauge field (not implemented)");
+  int singular = 0;
+  if ((rc = clover_build(c, U->prec, A ? A->data : nullptr, A ? A->subset : 0, Ainv ? Ainv->data : nullptr,
+                         Ainv ? Ainv->subset : 0, U->data, mass, csw, &singular)))
+    return rc;
+  if (singular) return set_error(c, QDP_ESINGULAR, "clover_build: zero pivot in a 6x6 block");
+  return QDP_OK;
+}
+
+extern "C" int qdp_clover_apply(qdp_field out, const qdp_field A, const qdp_field in, int parity) {
+  if (!out || !A || !in) return QDP_EINVAL;
+  int rc;
+  if ((rc = check_pair(out, A)) || (rc = check_pair(out, in))) return rc;
+  qdp_ctx c = out->ctx;
+  if (out->kind != QDP_FERMION || in->kind != QDP_FERMION || A->kind != QDP_CLOVER)
+    return set_error(c, QDP_EINVAL, "clover_apply: kinds (fermion, clover, fermion)");
+  if (!valid_subset(parity)) return set_error(c, QDP_EINVAL, "clover_apply: bad parity");
+  const int first = parity == QDP_ALL ? 0 : parity, last = parity == QDP_ALL ? 1 : parity;
+  for (int p = first; p <= last; p++) {
+    char *o = block_of(out, p), *i = block_of(in, p), *a = block_of(A, p);
+    if (!o || !i || !a) return set_error(c, QDP_EINVAL, "clover_apply: subset mismatch");
+  }
+  for (int p = first; p <= last; p++)
+    if ((rc = clover_apply(c, out->prec, block_of(out, p), block_of(A, p), block_of(in, p), 1))) return rc;
+  return QDP_OK;
+}
+
+extern "C" int qdp_cg_solve(qdp_field x, const qdp_field b, const qdp_field U, const qdp_field A, const qdp_field Ainv,
+                            double mass, double tol, int maxit, int *iters, double *resid_hist, int hist_cap,
+                            double *true_resid) {
+  if (!x || !b || !U) return QDP_EINVAL;
+  int rc;
+  if ((rc = check_pair(x, b)) || (rc = check_pair(x, U))) return rc;
+  qdp_ctx c = x->ctx;
+  if (x->kind != QDP_FERMION || b->kind != QDP_FERMION || U->kind != QDP_GAUGE)
+    return set_error(c, QDP_EINVAL, "cg: kinds (fermion, fermion, gauge)");
+  if (x->subset != QDP_ALL || b->subset != QDP_ALL) return set_error(c, QDP_EINVAL, "cg: x and b must be QDP_ALL");
+  if (x->data == b->data) return set_error(c, QDP_EALIAS, "cg: x aliases b");
+  if ((A == nullptr) != (Ainv == nullptr)) return set_error(c, QDP_EINVAL, "cg: give both A and Ainv, or neither");
+  if (A) {
+    if ((rc = check_pair(x, A)) || (rc = check_pair(x, Ainv))) return rc;
+    if (A->kind != QDP_CLOVER || Ainv->kind != QDP_CLOVER) return set_error(c, QDP_EINVAL, "cg: A, Ainv must be clover");
+    if (!block_of(A, 1) || !block_of(Ainv, 0)) return set_error(c, QDP_EINVAL, "cg: A must cover odd, Ainv even sites");
+    if (true_resid && A->subset != QDP_ALL) return set_error(c, QDP_EINVAL, "cg: true_resid needs A on all sites");
+  }
+  if (maxit < 0 || !(tol >= 0)) return set_error(c, QDP_EINVAL, "cg: bad tol/maxit");
+  return cg_solve(x, b, U, A, Ainv, mass, tol, maxit, iters, resid_hist, hist_cap, true_resid);
+}
+
+// ---------------------------------------------------------------------------- diagnostics
+extern "C" const char *qdp_strerror(int s) {
+  switch (s) {
+    case QDP_OK: return "ok";
+    case QDP_NOT_CONVERGED: return "not converged";
+    case QDP_EINVAL: return "invalid argument";
+    case QDP_ESHAPE: return "shape mismatch";
+    case QDP_EPREC: return "precision mismatch";
+    case QDP_EALIAS: return "aliased arguments";
+    case QDP_ENOMEM: return "out of memory";
+    case QDP_ECUDA: return "CUDA error";
+    case QDP_ENCCL: return "NCCL error";
+    case QDP_ESINGULAR: return "singular clover block";
+    case QDP_EUNSUPPORTED: return "unsupported";
+  }
+  return "unknown status";
+}
+
+extern "C" const char *qdp_last_error(qdp_ctx c) { return c ? c->last_error.c_str() : ""; }
+
+extern "C" int qdp_profile_query(qdp_ctx c, int cls, long *launches, double *ms) {
+  if (!c || cls < -1 || cls >= QDP_PK_COUNT) return QDP_EINVAL;
+  int rc;
+  if ((rc = resolve_profile(c))) return rc;
+  long n = 0;
+  double t = 0;
+  for (int k = 0; k < QDP_PK_COUNT; k++)
+    if (cls == -1 || cls == k) {
+      n += c->launches[k];
+      t += c->prof_ms[k];
+    }
+  if (launches) *launches = n;
+  if (ms) *ms = t;
+  return QDP_OK;
+}
+
+extern "C" int qdp_profile_reset(qdp_ctx c) {
+  if (!c) return QDP_EINVAL;
+  int rc;
+  if ((rc = resolve_profile(c))) return rc;
+  for (int k = 0; k < QDP_PK_COUNT; k++) {
+    c->launches[k] = 0;
+    c->prof_ms[k] = 0;
+  }
+  return QDP_OK;
+}

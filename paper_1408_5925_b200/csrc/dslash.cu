@@ -1,0 +1,447 @@
+// dslash.cu -- fused even-odd Wilson hopping term (section VIII-C) with
+// face packing and interior/exterior split for the halo overlap of section V
+// (PAPER.md:208-214).
+//
+//   (H psi)(x) = sum_mu [(1 - gamma_mu) U_mu(x) psi(x+mu) + (1 + gamma_mu) U_mu(x-mu)^dag psi(x-mu)]
+//
+// One thread per output site.  Per direction: load the neighbour spinor, spin-project to a
+// half spinor with (1 -/+ gamma_mu) (12 flop), multiply by U or U^dag (2 x 66 flop),
+// reconstruct rows 2,3 from rows 0,1 and accumulate (24 flop) -> 1320 flop per site
+// (DESIGN.md "Flop and byte accounting").  Projection/reconstruction follow the
+// DeGrand-Rossi basis (reading R1); the derivation is in DESIGN.md "Spin projection".
+//
+// Epilogues (fused into the same kernel, so the hopping result never round-trips HBM):
+//   EPI_PLAIN    out = b [g5] H psi
+//   EPI_XPAY     out = a x + b [g5] H psi
+//   EPI_CLOVINV  out = A^{-1} (a x + b [g5] H psi)         (x optional)
+//   EPI_CLOVXPAY out = A x + b [g5] H psi
+// g5_in applies gamma5 to psi as it is loaded (Mhat^dag = g5 Mhat g5).
+#include "internal.h"
+
+namespace qdpb {
+
+template <typename R> struct HalfGhost;  // ghost half-spinor SoA: 6 complex per face site
+template <> struct HalfGhost<double> {
+  static __device__ __forceinline__ void store(void *buf, int n, int f, const Half<double> &h) {
+    double2 *q = (double2 *)buf;
+#pragma unroll
+    for (int k = 0; k < 6; k++) q[(size_t)k * n + f] = make_double2(h.c[k].re, h.c[k].im);
+  }
+  static __device__ __forceinline__ Half<double> load(const void *buf, int n, int f) {
+    const double2 *q = (const double2 *)buf;
+    Half<double> h;
+#pragma unroll
+    for (int k = 0; k < 6; k++) {
+      double2 v = ld_stream(q + (size_t)k * n + f);
+      h.c[k] = {v.x, v.y};
+    }
+    return h;
+  }
+};
+template <> struct HalfGhost<float> {
+  static __device__ __forceinline__ void store(void *buf, int n, int f, const Half<float> &h) {
+    float4 *q = (float4 *)buf;
+#pragma unroll
+    for (int k = 0; k < 3; k++)
+      q[(size_t)k * n + f] = make_float4(h.c[2 * k].re, h.c[2 * k].im, h.c[2 * k + 1].re, h.c[2 * k + 1].im);
+  }
+  static __device__ __forceinline__ Half<float> load(const void *buf, int n, int f) {
+    const float4 *q = (const float4 *)buf;
+    Half<float> h;
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+      float4 v = ld_stream(q + (size_t)k * n + f);
+      h.c[2 * k] = {v.x, v.y};
+      h.c[2 * k + 1] = {v.z, v.w};
+    }
+    return h;
+  }
+};
+
+// rows 0,1 of (1 + S gamma_mu) psi  (S = -1: forward hop, S = +1: backward hop)
+template <int MU, int S, typename R>
+__device__ __forceinline__ Half<R> project(const Spinor<R> &p) {
+  Half<R> h;
+#pragma unroll
+  for (int c = 0; c < 3; c++) {
+    const cx<R> p0 = p.c[c], p1 = p.c[3 + c], p2 = p.c[6 + c], p3 = p.c[9 + c];
+    if (MU == 0) {        // h0 = p0 + S i p3, h1 = p1 + S i p2
+      h.c[c] = S > 0 ? p0 + times_i(p3) : p0 - times_i(p3);
+      h.c[3 + c] = S > 0 ? p1 + times_i(p2) : p1 - times_i(p2);
+    } else if (MU == 1) { // h0 = p0 - S p3, h1 = p1 + S p2
+      h.c[c] = S > 0 ? p0 - p3 : p0 + p3;
+      h.c[3 + c] = S > 0 ? p1 + p2 : p1 - p2;
+    } else if (MU == 2) { // h0 = p0 + S i p2, h1 = p1 - S i p3
+      h.c[c] = S > 0 ? p0 + times_i(p2) : p0 - times_i(p2);
+      h.c[3 + c] = S > 0 ? p1 - times_i(p3) : p1 + times_i(p3);
+    } else {              // h0 = p0 + S p2, h1 = p1 + S p3
+      h.c[c] = S > 0 ? p0 + p2 : p0 - p2;
+      h.c[3 + c] = S > 0 ? p1 + p3 : p1 - p3;
+    }
+  }
+  return h;
+}
+
+// acc += (1 + S gamma_mu) reconstructed from its rows 0,1 (h already colour-multiplied)
+template <int MU, int S, typename R>
+__device__ __forceinline__ void accum_recon(Spinor<R> &acc, const Half<R> &h) {
+#pragma unroll
+  for (int c = 0; c < 3; c++) {
+    const cx<R> h0 = h.c[c], h1 = h.c[3 + c];
+    acc.c[c] = acc.c[c] + h0;
+    acc.c[3 + c] = acc.c[3 + c] + h1;
+    if (MU == 0) {        // r2 = -S i h1, r3 = -S i h0
+      acc.c[6 + c] = S > 0 ? acc.c[6 + c] - times_i(h1) : acc.c[6 + c] + times_i(h1);
+      acc.c[9 + c] = S > 0 ? acc.c[9 + c] - times_i(h0) : acc.c[9 + c] + times_i(h0);
+    } else if (MU == 1) { // r2 = S h1, r3 = -S h0
+      acc.c[6 + c] = S > 0 ? acc.c[6 + c] + h1 : acc.c[6 + c] - h1;
+      acc.c[9 + c] = S > 0 ? acc.c[9 + c] - h0 : acc.c[9 + c] + h0;
+    } else if (MU == 2) { // r2 = -S i h0, r3 = S i h1
+      acc.c[6 + c] = S > 0 ? acc.c[6 + c] - times_i(h0) : acc.c[6 + c] + times_i(h0);
+      acc.c[9 + c] = S > 0 ? acc.c[9 + c] + times_i(h1) : acc.c[9 + c] - times_i(h1);
+    } else {              // r2 = S h0, r3 = S h1
+      acc.c[6 + c] = S > 0 ? acc.c[6 + c] + h0 : acc.c[6 + c] - h0;
+      acc.c[9 + c] = S > 0 ? acc.c[9 + c] + h1 : acc.c[9 + c] - h1;
+    }
+  }
+}
+
+template <typename R>
+__device__ __forceinline__ Half<R> mul_link(const Link<R> &u, const Half<R> &h) {  // U h
+  Half<R> r;
+#pragma unroll
+  for (int s = 0; s < 2; s++)
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+      cx<R> acc = cmul(u.m[3 * a], h.c[3 * s]);
+      acc = cmadd(u.m[3 * a + 1], h.c[3 * s + 1], acc);
+      acc = cmadd(u.m[3 * a + 2], h.c[3 * s + 2], acc);
+      r.c[3 * s + a] = acc;
+    }
+  return r;
+}
+template <typename R>
+__device__ __forceinline__ Half<R> mul_link_dag(const Link<R> &u, const Half<R> &h) {  // U^dag h
+  Half<R> r;
+#pragma unroll
+  for (int s = 0; s < 2; s++)
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+      cx<R> acc = {u.m[a].re * h.c[3 * s].re + u.m[a].im * h.c[3 * s].im,
+                   u.m[a].re * h.c[3 * s].im - u.m[a].im * h.c[3 * s].re};
+      acc = cjmadd(u.m[3 + a], h.c[3 * s + 1], acc);
+      acc = cjmadd(u.m[6 + a], h.c[3 * s + 2], acc);
+      r.c[3 * s + a] = acc;
+    }
+  return r;
+}
+
+template <typename R>
+__device__ __forceinline__ void g5(Spinor<R> &s) {
+#pragma unroll
+  for (int k = 6; k < 12; k++) s.c[k] = -s.c[k];
+}
+
+template <typename R> struct KParams {
+  FermView<R> out, psi, x;
+  GaugeView<R> U;
+  CloverView<R> A;
+  int parity;
+  R a, b;
+  // ghost buffers (exterior): [mu][dir], dir 0 = from -mu (already U^dag P+ psi), 1 = from +mu (P- psi)
+  const void *ghost[4][2];
+  // pack destinations: [mu][dir], dir 0 = to -mu neighbour, 1 = to +mu neighbour
+  void *dst[4][2];
+};
+
+template <typename R, int MU>
+__device__ __forceinline__ void hop_dir(const Geom &g, const KParams<R> &P, const int c[4], int cb, int p,
+                                        bool G5IN, bool halo, Spinor<R> &acc) {
+  // forward: (1 - gamma_mu) U_mu(x) psi(x + mu)
+  {
+    const bool remote = halo && ((g.part >> MU) & 1) && c[MU] == g.L[MU] - 1;
+    if (!remote) {
+      int n[4] = {c[0], c[1], c[2], c[3]};
+      n[MU] = (c[MU] + 1 == g.L[MU]) ? 0 : c[MU] + 1;
+      Spinor<R> s = P.psi.load(coords_cb(g, n));
+      if (G5IN) g5(s);
+      Half<R> h = project<MU, -1>(s);
+      Link<R> u = P.U.load(MU, p, cb);
+      accum_recon<MU, -1>(acc, mul_link(u, h));
+    }
+  }
+  // backward: (1 + gamma_mu) U_mu(x - mu)^dag psi(x - mu)
+  {
+    const bool remote = halo && ((g.part >> MU) & 1) && c[MU] == 0;
+    if (!remote) {
+      int n[4] = {c[0], c[1], c[2], c[3]};
+      n[MU] = (c[MU] == 0) ? g.L[MU] - 1 : c[MU] - 1;
+      const int ncb = coords_cb(g, n);
+      Spinor<R> s = P.psi.load(ncb);
+      if (G5IN) g5(s);
+      Half<R> h = project<MU, +1>(s);
+      Link<R> u = P.U.load(MU, 1 - p, ncb);
+      accum_recon<MU, +1>(acc, mul_link_dag(u, h));
+    }
+  }
+}
+
+template <typename R, int EPI>
+__device__ __forceinline__ void epilogue(const KParams<R> &P, int cb, Spinor<R> &acc, bool G5OUT) {
+  if (G5OUT) g5(acc);
+  Spinor<R> o;
+  if (EPI == EPI_PLAIN) {
+#pragma unroll
+    for (int k = 0; k < 12; k++) o.c[k] = P.b * acc.c[k];
+  } else if (EPI == EPI_XPAY) {
+    Spinor<R> xv = P.x.load_stream(cb);
+#pragma unroll
+    for (int k = 0; k < 12; k++) o.c[k] = P.a * xv.c[k] + P.b * acc.c[k];
+  } else if (EPI == EPI_CLOVINV) {
+    if (P.x.p) {
+      Spinor<R> xv = P.x.load_stream(cb);
+#pragma unroll
+      for (int k = 0; k < 12; k++) acc.c[k] = P.a * xv.c[k] + P.b * acc.c[k];
+    } else {
+#pragma unroll
+      for (int k = 0; k < 12; k++) acc.c[k] = P.b * acc.c[k];
+    }
+    o = clover_mul(P.A, cb, acc);
+  } else {  // EPI_CLOVXPAY
+    Spinor<R> xv = P.x.load_stream(cb);
+    Spinor<R> ax = clover_mul(P.A, cb, xv);
+#pragma unroll
+    for (int k = 0; k < 12; k++) o.c[k] = ax.c[k] + P.b * acc.c[k];
+  }
+  P.out.store(cb, o);
+}
+
+// Whole-lattice (HALO=false) or interior (HALO=true: remote hops skipped) kernel.
+template <typename R, int EPI, bool G5IN, bool G5OUT, bool HALO>
+__global__ void __launch_bounds__(128) dslash_kernel(const Geom g, const KParams<R> P) {
+  const int cb = blockIdx.x * blockDim.x + threadIdx.x;
+  if (cb >= g.Vh) return;
+  const int p = P.parity;
+  int c[4];
+  cb_coords(g, cb, p, c);
+  Spinor<R> acc;
+#pragma unroll
+  for (int k = 0; k < 12; k++) acc.c[k] = {R(0), R(0)};
+  hop_dir<R, 0>(g, P, c, cb, p, G5IN, HALO, acc);
+  hop_dir<R, 1>(g, P, c, cb, p, G5IN, HALO, acc);
+  hop_dir<R, 2>(g, P, c, cb, p, G5IN, HALO, acc);
+  hop_dir<R, 3>(g, P, c, cb, p, G5IN, HALO, acc);
+  epilogue<R, EPI>(P, cb, acc, G5OUT);
+}
+
+// Face packing for dim MU: input psi has parity q = 1 - p.
+//   f <  faceVh: my sites at x_mu = 0      -> P^- psi          -> dst[mu][0] (the -mu neighbour's forward ghost)
+//   f >= faceVh: my sites at x_mu = L-1    -> U_mu^dag P^+ psi  -> dst[mu][1] (the +mu neighbour's backward ghost)
+template <typename R, bool G5IN>
+__global__ void __launch_bounds__(128) pack_kernel(const Geom g, const KParams<R> P, int mu) {
+  const int n = g.faceVh[mu];
+  int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= 2 * n) return;
+  const int q = 1 - P.parity;
+  const bool fwd = f >= n;
+  if (fwd) f -= n;
+  int c[4];
+  face_coords(g, mu, fwd ? g.L[mu] - 1 : 0, f, q, c);
+  const int cb = coords_cb(g, c);
+  Spinor<R> s = P.psi.load(cb);
+  if (G5IN) g5(s);
+  Half<R> h;
+  if (!fwd) {
+    switch (mu) {
+      case 0: h = project<0, -1>(s); break;
+      case 1: h = project<1, -1>(s); break;
+      case 2: h = project<2, -1>(s); break;
+      default: h = project<3, -1>(s); break;
+    }
+    HalfGhost<R>::store(P.dst[mu][0], n, f, h);
+  } else {
+    switch (mu) {
+      case 0: h = project<0, +1>(s); break;
+      case 1: h = project<1, +1>(s); break;
+      case 2: h = project<2, +1>(s); break;
+      default: h = project<3, +1>(s); break;
+    }
+    Link<R> u = P.U.load(mu, q, cb);
+    HalfGhost<R>::store(P.dst[mu][1], n, f, mul_link_dag(u, h));
+  }
+}
+
+// Exterior: add the remote hops of dim mu for the output sites on its two faces.
+template <typename R, int EPI, bool G5OUT>
+__global__ void __launch_bounds__(128) exterior_kernel(const Geom g, const KParams<R> P, int mu) {
+  const int n = g.faceVh[mu];
+  int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= 2 * n) return;
+  const int p = P.parity;
+  const bool fwd = f >= n;  // fwd: site at x_mu = L-1 needs psi(x+mu) from the +mu neighbour
+  if (fwd) f -= n;
+  int c[4];
+  face_coords(g, mu, fwd ? g.L[mu] - 1 : 0, f, p, c);
+  const int cb = coords_cb(g, c);
+  Spinor<R> acc;
+#pragma unroll
+  for (int k = 0; k < 12; k++) acc.c[k] = {R(0), R(0)};
+  if (fwd) {
+    Half<R> h = HalfGhost<R>::load(P.ghost[mu][1], n, f);
+    Link<R> u = P.U.load(mu, p, cb);
+    Half<R> uh = mul_link(u, h);
+    switch (mu) {
+      case 0: accum_recon<0, -1>(acc, uh); break;
+      case 1: accum_recon<1, -1>(acc, uh); break;
+      case 2: accum_recon<2, -1>(acc, uh); break;
+      default: accum_recon<3, -1>(acc, uh); break;
+    }
+  } else {
+    Half<R> uh = HalfGhost<R>::load(P.ghost[mu][0], n, f);
+    switch (mu) {
+      case 0: accum_recon<0, +1>(acc, uh); break;
+      case 1: accum_recon<1, +1>(acc, uh); break;
+      case 2: accum_recon<2, +1>(acc, uh); break;
+      default: accum_recon<3, +1>(acc, uh); break;
+    }
+  }
+  if (G5OUT) g5(acc);
+#pragma unroll
+  for (int k = 0; k < 12; k++) acc.c[k] = P.b * acc.c[k];
+  if (EPI == EPI_CLOVINV) acc = clover_mul(P.A, cb, acc);
+  Spinor<R> o = P.out.load_plain(cb);
+#pragma unroll
+  for (int k = 0; k < 12; k++) o.c[k] = o.c[k] + acc.c[k];
+  P.out.store(cb, o);
+}
+
+// ------------------------------------------------------------------ host side
+template <typename R> static FermView<R> fview(const void *p, int stride);
+template <> FermView<double> fview<double>(const void *p, int stride) { return {(double2 *)p, stride}; }
+template <> FermView<float> fview<float>(const void *p, int stride) { return {(float4 *)p, stride}; }
+template <typename R> static GaugeView<R> gview(const void *p, int stride);
+template <> GaugeView<double> gview<double>(const void *p, int stride) { return {(const double2 *)p, stride}; }
+template <> GaugeView<float> gview<float>(const void *p, int stride) { return {(const float *)p, stride}; }
+template <typename R> static CloverView<R> cview(const void *p, int stride);
+template <> CloverView<double> cview<double>(const void *p, int stride) { return {(const double2 *)p, stride}; }
+template <> CloverView<float> cview<float>(const void *p, int stride) { return {(const float4 *)p, stride}; }
+
+template <typename R, int EPI, bool G5IN, bool G5OUT, bool HALO>
+static void launch_main(qdp_ctx ctx, const KParams<R> &P, int block) {
+  const Geom &g = ctx->geom;
+  dslash_kernel<R, EPI, G5IN, G5OUT, HALO><<<grid_for(g.Vh, block), block, 0, ctx->stream>>>(g, P);
+}
+
+template <typename R, int EPI>
+static void launch_main_dispatch(qdp_ctx ctx, const KParams<R> &P, bool g5i, bool g5o, bool halo, int block) {
+#define QDPB_L(A, B, C) launch_main<R, EPI, A, B, C>(ctx, P, block)
+  if (halo) {
+    if (g5i) { if (g5o) QDPB_L(true, true, true); else QDPB_L(true, false, true); }
+    else { if (g5o) QDPB_L(false, true, true); else QDPB_L(false, false, true); }
+  } else {
+    if (g5i) { if (g5o) QDPB_L(true, true, false); else QDPB_L(true, false, false); }
+    else { if (g5o) QDPB_L(false, true, false); else QDPB_L(false, false, false); }
+  }
+#undef QDPB_L
+}
+
+template <typename R, int EPI>
+static void launch_ext(qdp_ctx ctx, const KParams<R> &P, int mu, bool g5o) {
+  const Geom &g = ctx->geom;
+  const int n = 2 * g.faceVh[mu];
+  if (g5o) exterior_kernel<R, EPI, true><<<grid_for(n, 128), 128, 0, ctx->stream>>>(g, P, mu);
+  else exterior_kernel<R, EPI, false><<<grid_for(n, 128), 128, 0, ctx->stream>>>(g, P, mu);
+}
+
+template <typename R>
+static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
+  const Geom &g = ctx->geom;
+  const int prec = sizeof(R) == 8 ? QDP_F64 : QDP_F32;
+  KParams<R> P = {};
+  P.out = fview<R>(a.out, g.stride);
+  P.psi = fview<R>(a.psi, g.stride);
+  P.x = fview<R>(a.x, g.stride);
+  P.U = gview<R>(a.U, g.stride);
+  P.A = cview<R>(a.clov, g.stride);
+  P.parity = a.parity;
+  P.a = (R)a.a;
+  P.b = (R)a.b;
+  const int block = ctx->block > 0 ? ctx->block : 128;
+  const bool halo = g.part != 0;
+  int rc;
+
+  if (halo) {
+    if ((rc = ensure_halo(ctx, prec))) return rc;
+    // destinations: self-halo dims pack straight into our own ghost buffers (the peer is
+    // this rank); communicated dims pack into send buffers for NCCL.
+    bool any_comm = false;
+    size_t face_bytes[4] = {0, 0, 0, 0};
+    for (int mu = 0; mu < 4; mu++) {
+      if (!((g.part >> mu) & 1)) continue;
+      const bool self = ctx->pgrid[mu] == 1;
+      any_comm |= !self;
+      face_bytes[mu] = (size_t)g.faceVh[mu] * 12 * sizeof(R);
+      P.dst[mu][0] = self ? ctx->halo_recv[prec][mu][1] : ctx->halo_send[prec][mu][0];
+      P.dst[mu][1] = self ? ctx->halo_recv[prec][mu][0] : ctx->halo_send[prec][mu][1];
+      P.ghost[mu][0] = ctx->halo_recv[prec][mu][0];
+      P.ghost[mu][1] = ctx->halo_recv[prec][mu][1];
+    }
+    for (int mu = 0; mu < 4; mu++) {
+      if (!((g.part >> mu) & 1)) continue;
+      ProfEvent ev;
+      prof_begin(ctx, QDP_PK_PACK, &ev);
+      const int n = 2 * g.faceVh[mu];
+      if (a.g5_in) pack_kernel<R, true><<<grid_for(n, 128), 128, 0, ctx->stream>>>(g, P, mu);
+      else pack_kernel<R, false><<<grid_for(n, 128), 128, 0, ctx->stream>>>(g, P, mu);
+      if ((rc = prof_end(ctx, &ev))) return rc;
+    }
+    const bool overlap = ctx->overlap && any_comm;
+    if (any_comm) {
+      if (overlap) {
+        QDP_CUDA(ctx, cudaEventRecord(ctx->ev_packed, ctx->stream));
+        QDP_CUDA(ctx, cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_packed, 0));
+        if ((rc = comm_exchange(ctx, prec, face_bytes, ctx->comm_stream))) return rc;
+        QDP_CUDA(ctx, cudaEventRecord(ctx->ev_comm, ctx->comm_stream));
+      } else {
+        if ((rc = comm_exchange(ctx, prec, face_bytes, ctx->stream))) return rc;
+      }
+    }
+    {
+      ProfEvent ev;
+      prof_begin(ctx, QDP_PK_DSLASH, &ev);
+      switch (a.epi) {
+        case EPI_PLAIN: launch_main_dispatch<R, EPI_PLAIN>(ctx, P, a.g5_in, a.g5_out, true, block); break;
+        case EPI_XPAY: launch_main_dispatch<R, EPI_XPAY>(ctx, P, a.g5_in, a.g5_out, true, block); break;
+        case EPI_CLOVINV: launch_main_dispatch<R, EPI_CLOVINV>(ctx, P, a.g5_in, a.g5_out, true, block); break;
+        default: launch_main_dispatch<R, EPI_CLOVXPAY>(ctx, P, a.g5_in, a.g5_out, true, block); break;
+      }
+      if ((rc = prof_end(ctx, &ev))) return rc;
+    }
+    if (overlap) QDP_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_comm, 0));
+    for (int mu = 0; mu < 4; mu++) {
+      if (!((g.part >> mu) & 1)) continue;
+      ProfEvent ev;
+      prof_begin(ctx, QDP_PK_DSLASH_EXT, &ev);
+      if (a.epi == EPI_CLOVINV) launch_ext<R, EPI_CLOVINV>(ctx, P, mu, a.g5_out);
+      else launch_ext<R, EPI_PLAIN>(ctx, P, mu, a.g5_out);
+      if ((rc = prof_end(ctx, &ev))) return rc;
+    }
+    return QDP_OK;
+  }
+
+  ProfEvent ev;
+  prof_begin(ctx, QDP_PK_DSLASH, &ev);
+  switch (a.epi) {
+    case EPI_PLAIN: launch_main_dispatch<R, EPI_PLAIN>(ctx, P, a.g5_in, a.g5_out, false, block); break;
+    case EPI_XPAY: launch_main_dispatch<R, EPI_XPAY>(ctx, P, a.g5_in, a.g5_out, false, block); break;
+    case EPI_CLOVINV: launch_main_dispatch<R, EPI_CLOVINV>(ctx, P, a.g5_in, a.g5_out, false, block); break;
+    default: launch_main_dispatch<R, EPI_CLOVXPAY>(ctx, P, a.g5_in, a.g5_out, false, block); break;
+  }
+  return prof_end(ctx, &ev);
+}
+
+int dslash(qdp_ctx ctx, int prec, const DslashArgs &a) {
+  return prec == QDP_F64 ? dslash_t<double>(ctx, a) : dslash_t<float>(ctx, a);
+}
+
+}  // namespace qdpb

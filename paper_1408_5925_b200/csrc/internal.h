@@ -1,0 +1,469 @@
+// internal.h -- shared declarations of the qdpb CUDA library (not part of the ABI).
+//
+// Device layout: structure-of-arrays with the
+// checkerboard site index fastest, the coalescing condition of PAPER.md:156-160
+// (section III-B, layout function I(i_V, i_S, i_C, i_R)), but with re/im interleaved so
+// that one 16-byte load moves one complex double (or two complex floats):
+//   fermion F64 : double2 plane[parity][12 = 3*spin+colour][stride]
+//   fermion F32 : float4  plane[parity][6 = pairs of (spin,colour)][stride]
+//   gauge   F64 : double2 plane[mu][parity][9 = 3*row+col][stride]
+//   gauge   F32 : per (mu,parity): float4 plane[4][stride] (elements 0..7) + float2 plane[stride] (element 8)
+//   clover  F64 : double2 plane[parity][36][stride]   (per chiral block b: 3 diag pairs + 15 off-diag)
+//   clover  F32 : float4  plane[parity][18][stride]
+// stride = Vh rounded up to a multiple of 64 sites (1 KB-aligned planes).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include <vector>
+
+#include "../../include/qdpb.h"
+
+namespace qdpb {
+
+// ------------------------------------------------------------------ geometry
+struct Geom {
+  int L[4];        // local extents (all even)
+  int Lh0;         // L[0] / 2
+  int Vh;          // local sites per parity
+  int stride;      // plane stride (sites)
+  int part;        // bitmask: dims whose neighbours are reached through the halo path
+  int faceVh[4];   // sites per parity on a face orthogonal to mu: V / L[mu] / 2
+};
+
+// site coordinates of checkerboard index cb on parity p
+__host__ __device__ inline void cb_coords(const Geom &g, int cb, int p, int c[4]) {
+  int xh = cb % g.Lh0;
+  int r = cb / g.Lh0;
+  c[1] = r % g.L[1];
+  int r2 = r / g.L[1];
+  c[2] = r2 % g.L[2];
+  c[3] = r2 / g.L[2];
+  c[0] = 2 * xh + ((p + c[1] + c[2] + c[3]) & 1);
+}
+__host__ __device__ inline int coords_cb(const Geom &g, const int c[4]) {
+  return (c[0] >> 1) + g.Lh0 * (c[1] + g.L[1] * (c[2] + g.L[2] * c[3]));
+}
+__host__ __device__ inline int coords_parity(const int c[4]) { return (c[0] + c[1] + c[2] + c[3]) & 1; }
+
+// Face index of a site on the face orthogonal to mu: lexicographic index of the three
+// other coordinates (in x,y,z,t order), halved.  Bijective per parity because the first
+// remaining extent is even; sender and receiver compute the same index.
+__host__ __device__ inline int face_index(const Geom &g, int mu, const int c[4]) {
+  int lex = 0, mul = 1;
+#pragma unroll
+  for (int d = 0; d < 4; d++) {
+    if (d == mu) continue;
+    lex += c[d] * mul;
+    mul *= g.L[d];
+  }
+  return lex >> 1;
+}
+// inverse: coordinates of face site f on the face x_mu = xmu with site parity p
+__host__ __device__ inline void face_coords(const Geom &g, int mu, int xmu, int f, int p, int c[4]) {
+  int dims[3], k = 0;
+#pragma unroll
+  for (int d = 0; d < 4; d++)
+    if (d != mu) dims[k++] = d;
+  int A = g.L[dims[0]], B = g.L[dims[1]];
+  int ah = f % (A >> 1);
+  int rest = f / (A >> 1);
+  int b = rest % B;
+  int cc = rest / B;
+  c[mu] = xmu;
+  c[dims[1]] = b;
+  c[dims[2]] = cc;
+  c[dims[0]] = 2 * ah + ((p + xmu + b + cc) & 1);
+}
+
+#ifdef __CUDACC__
+// ------------------------------------------------------------------ complex helpers
+template <typename R> struct cx { R re, im; };
+template <typename R> __device__ __forceinline__ cx<R> mk(R a, R b) { return {a, b}; }
+template <typename R> __device__ __forceinline__ cx<R> operator+(cx<R> a, cx<R> b) { return {a.re + b.re, a.im + b.im}; }
+template <typename R> __device__ __forceinline__ cx<R> operator-(cx<R> a, cx<R> b) { return {a.re - b.re, a.im - b.im}; }
+template <typename R> __device__ __forceinline__ cx<R> operator*(R s, cx<R> a) { return {s * a.re, s * a.im}; }
+template <typename R> __device__ __forceinline__ cx<R> operator-(cx<R> a) { return {-a.re, -a.im}; }
+template <typename R> __device__ __forceinline__ cx<R> cmul(cx<R> a, cx<R> b) {
+  return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re};
+}
+// conj(a) * b
+template <typename R> __device__ __forceinline__ cx<R> cjmul(cx<R> a, cx<R> b) {
+  return {a.re * b.re + a.im * b.im, a.re * b.im - a.im * b.re};
+}
+template <typename R> __device__ __forceinline__ cx<R> cmadd(cx<R> a, cx<R> b, cx<R> acc) {  // acc + a*b
+  acc.re = fma(a.re, b.re, acc.re);
+  acc.re = fma(-a.im, b.im, acc.re);
+  acc.im = fma(a.re, b.im, acc.im);
+  acc.im = fma(a.im, b.re, acc.im);
+  return acc;
+}
+template <typename R> __device__ __forceinline__ cx<R> cjmadd(cx<R> a, cx<R> b, cx<R> acc) {  // acc + conj(a)*b
+  acc.re = fma(a.re, b.re, acc.re);
+  acc.re = fma(a.im, b.im, acc.re);
+  acc.im = fma(a.re, b.im, acc.im);
+  acc.im = fma(-a.im, b.re, acc.im);
+  return acc;
+}
+template <typename R> __device__ __forceinline__ cx<R> times_i(cx<R> a) { return {-a.im, a.re}; }
+template <typename R> __device__ __forceinline__ cx<R> times_mi(cx<R> a) { return {a.im, -a.re}; }
+
+// ------------------------------------------------------------------ memory access
+// Streaming (read-once) loads: read-only path, no L1 allocation.
+__device__ __forceinline__ double2 ld_stream(const double2 *p) {
+  double2 r;
+  asm("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ float4 ld_stream(const float4 *p) {
+  float4 r;
+  asm("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ float2 ld_stream(const float2 *p) {
+  float2 r;
+  asm("ld.global.nc.L1::no_allocate.v2.f32 {%0,%1}, [%2];" : "=f"(r.x), "=f"(r.y) : "l"(p));
+  return r;
+}
+// Re-used loads (neighbour spinors: 8 readers per site) go through the normal path.
+__device__ __forceinline__ double2 ld_reuse(const double2 *p) { return __ldg(p); }
+__device__ __forceinline__ float4 ld_reuse(const float4 *p) { return __ldg(p); }
+// Streaming stores.
+__device__ __forceinline__ void st_stream(double2 *p, double2 v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream(float4 *p, float4 v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream(float2 *p, float2 v) { __stcs(p, v); }
+
+// Spinor: 12 complex, index 3*spin + colour.
+template <typename R> struct Spinor { cx<R> c[12]; };
+// Half spinor: 6 complex, index 3*h + colour (h = 0,1).
+template <typename R> struct Half { cx<R> c[6]; };
+template <typename R> struct Link { cx<R> m[9]; };  // row-major
+
+template <typename R> struct FermView;
+template <> struct FermView<double> {
+  double2 *p;  // parity block base
+  int stride;
+  __device__ __forceinline__ Spinor<double> load(int cb) const {
+    Spinor<double> s;
+#pragma unroll
+    for (int k = 0; k < 12; k++) {
+      double2 v = ld_reuse(p + (size_t)k * stride + cb);
+      s.c[k] = {v.x, v.y};
+    }
+    return s;
+  }
+  __device__ __forceinline__ Spinor<double> load_stream(int cb) const {
+    Spinor<double> s;
+#pragma unroll
+    for (int k = 0; k < 12; k++) {
+      double2 v = ld_stream(p + (size_t)k * stride + cb);
+      s.c[k] = {v.x, v.y};
+    }
+    return s;
+  }
+  __device__ __forceinline__ Spinor<double> load_plain(int cb) const {
+    Spinor<double> s;
+#pragma unroll
+    for (int k = 0; k < 12; k++) {
+      double2 v = p[(size_t)k * stride + cb];
+      s.c[k] = {v.x, v.y};
+    }
+    return s;
+  }
+  __device__ __forceinline__ void store(int cb, const Spinor<double> &s) const {
+#pragma unroll
+    for (int k = 0; k < 12; k++) st_stream(p + (size_t)k * stride + cb, make_double2(s.c[k].re, s.c[k].im));
+  }
+};
+template <> struct FermView<float> {
+  float4 *p;
+  int stride;
+  __device__ __forceinline__ Spinor<float> load(int cb) const {
+    Spinor<float> s;
+#pragma unroll
+    for (int k = 0; k < 6; k++) {
+      float4 v = ld_reuse(p + (size_t)k * stride + cb);
+      s.c[2 * k] = {v.x, v.y};
+      s.c[2 * k + 1] = {v.z, v.w};
+    }
+    return s;
+  }
+  __device__ __forceinline__ Spinor<float> load_stream(int cb) const {
+    Spinor<float> s;
+#pragma unroll
+    for (int k = 0; k < 6; k++) {
+      float4 v = ld_stream(p + (size_t)k * stride + cb);
+      s.c[2 * k] = {v.x, v.y};
+      s.c[2 * k + 1] = {v.z, v.w};
+    }
+    return s;
+  }
+  __device__ __forceinline__ Spinor<float> load_plain(int cb) const {
+    Spinor<float> s;
+#pragma unroll
+    for (int k = 0; k < 6; k++) {
+      float4 v = p[(size_t)k * stride + cb];
+      s.c[2 * k] = {v.x, v.y};
+      s.c[2 * k + 1] = {v.z, v.w};
+    }
+    return s;
+  }
+  __device__ __forceinline__ void store(int cb, const Spinor<float> &s) const {
+#pragma unroll
+    for (int k = 0; k < 6; k++)
+      st_stream(p + (size_t)k * stride + cb, make_float4(s.c[2 * k].re, s.c[2 * k].im, s.c[2 * k + 1].re, s.c[2 * k + 1].im));
+  }
+};
+
+// Gauge field: base of the whole field; link (mu, parity, cb).
+template <typename R> struct GaugeView;
+template <> struct GaugeView<double> {
+  const double2 *p;
+  int stride;
+  __device__ __forceinline__ const double2 *block(int mu, int par) const { return p + (size_t)(mu * 2 + par) * 9 * stride; }
+  __device__ __forceinline__ Link<double> load(int mu, int par, int cb) const {
+    const double2 *b = block(mu, par);
+    Link<double> u;
+#pragma unroll
+    for (int k = 0; k < 9; k++) {
+      double2 v = ld_stream(b + (size_t)k * stride + cb);
+      u.m[k] = {v.x, v.y};
+    }
+    return u;
+  }
+};
+template <> struct GaugeView<float> {
+  const float *p;  // byte layout: per (mu,par) block of stride*(4*16+8) bytes
+  int stride;
+  __device__ __forceinline__ Link<float> load(int mu, int par, int cb) const {
+    const char *b = (const char *)p + (size_t)(mu * 2 + par) * stride * 72;
+    const float4 *q = (const float4 *)b;
+    const float2 *q2 = (const float2 *)(b + (size_t)stride * 64);
+    Link<float> u;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      float4 v = ld_stream(q + (size_t)k * stride + cb);
+      u.m[2 * k] = {v.x, v.y};
+      u.m[2 * k + 1] = {v.z, v.w};
+    }
+    float2 v = ld_stream(q2 + cb);
+    u.m[8] = {v.x, v.y};
+    return u;
+  }
+};
+
+// Packed Hermitian clover block pair: per chiral block b: d[6] real + off[15] complex
+// (strictly lower triangle, row-major: (i,j), i>j -> i(i-1)/2 + j).  36 "complex slots"
+// per site: block b occupies slots 18b .. 18b+17 = (d0,d1),(d2,d3),(d4,d5),off[0..14].
+template <typename R> struct CloverBlock { R d[6]; cx<R> off[15]; };
+template <typename R> struct CloverView;
+template <> struct CloverView<double> {
+  const double2 *p;  // parity block base
+  int stride;
+  __device__ __forceinline__ CloverBlock<double> load(int b, int cb) const {
+    CloverBlock<double> B;
+    const double2 *q = p + (size_t)18 * b * stride + cb;
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+      double2 v = ld_stream(q + (size_t)k * stride);
+      B.d[2 * k] = v.x;
+      B.d[2 * k + 1] = v.y;
+    }
+#pragma unroll
+    for (int k = 0; k < 15; k++) {
+      double2 v = ld_stream(q + (size_t)(3 + k) * stride);
+      B.off[k] = {v.x, v.y};
+    }
+    return B;
+  }
+};
+template <> struct CloverView<float> {
+  const float4 *p;
+  int stride;
+  __device__ __forceinline__ CloverBlock<float> load(int b, int cb) const {
+    // per block: 36 floats = 9 float4: d0..d5, off0.re,off0.im, then off1..off14 (28 floats)
+    CloverBlock<float> B;
+    const float4 *q = p + (size_t)9 * b * stride + cb;
+    float f[36];
+#pragma unroll
+    for (int k = 0; k < 9; k++) {
+      float4 v = ld_stream(q + (size_t)k * stride);
+      f[4 * k] = v.x; f[4 * k + 1] = v.y; f[4 * k + 2] = v.z; f[4 * k + 3] = v.w;
+    }
+#pragma unroll
+    for (int k = 0; k < 6; k++) B.d[k] = f[k];
+#pragma unroll
+    for (int k = 0; k < 15; k++) B.off[k] = {f[6 + 2 * k], f[7 + 2 * k]};
+    return B;
+  }
+};
+
+// y = B v for one packed Hermitian 6x6 block
+template <typename R>
+__device__ __forceinline__ void clover_block_mul(const CloverBlock<R> &B, const cx<R> v[6], cx<R> y[6]) {
+#pragma unroll
+  for (int i = 0; i < 6; i++) y[i] = B.d[i] * v[i];
+#pragma unroll
+  for (int i = 1; i < 6; i++)
+#pragma unroll
+    for (int j = 0; j < i; j++) {
+      const cx<R> o = B.off[i * (i - 1) / 2 + j];
+      y[i] = cmadd(o, v[j], y[i]);    // lower: M[i][j] = o
+      y[j] = cjmadd(o, v[i], y[j]);   // upper: M[j][i] = conj(o)
+    }
+}
+// out = A in (both chiral blocks: spins {0,1} -> block 0, {2,3} -> block 1)
+template <typename R>
+__device__ __forceinline__ Spinor<R> clover_mul(const CloverView<R> &A, int cb, const Spinor<R> &in) {
+  Spinor<R> out;
+#pragma unroll
+  for (int b = 0; b < 2; b++) {
+    CloverBlock<R> B = A.load(b, cb);
+    cx<R> v[6], y[6];
+#pragma unroll
+    for (int i = 0; i < 6; i++) v[i] = in.c[6 * b + i];
+    clover_block_mul(B, v, y);
+#pragma unroll
+    for (int i = 0; i < 6; i++) out.c[6 * b + i] = y[i];
+  }
+  return out;
+}
+
+#endif  // __CUDACC__
+
+// ------------------------------------------------------------------ host-side objects
+enum { KIND_FERMION = QDP_FERMION, KIND_GAUGE = QDP_GAUGE, KIND_CLOVER = QDP_CLOVER };
+
+size_t parity_block_bytes(int kind, int prec, int stride);  // bytes of one parity block
+size_t host_site_reals(int kind);                           // 24 / 72 / 288
+
+struct Comm;  // comm.cpp
+
+struct ProfEvent {
+  int cls;
+  cudaEvent_t a, b;
+};
+
+}  // namespace qdpb
+
+struct qdp_field_s {
+  qdp_ctx ctx;
+  int kind, prec, subset;
+  void *data;
+  size_t bytes;
+  bool owned;
+};
+
+struct qdp_ctx_s {
+  int gdims[4], pgrid[4], pcoord[4];
+  int rank, nranks, device;
+  qdpb::Geom geom;
+  long V;
+  cudaStream_t stream = nullptr, comm_stream = nullptr;
+  bool own_stream = false;
+  cudaEvent_t ev_packed = nullptr, ev_comm = nullptr;
+  // options
+  int overlap = 1, self_halo = 0, profiling = 0, block = 0, det_reduce = 1;
+  // scratch (device)
+  void *staging = nullptr;
+  size_t staging_bytes = 0;
+  double *red_partials = nullptr;  // per-block partial sums (2 doubles per block)
+  int red_capacity = 0;            // number of blocks
+  double *red_result = nullptr;    // device scalars: [0..7]
+  double *red_gather = nullptr;    // [nranks * 2] gathered per-rank sums
+  double *host_pinned = nullptr;   // pinned host scratch (64 doubles)
+  // halo buffers: [prec][mu][dir] for send and recv (dir 0 = to/from -mu, 1 = to/from +mu)
+  void *halo_send[2][4][2] = {}, *halo_recv[2][4][2] = {};
+  size_t halo_bytes[2] = {0, 0};
+  qdpb::Comm *comm = nullptr;
+  int neighbour[4][2];  // ranks of -mu / +mu neighbours
+  // profiling / counting
+  long launches[QDP_PK_COUNT] = {};
+  double prof_ms[QDP_PK_COUNT] = {};
+  std::vector<qdpb::ProfEvent> pending;
+  std::vector<cudaEvent_t> event_pool;
+  std::string last_error;
+};
+
+namespace qdpb {
+// error helpers (capi.cu)
+int set_error(qdp_ctx ctx, int status, const char *fmt, ...);
+int cuda_check(qdp_ctx ctx, cudaError_t e, const char *what);
+#define QDP_CUDA(ctx, call)                                   \
+  do {                                                        \
+    cudaError_t _e = (call);                                  \
+    if (_e != cudaSuccess) return qdpb::cuda_check(ctx, _e, #call); \
+  } while (0)
+
+// launch bookkeeping: call before/after each kernel launch
+void prof_begin(qdp_ctx ctx, int cls, ProfEvent *ev);
+int prof_end(qdp_ctx ctx, ProfEvent *ev);  // checks cudaGetLastError
+
+int ensure_staging(qdp_ctx ctx, size_t bytes);
+int ensure_reduce(qdp_ctx ctx, int blocks);
+int ensure_halo(qdp_ctx ctx, int prec);
+
+// ---- kernels entry points (host wrappers, each enqueues on ctx->stream) ----
+// layout.cu
+int layout_import(qdp_field f, const void *dev_aos);      // staging (device AoS) -> field
+int layout_export(const qdp_field f, void *dev_aos);      // field -> staging
+int field_copy_parity(qdp_ctx ctx, int kind, int prec, void *dst, const void *src, size_t bytes);
+
+// blas.cu: operate on parity blocks (n_par = 1 or 2 consecutive blocks)
+// y = a x + y
+int blas_axpy(qdp_ctx ctx, int prec, double ar, double ai, const void *x, void *y, int nblk);
+// partial sums -> red_result[slot] (and slot+1 for the imaginary part)
+int blas_norm2(qdp_ctx ctx, int prec, const void *a, int nblk, int slot);
+int blas_inner(qdp_ctx ctx, int prec, const void *a, const void *b, int nblk, int slot);
+// finish a reduction: cross-rank sum of red_result[slot..slot+n-1]
+int reduce_global(qdp_ctx ctx, int slot, int n);
+// CG helpers (device scalars in red_result)
+int blas_cg_update_xr(qdp_ctx ctx, int prec, void *x, void *r, const void *p, const void *q,
+                      int rho_slot, int pq_slot, int rr_slot);
+int blas_cg_update_p(qdp_ctx ctx, int prec, void *p, const void *r, int rho_new_slot, int rho_old_slot);
+int blas_xpay(qdp_ctx ctx, int prec, const void *x, double a, void *y, int nblk);  // y = x + a y
+int blas_scale_copy(qdp_ctx ctx, int prec, void *dst, const void *src, double a, int nblk);  // dst = a src
+
+// dslash.cu
+enum Epi { EPI_PLAIN = 0, EPI_XPAY = 1, EPI_CLOVINV = 2, EPI_CLOVXPAY = 3 };
+struct DslashArgs {
+  void *out;              // output parity block
+  const void *psi;        // input parity block (parity 1-p)
+  const void *U;          // gauge field base
+  const void *x;          // xpay vector (output parity block) or nullptr
+  const void *clov;       // clover parity block for output parity (A or A^-1) or nullptr
+  int parity;             // output parity p
+  double a, b;            // epilogue scalars
+  int epi;                // Epi
+  bool g5_in, g5_out;
+};
+int dslash(qdp_ctx ctx, int prec, const DslashArgs &a);
+
+// clover.cu
+int clover_build(qdp_ctx ctx, int prec, void *A, int A_subset, void *Ainv, int Ainv_subset,
+                 const void *U, double mass, double csw, int *singular_flag_host);
+int clover_apply(qdp_ctx ctx, int prec, void *out, const void *A, const void *in, int nblk);
+
+// shift.cu
+int shift_field(qdp_ctx ctx, qdp_field out, const qdp_field in, int mu, int sign);
+
+// solver.cu
+int cg_solve(qdp_field x, const qdp_field b, const qdp_field U, const qdp_field A,
+             const qdp_field Ainv, double mass, double tol, int maxit, int *iters,
+             double *hist, int hist_cap, double *true_resid);
+
+// comm.cpp
+int comm_get_unique_id(unsigned char id[128]);
+int comm_init(qdp_ctx ctx, const unsigned char *id);
+void comm_destroy(qdp_ctx ctx);
+// exchange halo buffers of `bytes[mu]` per face for every partitioned dim, on `stream`
+int comm_exchange(qdp_ctx ctx, int prec, const size_t face_bytes[4], cudaStream_t stream);
+int comm_sendrecv(qdp_ctx ctx, const void *send, size_t bytes, int to, void *recv, int from, cudaStream_t stream);
+int comm_allgather_f64(qdp_ctx ctx, const double *send, double *recv, int count, cudaStream_t stream);
+int comm_allreduce_f64(qdp_ctx ctx, double *buf, int count, cudaStream_t stream);
+
+inline size_t fermion_block_bytes(int prec, int stride) { return (size_t)stride * (prec == QDP_F64 ? 12 * 16 : 6 * 16); }
+inline int grid_for(long n, int block) { return (int)((n + block - 1) / block); }
+
+}  // namespace qdpb

@@ -1,0 +1,162 @@
+// layout.cu -- host canonical (AoS, Table I order spin->colour->re/im) <->
+// device structure-of-arrays conversion (section III-B), done on the
+// device: the host array is copied as-is into a device staging buffer, then one thread per
+// site scatters / gathers its components.  Also the slot maps shared with shift.cu.
+#include "internal.h"
+#include "slots.h"
+
+namespace qdpb {
+
+size_t host_site_reals(int kind) { return kind == KIND_FERMION ? 24 : kind == KIND_GAUGE ? 72 : 288; }
+
+size_t parity_block_bytes(int kind, int prec, int stride) {
+  if (kind == KIND_FERMION) return fermion_block_bytes(prec, stride);
+  if (kind == KIND_GAUGE) return (size_t)4 * stride * (prec == QDP_F64 ? 9 * 16 : 72);  // 4 mu per parity
+  return (size_t)stride * (prec == QDP_F64 ? 36 * 16 : 18 * 16);
+}
+
+SlotMap make_slot_map(int kind, int prec, int stride, int subset) {
+  SlotMap m = {};
+  const size_t S = (size_t)stride;
+  if (kind == KIND_FERMION) {
+    m.n = 12;
+    const size_t blk = fermion_block_bytes(prec, stride);
+    for (int p = 0; p < 2; p++) {
+      const long long base = subset == QDP_ALL ? (long long)(p * blk) : (p == subset ? 0 : -1);
+      for (int k = 0; k < 12; k++) {
+        if (prec == QDP_F64) { m.off[p][k] = base < 0 ? -1 : base + (long long)(k * S * 16); m.step[k] = 16; }
+        else { m.off[p][k] = base < 0 ? -1 : base + (long long)((k / 2) * S * 16 + (k & 1) * 8); m.step[k] = 16; }
+      }
+    }
+  } else {  // gauge: slot = mu*9 + e
+    m.n = 36;
+    for (int p = 0; p < 2; p++)
+      for (int mu = 0; mu < 4; mu++)
+        for (int e = 0; e < 9; e++) {
+          const int k = mu * 9 + e;
+          if (prec == QDP_F64) {
+            m.off[p][k] = (long long)(((mu * 2 + p) * 9 + e) * S * 16);
+            m.step[k] = 16;
+          } else {
+            const long long blk = (long long)((mu * 2 + p) * S * 72);
+            m.off[p][k] = blk + (long long)(e < 8 ? (e / 2) * S * 16 + (e & 1) * 8 : S * 64);
+            m.step[k] = e < 8 ? 16 : 8;
+          }
+        }
+  }
+  return m;
+}
+
+// host record i -> (parity, cb)
+__device__ __forceinline__ void record_site(const Geom &g, int subset, long i, int &p, int &cb) {
+  if (subset == QDP_ALL) {
+    int c[4];
+    long s = i;
+    c[0] = (int)(s % g.L[0]); s /= g.L[0];
+    c[1] = (int)(s % g.L[1]); s /= g.L[1];
+    c[2] = (int)(s % g.L[2]);
+    c[3] = (int)(s / g.L[2]);
+    p = coords_parity(c);
+    cb = (int)(i >> 1);
+  } else {
+    p = subset;
+    cb = (int)i;
+  }
+}
+
+template <typename R, bool IMPORT>
+__global__ void slots_kernel(const Geom g, const SlotMap m, int subset, long nrec, char *data, R *aos) {
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nrec) return;
+  int p, cb;
+  record_site(g, subset, i, p, cb);
+  R *rec = aos + i * m.n * 2;
+  for (int k = 0; k < m.n; k++) {
+    R *d = (R *)(data + m.off[p][k] + (long long)cb * m.step[k]);
+    if (IMPORT) { d[0] = rec[2 * k]; d[1] = rec[2 * k + 1]; }
+    else { rec[2 * k] = d[0]; rec[2 * k + 1] = d[1]; }
+  }
+}
+
+// packed clover real j (0..71) of a parity block -> byte offset for cb = 0 (step 16 bytes)
+template <typename R>
+__device__ __forceinline__ long long clover_real_off(int j, int stride) {
+  const int b = j / 36, r = j % 36;
+  if (sizeof(R) == 8) {
+    if (r < 6) return (long long)(18 * b + r / 2) * stride * 16 + (r & 1) * 8;
+    const int k = (r - 6) / 2;
+    return (long long)(18 * b + 3 + k) * stride * 16 + ((r - 6) & 1) * 8;
+  }
+  return (long long)(9 * b + r / 4) * stride * 16 + (r % 4) * 4;
+}
+
+// dense (row, col) of block-b packed real r: returns (row, col, part, conj-mirror)
+template <typename R, bool IMPORT>
+__global__ void clover_kernel(const Geom g, int subset, long nrec, char *data, size_t blk_bytes, R *aos) {
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nrec) return;
+  int p, cb;
+  record_site(g, subset, i, p, cb);
+  char *base = data + (subset == QDP_ALL ? p * blk_bytes : 0) + (size_t)cb * 16;
+  R *rec = aos + i * 288;  // [12][12][2]
+  if (!IMPORT)
+    for (int k = 0; k < 288; k++) rec[k] = R(0);
+  for (int b = 0; b < 2; b++) {
+    for (int ii = 0; ii < 6; ii++) {  // diagonal
+      R *d = (R *)(base + clover_real_off<R>(36 * b + ii, g.stride));
+      const int row = 6 * b + ii;
+      if (IMPORT) *d = rec[(row * 12 + row) * 2];
+      else rec[(row * 12 + row) * 2] = *d;
+    }
+    for (int a = 1; a < 6; a++)
+      for (int c = 0; c < a; c++) {
+        const int k = a * (a - 1) / 2 + c;
+        R *re = (R *)(base + clover_real_off<R>(36 * b + 6 + 2 * k, g.stride));
+        R *im = (R *)(base + clover_real_off<R>(36 * b + 7 + 2 * k, g.stride));
+        const int row = 6 * b + a, col = 6 * b + c;
+        if (IMPORT) {
+          *re = rec[(row * 12 + col) * 2];
+          *im = rec[(row * 12 + col) * 2 + 1];
+        } else {
+          rec[(row * 12 + col) * 2] = *re;
+          rec[(row * 12 + col) * 2 + 1] = *im;
+          rec[(col * 12 + row) * 2] = *re;
+          rec[(col * 12 + row) * 2 + 1] = -*im;
+        }
+      }
+  }
+}
+
+static int layout_run(qdp_field f, void *dev_aos, bool import) {
+  qdp_ctx ctx = f->ctx;
+  const Geom &g = ctx->geom;
+  const long nrec = f->subset == QDP_ALL ? ctx->V : g.Vh;
+  const int blocks = grid_for(nrec, 128);
+  ProfEvent ev;
+  prof_begin(ctx, QDP_PK_LAYOUT, &ev);
+  if (f->kind == KIND_CLOVER) {
+    const size_t blk = parity_block_bytes(KIND_CLOVER, f->prec, g.stride);
+    if (f->prec == QDP_F64) {
+      if (import) clover_kernel<double, true><<<blocks, 128, 0, ctx->stream>>>(g, f->subset, nrec, (char *)f->data, blk, (double *)dev_aos);
+      else clover_kernel<double, false><<<blocks, 128, 0, ctx->stream>>>(g, f->subset, nrec, (char *)f->data, blk, (double *)dev_aos);
+    } else {
+      if (import) clover_kernel<float, true><<<blocks, 128, 0, ctx->stream>>>(g, f->subset, nrec, (char *)f->data, blk, (float *)dev_aos);
+      else clover_kernel<float, false><<<blocks, 128, 0, ctx->stream>>>(g, f->subset, nrec, (char *)f->data, blk, (float *)dev_aos);
+    }
+  } else {
+    SlotMap m = make_slot_map(f->kind, f->prec, g.stride, f->subset);
+    if (f->prec == QDP_F64) {
+      if (import) slots_kernel<double, true><<<blocks, 128, 0, ctx->stream>>>(g, m, f->subset, nrec, (char *)f->data, (double *)dev_aos);
+      else slots_kernel<double, false><<<blocks, 128, 0, ctx->stream>>>(g, m, f->subset, nrec, (char *)f->data, (double *)dev_aos);
+    } else {
+      if (import) slots_kernel<float, true><<<blocks, 128, 0, ctx->stream>>>(g, m, f->subset, nrec, (char *)f->data, (float *)dev_aos);
+      else slots_kernel<float, false><<<blocks, 128, 0, ctx->stream>>>(g, m, f->subset, nrec, (char *)f->data, (float *)dev_aos);
+    }
+  }
+  return prof_end(ctx, &ev);
+}
+
+int layout_import(qdp_field f, const void *dev_aos) { return layout_run(f, (void *)dev_aos, true); }
+int layout_export(const qdp_field f, void *dev_aos) { return layout_run((qdp_field)f, dev_aos, false); }
+
+}  // namespace qdpb
