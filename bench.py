@@ -1,0 +1,356 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200-native QDP hot path (arXiv:1408.5925) -- one JSON line on rank 0.
+
+Step = one even-odd preconditioned Wilson-clover CGNR solve (fp64) with a fixed number of
+iterations (tol = 0), through the C ABI (qdp_cg_solve): every row of SURVEY.md 8(a) runs in
+it -- SoA fields (A1), fused EO dslash with clover epilogues (A4, A5), reductions (A6), fused
+CG updates (A7), the CG driver (A8) and, for N > 1, face packing + NCCL halo exchange
+overlapped with the interior kernel (A2, A9).  Workload: config 4 of BASELINE.json read as
+weak scaling (R20): 40^3 x 32 sites per GPU, split along t, so N = 8 is the
+paper's 40^3 x 256 production lattice.
+
+value    = whole-job algorithmic GFLOPS of the step (Table II convention, 1320 flop per
+           dslash output site), fields resident in HBM;
+e2e      = the same with b imported from pinned host memory and x exported every step;
+roofline = the dslash kernel: compulsory bytes per launch / live CUDA-event launch time;
+cpu_baseline = the C oracle timed on the host cores on a bounded sample of the workload.
+
+--impl reference times the oracle (the tier's reference arm) on the same config and metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import shutil
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Wilson dslash GFLOPS & HBM GB/s (fp64/fp32) at 1/2/4/8 B200; CG iters/s"
+LOCAL = (40, 40, 40, 32)
+MASS, CSW = 0.1, 1.0
+HBM_FALLBACK = 6650.0  # GB/s, B200_PROFILING.md fallback (used only without MEASURED_PEAKS.json)
+
+
+# ---------------------------------------------------------------- accounting
+def cg_flops(Vh: int, iters: int, clover: bool = True) -> float:
+    """Algorithmic flops of one qdp_cg_solve (same count the library's counters produce).
+
+    clover: per iteration 2 x Mhat (dslash+A^-1: 1320+504+24; dslash+A x xpay: 1320+504+48)
+            + Re<p,q> 96 (fused into the last dslash) + r update with |r|^2 96
+            + x and p update 96                                        = 7728 / odd site
+            (the last iteration skips the p update: -48)
+            setup: A^-1 b_e 504, bhat 1392, r0 = Mhat^dag bhat 3720, |r0|^2 48 = 5664
+            finish: x_e 1896, true residual 2 x 1872 + 96 + 2 x 96     = 5928
+    Wilson: 5712 / iteration, setup 4176, finish 4464."""
+    last = -48 if iters > 0 else 0
+    if clover:
+        return Vh * (5664 + 5928 + 7728 * iters + last)
+    return Vh * (4176 + 4464 + 5712 * iters + last)
+
+
+def dslash_bytes_per_site(prec_bytes: int = 8) -> int:
+    """Compulsory bytes of one EO dslash output site: 8 links + input + output = 192 reals."""
+    return (8 * 18 + 24 + 24) * prec_bytes
+
+
+# ---------------------------------------------------------------- helpers
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (torch copy, measured)"
+    return HBM_FALLBACK, "B200_PROFILING.md fallback 6.65 TB/s"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{index}.csv")
+
+    def __enter__(self):
+        if shutil.which("nvidia-smi"):
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+            self.f.close()
+
+    def summary(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def gen_fields(L, rank):
+    import fieldgen
+    U = fieldgen.random_gauge(L, 1004 + 7919 * rank)
+    b = fieldgen.random_spinor(L, 2005 + 7919 * rank)
+    return U, b
+
+
+# ---------------------------------------------------------------- oracle (reference arm / cpu baseline)
+def oracle_solve_timed(U, b, L, iters):
+    import oracle
+    A = oracle.clover_build(U, L, MASS, CSW)
+    t0 = time.perf_counter()
+    res = oracle.cg_solve(U, b, L, MASS, A=A, tol=0.0, maxit=iters)
+    dt = time.perf_counter() - t0
+    assert res["iters"] == iters
+    return dt, res
+
+
+def run_reference(args, rank, world):
+    """The tier's reference arm: the C oracle as it stands, on the host cores, same metric."""
+    if rank != 0:
+        return
+    import oracle
+    L = LOCAL
+    Vh = L[0] * L[1] * L[2] * L[3] // 2
+    U, b = gen_fields(L, 0)
+    times = []
+    for i in range(args.warmup + args.steps):
+        dt, _ = oracle_solve_timed(U, b, L, args.ref_iters)
+        if i >= args.warmup:
+            times.append(dt)
+    t = sum(times)
+    flops = cg_flops(Vh, args.ref_iters) * args.steps
+    v = flops / t * 1e-9
+    sample = (f"oracle/oracle.c even-odd clover CGNR on one 40^3x32 sub-lattice, {args.ref_iters} iteration(s) "
+              f"per step incl. its clover inversion, setup, reconstruction and true residual; fp64")
+    out = {"metric": METRIC, "value": v, "unit": "GFLOPS", "impl": "reference", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": config_dict(args, world=1),
+           "cpu_baseline": {"value": v, "unit": "GFLOPS", "cores": oracle.max_threads(), "kind": "oracle",
+                            "sample": sample},
+           "e2e": {"value": v, "unit": "GFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def config_dict(args, world):
+    gl = (LOCAL[0], LOCAL[1], LOCAL[2], LOCAL[3] * world)
+    return {"workload": "BASELINE config 4 (40^3x256 production lattice) as weak scaling: 40^3x32 sites per GPU, "
+                        "t-split; even-odd Wilson-clover CGNR solve, fixed iterations",
+            "global_lattice": "x".join(map(str, gl)), "local_lattice": "x".join(map(str, LOCAL)),
+            "operator": f"Wilson-clover m={MASS} c_SW={CSW}, hot random SU(3) gauge field",
+            "cg_iters_per_step": args.iters, "parallelism": f"t-split x{world}" if world > 1 else "single GPU",
+            "l2": "inputs larger than L2 (gauge 1.18 GB + clover 1.2 GB + 6 fermion vectors per GPU), no flush"}
+
+
+# ---------------------------------------------------------------- native arm
+def run_native(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import fieldgen
+    from paper_1408_5925_b200 import dist as qdist
+    from paper_1408_5925_b200 import qdpb as q
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    stream = torch.cuda.current_stream()
+    gdims = (LOCAL[0], LOCAL[1], LOCAL[2], LOCAL[3] * world)
+    P = qdist.proc_grid_for(world, gdims, split=(3,))
+    ctx = qdist.bootstrap(gdims, P, stream=stream)
+    q.qdp_set_option(ctx, q.QDP_OPT_OVERLAP, 0 if args.no_overlap else 1)
+    L = LOCAL
+    Vh = L[0] * L[1] * L[2] * L[3] // 2
+
+    U, b = gen_fields(L, rank)
+    fU = q.qdp_field_alloc(ctx, q.QDP_GAUGE, q.QDP_F64, q.QDP_ALL)
+    fb = q.qdp_field_alloc(ctx, q.QDP_FERMION, q.QDP_F64, q.QDP_ALL)
+    fx = q.qdp_field_alloc(ctx, q.QDP_FERMION, q.QDP_F64, q.QDP_ALL)
+    fA = q.qdp_field_alloc(ctx, q.QDP_CLOVER, q.QDP_F64, q.QDP_ALL)
+    fAi = q.qdp_field_alloc(ctx, q.QDP_CLOVER, q.QDP_F64, q.QDP_EVEN)
+    q.qdp_field_import(fU, U)
+    q.qdp_field_import(fb, b)
+    q.qdp_clover_build(fA, fAi, fU, MASS, CSW)
+
+    def step():
+        return q.qdp_cg_solve(fx, fb, fU, fA, fAi, mass=MASS, tol=0.0, maxit=args.iters)
+
+    # parity spot check of this exact configuration (rank 0, N = 1): first solve's history vs oracle
+    parity = None
+    for _ in range(args.warmup):
+        r = step()
+    if args.check and world == 1:
+        import oracle
+        _, ref = oracle_solve_timed(U, b, L, 2)
+        got = q.qdp_cg_solve(fx, fb, fU, fA, fAi, mass=MASS, tol=0.0, maxit=2)
+        parity = {"cg_hist_max_rel_diff_2it": float(np.max(np.abs(got["hist"] - ref["hist"]) / ref["hist"])),
+                  "x_max_site_rel_err_2it": _site_err(q.qdp_field_export(fx), ref["x"])}
+
+    # ---- timed region: K solves, fields resident in HBM
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    q.qdp_profile_reset(ctx)
+    q.qdp_set_option(ctx, q.QDP_OPT_PROFILE, 1)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local_rank) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            r = step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    n_dsl, ms_dsl = q.qdp_profile_query(ctx, q.QDP_PK_DSLASH)
+    f_dsl, b_dsl = q.qdp_profile_work(ctx, q.QDP_PK_DSLASH)
+    f_all, _ = q.qdp_profile_work(ctx, -1)
+    n_all, ms_all = q.qdp_profile_query(ctx, -1)
+    q.qdp_set_option(ctx, q.QDP_OPT_PROFILE, 0)
+    assert abs(f_all - cg_flops(Vh, args.iters) * args.steps) <= 1e-9 * f_all, (f_all, cg_flops(Vh, args.iters))
+    ms_max = qdist.max_over_ranks(ms)
+    flops_job = qdist.sum_over_ranks(f_all)
+    value = flops_job / (ms_max * 1e-3) * 1e-9
+
+    # ---- e2e: the same solves through the C ABI with host buffers (pinned), copies inside
+    hb = torch.from_numpy(b).pin_memory()
+    hx = torch.empty_like(hb).pin_memory()
+    k2 = max(1, min(args.steps, args.e2e_steps))
+    q.qdp_field_import(fb, hb)
+    step()
+    q.qdp_field_export(fx, hx)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    f0, _ = q.qdp_profile_work(ctx, -1)
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    for _ in range(k2):
+        q.qdp_field_import(fb, hb)
+        step()
+        q.qdp_field_export(fx, hx)
+    e3.record(stream)
+    torch.cuda.synchronize()
+    f1, _ = q.qdp_profile_work(ctx, -1)
+    ms_e2e = qdist.max_over_ranks(e2.elapsed_time(e3))
+    e2e_flops = qdist.sum_over_ranks(cg_flops(Vh, args.iters) * k2)
+    e2e_value = e2e_flops / (ms_e2e * 1e-3) * 1e-9
+    bytes_b = hb.numel() * hb.element_size()
+
+    # ---- CPU baseline (oracle, rank 0 at N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        import oracle
+        dt, _ = oracle_solve_timed(U, b, L, args.cpu_iters)
+        cpu = {"value": cg_flops(Vh, args.cpu_iters) / dt * 1e-9, "unit": "GFLOPS", "cores": oracle.max_threads(),
+               "kind": "oracle", "seconds": dt,
+               "sample": f"oracle/oracle.c even-odd clover CGNR, same 40^3x32 lattice and fields, {args.cpu_iters} "
+                         f"iterations incl. its clover inversion, setup, reconstruction and true residual"}
+
+    peak, peak_src = measured_peak()
+    us_dsl = ms_dsl / n_dsl * 1e3
+    gbs = (b_dsl / n_dsl) / (us_dsl * 1e-6) * 1e-9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "dslash_ncu_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+    out = {
+        "metric": METRIC, "value": value, "unit": "GFLOPS", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded hot random SU(3) gauge field, Gaussian source)",
+        "config": config_dict(args, world),
+        "cg_iters_per_s": args.iters * args.steps / (ms_max * 1e-3),
+        "dslash": {"launches": n_dsl, "us_per_launch": us_dsl, "gflops_per_gpu": f_dsl / n_dsl / (us_dsl * 1e-6) * 1e-9,
+                   "gbs_compulsory_per_gpu": gbs, "bytes_per_site": (b_dsl / n_dsl) / Vh,
+                   "share_of_step": ms_dsl / ms, "frac_of_8TBs": gbs / 8000.0},
+        "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+                     "traffic": traffic, "kernel": "dslash_kernel<double> (fused EO hopping term + clover epilogue)",
+                     "peak_source": peak_src},
+        "e2e": {"value": e2e_value, "unit": "GFLOPS", "h2d_bytes_per_step": bytes_b, "d2h_bytes_per_step": bytes_b,
+                "steps": k2},
+        "gpu_launches": n_all,
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+        "parity": parity,
+        "overlap": not args.no_overlap,
+    }
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    for f in (fU, fb, fx, fA, fAi):
+        q.qdp_field_free(f)
+    q.qdp_finalize(ctx)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _site_err(got, ref):
+    import numpy as np
+    g = got.reshape(len(got), -1)
+    o = ref.reshape(len(ref), -1)
+    return float(np.max(np.linalg.norm(g - o, axis=1) / np.linalg.norm(o, axis=1)))
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["native", "reference"], default="native")
+    ap.add_argument("--iters", type=int, default=32, help="CG iterations per step (tol = 0)")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-iters", type=int, default=2)
+    ap.add_argument("--ref-iters", type=int, default=1)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-overlap", action="store_true")
+    ap.add_argument("--check", action="store_true", default=True)
+    ap.add_argument("--no-check", dest="check", action="store_false")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        ap.error(f"--gpus {args.gpus} but WORLD_SIZE={world} (launch N > 1 with torch.distributed.run)")
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_native(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

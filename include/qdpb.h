@@ -102,7 +102,8 @@ int qdp_get_geometry(qdp_ctx ctx, int local_dims[4], int proc_coords[4]);
  *                     partitioned: faces are packed and the halo path runs, the peer being
  *                     this rank (single-GPU test mode of the multi-GPU code).
  *  QDP_OPT_PROFILE    1: bracket every launch with CUDA events (see qdp_profile_query).
- *  QDP_OPT_BLOCK      threads per block of the dslash kernels (0 = auto-tuned default).
+ *  QDP_OPT_BLOCK      threads per block of the dslash kernels, a multiple of 32 <= 256
+ *                     (0 = the default, 128).
  *  QDP_OPT_DET_REDUCE 1 (default): cross-rank sums by allgather + rank-ordered sum
  *                     (deterministic); 0: ncclAllReduce. */
 enum { QDP_OPT_OVERLAP = 0, QDP_OPT_SELF_HALO = 1, QDP_OPT_PROFILE = 2, QDP_OPT_BLOCK = 3,
@@ -197,6 +198,12 @@ enum { QDP_PK_DSLASH = 0,  /* interior / whole-lattice dslash */
  * total_ms: sum of their CUDA-event durations (only while QDP_OPT_PROFILE = 1; resolving
  * the events synchronises the stream).  kernel_class = -1: totals over all classes. */
 int qdp_profile_query(qdp_ctx ctx, int kernel_class, long *launches, double *total_ms);
+/* Algorithmic work of the launches counted above (always counted): flops by the paper's
+ * Table II convention (complex mul 6, complex add 2, real x complex 2; PAPER.md:71-79;
+ * hopping term 1320 per output site, clover apply 504) and compulsory bytes (every
+ * operand read once and every result written once; for the dslash: 8 links, the input
+ * spinor once, the output once = 1536 B/site fp64, 768 fp32).  DESIGN.md "Accounting". */
+int qdp_profile_work(qdp_ctx ctx, int kernel_class, double *flops, double *bytes);
 int qdp_profile_reset(qdp_ctx ctx);
 
 #ifdef __cplusplus

@@ -174,49 +174,51 @@ __global__ void __launch_bounds__(RB) scale_copy_kernel(const Geom g, typename E
       }
 }
 
-// x += alpha p ; r -= alpha q ; partial |r|^2   with alpha = res[rho] / res[pq]  (CG step 5)
+// r -= alpha q ; partial |r|^2   with alpha = res[rho] / res[pq]  (CG step 5)
 template <typename R>
-__global__ void __launch_bounds__(RB) cg_xr_kernel(const Geom g, typename E<R>::T *x, typename E<R>::T *r,
-                                                   const typename E<R>::T *p, const typename E<R>::T *q,
-                                                   const double *res, int rho_slot, int pq_slot, double *partials) {
+__global__ void __launch_bounds__(RB) cg_r_kernel(const Geom g, typename E<R>::T *r, const typename E<R>::T *q,
+                                                  const double *res, int rho_slot, int pq_slot, double *partials) {
   const R alpha = (R)(res[rho_slot] / res[pq_slot]);
   double acc = 0.0;
   for (int cb = blockIdx.x * blockDim.x + threadIdx.x; cb < g.Vh; cb += gridDim.x * blockDim.x)
 #pragma unroll
     for (int k = 0; k < E<R>::NP; k++) {
       const size_t i = (size_t)k * g.stride + cb;
-      R xv[E<R>::NR], rv[E<R>::NR], pv[E<R>::NR], qv[E<R>::NR];
-      E<R>::get(x[i], xv);
+      R rv[E<R>::NR], qv[E<R>::NR];
       E<R>::get(r[i], rv);
-      E<R>::get(p[i], pv);
       E<R>::get(q[i], qv);
 #pragma unroll
       for (int j = 0; j < E<R>::NR; j++) {
-        xv[j] = xv[j] + alpha * pv[j];
         rv[j] = rv[j] - alpha * qv[j];
         acc += (double)rv[j] * (double)rv[j];
       }
-      x[i] = E<R>::put(xv);
       r[i] = E<R>::put(rv);
     }
   block_partial(acc, 0.0, partials);
 }
 
-// p = r + beta p, beta = res[rn] / res[ro]
-template <typename R>
-__global__ void __launch_bounds__(RB) cg_p_kernel(const Geom g, typename E<R>::T *p, const typename E<R>::T *r,
-                                                  const double *res, int rn, int ro) {
-  const R beta = (R)(res[rn] / res[ro]);
+// x += alpha p ; p = r + beta p (UPD_P), alpha = res[rho] / res[pq], beta = res[rr] / res[rho]
+template <typename R, bool UPD_P>
+__global__ void __launch_bounds__(RB) cg_xp_kernel(const Geom g, typename E<R>::T *x, typename E<R>::T *p,
+                                                   const typename E<R>::T *r, const double *res, int rho_slot,
+                                                   int pq_slot, int rr_slot) {
+  const R alpha = (R)(res[rho_slot] / res[pq_slot]);
+  const R beta = (R)(res[rr_slot] / res[rho_slot]);
   for (int cb = blockIdx.x * blockDim.x + threadIdx.x; cb < g.Vh; cb += gridDim.x * blockDim.x)
 #pragma unroll
     for (int k = 0; k < E<R>::NP; k++) {
       const size_t i = (size_t)k * g.stride + cb;
-      R pv[E<R>::NR], rv[E<R>::NR];
+      R xv[E<R>::NR], pv[E<R>::NR], rv[E<R>::NR];
+      E<R>::get(x[i], xv);
       E<R>::get(p[i], pv);
-      E<R>::get(r[i], rv);
+      if (UPD_P) E<R>::get(r[i], rv);
 #pragma unroll
-      for (int j = 0; j < E<R>::NR; j++) pv[j] = rv[j] + beta * pv[j];
-      p[i] = E<R>::put(pv);
+      for (int j = 0; j < E<R>::NR; j++) {
+        xv[j] = xv[j] + alpha * pv[j];
+        if (UPD_P) pv[j] = rv[j] + beta * pv[j];
+      }
+      x[i] = E<R>::put(xv);
+      if (UPD_P) p[i] = E<R>::put(pv);
     }
 }
 
@@ -228,7 +230,7 @@ static int red_grid(const Geom &g) {
 
 template <typename R> using T_ = typename E<R>::T;
 
-static int finish(qdp_ctx ctx, int nparts, int slot) {
+int reduce_partials(qdp_ctx ctx, int nparts, int slot) {
   ProfEvent ev;
   prof_begin(ctx, QDP_PK_REDUCE, &ev);
   final_kernel<<<1, 1024, 0, ctx->stream>>>(ctx->red_partials, nparts, ctx->red_result, slot);
@@ -242,10 +244,11 @@ int blas_norm2(qdp_ctx ctx, int prec, const void *a, int nblk, int slot) {
   if ((rc = ensure_reduce(ctx, nb))) return rc;
   ProfEvent ev;
   prof_begin(ctx, QDP_PK_REDUCE, &ev);
+  prof_work(ctx, QDP_PK_REDUCE, 48.0 * g.Vh * nblk, 24.0 * g.Vh * nblk * (prec == QDP_F64 ? 8 : 4));
   if (prec == QDP_F64) norm2_kernel<double><<<nb, RB, 0, ctx->stream>>>(g, (const T_<double> *)a, nblk, ctx->red_partials);
   else norm2_kernel<float><<<nb, RB, 0, ctx->stream>>>(g, (const T_<float> *)a, nblk, ctx->red_partials);
   if ((rc = prof_end(ctx, &ev))) return rc;
-  return finish(ctx, nb, slot);
+  return reduce_partials(ctx, nb, slot);
 }
 
 int blas_inner(qdp_ctx ctx, int prec, const void *a, const void *b, int nblk, int slot) {
@@ -255,12 +258,13 @@ int blas_inner(qdp_ctx ctx, int prec, const void *a, const void *b, int nblk, in
   if ((rc = ensure_reduce(ctx, nb))) return rc;
   ProfEvent ev;
   prof_begin(ctx, QDP_PK_REDUCE, &ev);
+  prof_work(ctx, QDP_PK_REDUCE, 96.0 * g.Vh * nblk, 48.0 * g.Vh * nblk * (prec == QDP_F64 ? 8 : 4));
   if (prec == QDP_F64)
     inner_kernel<double><<<nb, RB, 0, ctx->stream>>>(g, (const T_<double> *)a, (const T_<double> *)b, nblk, ctx->red_partials);
   else
     inner_kernel<float><<<nb, RB, 0, ctx->stream>>>(g, (const T_<float> *)a, (const T_<float> *)b, nblk, ctx->red_partials);
   if ((rc = prof_end(ctx, &ev))) return rc;
-  return finish(ctx, nb, slot);
+  return reduce_partials(ctx, nb, slot);
 }
 
 int reduce_global(qdp_ctx ctx, int slot, int n) {
@@ -280,6 +284,7 @@ int blas_axpy(qdp_ctx ctx, int prec, double ar, double ai, const void *x, void *
   const Geom &g = ctx->geom;
   ProfEvent ev;
   prof_begin(ctx, QDP_PK_BLAS, &ev);
+  prof_work(ctx, QDP_PK_BLAS, 96.0 * g.Vh * nblk, 72.0 * g.Vh * nblk * (prec == QDP_F64 ? 8 : 4));
   const int nb = grid_for(g.Vh, RB);
   if (prec == QDP_F64) axpy_kernel<double><<<nb, RB, 0, ctx->stream>>>(g, ar, ai, (const T_<double> *)x, (T_<double> *)y, nblk);
   else axpy_kernel<float><<<nb, RB, 0, ctx->stream>>>(g, (float)ar, (float)ai, (const T_<float> *)x, (T_<float> *)y, nblk);
@@ -290,6 +295,7 @@ int blas_xpay(qdp_ctx ctx, int prec, const void *x, double a, void *y, int nblk)
   const Geom &g = ctx->geom;
   ProfEvent ev;
   prof_begin(ctx, QDP_PK_BLAS, &ev);
+  prof_work(ctx, QDP_PK_BLAS, 48.0 * g.Vh * nblk, 72.0 * g.Vh * nblk * (prec == QDP_F64 ? 8 : 4));
   const int nb = grid_for(g.Vh, RB);
   if (prec == QDP_F64) xpay_kernel<double><<<nb, RB, 0, ctx->stream>>>(g, (const T_<double> *)x, a, (T_<double> *)y, nblk);
   else xpay_kernel<float><<<nb, RB, 0, ctx->stream>>>(g, (const T_<float> *)x, (float)a, (T_<float> *)y, nblk);
@@ -300,40 +306,46 @@ int blas_scale_copy(qdp_ctx ctx, int prec, void *dst, const void *src, double a,
   const Geom &g = ctx->geom;
   ProfEvent ev;
   prof_begin(ctx, QDP_PK_BLAS, &ev);
+  prof_work(ctx, QDP_PK_BLAS, 24.0 * g.Vh * nblk, 48.0 * g.Vh * nblk * (prec == QDP_F64 ? 8 : 4));
   const int nb = grid_for(g.Vh, RB);
   if (prec == QDP_F64) scale_copy_kernel<double><<<nb, RB, 0, ctx->stream>>>(g, (T_<double> *)dst, (const T_<double> *)src, a, nblk);
   else scale_copy_kernel<float><<<nb, RB, 0, ctx->stream>>>(g, (T_<float> *)dst, (const T_<float> *)src, (float)a, nblk);
   return prof_end(ctx, &ev);
 }
 
-int blas_cg_update_xr(qdp_ctx ctx, int prec, void *x, void *r, const void *p, const void *q, int rho_slot,
-                      int pq_slot, int rr_slot) {
+int blas_cg_update_r(qdp_ctx ctx, int prec, void *r, const void *q, int rho_slot, int pq_slot, int rr_slot) {
   const Geom &g = ctx->geom;
   const int nb = red_grid(g);
   int rc;
   if ((rc = ensure_reduce(ctx, nb))) return rc;
   ProfEvent ev;
   prof_begin(ctx, QDP_PK_BLAS, &ev);
+  prof_work(ctx, QDP_PK_BLAS, 96.0 * g.Vh, 72.0 * g.Vh * (prec == QDP_F64 ? 8 : 4));
   if (prec == QDP_F64)
-    cg_xr_kernel<double><<<nb, RB, 0, ctx->stream>>>(g, (T_<double> *)x, (T_<double> *)r, (const T_<double> *)p,
-                                                      (const T_<double> *)q, ctx->red_result, rho_slot, pq_slot, ctx->red_partials);
+    cg_r_kernel<double><<<nb, RB, 0, ctx->stream>>>(g, (T_<double> *)r, (const T_<double> *)q, ctx->red_result, rho_slot,
+                                                     pq_slot, ctx->red_partials);
   else
-    cg_xr_kernel<float><<<nb, RB, 0, ctx->stream>>>(g, (T_<float> *)x, (T_<float> *)r, (const T_<float> *)p,
-                                                     (const T_<float> *)q, ctx->red_result, rho_slot, pq_slot, ctx->red_partials);
+    cg_r_kernel<float><<<nb, RB, 0, ctx->stream>>>(g, (T_<float> *)r, (const T_<float> *)q, ctx->red_result, rho_slot,
+                                                    pq_slot, ctx->red_partials);
   if ((rc = prof_end(ctx, &ev))) return rc;
-  if ((rc = finish(ctx, nb, rr_slot))) return rc;
+  if ((rc = reduce_partials(ctx, nb, rr_slot))) return rc;
   return reduce_global(ctx, rr_slot, 1);
 }
 
-int blas_cg_update_p(qdp_ctx ctx, int prec, void *p, const void *r, int rn, int ro) {
+int blas_cg_update_xp(qdp_ctx ctx, int prec, void *x, void *p, const void *r, int rho_slot, int pq_slot, int rr_slot,
+                      bool update_p) {
   const Geom &g = ctx->geom;
   ProfEvent ev;
   prof_begin(ctx, QDP_PK_BLAS, &ev);
+  prof_work(ctx, QDP_PK_BLAS, (update_p ? 96.0 : 48.0) * g.Vh,
+            (update_p ? 120.0 : 72.0) * g.Vh * (prec == QDP_F64 ? 8 : 4));
   const int nb = grid_for(g.Vh, RB);
-  if (prec == QDP_F64)
-    cg_p_kernel<double><<<nb, RB, 0, ctx->stream>>>(g, (T_<double> *)p, (const T_<double> *)r, ctx->red_result, rn, ro);
-  else
-    cg_p_kernel<float><<<nb, RB, 0, ctx->stream>>>(g, (T_<float> *)p, (const T_<float> *)r, ctx->red_result, rn, ro);
+#define QDPB_XP(Rt, U)                                                                                              \
+  cg_xp_kernel<Rt, U><<<nb, RB, 0, ctx->stream>>>(g, (T_<Rt> *)x, (T_<Rt> *)p, (const T_<Rt> *)r, ctx->red_result, \
+                                                  rho_slot, pq_slot, rr_slot)
+  if (prec == QDP_F64) { if (update_p) QDPB_XP(double, true); else QDPB_XP(double, false); }
+  else { if (update_p) QDPB_XP(float, true); else QDPB_XP(float, false); }
+#undef QDPB_XP
   return prof_end(ctx, &ev);
 }
 

@@ -132,6 +132,22 @@ int ensure_halo(qdp_ctx ctx, int prec) {
   return QDP_OK;
 }
 
+int ensure_cg_work(qdp_ctx ctx, size_t bytes) {
+  if (ctx->cg_work_bytes >= bytes) return QDP_OK;
+  if (ctx->cg_work) {
+    QDP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    cudaFree(ctx->cg_work);
+  }
+  ctx->cg_work = nullptr;
+  ctx->cg_work_bytes = 0;
+  if (cudaMalloc(&ctx->cg_work, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return set_error(ctx, QDP_ENOMEM, "CG work vectors (%zu bytes)", bytes);
+  }
+  ctx->cg_work_bytes = bytes;
+  return QDP_OK;
+}
+
 static void update_partition(qdp_ctx ctx) {
   int part = 0;
   for (int mu = 0; mu < 4; mu++)
@@ -249,6 +265,7 @@ extern "C" int qdp_finalize(qdp_ctx c) {
         if (c->halo_recv[p][mu][d]) cudaFree(c->halo_recv[p][mu][d]);
       }
   if (c->staging) cudaFree(c->staging);
+  if (c->cg_work) cudaFree(c->cg_work);
   if (c->red_partials) cudaFree(c->red_partials);
   if (c->red_result) cudaFree(c->red_result);
   if (c->red_gather) cudaFree(c->red_gather);
@@ -302,7 +319,7 @@ extern "C" int qdp_set_option(qdp_ctx c, int opt, long v) {
       c->profiling = v ? 1 : 0;
       return QDP_OK;
     case QDP_OPT_BLOCK:
-      if (v < 0 || v > 1024 || (v % 32)) return set_error(c, QDP_EINVAL, "block must be a multiple of 32 <= 1024");
+      if (v < 0 || v > 256 || (v % 32)) return set_error(c, QDP_EINVAL, "block must be a multiple of 32 <= 256");
       c->block = (int)v;
       return QDP_OK;
     case QDP_OPT_DET_REDUCE: c->det_reduce = v ? 1 : 0; return QDP_OK;
@@ -638,6 +655,19 @@ extern "C" int qdp_profile_query(qdp_ctx c, int cls, long *launches, double *ms)
   return QDP_OK;
 }
 
+extern "C" int qdp_profile_work(qdp_ctx c, int cls, double *flops, double *bytes) {
+  if (!c || cls < -1 || cls >= QDP_PK_COUNT) return QDP_EINVAL;
+  double f = 0, b = 0;
+  for (int k = 0; k < QDP_PK_COUNT; k++)
+    if (cls == -1 || cls == k) {
+      f += c->work_flops[k];
+      b += c->work_bytes[k];
+    }
+  if (flops) *flops = f;
+  if (bytes) *bytes = b;
+  return QDP_OK;
+}
+
 extern "C" int qdp_profile_reset(qdp_ctx c) {
   if (!c) return QDP_EINVAL;
   int rc;
@@ -645,6 +675,8 @@ extern "C" int qdp_profile_reset(qdp_ctx c) {
   for (int k = 0; k < QDP_PK_COUNT; k++) {
     c->launches[k] = 0;
     c->prof_ms[k] = 0;
+    c->work_flops[k] = 0;
+    c->work_bytes[k] = 0;
   }
   return QDP_OK;
 }

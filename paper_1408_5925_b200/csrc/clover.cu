@@ -247,6 +247,8 @@ int clover_apply(qdp_ctx ctx, int prec, void *out, const void *A, const void *in
   for (int b = 0; b < nblk; b++) {
     ProfEvent ev;
     prof_begin(ctx, QDP_PK_CLOVER, &ev);
+    // Table II "clover": 504 flop, A (72 reals) + psi + out
+    prof_work(ctx, QDP_PK_CLOVER, 504.0 * g.Vh, (72.0 + 24 + 24) * g.Vh * (prec == QDP_F64 ? 8 : 4));
     if (prec == QDP_F64)
       clover_apply_kernel<double><<<grid_for(g.Vh, 128), 128, 0, ctx->stream>>>(
           g, {(double2 *)((char *)out + b * fb), g.stride}, {(const double2 *)((const char *)A + b * cbk), g.stride},

@@ -152,6 +152,9 @@ template <typename R> struct KParams {
   const void *ghost[4][2];
   // pack destinations: [mu][dir], dir 0 = to -mu neighbour, 1 = to +mu neighbour
   void *dst[4][2];
+  // fused Re<dotx, out>: per-block partials
+  FermView<R> dotx;
+  double *dot_part;
 };
 
 template <typename R, int MU>
@@ -187,7 +190,7 @@ __device__ __forceinline__ void hop_dir(const Geom &g, const KParams<R> &P, cons
 }
 
 template <typename R, int EPI>
-__device__ __forceinline__ void epilogue(const KParams<R> &P, int cb, Spinor<R> &acc, bool G5OUT) {
+__device__ __forceinline__ Spinor<R> epilogue(const KParams<R> &P, int cb, Spinor<R> &acc, bool G5OUT) {
   if (G5OUT) g5(acc);
   Spinor<R> o;
   if (EPI == EPI_PLAIN) {
@@ -213,25 +216,59 @@ __device__ __forceinline__ void epilogue(const KParams<R> &P, int cb, Spinor<R> 
 #pragma unroll
     for (int k = 0; k < 12; k++) o.c[k] = ax.c[k] + P.b * acc.c[k];
   }
-  P.out.store(cb, o);
+  return o;
+}
+
+// Re<d, o> for the fused inner product (fp64 accumulation)
+template <typename R>
+__device__ __forceinline__ double re_dot(const Spinor<R> &d, const Spinor<R> &o) {
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 12; k++) s += (double)d.c[k].re * o.c[k].re + (double)d.c[k].im * o.c[k].im;
+  return s;
+}
+
+// block sum of v -> part[2 * blockIdx.x] (re), part[2 * blockIdx.x + 1] = 0; blockDim <= 256
+__device__ __forceinline__ void dot_block_partial(double v, double *part) {
+  __shared__ double sm[8];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) sm[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = l < (int)(blockDim.x >> 5) ? sm[l] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (l == 0) {
+      part[2 * blockIdx.x] = v;
+      part[2 * blockIdx.x + 1] = 0.0;
+    }
+  }
 }
 
 // Whole-lattice (HALO=false) or interior (HALO=true: remote hops skipped) kernel.
-template <typename R, int EPI, bool G5IN, bool G5OUT, bool HALO>
-__global__ void __launch_bounds__(128) dslash_kernel(const Geom g, const KParams<R> P) {
+// DOT: also accumulate Re<dot, out> per block into dot_part (fused inner product).
+template <typename R, int EPI, bool G5IN, bool G5OUT, bool HALO, bool DOT>
+__global__ void __launch_bounds__(256) dslash_kernel(const Geom g, const KParams<R> P) {
   const int cb = blockIdx.x * blockDim.x + threadIdx.x;
-  if (cb >= g.Vh) return;
-  const int p = P.parity;
-  int c[4];
-  cb_coords(g, cb, p, c);
-  Spinor<R> acc;
+  double dot = 0.0;
+  if (cb < g.Vh) {
+    const int p = P.parity;
+    int c[4];
+    cb_coords(g, cb, p, c);
+    Spinor<R> acc;
 #pragma unroll
-  for (int k = 0; k < 12; k++) acc.c[k] = {R(0), R(0)};
-  hop_dir<R, 0>(g, P, c, cb, p, G5IN, HALO, acc);
-  hop_dir<R, 1>(g, P, c, cb, p, G5IN, HALO, acc);
-  hop_dir<R, 2>(g, P, c, cb, p, G5IN, HALO, acc);
-  hop_dir<R, 3>(g, P, c, cb, p, G5IN, HALO, acc);
-  epilogue<R, EPI>(P, cb, acc, G5OUT);
+    for (int k = 0; k < 12; k++) acc.c[k] = {R(0), R(0)};
+    hop_dir<R, 0>(g, P, c, cb, p, G5IN, HALO, acc);
+    hop_dir<R, 1>(g, P, c, cb, p, G5IN, HALO, acc);
+    hop_dir<R, 2>(g, P, c, cb, p, G5IN, HALO, acc);
+    hop_dir<R, 3>(g, P, c, cb, p, G5IN, HALO, acc);
+    Spinor<R> o = epilogue<R, EPI>(P, cb, acc, G5OUT);
+    P.out.store(cb, o);
+    if (DOT) dot = re_dot(P.dotx.load_stream(cb), o);
+  }
+  if (DOT) dot_block_partial(dot, P.dot_part);
 }
 
 // Face packing for dim MU: input psi has parity q = 1 - p.
@@ -271,48 +308,54 @@ __global__ void __launch_bounds__(128) pack_kernel(const Geom g, const KParams<R
   }
 }
 
-// Exterior: add the remote hops of dim mu for the output sites on its two faces.
-template <typename R, int EPI, bool G5OUT>
-__global__ void __launch_bounds__(128) exterior_kernel(const Geom g, const KParams<R> P, int mu) {
+// Exterior: add the remote hops of dim mu for the output sites on its two faces.  With DOT,
+// Re<dotx, increment> is accumulated: by linearity the interior's partial plus these give
+// Re<dotx, out> of the final output.
+template <typename R, int EPI, bool G5OUT, bool DOT>
+__global__ void __launch_bounds__(128) exterior_kernel(const Geom g, const KParams<R> P, int mu, double *dot_part) {
   const int n = g.faceVh[mu];
   int f = blockIdx.x * blockDim.x + threadIdx.x;
-  if (f >= 2 * n) return;
-  const int p = P.parity;
-  const bool fwd = f >= n;  // fwd: site at x_mu = L-1 needs psi(x+mu) from the +mu neighbour
-  if (fwd) f -= n;
-  int c[4];
-  face_coords(g, mu, fwd ? g.L[mu] - 1 : 0, f, p, c);
-  const int cb = coords_cb(g, c);
-  Spinor<R> acc;
+  double dot = 0.0;
+  if (f < 2 * n) {
+    const int p = P.parity;
+    const bool fwd = f >= n;  // fwd: site at x_mu = L-1 needs psi(x+mu) from the +mu neighbour
+    if (fwd) f -= n;
+    int c[4];
+    face_coords(g, mu, fwd ? g.L[mu] - 1 : 0, f, p, c);
+    const int cb = coords_cb(g, c);
+    Spinor<R> acc;
 #pragma unroll
-  for (int k = 0; k < 12; k++) acc.c[k] = {R(0), R(0)};
-  if (fwd) {
-    Half<R> h = HalfGhost<R>::load(P.ghost[mu][1], n, f);
-    Link<R> u = P.U.load(mu, p, cb);
-    Half<R> uh = mul_link(u, h);
-    switch (mu) {
-      case 0: accum_recon<0, -1>(acc, uh); break;
-      case 1: accum_recon<1, -1>(acc, uh); break;
-      case 2: accum_recon<2, -1>(acc, uh); break;
-      default: accum_recon<3, -1>(acc, uh); break;
+    for (int k = 0; k < 12; k++) acc.c[k] = {R(0), R(0)};
+    if (fwd) {
+      Half<R> h = HalfGhost<R>::load(P.ghost[mu][1], n, f);
+      Link<R> u = P.U.load(mu, p, cb);
+      Half<R> uh = mul_link(u, h);
+      switch (mu) {
+        case 0: accum_recon<0, -1>(acc, uh); break;
+        case 1: accum_recon<1, -1>(acc, uh); break;
+        case 2: accum_recon<2, -1>(acc, uh); break;
+        default: accum_recon<3, -1>(acc, uh); break;
+      }
+    } else {
+      Half<R> uh = HalfGhost<R>::load(P.ghost[mu][0], n, f);
+      switch (mu) {
+        case 0: accum_recon<0, +1>(acc, uh); break;
+        case 1: accum_recon<1, +1>(acc, uh); break;
+        case 2: accum_recon<2, +1>(acc, uh); break;
+        default: accum_recon<3, +1>(acc, uh); break;
+      }
     }
-  } else {
-    Half<R> uh = HalfGhost<R>::load(P.ghost[mu][0], n, f);
-    switch (mu) {
-      case 0: accum_recon<0, +1>(acc, uh); break;
-      case 1: accum_recon<1, +1>(acc, uh); break;
-      case 2: accum_recon<2, +1>(acc, uh); break;
-      default: accum_recon<3, +1>(acc, uh); break;
-    }
+    if (G5OUT) g5(acc);
+#pragma unroll
+    for (int k = 0; k < 12; k++) acc.c[k] = P.b * acc.c[k];
+    if (EPI == EPI_CLOVINV) acc = clover_mul(P.A, cb, acc);
+    Spinor<R> o = P.out.load_plain(cb);
+#pragma unroll
+    for (int k = 0; k < 12; k++) o.c[k] = o.c[k] + acc.c[k];
+    P.out.store(cb, o);
+    if (DOT) dot = re_dot(P.dotx.load_stream(cb), acc);
   }
-  if (G5OUT) g5(acc);
-#pragma unroll
-  for (int k = 0; k < 12; k++) acc.c[k] = P.b * acc.c[k];
-  if (EPI == EPI_CLOVINV) acc = clover_mul(P.A, cb, acc);
-  Spinor<R> o = P.out.load_plain(cb);
-#pragma unroll
-  for (int k = 0; k < 12; k++) o.c[k] = o.c[k] + acc.c[k];
-  P.out.store(cb, o);
+  if (DOT) dot_block_partial(dot, dot_part);
 }
 
 // ------------------------------------------------------------------ host side
@@ -326,15 +369,22 @@ template <typename R> static CloverView<R> cview(const void *p, int stride);
 template <> CloverView<double> cview<double>(const void *p, int stride) { return {(const double2 *)p, stride}; }
 template <> CloverView<float> cview<float>(const void *p, int stride) { return {(const float4 *)p, stride}; }
 
-template <typename R, int EPI, bool G5IN, bool G5OUT, bool HALO>
+template <typename R, int EPI, bool G5IN, bool G5OUT, bool HALO, bool DOT>
 static void launch_main(qdp_ctx ctx, const KParams<R> &P, int block) {
   const Geom &g = ctx->geom;
-  dslash_kernel<R, EPI, G5IN, G5OUT, HALO><<<grid_for(g.Vh, block), block, 0, ctx->stream>>>(g, P);
+  dslash_kernel<R, EPI, G5IN, G5OUT, HALO, DOT><<<grid_for(g.Vh, block), block, 0, ctx->stream>>>(g, P);
 }
 
 template <typename R, int EPI>
-static void launch_main_dispatch(qdp_ctx ctx, const KParams<R> &P, bool g5i, bool g5o, bool halo, int block) {
-#define QDPB_L(A, B, C) launch_main<R, EPI, A, B, C>(ctx, P, block)
+static void launch_main_dispatch(qdp_ctx ctx, const KParams<R> &P, bool g5i, bool g5o, bool halo, bool dot, int block) {
+  if (dot) {  // fused inner product: only the Mhat^dag output step (g5_out, no g5_in) uses it
+    if constexpr (EPI == EPI_XPAY || EPI == EPI_CLOVXPAY) {
+      if (halo) launch_main<R, EPI, false, true, true, true>(ctx, P, block);
+      else launch_main<R, EPI, false, true, false, true>(ctx, P, block);
+    }
+    return;
+  }
+#define QDPB_L(A, B, C) launch_main<R, EPI, A, B, C, false>(ctx, P, block)
   if (halo) {
     if (g5i) { if (g5o) QDPB_L(true, true, true); else QDPB_L(true, false, true); }
     else { if (g5o) QDPB_L(false, true, true); else QDPB_L(false, false, true); }
@@ -346,11 +396,45 @@ static void launch_main_dispatch(qdp_ctx ctx, const KParams<R> &P, bool g5i, boo
 }
 
 template <typename R, int EPI>
-static void launch_ext(qdp_ctx ctx, const KParams<R> &P, int mu, bool g5o) {
+static void launch_ext(qdp_ctx ctx, const KParams<R> &P, int mu, bool g5o, double *dot_part) {
   const Geom &g = ctx->geom;
   const int n = 2 * g.faceVh[mu];
-  if (g5o) exterior_kernel<R, EPI, true><<<grid_for(n, 128), 128, 0, ctx->stream>>>(g, P, mu);
-  else exterior_kernel<R, EPI, false><<<grid_for(n, 128), 128, 0, ctx->stream>>>(g, P, mu);
+  if (dot_part) exterior_kernel<R, EPI, true, true><<<grid_for(n, 128), 128, 0, ctx->stream>>>(g, P, mu, dot_part);
+  else if (g5o) exterior_kernel<R, EPI, true, false><<<grid_for(n, 128), 128, 0, ctx->stream>>>(g, P, mu, nullptr);
+  else exterior_kernel<R, EPI, false, false><<<grid_for(n, 128), 128, 0, ctx->stream>>>(g, P, mu, nullptr);
+}
+
+// Algorithmic work of one EO dslash launch: 1320 flop per output
+// site for the hopping term (8 x (12 projection + 132 SU(3) x half spinor) + 7 x 24
+// accumulate) plus the epilogue; compulsory bytes 8 links + input + output (+ x, + clover,
+// + the fused inner product's second vector).
+template <typename R>
+static void dslash_work(qdp_ctx ctx, const DslashArgs &a) {
+  double f = 1320, r = 8 * 18 + 24 + 24;
+  switch (a.epi) {
+    case EPI_PLAIN: f += a.b != 1.0 ? 24 : 0; break;
+    case EPI_XPAY: f += 72; r += 24; break;
+    case EPI_CLOVINV: f += 504 + 24 + (a.x ? 48 : 0); r += 72 + (a.x ? 24 : 0); break;
+    default: f += 504 + 48; r += 72 + 24; break;
+  }
+  if (a.dot_x) { f += 96; r += 24; }
+  const double vh = ctx->geom.Vh;
+  prof_work(ctx, QDP_PK_DSLASH, f * vh, r * vh * sizeof(R));
+}
+
+template <typename R>
+static int launch_main_epi(qdp_ctx ctx, const DslashArgs &a, const KParams<R> &P, bool halo, int block) {
+  ProfEvent ev;
+  prof_begin(ctx, QDP_PK_DSLASH, &ev);
+  dslash_work<R>(ctx, a);
+  const bool dot = a.dot_x != nullptr;
+  switch (a.epi) {
+    case EPI_PLAIN: launch_main_dispatch<R, EPI_PLAIN>(ctx, P, a.g5_in, a.g5_out, halo, false, block); break;
+    case EPI_XPAY: launch_main_dispatch<R, EPI_XPAY>(ctx, P, a.g5_in, a.g5_out, halo, dot, block); break;
+    case EPI_CLOVINV: launch_main_dispatch<R, EPI_CLOVINV>(ctx, P, a.g5_in, a.g5_out, halo, false, block); break;
+    default: launch_main_dispatch<R, EPI_CLOVXPAY>(ctx, P, a.g5_in, a.g5_out, halo, dot, block); break;
+  }
+  return prof_end(ctx, &ev);
 }
 
 template <typename R>
@@ -368,7 +452,23 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
   P.b = (R)a.b;
   const int block = ctx->block > 0 ? ctx->block : 128;
   const bool halo = g.part != 0;
+  const bool dot = a.dot_x != nullptr;
   int rc;
+  if (dot && !(a.epi == EPI_XPAY || a.epi == EPI_CLOVXPAY) ) return set_error(ctx, QDP_EINVAL, "fused dot: XPAY epilogues only");
+  if (dot && (a.g5_in || !a.g5_out)) return set_error(ctx, QDP_EINVAL, "fused dot: Mhat^dag output step only");
+  // partial-sum layout of the fused inner product: interior blocks, then each exterior's blocks
+  int nparts = 0, ext_off[4] = {0, 0, 0, 0};
+  if (dot) {
+    nparts = grid_for(g.Vh, block);
+    for (int mu = 0; mu < 4; mu++)
+      if ((g.part >> mu) & 1) {
+        ext_off[mu] = nparts;
+        nparts += grid_for(2 * g.faceVh[mu], 128);
+      }
+    if ((rc = ensure_reduce(ctx, nparts))) return rc;
+    P.dotx = fview<R>(a.dot_x, g.stride);
+    P.dot_part = ctx->red_partials;
+  }
 
   if (halo) {
     if ((rc = ensure_halo(ctx, prec))) return rc;
@@ -390,6 +490,8 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
       if (!((g.part >> mu) & 1)) continue;
       ProfEvent ev;
       prof_begin(ctx, QDP_PK_PACK, &ev);
+      // compulsory: psi read on both faces, the forward face's link, the half spinors written
+      prof_work(ctx, QDP_PK_PACK, 0.0, (double)g.faceVh[mu] * (24 + 12 + 24 + 18 + 12) * sizeof(R));
       const int n = 2 * g.faceVh[mu];
       if (a.g5_in) pack_kernel<R, true><<<grid_for(n, 128), 128, 0, ctx->stream>>>(g, P, mu);
       else pack_kernel<R, false><<<grid_for(n, 128), 128, 0, ctx->stream>>>(g, P, mu);
@@ -406,38 +508,29 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
         if ((rc = comm_exchange(ctx, prec, face_bytes, ctx->stream))) return rc;
       }
     }
-    {
-      ProfEvent ev;
-      prof_begin(ctx, QDP_PK_DSLASH, &ev);
-      switch (a.epi) {
-        case EPI_PLAIN: launch_main_dispatch<R, EPI_PLAIN>(ctx, P, a.g5_in, a.g5_out, true, block); break;
-        case EPI_XPAY: launch_main_dispatch<R, EPI_XPAY>(ctx, P, a.g5_in, a.g5_out, true, block); break;
-        case EPI_CLOVINV: launch_main_dispatch<R, EPI_CLOVINV>(ctx, P, a.g5_in, a.g5_out, true, block); break;
-        default: launch_main_dispatch<R, EPI_CLOVXPAY>(ctx, P, a.g5_in, a.g5_out, true, block); break;
-      }
-      if ((rc = prof_end(ctx, &ev))) return rc;
-    }
+    if ((rc = launch_main_epi<R>(ctx, a, P, true, block))) return rc;
     if (overlap) QDP_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_comm, 0));
     for (int mu = 0; mu < 4; mu++) {
       if (!((g.part >> mu) & 1)) continue;
       ProfEvent ev;
       prof_begin(ctx, QDP_PK_DSLASH_EXT, &ev);
-      if (a.epi == EPI_CLOVINV) launch_ext<R, EPI_CLOVINV>(ctx, P, mu, a.g5_out);
-      else launch_ext<R, EPI_PLAIN>(ctx, P, mu, a.g5_out);
+      // ghost read, forward-face link, output read-modify-write (+ clover on CLOVINV)
+      prof_work(ctx, QDP_PK_DSLASH_EXT, 0.0,
+                (double)g.faceVh[mu] * (2 * 12 + 18 + 2 * 48 + (a.epi == EPI_CLOVINV ? 2 * 72 : 0) + (dot ? 48 : 0)) *
+                    sizeof(R));
+      double *dp = dot ? ctx->red_partials + 2 * ext_off[mu] : nullptr;
+      if (a.epi == EPI_CLOVINV) launch_ext<R, EPI_CLOVINV>(ctx, P, mu, a.g5_out, nullptr);
+      else launch_ext<R, EPI_PLAIN>(ctx, P, mu, a.g5_out, dp);
       if ((rc = prof_end(ctx, &ev))) return rc;
     }
-    return QDP_OK;
+  } else {
+    if ((rc = launch_main_epi<R>(ctx, a, P, false, block))) return rc;
   }
-
-  ProfEvent ev;
-  prof_begin(ctx, QDP_PK_DSLASH, &ev);
-  switch (a.epi) {
-    case EPI_PLAIN: launch_main_dispatch<R, EPI_PLAIN>(ctx, P, a.g5_in, a.g5_out, false, block); break;
-    case EPI_XPAY: launch_main_dispatch<R, EPI_XPAY>(ctx, P, a.g5_in, a.g5_out, false, block); break;
-    case EPI_CLOVINV: launch_main_dispatch<R, EPI_CLOVINV>(ctx, P, a.g5_in, a.g5_out, false, block); break;
-    default: launch_main_dispatch<R, EPI_CLOVXPAY>(ctx, P, a.g5_in, a.g5_out, false, block); break;
+  if (dot) {
+    if ((rc = reduce_partials(ctx, nparts, a.dot_slot))) return rc;
+    return reduce_global(ctx, a.dot_slot, 2);
   }
-  return prof_end(ctx, &ev);
+  return QDP_OK;
 }
 
 int dslash(qdp_ctx ctx, int prec, const DslashArgs &a) {

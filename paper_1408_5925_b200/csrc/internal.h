@@ -373,6 +373,8 @@ struct qdp_ctx_s {
   double *red_result = nullptr;    // device scalars: [0..7]
   double *red_gather = nullptr;    // [nranks * 2] gathered per-rank sums
   double *host_pinned = nullptr;   // pinned host scratch (64 doubles)
+  void *cg_work = nullptr;         // persistent CG work vectors
+  size_t cg_work_bytes = 0;
   // halo buffers: [prec][mu][dir] for send and recv (dir 0 = to/from -mu, 1 = to/from +mu)
   void *halo_send[2][4][2] = {}, *halo_recv[2][4][2] = {};
   size_t halo_bytes[2] = {0, 0};
@@ -380,6 +382,7 @@ struct qdp_ctx_s {
   int neighbour[4][2];  // ranks of -mu / +mu neighbours
   // profiling / counting
   long launches[QDP_PK_COUNT] = {};
+  double work_flops[QDP_PK_COUNT] = {}, work_bytes[QDP_PK_COUNT] = {};
   double prof_ms[QDP_PK_COUNT] = {};
   std::vector<qdpb::ProfEvent> pending;
   std::vector<cudaEvent_t> event_pool;
@@ -398,11 +401,17 @@ int cuda_check(qdp_ctx ctx, cudaError_t e, const char *what);
 
 // launch bookkeeping: call before/after each kernel launch
 void prof_begin(qdp_ctx ctx, int cls, ProfEvent *ev);
+// algorithmic work of the launch just begun (flops, compulsory bytes)
+inline void prof_work(qdp_ctx ctx, int cls, double flops, double bytes) {
+  ctx->work_flops[cls] += flops;
+  ctx->work_bytes[cls] += bytes;
+}
 int prof_end(qdp_ctx ctx, ProfEvent *ev);  // checks cudaGetLastError
 
 int ensure_staging(qdp_ctx ctx, size_t bytes);
 int ensure_reduce(qdp_ctx ctx, int blocks);
 int ensure_halo(qdp_ctx ctx, int prec);
+int ensure_cg_work(qdp_ctx ctx, size_t bytes);
 
 // ---- kernels entry points (host wrappers, each enqueues on ctx->stream) ----
 // layout.cu
@@ -416,12 +425,16 @@ int blas_axpy(qdp_ctx ctx, int prec, double ar, double ai, const void *x, void *
 // partial sums -> red_result[slot] (and slot+1 for the imaginary part)
 int blas_norm2(qdp_ctx ctx, int prec, const void *a, int nblk, int slot);
 int blas_inner(qdp_ctx ctx, int prec, const void *a, const void *b, int nblk, int slot);
+// sum nparts block partial pairs in red_partials -> red_result[slot], [slot+1]
+int reduce_partials(qdp_ctx ctx, int nparts, int slot);
 // finish a reduction: cross-rank sum of red_result[slot..slot+n-1]
 int reduce_global(qdp_ctx ctx, int slot, int n);
 // CG helpers (device scalars in red_result)
-int blas_cg_update_xr(qdp_ctx ctx, int prec, void *x, void *r, const void *p, const void *q,
-                      int rho_slot, int pq_slot, int rr_slot);
-int blas_cg_update_p(qdp_ctx ctx, int prec, void *p, const void *r, int rho_new_slot, int rho_old_slot);
+// r -= alpha q ; red_result[rr_slot] = |r|^2 (global), alpha = res[rho] / res[pq]
+int blas_cg_update_r(qdp_ctx ctx, int prec, void *r, const void *q, int rho_slot, int pq_slot, int rr_slot);
+// x += alpha p ; if update_p: p = r + beta p with beta = res[rr] / res[rho]
+int blas_cg_update_xp(qdp_ctx ctx, int prec, void *x, void *p, const void *r, int rho_slot, int pq_slot, int rr_slot,
+                      bool update_p);
 int blas_xpay(qdp_ctx ctx, int prec, const void *x, double a, void *y, int nblk);  // y = x + a y
 int blas_scale_copy(qdp_ctx ctx, int prec, void *dst, const void *src, double a, int nblk);  // dst = a src
 
@@ -437,6 +450,8 @@ struct DslashArgs {
   double a, b;            // epilogue scalars
   int epi;                // Epi
   bool g5_in, g5_out;
+  const void *dot_x;      // if set: red_result[dot_slot] = Re<dot_x, out> (global), [dot_slot+1] = 0
+  int dot_slot;
 };
 int dslash(qdp_ctx ctx, int prec, const DslashArgs &a);
 

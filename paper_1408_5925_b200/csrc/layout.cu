@@ -134,6 +134,7 @@ static int layout_run(qdp_field f, void *dev_aos, bool import) {
   const int blocks = grid_for(nrec, 128);
   ProfEvent ev;
   prof_begin(ctx, QDP_PK_LAYOUT, &ev);
+  prof_work(ctx, QDP_PK_LAYOUT, 0.0, 2.0 * nrec * host_site_reals(f->kind) * (f->prec == QDP_F64 ? 8 : 4));
   if (f->kind == KIND_CLOVER) {
     const size_t blk = parity_block_bytes(KIND_CLOVER, f->prec, g.stride);
     if (f->prec == QDP_F64) {

@@ -78,6 +78,7 @@ int shift_field(qdp_ctx ctx, qdp_field out, const qdp_field in, int mu, int sign
     const int xmu = sign > 0 ? 0 : g.L[mu] - 1;
     ProfEvent ev;
     prof_begin(ctx, QDP_PK_PACK, &ev);
+    prof_work(ctx, QDP_PK_PACK, 0.0, 2.0 * nq * g.faceVh[mu] * mi.n * cbytes);
     const int nth = nq * g.faceVh[mu];
     char *dst = self ? recv : send;
     if (in->prec == QDP_F64)
@@ -93,6 +94,7 @@ int shift_field(qdp_ctx ctx, qdp_field out, const qdp_field in, int mu, int sign
   }
   ProfEvent ev;
   prof_begin(ctx, QDP_PK_SHIFT, &ev);
+  prof_work(ctx, QDP_PK_SHIFT, 0.0, 2.0 * np * g.Vh * mo.n * cbytes);
   const int nth = np * g.Vh;
   if (in->prec == QDP_F64)
     shift_kernel<double><<<grid_for(nth, 128), 128, 0, ctx->stream>>>(g, mo, mi, (char *)out->data, (const char *)in->data, mu, sign,

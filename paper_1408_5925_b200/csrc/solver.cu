@@ -1,7 +1,10 @@
 // solver.cu -- even-odd preconditioned CGNR for M x = b, M = A - H/2 (readings R3, R12-R14;
 // the linear solves of PAPER.md:31).  Host-driven loop; every vector operation is one of
 // this library's kernels and the scalars alpha, beta live on the device, so an iteration
-// needs exactly one device->host read (rho, for the convergence test).
+// needs exactly one device->host read (rho, for the convergence test).  Per iteration:
+//   q = Mhat^dag Mhat p    4 fused dslash launches; the last also forms Re<p, q>
+//   r -= alpha q, |r|^2    one pass (alpha = rho / Re<p,q> read on the device)
+//   x += alpha p, p = r + beta p   one pass (beta = |r|^2 / rho)
 //
 //   Mhat v      = A_oo v - 1/4 H_oe A_ee^-1 H_eo v         (2 fused dslash launches)
 //   Mhat^dag v  = gamma5 Mhat gamma5 v                       (gamma5 folded into the kernels)
@@ -27,8 +30,8 @@ struct Op {
   void *t;             // even scratch block
 };
 
-// out_o = Mhat v_o  (dag: Mhat^dag)
-int apply_mhat(const Op &op, void *out, const void *v, bool dag) {
+// out_o = Mhat v_o  (dag: Mhat^dag); dot_x: also red_result[dot_slot] = Re<dot_x, out>
+int apply_mhat(const Op &op, void *out, const void *v, bool dag, const void *dot_x = nullptr, int dot_slot = 0) {
   DslashArgs a = {};
   int rc;
   a.U = op.U;
@@ -53,6 +56,8 @@ int apply_mhat(const Op &op, void *out, const void *v, bool dag) {
   c.x = v;
   c.parity = 1;
   c.g5_out = dag;
+  c.dot_x = dot_x;
+  c.dot_slot = dot_slot;
   if (op.A_o) {
     c.epi = EPI_CLOVXPAY;
     c.clov = op.A_o;
@@ -84,10 +89,10 @@ int cg_solve(qdp_field x, const qdp_field b, const qdp_field U, const qdp_field 
   op.Ainv_e = clover ? Ainv->data : nullptr;
   op.diag = 4.0 + mass;
 
-  // work: [t | r | p | q | mp | bh]
-  char *work = nullptr;
-  QDP_CUDA(ctx, cudaMallocAsync((void **)&work, 6 * blk, ctx->stream));
-  QDP_CUDA(ctx, cudaMemsetAsync(work, 0, 6 * blk, ctx->stream));
+  // work: [t | r | p | q | mp | bh], persistent in the context (every block is fully
+  // written before it is read, so no clearing is needed)
+  if ((rc = ensure_cg_work(ctx, 6 * blk))) return rc;
+  char *work = (char *)ctx->cg_work;
   op.t = work;
   void *r = work + blk, *p = work + 2 * blk, *q = work + 3 * blk, *mp = work + 4 * blk, *bh = work + 5 * blk;
   const char *b_e = (const char *)b->data, *b_o = b_e + blk;
@@ -96,10 +101,7 @@ int cg_solve(qdp_field x, const qdp_field b, const qdp_field U, const qdp_field 
   int k = 0, status = QDP_NOT_CONVERGED;
   double rho0 = 0.0, rho = 0.0;
 
-  auto fail = [&](int e) {
-    cudaFreeAsync(work, ctx->stream);
-    return e;
-  };
+  auto fail = [&](int e) { return e; };
   auto read_slot = [&](int slot, double *v) -> int {
     cudaError_t e = cudaMemcpyAsync(h, ctx->red_result + slot, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
@@ -136,22 +138,24 @@ int cg_solve(qdp_field x, const qdp_field b, const qdp_field U, const qdp_field 
   if (rho0 == 0.0) status = QDP_OK;
 
   while (status == QDP_NOT_CONVERGED && k < maxit) {
+    // q = Mhat^dag Mhat p, with Re<p, q> -> S_PQ fused into the last launch
     if ((rc = apply_mhat(op, mp, p, false))) return fail(rc);
-    if ((rc = apply_mhat(op, q, mp, true))) return fail(rc);
-    if ((rc = blas_inner(ctx, prec, p, q, 1, S_PQ)) || (rc = reduce_global(ctx, S_PQ, 2))) return fail(rc);
-    // x += alpha p ; r -= alpha q ; rr = |r|^2   (alpha = rho / Re<p,q> on the device)
-    if ((rc = blas_cg_update_xr(ctx, prec, x_o, r, p, q, S_RHO, S_PQ, S_RR))) return fail(rc);
+    if ((rc = apply_mhat(op, q, mp, true, p, S_PQ))) return fail(rc);
+    // r -= alpha q ; rr = |r|^2
+    if ((rc = blas_cg_update_r(ctx, prec, r, q, S_RHO, S_PQ, S_RR))) return fail(rc);
     double rho_new;
     if ((rc = read_slot(S_RR, &rho_new))) return fail(rc);
     k++;
     if (hist && k < hist_cap) hist[k] = sqrt(rho_new / rho0);
-    if (rho_new <= tol * tol * rho0) {
+    const bool done = rho_new <= tol * tol * rho0;
+    // x += alpha p ; p = r + beta p (skipped on the last iteration)
+    const bool last = done || k == maxit;
+    if ((rc = blas_cg_update_xp(ctx, prec, x_o, p, r, S_RHO, S_PQ, S_RR, !last))) return fail(rc);
+    if (done) {
       status = QDP_OK;
       rho = rho_new;
       break;
     }
-    // p = r + beta p, beta = rr / rho ; rho <- rr
-    if ((rc = blas_cg_update_p(ctx, prec, p, r, S_RR, S_RHO))) return fail(rc);
     if (cudaMemcpyAsync(ctx->red_result + S_RHO, ctx->red_result + S_RR, sizeof(double), cudaMemcpyDeviceToDevice,
                         ctx->stream) != cudaSuccess)
       return fail(set_error(ctx, QDP_ECUDA, "cg: scalar copy"));
@@ -209,7 +213,6 @@ int cg_solve(qdp_field x, const qdp_field b, const qdp_field U, const qdp_field 
       return fail(rc);
     *true_resid = bb > 0 ? sqrt(rr / bb) : 0.0;
   }
-  QDP_CUDA(ctx, cudaFreeAsync(work, ctx->stream));
   QDP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   return status;
 }

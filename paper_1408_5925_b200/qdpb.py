@@ -63,6 +63,7 @@ _SIGS = {
     "qdp_strerror": [ctypes.c_int],
     "qdp_last_error": [_vp],
     "qdp_profile_query": [_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_long), _dp],
+    "qdp_profile_work": [_vp, ctypes.c_int, _dp, _dp],
     "qdp_profile_reset": [_vp],
 }
 
@@ -328,6 +329,13 @@ def qdp_profile_query(ctx: Ctx, kernel_class: int = -1):
     n, ms = ctypes.c_long(), ctypes.c_double()
     _check(lib().qdp_profile_query(ctx, int(kernel_class), ctypes.byref(n), ctypes.byref(ms)), ctx)
     return n.value, ms.value
+
+
+def qdp_profile_work(ctx: Ctx, kernel_class: int = -1):
+    """(algorithmic flops, compulsory bytes) of the launches counted since the last reset."""
+    f, b = ctypes.c_double(), ctypes.c_double()
+    _check(lib().qdp_profile_work(ctx, int(kernel_class), ctypes.byref(f), ctypes.byref(b)), ctx)
+    return f.value, b.value
 
 
 def qdp_profile_reset(ctx: Ctx) -> None:
