@@ -102,8 +102,8 @@ int qdp_get_geometry(qdp_ctx ctx, int local_dims[4], int proc_coords[4]);
  *                     partitioned: faces are packed and the halo path runs, the peer being
  *                     this rank (single-GPU test mode of the multi-GPU code).
  *  QDP_OPT_PROFILE    1: bracket every launch with CUDA events (see qdp_profile_query).
- *  QDP_OPT_BLOCK      threads per block of the dslash kernels, a multiple of 32 <= 256
- *                     (0 = the default, 128).
+ *  QDP_OPT_BLOCK      threads per block of the main dslash kernel: 0 (the build's default,
+ *                     64) or a multiple of 32 up to the build's launch bound (64).
  *  QDP_OPT_DET_REDUCE 1 (default): cross-rank sums by allgather + rank-ordered sum
  *                     (deterministic); 0: ncclAllReduce. */
 enum { QDP_OPT_OVERLAP = 0, QDP_OPT_SELF_HALO = 1, QDP_OPT_PROFILE = 2, QDP_OPT_BLOCK = 3,

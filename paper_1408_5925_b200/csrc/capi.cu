@@ -319,7 +319,8 @@ extern "C" int qdp_set_option(qdp_ctx c, int opt, long v) {
       c->profiling = v ? 1 : 0;
       return QDP_OK;
     case QDP_OPT_BLOCK:
-      if (v < 0 || v > 256 || (v % 32)) return set_error(c, QDP_EINVAL, "block must be a multiple of 32 <= 256");
+      if (v < 0 || v > QDPB_DSLASH_MAXT || (v % 32))
+        return set_error(c, QDP_EINVAL, "block must be a multiple of 32 <= %d", QDPB_DSLASH_MAXT);
       c->block = (int)v;
       return QDP_OK;
     case QDP_OPT_DET_REDUCE: c->det_reduce = v ? 1 : 0; return QDP_OK;

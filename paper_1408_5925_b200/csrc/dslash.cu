@@ -250,7 +250,7 @@ __device__ __forceinline__ void dot_block_partial(double v, double *part) {
 // Whole-lattice (HALO=false) or interior (HALO=true: remote hops skipped) kernel.
 // DOT: also accumulate Re<dot, out> per block into dot_part (fused inner product).
 template <typename R, int EPI, bool G5IN, bool G5OUT, bool HALO, bool DOT>
-__global__ void __launch_bounds__(256) dslash_kernel(const Geom g, const KParams<R> P) {
+__global__ void __launch_bounds__(QDPB_DSLASH_MAXT, QDPB_DSLASH_MINB) dslash_kernel(const Geom g, const KParams<R> P) {
   const int cb = blockIdx.x * blockDim.x + threadIdx.x;
   double dot = 0.0;
   if (cb < g.Vh) {
@@ -450,7 +450,7 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
   P.parity = a.parity;
   P.a = (R)a.a;
   P.b = (R)a.b;
-  const int block = ctx->block > 0 ? ctx->block : 128;
+  const int block = ctx->block > 0 ? ctx->block : QDPB_DSLASH_BLOCK;
   const bool halo = g.part != 0;
   const bool dot = a.dot_x != nullptr;
   int rc;

@@ -19,6 +19,18 @@
 
 #include "../../include/qdpb.h"
 
+// Occupancy target of the main dslash kernel: __launch_bounds__(QDPB_DSLASH_MAXT, QDPB_DSLASH_MINB)
+// caps it at 168 registers (6 x 64 threads per SM), measured best on B200.
+#ifndef QDPB_DSLASH_MAXT
+#define QDPB_DSLASH_MAXT 64
+#endif
+#ifndef QDPB_DSLASH_MINB
+#define QDPB_DSLASH_MINB 6
+#endif
+#ifndef QDPB_DSLASH_BLOCK
+#define QDPB_DSLASH_BLOCK 64
+#endif
+
 namespace qdpb {
 
 // ------------------------------------------------------------------ geometry

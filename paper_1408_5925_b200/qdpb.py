@@ -13,7 +13,8 @@ import re
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libqdpb.so")
+# QDPB_LIB selects a tuning-variant build of the same library (development only)
+LIB_PATH = os.environ.get("QDPB_LIB") or os.path.join(_HERE, "libqdpb.so")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "qdpb.h")
 
 QDP_F64, QDP_F32 = 0, 1
