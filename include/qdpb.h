@@ -161,7 +161,9 @@ int qdp_axpy(double a_re, double a_im, const qdp_field x, qdp_field y);
  *   sigma_mu,nu = [gamma_mu, gamma_nu] / (2i),  F = traceless part of (Q - Q^dag)/(8i),
  * Q the four clover leaves.  A (nullable) receives A on its subset's sites, Ainv (nullable)
  * A^{-1} on its subset's sites.  Both QDP_CLOVER fields of U's precision.  Computed in fp64
- * internally.  Returns QDP_ESINGULAR if a 6x6 block has a zero pivot. */
+ * internally.  On a partitioned lattice the leaves' off-site links come from shifted copies
+ * of U ("shifts of shifts", executed without overlap as in PAPER.md:214; 8 gauge-field
+ * temporaries).  Returns QDP_ESINGULAR if a 6x6 block has a zero pivot. */
 int qdp_clover_build(qdp_field A, qdp_field Ainv, const qdp_field U, double mass, double csw);
 /* out(x) = A(x) in(x) on the sites of `parity` (QDP_ALL: all); out may equal in. */
 int qdp_clover_apply(qdp_field out, const qdp_field A, const qdp_field in, int parity);

@@ -569,12 +569,9 @@ extern "C" int qdp_clover_build(qdp_field A, qdp_field Ainv, const qdp_field U, 
     if (f->kind != QDP_CLOVER) return set_error(c, QDP_EINVAL, "clover_build: outputs must be clover fields");
   }
   if (A && Ainv && A->data == Ainv->data) return set_error(c, QDP_EALIAS, "clover_build: A aliases Ainv");
-  for (int mu = 0; mu < 4; mu++)
-    if (c->pgrid[mu] > 1)
-      return set_error(c, QDP_EUNSUPPORTED, "clover_build: partitioned lattices need the extended gauge field (not implemented)");
   int singular = 0;
-  if ((rc = clover_build(c, U->prec, A ? A->data : nullptr, A ? A->subset : 0, Ainv ? Ainv->data : nullptr,
-                         Ainv ? Ainv->subset : 0, U->data, mass, csw, &singular)))
+  if ((rc = clover_build(c, U, A ? A->data : nullptr, A ? A->subset : 0, Ainv ? Ainv->data : nullptr,
+                         Ainv ? Ainv->subset : 0, mass, csw, &singular)))
     return rc;
   if (singular) return set_error(c, QDP_ESINGULAR, "clover_build: zero pivot in a 6x6 block");
   return QDP_OK;

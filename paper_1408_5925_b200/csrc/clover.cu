@@ -15,6 +15,7 @@
 namespace qdpb {
 
 struct M3 { double2 m[9]; };
+template <typename R> struct ShiftSet { GaugeView<R> s[7]; };
 
 __device__ __forceinline__ double2 c_add(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 c_sub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
@@ -146,22 +147,14 @@ __device__ bool hermitian_inverse6(const double d[6], const double2 off[15], dou
   return true;
 }
 
+// Assemble the two packed blocks of A from the six F_mu,nu (01 02 03 12 13 23) of one site,
+// store A and / or A^-1 (fp64 arithmetic, stored in the field precision R).
 template <typename R>
-__global__ void __launch_bounds__(128) clover_build_kernel(const Geom g, GaugeView<R> U, int p, char *A, char *Ainv,
-                                                           double mass, double csw, int *singular) {
-  const int cb = blockIdx.x * blockDim.x + threadIdx.x;
-  if (cb >= g.Vh) return;
-  int c[4];
-  cb_coords(g, cb, p, c);
-  M3 F[6];  // 01 02 03 12 13 23
-  {
-    int k = 0;
-    for (int mu = 0; mu < 4; mu++)
-      for (int nu = mu + 1; nu < 4; nu++) F[k++] = field_strength(g, U, c, mu, nu);
-  }
+__device__ void assemble_store(const Geom &g, const M3 F[6], int cb, char *A, char *Ainv, double mass, double csw,
+                               int *singular) {
   const double h = 0.5 * csw;
   for (int b = 0; b < 2; b++) {
-    // 2x2 spin blocks with 3x3 colour entries: B00, B11, B10 (lower); B01 = B10^dag
+    // 2x2 spin blocks with 3x3 colour entries: B00, B11, B01 (upper); B10 = B01^dag
     M3 B00, B11, B01;
     const double s23 = b == 0 ? 1.0 : -1.0;   // sign of F23 in B00 (block 0: +, block 1: -)
     const double s03 = b == 0 ? 1.0 : -1.0;
@@ -206,6 +199,82 @@ __global__ void __launch_bounds__(128) clover_build_kernel(const Geom g, GaugeVi
   }
 }
 
+// Single-rank build: the leaves read their off-site links directly (periodic wrap).
+template <typename R>
+__global__ void __launch_bounds__(128) clover_build_kernel(const Geom g, GaugeView<R> U, int p, char *A, char *Ainv,
+                                                           double mass, double csw, int *singular) {
+  const int cb = blockIdx.x * blockDim.x + threadIdx.x;
+  if (cb >= g.Vh) return;
+  int c[4];
+  cb_coords(g, cb, p, c);
+  M3 F[6];  // 01 02 03 12 13 23
+  {
+    int k = 0;
+    for (int mu = 0; mu < 4; mu++)
+      for (int nu = mu + 1; nu < 4; nu++) F[k++] = field_strength(g, U, c, mu, nu);
+  }
+  assemble_store<R>(g, F, cb, A, Ainv, mass, csw, singular);
+}
+
+// Partitioned build ("shifts of shifts"): the seven displaced gauge fields
+// S[k](x) = U(x + d_k), d = (+mu, +nu, -mu, -nu, -mu+nu, -mu-nu, +mu-nu), were formed with
+// qdp_shift (halo exchange included), so every leaf link is local to x.  Writes F_mu,nu of
+// both parities into Fbuf[plane][parity][9][stride] (fp64).
+template <typename R>
+__global__ void __launch_bounds__(128) clover_leaf_kernel(const Geom g, GaugeView<R> U, ShiftSet<R> S, int mu, int nu,
+                                                          int plane, double2 *Fbuf) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 2 * g.Vh) return;
+  const int p = i / g.Vh, cb = i % g.Vh;
+  auto L = [&](const GaugeView<R> &G, int d) {
+    Link<R> l = G.load(d, p, cb);
+    M3 r;
+#pragma unroll
+    for (int k = 0; k < 9; k++) r.m[k] = make_double2((double)l.m[k].re, (double)l.m[k].im);
+    return r;
+  };
+  const GaugeView<R> &Pm = S.s[0], &Pn = S.s[1], &Mm = S.s[2], &Mn = S.s[3], &MmPn = S.s[4], &MmMn = S.s[5],
+                     &PmMn = S.s[6];
+  M3 q, t;
+  q = m3_mul(m3_mul(L(U, mu), L(Pm, nu)), m3_mul(m3_dag(L(Pn, mu)), m3_dag(L(U, nu))));
+  t = m3_mul(m3_mul(L(U, nu), m3_dag(L(MmPn, mu))), m3_mul(m3_dag(L(Mm, nu)), L(Mm, mu)));
+#pragma unroll
+  for (int k = 0; k < 9; k++) q.m[k] = c_add(q.m[k], t.m[k]);
+  t = m3_mul(m3_mul(m3_dag(L(Mm, mu)), m3_dag(L(MmMn, nu))), m3_mul(L(MmMn, mu), L(Mn, nu)));
+#pragma unroll
+  for (int k = 0; k < 9; k++) q.m[k] = c_add(q.m[k], t.m[k]);
+  t = m3_mul(m3_mul(m3_dag(L(Mn, nu)), L(Mn, mu)), m3_mul(L(PmMn, nu), m3_dag(L(U, mu))));
+#pragma unroll
+  for (int k = 0; k < 9; k++) q.m[k] = c_add(q.m[k], t.m[k]);
+  double2 *Fo = Fbuf + ((size_t)(plane * 2 + p) * 9) * g.stride + cb;
+  double tr = 0.0;
+  double2 f[9];
+#pragma unroll
+  for (int a = 0; a < 3; a++)
+#pragma unroll
+    for (int b = 0; b < 3; b++) {
+      double2 d = c_sub(q.m[3 * a + b], c_conj(q.m[3 * b + a]));
+      f[3 * a + b] = make_double2(d.y / 8.0, -d.x / 8.0);
+    }
+  tr = (f[0].x + f[4].x + f[8].x) / 3.0;
+  f[0].x -= tr;
+  f[4].x -= tr;
+  f[8].x -= tr;
+#pragma unroll
+  for (int k = 0; k < 9; k++) Fo[(size_t)k * g.stride] = f[k];
+}
+
+template <typename R>
+__global__ void __launch_bounds__(128) clover_assemble_kernel(const Geom g, const double2 *Fbuf, int p, char *A,
+                                                              char *Ainv, double mass, double csw, int *singular) {
+  const int cb = blockIdx.x * blockDim.x + threadIdx.x;
+  if (cb >= g.Vh) return;
+  M3 F[6];
+  for (int k = 0; k < 6; k++)
+    for (int e = 0; e < 9; e++) F[k].m[e] = Fbuf[((size_t)(k * 2 + p) * 9 + e) * g.stride + cb];
+  assemble_store<R>(g, F, cb, A, Ainv, mass, csw, singular);
+}
+
 template <typename R>
 __global__ void __launch_bounds__(128) clover_apply_kernel(const Geom g, FermView<R> out, CloverView<R> A, FermView<R> in) {
   const int cb = blockIdx.x * blockDim.x + threadIdx.x;
@@ -214,12 +283,64 @@ __global__ void __launch_bounds__(128) clover_apply_kernel(const Geom g, FermVie
   out.store(cb, clover_mul(A, cb, s));
 }
 
-int clover_build(qdp_ctx ctx, int prec, void *A, int A_subset, void *Ainv, int Ainv_subset, const void *U,
-                 double mass, double csw, int *singular_host) {
+// Partitioned lattice: F_mu,nu from local leaves on shifted gauge fields (see clover_leaf_kernel).
+template <typename R>
+static int build_F_by_shifts(qdp_ctx ctx, const qdp_field U, double2 *Fbuf) {
   const Geom &g = ctx->geom;
+  const int prec = U->prec;
+  const size_t gb = 2 * parity_block_bytes(KIND_GAUGE, prec, g.stride);
+  char *tmp = nullptr;
+  QDP_CUDA(ctx, cudaMallocAsync((void **)&tmp, 8 * gb, ctx->stream));
+  qdp_field_s f[8];
+  for (int k = 0; k < 8; k++) {
+    f[k].ctx = ctx;
+    f[k].kind = KIND_GAUGE;
+    f[k].prec = prec;
+    f[k].subset = QDP_ALL;
+    f[k].data = tmp + k * gb;
+    f[k].bytes = gb;
+    f[k].owned = false;
+  }
+  // f[0..6] = U(x + d_k) in the order of ShiftSet; f[7] scratch
+  int rc = QDP_OK, plane = 0;
+  for (int mu = 0; mu < 4 && !rc; mu++)
+    for (int nu = mu + 1; nu < 4 && !rc; nu++, plane++) {
+      if ((rc = shift_field(ctx, &f[0], U, mu, +1))) break;      // U(x+mu)
+      if ((rc = shift_field(ctx, &f[1], U, nu, +1))) break;      // U(x+nu)
+      if ((rc = shift_field(ctx, &f[2], U, mu, -1))) break;      // U(x-mu)
+      if ((rc = shift_field(ctx, &f[3], U, nu, -1))) break;      // U(x-nu)
+      if ((rc = shift_field(ctx, &f[4], &f[1], mu, -1))) break;  // U(x-mu+nu)  (shift of a shift)
+      if ((rc = shift_field(ctx, &f[5], &f[3], mu, -1))) break;  // U(x-mu-nu)
+      if ((rc = shift_field(ctx, &f[6], &f[3], mu, +1))) break;  // U(x+mu-nu)
+      ShiftSet<R> S;
+      for (int k = 0; k < 7; k++) S.s[k] = GaugeView<R>{(decltype(S.s[k].p))f[k].data, g.stride};
+      ProfEvent ev;
+      prof_begin(ctx, QDP_PK_CLOVER, &ev);
+      clover_leaf_kernel<R><<<grid_for(2 * g.Vh, 128), 128, 0, ctx->stream>>>(
+          g, GaugeView<R>{(decltype(S.s[0].p))U->data, g.stride}, S, mu, nu, plane, Fbuf);
+      if ((rc = prof_end(ctx, &ev))) break;
+    }
+  cudaFreeAsync(tmp, ctx->stream);
+  return rc;
+}
+
+int clover_build(qdp_ctx ctx, const qdp_field U, void *A, int A_subset, void *Ainv, int Ainv_subset, double mass,
+                 double csw, int *singular_host) {
+  const Geom &g = ctx->geom;
+  const int prec = U->prec;
   const size_t blk = parity_block_bytes(KIND_CLOVER, prec, g.stride);
   int *flag = (int *)(ctx->red_result + 62);  // scratch int in the reduction scalars
   QDP_CUDA(ctx, cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
+  double2 *Fbuf = nullptr;
+  int rc;
+  if (g.part) {  // some neighbours live across a rank (or self-halo) boundary: shifts of shifts
+    QDP_CUDA(ctx, cudaMallocAsync((void **)&Fbuf, (size_t)6 * 2 * 9 * g.stride * sizeof(double2), ctx->stream));
+    rc = prec == QDP_F64 ? build_F_by_shifts<double>(ctx, U, Fbuf) : build_F_by_shifts<float>(ctx, U, Fbuf);
+    if (rc) {
+      cudaFreeAsync(Fbuf, ctx->stream);
+      return rc;
+    }
+  }
   for (int p = 0; p < 2; p++) {
     char *a = nullptr, *ai = nullptr;
     if (A && (A_subset == QDP_ALL || A_subset == p)) a = (char *)A + (A_subset == QDP_ALL ? p * blk : 0);
@@ -227,13 +348,19 @@ int clover_build(qdp_ctx ctx, int prec, void *A, int A_subset, void *Ainv, int A
     if (!a && !ai) continue;
     ProfEvent ev;
     prof_begin(ctx, QDP_PK_CLOVER, &ev);
-    if (prec == QDP_F64)
-      clover_build_kernel<double><<<grid_for(g.Vh, 128), 128, 0, ctx->stream>>>(g, {(const double2 *)U, g.stride}, p, a, ai, mass, csw, flag);
-    else
-      clover_build_kernel<float><<<grid_for(g.Vh, 128), 128, 0, ctx->stream>>>(g, {(const float *)U, g.stride}, p, a, ai, mass, csw, flag);
-    int rc = prof_end(ctx, &ev);
-    if (rc) return rc;
+    const int nb = grid_for(g.Vh, 128);
+    if (Fbuf) {
+      if (prec == QDP_F64) clover_assemble_kernel<double><<<nb, 128, 0, ctx->stream>>>(g, Fbuf, p, a, ai, mass, csw, flag);
+      else clover_assemble_kernel<float><<<nb, 128, 0, ctx->stream>>>(g, Fbuf, p, a, ai, mass, csw, flag);
+    } else {
+      if (prec == QDP_F64)
+        clover_build_kernel<double><<<nb, 128, 0, ctx->stream>>>(g, {(const double2 *)U->data, g.stride}, p, a, ai, mass, csw, flag);
+      else
+        clover_build_kernel<float><<<nb, 128, 0, ctx->stream>>>(g, {(const float *)U->data, g.stride}, p, a, ai, mass, csw, flag);
+    }
+    if ((rc = prof_end(ctx, &ev))) return rc;
   }
+  if (Fbuf) QDP_CUDA(ctx, cudaFreeAsync(Fbuf, ctx->stream));
   int h = 0;
   QDP_CUDA(ctx, cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   QDP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));

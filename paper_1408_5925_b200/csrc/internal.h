@@ -468,8 +468,8 @@ struct DslashArgs {
 int dslash(qdp_ctx ctx, int prec, const DslashArgs &a);
 
 // clover.cu
-int clover_build(qdp_ctx ctx, int prec, void *A, int A_subset, void *Ainv, int Ainv_subset,
-                 const void *U, double mass, double csw, int *singular_flag_host);
+int clover_build(qdp_ctx ctx, const qdp_field U, void *A, int A_subset, void *Ainv, int Ainv_subset,
+                 double mass, double csw, int *singular_flag_host);
 int clover_apply(qdp_ctx ctx, int prec, void *out, const void *A, const void *in, int nblk);
 
 // shift.cu

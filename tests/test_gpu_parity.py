@@ -348,3 +348,119 @@ def test_wrap_torch_tensor(q):
         assert float(t.abs().sum()) > 0
     finally:
         q.qdp_finalize(c)
+
+
+@pytest.mark.parametrize("mask", [8, 15])
+def test_clover_build_shifts_of_shifts(q, mask):
+    """Partitioned build path (leaves from shifted gauge fields) via self-halo."""
+    L = (4, 6, 4, 4)
+    U = fieldgen.random_gauge(L, 1501)
+    A = oracle.clover_build(U, L, -0.1, 1.3)
+    Ai = oracle.clover_invert(A, L)
+    c = _ctx(q, L, self_halo=mask)
+    try:
+        fU = _field(q, c, q.QDP_GAUGE, 0, q.QDP_ALL, U)
+        fA = q.qdp_field_alloc(c, q.QDP_CLOVER, 0, q.QDP_ALL)
+        fAi = q.qdp_field_alloc(c, q.QDP_CLOVER, 0, q.QDP_ALL)
+        q.qdp_clover_build(fA, fAi, fU, -0.1, 1.3)
+        assert np.max(np.abs(q.qdp_field_export(fA) - A)) <= 1e-13 * np.max(np.abs(A))
+        assert np.max(np.abs(q.qdp_field_export(fAi) - Ai)) <= 1e-13 * np.max(np.abs(Ai))
+        n_shift, _ = q.qdp_profile_query(c, q.QDP_PK_SHIFT)
+        assert n_shift == 6 * 7
+    finally:
+        q.qdp_finalize(c)
+
+
+def test_cg_clover_self_halo(q):
+    L = (4, 4, 6, 4)
+    U = fieldgen.random_gauge(L, 1601)
+    b = fieldgen.random_spinor(L, 2601)
+    A = oracle.clover_build(U, L, 0.1, 1.0)
+    ref = oracle.cg_solve(U, b, L, 0.1, A=A, tol=1e-10, maxit=1000)
+    c = _ctx(q, L, self_halo=12)
+    try:
+        fU = _field(q, c, q.QDP_GAUGE, 0, q.QDP_ALL, U)
+        fb = _field(q, c, q.QDP_FERMION, 0, q.QDP_ALL, b)
+        fx = q.qdp_field_alloc(c, q.QDP_FERMION, 0, q.QDP_ALL)
+        fA = q.qdp_field_alloc(c, q.QDP_CLOVER, 0, q.QDP_ALL)
+        fAi = q.qdp_field_alloc(c, q.QDP_CLOVER, 0, q.QDP_EVEN)
+        q.qdp_clover_build(fA, fAi, fU, 0.1, 1.0)
+        res = q.qdp_cg_solve(fx, fb, fU, fA, fAi, mass=0.1, tol=1e-10, maxit=1000)
+        assert res["iters"] == ref["iters"]
+        assert np.max(np.abs(res["hist"] - ref["hist"]) / ref["hist"]) <= 1e-10
+        assert rel_site_err(q.qdp_field_export(fx), ref["x"]) <= 1e-9
+    finally:
+        q.qdp_finalize(c)
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+def test_dslash_bench_size(q, prec):
+    """The bench's per-GPU lattice (40^3 x 32) and launch configuration: every output site of
+    one EO dslash against the oracle."""
+    L = (40, 40, 40, 32)
+    U = _round(fieldgen.random_gauge(L, 1004), prec)
+    psi = _round(fieldgen.random_spinor(L, 2005), prec)
+    ref = oracle.hopping(U, psi, L, 0)
+    c = _ctx(q, L)
+    try:
+        fU = _field(q, c, q.QDP_GAUGE, prec, q.QDP_ALL, U)
+        fp = _field(q, c, q.QDP_FERMION, prec, 1, psi[fieldgen.cb_sites(L, 1)])
+        fo = q.qdp_field_alloc(c, q.QDP_FERMION, prec, 0)
+        q.qdp_dslash(fo, fU, fp, 0)
+        got = q.qdp_field_export(fo).astype(np.float64)
+        assert rel_site_err(got, ref[fieldgen.cb_sites(L, 0)]) <= TOL[prec]
+    finally:
+        q.qdp_finalize(c)
+
+
+def test_cg_bench_config_history(q):
+    """The bench step (40^3 x 32 clover CGNR, m = 0.1, c_SW = 1) for 3 iterations: history,
+    solution and true residual against the oracle."""
+    L = (40, 40, 40, 32)
+    U = fieldgen.random_gauge(L, 1004)
+    b = fieldgen.random_spinor(L, 2005)
+    A = oracle.clover_build(U, L, 0.1, 1.0)
+    ref = oracle.cg_solve(U, b, L, 0.1, A=A, tol=0.0, maxit=3)
+    del A
+    c = _ctx(q, L)
+    try:
+        fU = _field(q, c, q.QDP_GAUGE, 0, q.QDP_ALL, U)
+        fb = _field(q, c, q.QDP_FERMION, 0, q.QDP_ALL, b)
+        fx = q.qdp_field_alloc(c, q.QDP_FERMION, 0, q.QDP_ALL)
+        fA = q.qdp_field_alloc(c, q.QDP_CLOVER, 0, q.QDP_ALL)
+        fAi = q.qdp_field_alloc(c, q.QDP_CLOVER, 0, q.QDP_EVEN)
+        q.qdp_clover_build(fA, fAi, fU, 0.1, 1.0)
+        res = q.qdp_cg_solve(fx, fb, fU, fA, fAi, mass=0.1, tol=0.0, maxit=3)
+        assert res["status"] == q.QDP_NOT_CONVERGED and res["iters"] == 3
+        assert np.max(np.abs(res["hist"] - ref["hist"]) / ref["hist"]) <= 1e-10
+        assert abs(res["true_resid"] - ref["true_resid"]) <= 1e-10 * ref["true_resid"]
+        assert rel_site_err(q.qdp_field_export(fx), ref["x"]) <= 1e-11
+    finally:
+        q.qdp_finalize(c)
+
+
+def test_cg_config3_converges(q):
+    """Config 3: 32^3 x 64 Wilson-clover CG to 1e-10 (hot field); the first iterations'
+    history against the oracle, convergence and the true residual checked on the GPU run."""
+    L = (32, 32, 32, 64)
+    m = 0.1
+    U = fieldgen.random_gauge(L, 1003)
+    b = fieldgen.random_spinor(L, 2004)
+    A = oracle.clover_build(U, L, m, 1.0)
+    ref = oracle.cg_solve(U, b, L, m, A=A, tol=0.0, maxit=4)
+    del A
+    c = _ctx(q, L)
+    try:
+        fU = _field(q, c, q.QDP_GAUGE, 0, q.QDP_ALL, U)
+        fb = _field(q, c, q.QDP_FERMION, 0, q.QDP_ALL, b)
+        fx = q.qdp_field_alloc(c, q.QDP_FERMION, 0, q.QDP_ALL)
+        fA = q.qdp_field_alloc(c, q.QDP_CLOVER, 0, q.QDP_ALL)
+        fAi = q.qdp_field_alloc(c, q.QDP_CLOVER, 0, q.QDP_EVEN)
+        q.qdp_clover_build(fA, fAi, fU, m, 1.0)
+        res = q.qdp_cg_solve(fx, fb, fU, fA, fAi, mass=m, tol=1e-10, maxit=2000)
+        assert res["status"] == q.QDP_OK
+        assert np.max(np.abs(res["hist"][:5] - ref["hist"]) / ref["hist"]) <= 1e-10
+        assert res["hist"][-1] <= 1e-10 < res["hist"][-2]
+        assert res["true_resid"] <= 1e-9
+    finally:
+        q.qdp_finalize(c)
