@@ -105,9 +105,13 @@ int qdp_get_geometry(qdp_ctx ctx, int local_dims[4], int proc_coords[4]);
  *  QDP_OPT_BLOCK      threads per block of the main dslash kernel: 0 (the build's default,
  *                     64) or a multiple of 32 up to the build's launch bound (64).
  *  QDP_OPT_DET_REDUCE 1 (default): cross-rank sums by allgather + rank-ordered sum
- *                     (deterministic); 0: ncclAllReduce. */
+ *                     (deterministic); 0: ncclAllReduce.
+ *  QDP_OPT_SELF_NCCL  1: self-halo dims exchange their faces with ncclSend/ncclRecv to this
+ *                     rank (a one-rank communicator is created on first use; QDP_ENCCL if
+ *                     NCCL cannot be loaded) instead of packing straight into the ghost
+ *                     buffers -- the NCCL code path of a multi-GPU run, on one GPU. */
 enum { QDP_OPT_OVERLAP = 0, QDP_OPT_SELF_HALO = 1, QDP_OPT_PROFILE = 2, QDP_OPT_BLOCK = 3,
-       QDP_OPT_DET_REDUCE = 4 };
+       QDP_OPT_DET_REDUCE = 4, QDP_OPT_SELF_NCCL = 5 };
 int qdp_set_option(qdp_ctx ctx, int option, long value);
 int qdp_get_option(qdp_ctx ctx, int option, long *value);
 

@@ -324,6 +324,14 @@ extern "C" int qdp_set_option(qdp_ctx c, int opt, long v) {
       c->block = (int)v;
       return QDP_OK;
     case QDP_OPT_DET_REDUCE: c->det_reduce = v ? 1 : 0; return QDP_OK;
+    case QDP_OPT_SELF_NCCL: {
+      if (v) {
+        int rc = comm_ensure_self(c);
+        if (rc) return rc;
+      }
+      c->self_nccl = v ? 1 : 0;
+      return QDP_OK;
+    }
   }
   return set_error(c, QDP_EINVAL, "unknown option %d", opt);
 }
@@ -336,6 +344,7 @@ extern "C" int qdp_get_option(qdp_ctx c, int opt, long *v) {
     case QDP_OPT_PROFILE: *v = c->profiling; return QDP_OK;
     case QDP_OPT_BLOCK: *v = c->block; return QDP_OK;
     case QDP_OPT_DET_REDUCE: *v = c->det_reduce; return QDP_OK;
+    case QDP_OPT_SELF_NCCL: *v = c->self_nccl; return QDP_OK;
   }
   return set_error(c, QDP_EINVAL, "unknown option %d", opt);
 }

@@ -92,6 +92,25 @@ int comm_init(qdp_ctx ctx, const unsigned char *id) {
   return QDP_OK;
 }
 
+// One-rank communicator: self-halo dims then exchange through ncclSend / ncclRecv to this
+// rank (the same message order as P_mu = 2, where both neighbours are one peer).
+int comm_ensure_self(qdp_ctx ctx) {
+  if (ctx->comm) return QDP_OK;
+  if (ctx->nranks != 1) return set_error(ctx, QDP_ENCCL, "no communicator");
+  unsigned char id[128];
+  if (comm_get_unique_id(id)) return set_error(ctx, QDP_ENCCL, "cannot load NCCL / get a unique id");
+  ncclUniqueId u;
+  memcpy(&u, id, 128);
+  Comm *c = new Comm();
+  ncclResult_t r = g_nccl.CommInitRank(&c->comm, 1, u, 0);
+  if (r != ncclSuccess) {
+    delete c;
+    return nccl_err(ctx, r, "ncclCommInitRank(1 rank)");
+  }
+  ctx->comm = c;
+  return QDP_OK;
+}
+
 void comm_destroy(qdp_ctx ctx) {
   if (ctx->comm) {
     g_nccl.CommDestroy(ctx->comm->comm);
@@ -110,7 +129,7 @@ int comm_exchange(qdp_ctx ctx, int prec, const size_t face_bytes[4], cudaStream_
   ncclComm_t cm = ctx->comm->comm;
   QDPB_NCCL(ctx, g_nccl.GroupStart());
   for (int mu = 0; mu < 4; mu++) {
-    if (!face_bytes[mu] || ctx->pgrid[mu] == 1) continue;
+    if (!face_bytes[mu] || direct_self(ctx, mu)) continue;
     const size_t n = face_bytes[mu];
     QDPB_NCCL(ctx, g_nccl.Send(ctx->halo_send[prec][mu][1], n, ncclChar, ctx->neighbour[mu][1], cm, stream));
     QDPB_NCCL(ctx, g_nccl.Send(ctx->halo_send[prec][mu][0], n, ncclChar, ctx->neighbour[mu][0], cm, stream));

@@ -478,7 +478,7 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
     size_t face_bytes[4] = {0, 0, 0, 0};
     for (int mu = 0; mu < 4; mu++) {
       if (!((g.part >> mu) & 1)) continue;
-      const bool self = ctx->pgrid[mu] == 1;
+      const bool self = direct_self(ctx, mu);
       any_comm |= !self;
       face_bytes[mu] = (size_t)g.faceVh[mu] * 12 * sizeof(R);
       P.dst[mu][0] = self ? ctx->halo_recv[prec][mu][1] : ctx->halo_send[prec][mu][0];

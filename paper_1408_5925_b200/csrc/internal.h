@@ -376,7 +376,7 @@ struct qdp_ctx_s {
   bool own_stream = false;
   cudaEvent_t ev_packed = nullptr, ev_comm = nullptr;
   // options
-  int overlap = 1, self_halo = 0, profiling = 0, block = 0, det_reduce = 1;
+  int overlap = 1, self_halo = 0, profiling = 0, block = 0, det_reduce = 1, self_nccl = 0;
   // scratch (device)
   void *staging = nullptr;
   size_t staging_bytes = 0;
@@ -489,6 +489,12 @@ int comm_exchange(qdp_ctx ctx, int prec, const size_t face_bytes[4], cudaStream_
 int comm_sendrecv(qdp_ctx ctx, const void *send, size_t bytes, int to, void *recv, int from, cudaStream_t stream);
 int comm_allgather_f64(qdp_ctx ctx, const double *send, double *recv, int count, cudaStream_t stream);
 int comm_allreduce_f64(qdp_ctx ctx, double *buf, int count, cudaStream_t stream);
+
+// A partitioned dim whose neighbour is this rank and whose faces are written straight into
+// the local ghost buffers (self-halo without NCCL).
+inline bool direct_self(qdp_ctx ctx, int mu) { return ctx->pgrid[mu] == 1 && !ctx->self_nccl; }
+// create a one-rank NCCL communicator for QDP_OPT_SELF_NCCL (comm.cpp)
+int comm_ensure_self(qdp_ctx ctx);
 
 inline size_t fermion_block_bytes(int prec, int stride) { return (size_t)stride * (prec == QDP_F64 ? 12 * 16 : 6 * 16); }
 inline int grid_for(long n, int block) { return (int)((n + block - 1) / block); }

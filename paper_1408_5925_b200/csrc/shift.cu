@@ -73,7 +73,7 @@ int shift_field(qdp_ctx ctx, qdp_field out, const qdp_field in, int mu, int sign
     // scratch: [send | recv] in the staging buffer
     if ((rc = ensure_staging(ctx, 2 * bytes))) return rc;
     char *send = (char *)ctx->staging, *recv = send + bytes;
-    const bool self = ctx->pgrid[mu] == 1;
+    const bool self = direct_self(ctx, mu);
     // receiver needs in(x + sign mu) for its boundary sites: sign=+1 -> our x_mu=0 face goes to -mu
     const int xmu = sign > 0 ? 0 : g.L[mu] - 1;
     ProfEvent ev;
