@@ -59,7 +59,12 @@ typedef struct qdp_ctx_s *qdp_ctx;     /* one per process = one GPU: geometry, s
 typedef struct qdp_field_s *qdp_field; /* a lattice field on one context */
 
 enum { QDP_F64 = 0, QDP_F32 = 1 };                             /* precision */
-enum { QDP_FERMION = 0, QDP_GAUGE = 1, QDP_CLOVER = 2 };      /* kind */
+/* kind.  QDP_GAUGE12 is a gauge field stored as the first two rows of each link, the third
+ * rebuilt as conj(row0 x row1) on use ("reconstruction of SU(3) matrices from 12 real
+ * numbers"): same host layout as QDP_GAUGE; import rejects (QDP_EINVAL) links
+ * whose third row differs from conj(row0 x row1) by more than 1e-10 (F64) / 1e-5 (F32), and
+ * export returns the rebuilt third row.  Accepted wherever a QDP_GAUGE field is. */
+enum { QDP_FERMION = 0, QDP_GAUGE = 1, QDP_CLOVER = 2, QDP_GAUGE12 = 3 };
 enum { QDP_ALL = -1, QDP_EVEN = 0, QDP_ODD = 1 };             /* subset / parity */
 enum { QDP_FORWARD = +1, QDP_BACKWARD = -1 };                 /* shift direction */
 

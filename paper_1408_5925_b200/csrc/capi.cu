@@ -157,16 +157,16 @@ static void update_partition(qdp_ctx ctx) {
 
 static size_t field_device_bytes(qdp_ctx ctx, int kind, int prec, int subset) {
   const size_t blk = parity_block_bytes(kind, prec, ctx->geom.stride);
-  return (kind == KIND_GAUGE || subset == QDP_ALL) ? 2 * blk : blk;
+  return (is_gauge(kind) || subset == QDP_ALL) ? 2 * blk : blk;
 }
 static size_t field_host_bytes(qdp_ctx ctx, int kind, int prec, int subset) {
-  const long sites = (kind == KIND_GAUGE || subset == QDP_ALL) ? ctx->V : ctx->geom.Vh;
+  const long sites = (is_gauge(kind) || subset == QDP_ALL) ? ctx->V : ctx->geom.Vh;
   return (size_t)sites * host_site_reals(kind) * (prec == QDP_F64 ? 8 : 4);
 }
 
 }  // namespace qdpb
 
-static bool valid_kind(int k) { return k == QDP_FERMION || k == QDP_GAUGE || k == QDP_CLOVER; }
+static bool valid_kind(int k) { return k == QDP_FERMION || k == QDP_GAUGE || k == QDP_CLOVER || k == QDP_GAUGE12; }
 static bool valid_prec(int p) { return p == QDP_F64 || p == QDP_F32; }
 static bool valid_subset(int s) { return s == QDP_ALL || s == QDP_EVEN || s == QDP_ODD; }
 
@@ -352,7 +352,7 @@ extern "C" int qdp_get_option(qdp_ctx c, int opt, long *v) {
 // ---------------------------------------------------------------------------- fields
 extern "C" int qdp_field_bytes(qdp_ctx c, int kind, int prec, int subset, size_t *hb, size_t *db) {
   if (!c || !valid_kind(kind) || !valid_prec(prec) || !valid_subset(subset)) return QDP_EINVAL;
-  if (kind == QDP_GAUGE && subset != QDP_ALL) return set_error(c, QDP_EINVAL, "gauge fields are QDP_ALL");
+  if (is_gauge(kind) && subset != QDP_ALL) return set_error(c, QDP_EINVAL, "gauge fields are QDP_ALL");
   if (hb) *hb = field_host_bytes(c, kind, prec, subset);
   if (db) *db = field_device_bytes(c, kind, prec, subset);
   return QDP_OK;
@@ -451,7 +451,7 @@ extern "C" int qdp_field_zero(qdp_field f) {
 
 // parity block `par` of field f (nullptr if absent)
 static char *block_of(const qdp_field f, int par) {
-  if (f->kind == QDP_GAUGE) return nullptr;
+  if (is_gauge(f->kind)) return nullptr;
   const size_t blk = parity_block_bytes(f->kind, f->prec, f->ctx->geom.stride);
   if (f->subset == QDP_ALL) return (char *)f->data + par * blk;
   return f->subset == par ? (char *)f->data : nullptr;
@@ -470,7 +470,7 @@ extern "C" int qdp_field_copy(qdp_field dst, const qdp_field src) {
   qdp_ctx c = dst->ctx;
   if (dst->kind != src->kind) return set_error(c, QDP_EINVAL, "copy: kind mismatch");
   if (dst == src || dst->data == src->data) return QDP_OK;
-  if (dst->kind == QDP_GAUGE || dst->subset == src->subset) {
+  if (is_gauge(dst->kind) || dst->subset == src->subset) {
     QDP_CUDA(c, cudaMemcpyAsync(dst->data, src->data, field_device_bytes(c, dst->kind, dst->prec, dst->subset),
                                 cudaMemcpyDeviceToDevice, c->stream));
     return QDP_OK;
@@ -505,7 +505,7 @@ extern "C" int qdp_dslash(qdp_field out, const qdp_field U, const qdp_field psi,
   int rc;
   if ((rc = check_pair(out, psi)) || (rc = check_pair(out, U))) return rc;
   qdp_ctx c = out->ctx;
-  if (out->kind != QDP_FERMION || psi->kind != QDP_FERMION || U->kind != QDP_GAUGE)
+  if (out->kind != QDP_FERMION || psi->kind != QDP_FERMION || !is_gauge(U->kind))
     return set_error(c, QDP_EINVAL, "dslash: kinds (fermion, gauge, fermion)");
   if (!valid_subset(out_parity)) return set_error(c, QDP_EINVAL, "dslash: bad parity");
   if (out == psi || out->data == psi->data) return set_error(c, QDP_EALIAS, "dslash: out aliases psi");
@@ -519,6 +519,7 @@ extern "C" int qdp_dslash(qdp_field out, const qdp_field U, const qdp_field psi,
     a.out = block_of(out, p);
     a.psi = block_of(psi, 1 - p);
     a.U = U->data;
+    a.rec12 = U->kind == QDP_GAUGE12;
     a.parity = p;
     a.epi = EPI_PLAIN;
     a.b = 1.0;
@@ -571,7 +572,7 @@ extern "C" int qdp_clover_build(qdp_field A, qdp_field Ainv, const qdp_field U, 
   if (!U || (!A && !Ainv)) return QDP_EINVAL;
   qdp_ctx c = U->ctx;
   int rc;
-  if (U->kind != QDP_GAUGE) return set_error(c, QDP_EINVAL, "clover_build: U must be a gauge field");
+  if (!is_gauge(U->kind)) return set_error(c, QDP_EINVAL, "clover_build: U must be a gauge field");
   for (qdp_field f : {A, Ainv}) {
     if (!f) continue;
     if ((rc = check_pair(f, U))) return rc;
@@ -611,7 +612,7 @@ extern "C" int qdp_cg_solve(qdp_field x, const qdp_field b, const qdp_field U, c
   int rc;
   if ((rc = check_pair(x, b)) || (rc = check_pair(x, U))) return rc;
   qdp_ctx c = x->ctx;
-  if (x->kind != QDP_FERMION || b->kind != QDP_FERMION || U->kind != QDP_GAUGE)
+  if (x->kind != QDP_FERMION || b->kind != QDP_FERMION || !is_gauge(U->kind))
     return set_error(c, QDP_EINVAL, "cg: kinds (fermion, fermion, gauge)");
   if (x->subset != QDP_ALL || b->subset != QDP_ALL) return set_error(c, QDP_EINVAL, "cg: x and b must be QDP_ALL");
   if (x->data == b->data) return set_error(c, QDP_EALIAS, "cg: x aliases b");

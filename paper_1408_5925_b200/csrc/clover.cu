@@ -15,7 +15,7 @@
 namespace qdpb {
 
 struct M3 { double2 m[9]; };
-template <typename R> struct ShiftSet { GaugeView<R> s[7]; };
+template <typename R, int REC> struct ShiftSet { GaugeView<R, REC> s[7]; };
 
 __device__ __forceinline__ double2 c_add(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 c_sub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
@@ -45,12 +45,12 @@ __device__ __forceinline__ M3 m3_dag(const M3 &a) {
   return r;
 }
 
-template <typename R>
-__device__ __forceinline__ M3 link_at(const Geom &g, const GaugeView<R> &U, const int c0[4], int mu, int d1, int a, int d2, int b) {
+template <typename GV>
+__device__ __forceinline__ M3 link_at(const Geom &g, const GV &U, const int c0[4], int mu, int d1, int a, int d2, int b) {
   int c[4] = {c0[0], c0[1], c0[2], c0[3]};
   c[d1] = (c[d1] + a + g.L[d1]) % g.L[d1];
   c[d2] = (c[d2] + b + g.L[d2]) % g.L[d2];
-  Link<R> l = U.load(mu, coords_parity(c), coords_cb(g, c));
+  const auto l = U.load(mu, coords_parity(c), coords_cb(g, c));
   M3 r;
 #pragma unroll
   for (int k = 0; k < 9; k++) r.m[k] = make_double2((double)l.m[k].re, (double)l.m[k].im);
@@ -58,8 +58,8 @@ __device__ __forceinline__ M3 link_at(const Geom &g, const GaugeView<R> &U, cons
 }
 
 // Hermitian traceless F_mu,nu at c (reading R10)
-template <typename R>
-__device__ M3 field_strength(const Geom &g, const GaugeView<R> &U, const int c[4], int mu, int nu) {
+template <typename GV>
+__device__ M3 field_strength(const Geom &g, const GV &U, const int c[4], int mu, int nu) {
   M3 q, t;
   // U_mu(x) U_nu(x+mu) U_mu(x+nu)^dag U_nu(x)^dag
   q = m3_mul(m3_mul(link_at(g, U, c, mu, mu, 0, nu, 0), link_at(g, U, c, nu, mu, 1, nu, 0)),
@@ -200,8 +200,8 @@ __device__ void assemble_store(const Geom &g, const M3 F[6], int cb, char *A, ch
 }
 
 // Single-rank build: the leaves read their off-site links directly (periodic wrap).
-template <typename R>
-__global__ void __launch_bounds__(128) clover_build_kernel(const Geom g, GaugeView<R> U, int p, char *A, char *Ainv,
+template <typename R, int REC>
+__global__ void __launch_bounds__(128) clover_build_kernel(const Geom g, GaugeView<R, REC> U, int p, char *A, char *Ainv,
                                                            double mass, double csw, int *singular) {
   const int cb = blockIdx.x * blockDim.x + threadIdx.x;
   if (cb >= g.Vh) return;
@@ -220,21 +220,21 @@ __global__ void __launch_bounds__(128) clover_build_kernel(const Geom g, GaugeVi
 // S[k](x) = U(x + d_k), d = (+mu, +nu, -mu, -nu, -mu+nu, -mu-nu, +mu-nu), were formed with
 // qdp_shift (halo exchange included), so every leaf link is local to x.  Writes F_mu,nu of
 // both parities into Fbuf[plane][parity][9][stride] (fp64).
-template <typename R>
-__global__ void __launch_bounds__(128) clover_leaf_kernel(const Geom g, GaugeView<R> U, ShiftSet<R> S, int mu, int nu,
-                                                          int plane, double2 *Fbuf) {
+template <typename R, int REC>
+__global__ void __launch_bounds__(128) clover_leaf_kernel(const Geom g, GaugeView<R, REC> U, ShiftSet<R, REC> S, int mu,
+                                                          int nu, int plane, double2 *Fbuf) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= 2 * g.Vh) return;
   const int p = i / g.Vh, cb = i % g.Vh;
-  auto L = [&](const GaugeView<R> &G, int d) {
+  auto L = [&](const GaugeView<R, REC> &G, int d) {
     Link<R> l = G.load(d, p, cb);
     M3 r;
 #pragma unroll
     for (int k = 0; k < 9; k++) r.m[k] = make_double2((double)l.m[k].re, (double)l.m[k].im);
     return r;
   };
-  const GaugeView<R> &Pm = S.s[0], &Pn = S.s[1], &Mm = S.s[2], &Mn = S.s[3], &MmPn = S.s[4], &MmMn = S.s[5],
-                     &PmMn = S.s[6];
+  const GaugeView<R, REC> &Pm = S.s[0], &Pn = S.s[1], &Mm = S.s[2], &Mn = S.s[3], &MmPn = S.s[4], &MmMn = S.s[5],
+                          &PmMn = S.s[6];
   M3 q, t;
   q = m3_mul(m3_mul(L(U, mu), L(Pm, nu)), m3_mul(m3_dag(L(Pn, mu)), m3_dag(L(U, nu))));
   t = m3_mul(m3_mul(L(U, nu), m3_dag(L(MmPn, mu))), m3_mul(m3_dag(L(Mm, nu)), L(Mm, mu)));
@@ -284,17 +284,17 @@ __global__ void __launch_bounds__(128) clover_apply_kernel(const Geom g, FermVie
 }
 
 // Partitioned lattice: F_mu,nu from local leaves on shifted gauge fields (see clover_leaf_kernel).
-template <typename R>
+template <typename R, int REC>
 static int build_F_by_shifts(qdp_ctx ctx, const qdp_field U, double2 *Fbuf) {
   const Geom &g = ctx->geom;
   const int prec = U->prec;
-  const size_t gb = 2 * parity_block_bytes(KIND_GAUGE, prec, g.stride);
+  const size_t gb = 2 * parity_block_bytes(U->kind, prec, g.stride);
   char *tmp = nullptr;
   QDP_CUDA(ctx, cudaMallocAsync((void **)&tmp, 8 * gb, ctx->stream));
   qdp_field_s f[8];
   for (int k = 0; k < 8; k++) {
     f[k].ctx = ctx;
-    f[k].kind = KIND_GAUGE;
+    f[k].kind = U->kind;
     f[k].prec = prec;
     f[k].subset = QDP_ALL;
     f[k].data = tmp + k * gb;
@@ -312,12 +312,12 @@ static int build_F_by_shifts(qdp_ctx ctx, const qdp_field U, double2 *Fbuf) {
       if ((rc = shift_field(ctx, &f[4], &f[1], mu, -1))) break;  // U(x-mu+nu)  (shift of a shift)
       if ((rc = shift_field(ctx, &f[5], &f[3], mu, -1))) break;  // U(x-mu-nu)
       if ((rc = shift_field(ctx, &f[6], &f[3], mu, +1))) break;  // U(x+mu-nu)
-      ShiftSet<R> S;
-      for (int k = 0; k < 7; k++) S.s[k] = GaugeView<R>{(decltype(S.s[k].p))f[k].data, g.stride};
+      ShiftSet<R, REC> S;
+      for (int k = 0; k < 7; k++) S.s[k] = GaugeView<R, REC>{(decltype(S.s[k].p))f[k].data, g.stride};
       ProfEvent ev;
       prof_begin(ctx, QDP_PK_CLOVER, &ev);
-      clover_leaf_kernel<R><<<grid_for(2 * g.Vh, 128), 128, 0, ctx->stream>>>(
-          g, GaugeView<R>{(decltype(S.s[0].p))U->data, g.stride}, S, mu, nu, plane, Fbuf);
+      clover_leaf_kernel<R, REC><<<grid_for(2 * g.Vh, 128), 128, 0, ctx->stream>>>(
+          g, GaugeView<R, REC>{(decltype(S.s[0].p))U->data, g.stride}, S, mu, nu, plane, Fbuf);
       if ((rc = prof_end(ctx, &ev))) break;
     }
   cudaFreeAsync(tmp, ctx->stream);
@@ -335,7 +335,10 @@ int clover_build(qdp_ctx ctx, const qdp_field U, void *A, int A_subset, void *Ai
   int rc;
   if (g.part) {  // some neighbours live across a rank (or self-halo) boundary: shifts of shifts
     QDP_CUDA(ctx, cudaMallocAsync((void **)&Fbuf, (size_t)6 * 2 * 9 * g.stride * sizeof(double2), ctx->stream));
-    rc = prec == QDP_F64 ? build_F_by_shifts<double>(ctx, U, Fbuf) : build_F_by_shifts<float>(ctx, U, Fbuf);
+    if (U->kind == KIND_GAUGE12)
+      rc = prec == QDP_F64 ? build_F_by_shifts<double, 12>(ctx, U, Fbuf) : build_F_by_shifts<float, 12>(ctx, U, Fbuf);
+    else
+      rc = prec == QDP_F64 ? build_F_by_shifts<double, 18>(ctx, U, Fbuf) : build_F_by_shifts<float, 18>(ctx, U, Fbuf);
     if (rc) {
       cudaFreeAsync(Fbuf, ctx->stream);
       return rc;
@@ -353,10 +356,15 @@ int clover_build(qdp_ctx ctx, const qdp_field U, void *A, int A_subset, void *Ai
       if (prec == QDP_F64) clover_assemble_kernel<double><<<nb, 128, 0, ctx->stream>>>(g, Fbuf, p, a, ai, mass, csw, flag);
       else clover_assemble_kernel<float><<<nb, 128, 0, ctx->stream>>>(g, Fbuf, p, a, ai, mass, csw, flag);
     } else {
-      if (prec == QDP_F64)
-        clover_build_kernel<double><<<nb, 128, 0, ctx->stream>>>(g, {(const double2 *)U->data, g.stride}, p, a, ai, mass, csw, flag);
-      else
-        clover_build_kernel<float><<<nb, 128, 0, ctx->stream>>>(g, {(const float *)U->data, g.stride}, p, a, ai, mass, csw, flag);
+#define QDPB_CB(Rt, REC)                                                                                 \
+  clover_build_kernel<Rt, REC><<<nb, 128, 0, ctx->stream>>>(                                             \
+      g, GaugeView<Rt, REC>{(decltype(GaugeView<Rt, REC>::p))U->data, g.stride}, p, a, ai, mass, csw, flag)
+      if (U->kind == KIND_GAUGE12) {
+        if (prec == QDP_F64) QDPB_CB(double, 12); else QDPB_CB(float, 12);
+      } else {
+        if (prec == QDP_F64) QDPB_CB(double, 18); else QDPB_CB(float, 18);
+      }
+#undef QDPB_CB
     }
     if ((rc = prof_end(ctx, &ev))) return rc;
   }

@@ -142,9 +142,9 @@ __device__ __forceinline__ void g5(Spinor<R> &s) {
   for (int k = 6; k < 12; k++) s.c[k] = -s.c[k];
 }
 
-template <typename R> struct KParams {
+template <typename R, int REC = 18> struct KParams {
   FermView<R> out, psi, x;
-  GaugeView<R> U;
+  GaugeView<R, REC> U;
   CloverView<R> A;
   int parity;
   R a, b;
@@ -157,8 +157,8 @@ template <typename R> struct KParams {
   double *dot_part;
 };
 
-template <typename R, int MU>
-__device__ __forceinline__ void hop_dir(const Geom &g, const KParams<R> &P, const int c[4], int cb, int p,
+template <typename R, int MU, typename KP>
+__device__ __forceinline__ void hop_dir(const Geom &g, const KP &P, const int c[4], int cb, int p,
                                         bool G5IN, bool halo, Spinor<R> &acc) {
   // forward: (1 - gamma_mu) U_mu(x) psi(x + mu)
   {
@@ -189,8 +189,8 @@ __device__ __forceinline__ void hop_dir(const Geom &g, const KParams<R> &P, cons
   }
 }
 
-template <typename R, int EPI>
-__device__ __forceinline__ Spinor<R> epilogue(const KParams<R> &P, int cb, Spinor<R> &acc, bool G5OUT) {
+template <typename R, int EPI, typename KP>
+__device__ __forceinline__ Spinor<R> epilogue(const KP &P, int cb, Spinor<R> &acc, bool G5OUT) {
   if (G5OUT) g5(acc);
   Spinor<R> o;
   if (EPI == EPI_PLAIN) {
@@ -249,8 +249,8 @@ __device__ __forceinline__ void dot_block_partial(double v, double *part) {
 
 // Whole-lattice (HALO=false) or interior (HALO=true: remote hops skipped) kernel.
 // DOT: also accumulate Re<dot, out> per block into dot_part (fused inner product).
-template <typename R, int EPI, bool G5IN, bool G5OUT, bool HALO, bool DOT>
-__global__ void __launch_bounds__(QDPB_DSLASH_MAXT, QDPB_DSLASH_MINB) dslash_kernel(const Geom g, const KParams<R> P) {
+template <typename R, int REC, int EPI, bool G5IN, bool G5OUT, bool HALO, bool DOT>
+__global__ void __launch_bounds__(QDPB_DSLASH_MAXT, (dslash_minb<R, REC>())) dslash_kernel(const Geom g, const KParams<R, REC> P) {
   const int cb = blockIdx.x * blockDim.x + threadIdx.x;
   double dot = 0.0;
   if (cb < g.Vh) {
@@ -274,8 +274,8 @@ __global__ void __launch_bounds__(QDPB_DSLASH_MAXT, QDPB_DSLASH_MINB) dslash_ker
 // Face packing for dim MU: input psi has parity q = 1 - p.
 //   f <  faceVh: my sites at x_mu = 0      -> P^- psi          -> dst[mu][0] (the -mu neighbour's forward ghost)
 //   f >= faceVh: my sites at x_mu = L-1    -> U_mu^dag P^+ psi  -> dst[mu][1] (the +mu neighbour's backward ghost)
-template <typename R, bool G5IN>
-__global__ void __launch_bounds__(128) pack_kernel(const Geom g, const KParams<R> P, int mu) {
+template <typename R, int REC, bool G5IN>
+__global__ void __launch_bounds__(128) pack_kernel(const Geom g, const KParams<R, REC> P, int mu) {
   const int n = g.faceVh[mu];
   int f = blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= 2 * n) return;
@@ -311,8 +311,8 @@ __global__ void __launch_bounds__(128) pack_kernel(const Geom g, const KParams<R
 // Exterior: add the remote hops of dim mu for the output sites on its two faces.  With DOT,
 // Re<dotx, increment> is accumulated: by linearity the interior's partial plus these give
 // Re<dotx, out> of the final output.
-template <typename R, int EPI, bool G5OUT, bool DOT>
-__global__ void __launch_bounds__(128) exterior_kernel(const Geom g, const KParams<R> P, int mu, double *dot_part) {
+template <typename R, int REC, int EPI, bool G5OUT, bool DOT>
+__global__ void __launch_bounds__(128) exterior_kernel(const Geom g, const KParams<R, REC> P, int mu, double *dot_part) {
   const int n = g.faceVh[mu];
   int f = blockIdx.x * blockDim.x + threadIdx.x;
   double dot = 0.0;
@@ -362,29 +362,30 @@ __global__ void __launch_bounds__(128) exterior_kernel(const Geom g, const KPara
 template <typename R> static FermView<R> fview(const void *p, int stride);
 template <> FermView<double> fview<double>(const void *p, int stride) { return {(double2 *)p, stride}; }
 template <> FermView<float> fview<float>(const void *p, int stride) { return {(float4 *)p, stride}; }
-template <typename R> static GaugeView<R> gview(const void *p, int stride);
-template <> GaugeView<double> gview<double>(const void *p, int stride) { return {(const double2 *)p, stride}; }
-template <> GaugeView<float> gview<float>(const void *p, int stride) { return {(const float *)p, stride}; }
+template <typename R, int REC> static GaugeView<R, REC> gview(const void *p, int stride) {
+  return {(decltype(GaugeView<R, REC>::p))p, stride};
+}
 template <typename R> static CloverView<R> cview(const void *p, int stride);
 template <> CloverView<double> cview<double>(const void *p, int stride) { return {(const double2 *)p, stride}; }
 template <> CloverView<float> cview<float>(const void *p, int stride) { return {(const float4 *)p, stride}; }
 
-template <typename R, int EPI, bool G5IN, bool G5OUT, bool HALO, bool DOT>
-static void launch_main(qdp_ctx ctx, const KParams<R> &P, int block) {
+template <typename R, int REC, int EPI, bool G5IN, bool G5OUT, bool HALO, bool DOT>
+static void launch_main(qdp_ctx ctx, const KParams<R, REC> &P, int block) {
   const Geom &g = ctx->geom;
-  dslash_kernel<R, EPI, G5IN, G5OUT, HALO, DOT><<<grid_for(g.Vh, block), block, 0, ctx->stream>>>(g, P);
+  dslash_kernel<R, REC, EPI, G5IN, G5OUT, HALO, DOT><<<grid_for(g.Vh, block), block, 0, ctx->stream>>>(g, P);
 }
 
-template <typename R, int EPI>
-static void launch_main_dispatch(qdp_ctx ctx, const KParams<R> &P, bool g5i, bool g5o, bool halo, bool dot, int block) {
+template <typename R, int REC, int EPI>
+static void launch_main_dispatch(qdp_ctx ctx, const KParams<R, REC> &P, bool g5i, bool g5o, bool halo, bool dot,
+                                 int block) {
   if (dot) {  // fused inner product: only the Mhat^dag output step (g5_out, no g5_in) uses it
     if constexpr (EPI == EPI_XPAY || EPI == EPI_CLOVXPAY) {
-      if (halo) launch_main<R, EPI, false, true, true, true>(ctx, P, block);
-      else launch_main<R, EPI, false, true, false, true>(ctx, P, block);
+      if (halo) launch_main<R, REC, EPI, false, true, true, true>(ctx, P, block);
+      else launch_main<R, REC, EPI, false, true, false, true>(ctx, P, block);
     }
     return;
   }
-#define QDPB_L(A, B, C) launch_main<R, EPI, A, B, C, false>(ctx, P, block)
+#define QDPB_L(A, B, C) launch_main<R, REC, EPI, A, B, C, false>(ctx, P, block)
   if (halo) {
     if (g5i) { if (g5o) QDPB_L(true, true, true); else QDPB_L(true, false, true); }
     else { if (g5o) QDPB_L(false, true, true); else QDPB_L(false, false, true); }
@@ -395,22 +396,22 @@ static void launch_main_dispatch(qdp_ctx ctx, const KParams<R> &P, bool g5i, boo
 #undef QDPB_L
 }
 
-template <typename R, int EPI>
-static void launch_ext(qdp_ctx ctx, const KParams<R> &P, int mu, bool g5o, double *dot_part) {
+template <typename R, int REC, int EPI>
+static void launch_ext(qdp_ctx ctx, const KParams<R, REC> &P, int mu, bool g5o, double *dot_part) {
   const Geom &g = ctx->geom;
   const int n = 2 * g.faceVh[mu];
-  if (dot_part) exterior_kernel<R, EPI, true, true><<<grid_for(n, 128), 128, 0, ctx->stream>>>(g, P, mu, dot_part);
-  else if (g5o) exterior_kernel<R, EPI, true, false><<<grid_for(n, 128), 128, 0, ctx->stream>>>(g, P, mu, nullptr);
-  else exterior_kernel<R, EPI, false, false><<<grid_for(n, 128), 128, 0, ctx->stream>>>(g, P, mu, nullptr);
+  if (dot_part) exterior_kernel<R, REC, EPI, true, true><<<grid_for(n, 128), 128, 0, ctx->stream>>>(g, P, mu, dot_part);
+  else if (g5o) exterior_kernel<R, REC, EPI, true, false><<<grid_for(n, 128), 128, 0, ctx->stream>>>(g, P, mu, nullptr);
+  else exterior_kernel<R, REC, EPI, false, false><<<grid_for(n, 128), 128, 0, ctx->stream>>>(g, P, mu, nullptr);
 }
 
 // Algorithmic work of one EO dslash launch: 1320 flop per output
 // site for the hopping term (8 x (12 projection + 132 SU(3) x half spinor) + 7 x 24
 // accumulate) plus the epilogue; compulsory bytes 8 links + input + output (+ x, + clover,
 // + the fused inner product's second vector).
-template <typename R>
+template <typename R, int REC>
 static void dslash_work(qdp_ctx ctx, const DslashArgs &a) {
-  double f = 1320, r = 8 * 18 + 24 + 24;
+  double f = 1320, r = 8 * REC + 24 + 24;
   switch (a.epi) {
     case EPI_PLAIN: f += a.b != 1.0 ? 24 : 0; break;
     case EPI_XPAY: f += 72; r += 24; break;
@@ -422,30 +423,30 @@ static void dslash_work(qdp_ctx ctx, const DslashArgs &a) {
   prof_work(ctx, QDP_PK_DSLASH, f * vh, r * vh * sizeof(R));
 }
 
-template <typename R>
-static int launch_main_epi(qdp_ctx ctx, const DslashArgs &a, const KParams<R> &P, bool halo, int block) {
+template <typename R, int REC>
+static int launch_main_epi(qdp_ctx ctx, const DslashArgs &a, const KParams<R, REC> &P, bool halo, int block) {
   ProfEvent ev;
   prof_begin(ctx, QDP_PK_DSLASH, &ev);
-  dslash_work<R>(ctx, a);
+  dslash_work<R, REC>(ctx, a);
   const bool dot = a.dot_x != nullptr;
   switch (a.epi) {
-    case EPI_PLAIN: launch_main_dispatch<R, EPI_PLAIN>(ctx, P, a.g5_in, a.g5_out, halo, false, block); break;
-    case EPI_XPAY: launch_main_dispatch<R, EPI_XPAY>(ctx, P, a.g5_in, a.g5_out, halo, dot, block); break;
-    case EPI_CLOVINV: launch_main_dispatch<R, EPI_CLOVINV>(ctx, P, a.g5_in, a.g5_out, halo, false, block); break;
-    default: launch_main_dispatch<R, EPI_CLOVXPAY>(ctx, P, a.g5_in, a.g5_out, halo, dot, block); break;
+    case EPI_PLAIN: launch_main_dispatch<R, REC, EPI_PLAIN>(ctx, P, a.g5_in, a.g5_out, halo, false, block); break;
+    case EPI_XPAY: launch_main_dispatch<R, REC, EPI_XPAY>(ctx, P, a.g5_in, a.g5_out, halo, dot, block); break;
+    case EPI_CLOVINV: launch_main_dispatch<R, REC, EPI_CLOVINV>(ctx, P, a.g5_in, a.g5_out, halo, false, block); break;
+    default: launch_main_dispatch<R, REC, EPI_CLOVXPAY>(ctx, P, a.g5_in, a.g5_out, halo, dot, block); break;
   }
   return prof_end(ctx, &ev);
 }
 
-template <typename R>
+template <typename R, int REC>
 static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
   const Geom &g = ctx->geom;
   const int prec = sizeof(R) == 8 ? QDP_F64 : QDP_F32;
-  KParams<R> P = {};
+  KParams<R, REC> P = {};
   P.out = fview<R>(a.out, g.stride);
   P.psi = fview<R>(a.psi, g.stride);
   P.x = fview<R>(a.x, g.stride);
-  P.U = gview<R>(a.U, g.stride);
+  P.U = gview<R, REC>(a.U, g.stride);
   P.A = cview<R>(a.clov, g.stride);
   P.parity = a.parity;
   P.a = (R)a.a;
@@ -491,10 +492,10 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
       ProfEvent ev;
       prof_begin(ctx, QDP_PK_PACK, &ev);
       // compulsory: psi read on both faces, the forward face's link, the half spinors written
-      prof_work(ctx, QDP_PK_PACK, 0.0, (double)g.faceVh[mu] * (24 + 12 + 24 + 18 + 12) * sizeof(R));
+      prof_work(ctx, QDP_PK_PACK, 0.0, (double)g.faceVh[mu] * (24 + 12 + 24 + REC + 12) * sizeof(R));
       const int n = 2 * g.faceVh[mu];
-      if (a.g5_in) pack_kernel<R, true><<<grid_for(n, 128), 128, 0, ctx->stream>>>(g, P, mu);
-      else pack_kernel<R, false><<<grid_for(n, 128), 128, 0, ctx->stream>>>(g, P, mu);
+      if (a.g5_in) pack_kernel<R, REC, true><<<grid_for(n, 128), 128, 0, ctx->stream>>>(g, P, mu);
+      else pack_kernel<R, REC, false><<<grid_for(n, 128), 128, 0, ctx->stream>>>(g, P, mu);
       if ((rc = prof_end(ctx, &ev))) return rc;
     }
     const bool overlap = ctx->overlap && any_comm;
@@ -508,7 +509,7 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
         if ((rc = comm_exchange(ctx, prec, face_bytes, ctx->stream))) return rc;
       }
     }
-    if ((rc = launch_main_epi<R>(ctx, a, P, true, block))) return rc;
+    if ((rc = launch_main_epi<R, REC>(ctx, a, P, true, block))) return rc;
     if (overlap) QDP_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_comm, 0));
     for (int mu = 0; mu < 4; mu++) {
       if (!((g.part >> mu) & 1)) continue;
@@ -516,15 +517,15 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
       prof_begin(ctx, QDP_PK_DSLASH_EXT, &ev);
       // ghost read, forward-face link, output read-modify-write (+ clover on CLOVINV)
       prof_work(ctx, QDP_PK_DSLASH_EXT, 0.0,
-                (double)g.faceVh[mu] * (2 * 12 + 18 + 2 * 48 + (a.epi == EPI_CLOVINV ? 2 * 72 : 0) + (dot ? 48 : 0)) *
+                (double)g.faceVh[mu] * (2 * 12 + REC + 2 * 48 + (a.epi == EPI_CLOVINV ? 2 * 72 : 0) + (dot ? 48 : 0)) *
                     sizeof(R));
       double *dp = dot ? ctx->red_partials + 2 * ext_off[mu] : nullptr;
-      if (a.epi == EPI_CLOVINV) launch_ext<R, EPI_CLOVINV>(ctx, P, mu, a.g5_out, nullptr);
-      else launch_ext<R, EPI_PLAIN>(ctx, P, mu, a.g5_out, dp);
+      if (a.epi == EPI_CLOVINV) launch_ext<R, REC, EPI_CLOVINV>(ctx, P, mu, a.g5_out, nullptr);
+      else launch_ext<R, REC, EPI_PLAIN>(ctx, P, mu, a.g5_out, dp);
       if ((rc = prof_end(ctx, &ev))) return rc;
     }
   } else {
-    if ((rc = launch_main_epi<R>(ctx, a, P, false, block))) return rc;
+    if ((rc = launch_main_epi<R, REC>(ctx, a, P, false, block))) return rc;
   }
   if (dot) {
     if ((rc = reduce_partials(ctx, nparts, a.dot_slot))) return rc;
@@ -534,7 +535,8 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
 }
 
 int dslash(qdp_ctx ctx, int prec, const DslashArgs &a) {
-  return prec == QDP_F64 ? dslash_t<double>(ctx, a) : dslash_t<float>(ctx, a);
+  if (a.rec12) return prec == QDP_F64 ? dslash_t<double, 12>(ctx, a) : dslash_t<float, 12>(ctx, a);
+  return prec == QDP_F64 ? dslash_t<double, 18>(ctx, a) : dslash_t<float, 18>(ctx, a);
 }
 
 }  // namespace qdpb

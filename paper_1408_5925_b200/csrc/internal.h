@@ -27,6 +27,22 @@
 #ifndef QDPB_DSLASH_MINB
 #define QDPB_DSLASH_MINB 6
 #endif
+// per (precision, gauge storage) overrides of the minimum resident blocks
+#ifndef QDPB_MINB_D18
+#define QDPB_MINB_D18 QDPB_DSLASH_MINB
+#endif
+#ifndef QDPB_MINB_D12
+#define QDPB_MINB_D12 QDPB_DSLASH_MINB
+#endif
+#ifndef QDPB_MINB_F18
+#define QDPB_MINB_F18 QDPB_DSLASH_MINB
+#endif
+#ifndef QDPB_MINB_F12
+#define QDPB_MINB_F12 8  // fp32 + reconstruct-12: 128 registers, measured 110 -> 101 us at 40^3x32
+#endif
+template <typename R, int REC> constexpr int dslash_minb() {
+  return sizeof(R) == 8 ? (REC == 18 ? QDPB_MINB_D18 : QDPB_MINB_D12) : (REC == 18 ? QDPB_MINB_F18 : QDPB_MINB_F12);
+}
 #ifndef QDPB_DSLASH_BLOCK
 #define QDPB_DSLASH_BLOCK 64
 #endif
@@ -229,8 +245,19 @@ template <> struct FermView<float> {
 };
 
 // Gauge field: base of the whole field; link (mu, parity, cb).
-template <typename R> struct GaugeView;
-template <> struct GaugeView<double> {
+// Gauge field views.  REC = 18: full 3x3 links.  REC = 12 (QDP_GAUGE12): the first two rows
+// are stored and the third is rebuilt as conj(row0 x row1), exact for SU(3) links
+// (the "reconstruction from 12 real numbers" of PAPER.md:292).
+template <typename R> __device__ __forceinline__ void su3_third_row(Link<R> &u) {
+#pragma unroll
+  for (int a = 0; a < 3; a++) {
+    const int b = (a + 1) % 3, c = (a + 2) % 3;
+    const cx<R> t = cmul(u.m[b], u.m[3 + c]) - cmul(u.m[c], u.m[3 + b]);
+    u.m[6 + a] = {t.re, -t.im};
+  }
+}
+template <typename R, int REC = 18> struct GaugeView;
+template <> struct GaugeView<double, 18> {
   const double2 *p;
   int stride;
   __device__ __forceinline__ const double2 *block(int mu, int par) const { return p + (size_t)(mu * 2 + par) * 9 * stride; }
@@ -245,7 +272,38 @@ template <> struct GaugeView<double> {
     return u;
   }
 };
-template <> struct GaugeView<float> {
+template <> struct GaugeView<double, 12> {
+  const double2 *p;  // double2 [mu][parity][6][stride]
+  int stride;
+  __device__ __forceinline__ Link<double> load(int mu, int par, int cb) const {
+    const double2 *b = p + (size_t)(mu * 2 + par) * 6 * stride;
+    Link<double> u;
+#pragma unroll
+    for (int k = 0; k < 6; k++) {
+      double2 v = ld_stream(b + (size_t)k * stride + cb);
+      u.m[k] = {v.x, v.y};
+    }
+    su3_third_row(u);
+    return u;
+  }
+};
+template <> struct GaugeView<float, 12> {
+  const float4 *p;  // float4 [mu][parity][3][stride]
+  int stride;
+  __device__ __forceinline__ Link<float> load(int mu, int par, int cb) const {
+    const float4 *b = p + (size_t)(mu * 2 + par) * 3 * stride;
+    Link<float> u;
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+      float4 v = ld_stream(b + (size_t)k * stride + cb);
+      u.m[2 * k] = {v.x, v.y};
+      u.m[2 * k + 1] = {v.z, v.w};
+    }
+    su3_third_row(u);
+    return u;
+  }
+};
+template <> struct GaugeView<float, 18> {
   const float *p;  // byte layout: per (mu,par) block of stride*(4*16+8) bytes
   int stride;
   __device__ __forceinline__ Link<float> load(int mu, int par, int cb) const {
@@ -345,7 +403,8 @@ __device__ __forceinline__ Spinor<R> clover_mul(const CloverView<R> &A, int cb, 
 #endif  // __CUDACC__
 
 // ------------------------------------------------------------------ host-side objects
-enum { KIND_FERMION = QDP_FERMION, KIND_GAUGE = QDP_GAUGE, KIND_CLOVER = QDP_CLOVER };
+enum { KIND_FERMION = QDP_FERMION, KIND_GAUGE = QDP_GAUGE, KIND_CLOVER = QDP_CLOVER, KIND_GAUGE12 = QDP_GAUGE12 };
+inline bool is_gauge(int kind) { return kind == KIND_GAUGE || kind == KIND_GAUGE12; }
 
 size_t parity_block_bytes(int kind, int prec, int stride);  // bytes of one parity block
 size_t host_site_reals(int kind);                           // 24 / 72 / 288
@@ -464,6 +523,7 @@ struct DslashArgs {
   bool g5_in, g5_out;
   const void *dot_x;      // if set: red_result[dot_slot] = Re<dot_x, out> (global), [dot_slot+1] = 0
   int dot_slot;
+  bool rec12;             // U is a QDP_GAUGE12 field
 };
 int dslash(qdp_ctx ctx, int prec, const DslashArgs &a);
 

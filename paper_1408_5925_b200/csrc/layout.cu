@@ -7,11 +7,12 @@
 
 namespace qdpb {
 
-size_t host_site_reals(int kind) { return kind == KIND_FERMION ? 24 : kind == KIND_GAUGE ? 72 : 288; }
+size_t host_site_reals(int kind) { return kind == KIND_FERMION ? 24 : is_gauge(kind) ? 72 : 288; }
 
 size_t parity_block_bytes(int kind, int prec, int stride) {
   if (kind == KIND_FERMION) return fermion_block_bytes(prec, stride);
   if (kind == KIND_GAUGE) return (size_t)4 * stride * (prec == QDP_F64 ? 9 * 16 : 72);  // 4 mu per parity
+  if (kind == KIND_GAUGE12) return (size_t)4 * stride * (prec == QDP_F64 ? 6 * 16 : 3 * 16);
   return (size_t)stride * (prec == QDP_F64 ? 36 * 16 : 18 * 16);
 }
 
@@ -28,6 +29,16 @@ SlotMap make_slot_map(int kind, int prec, int stride, int subset) {
         else { m.off[p][k] = base < 0 ? -1 : base + (long long)((k / 2) * S * 16 + (k & 1) * 8); m.step[k] = 16; }
       }
     }
+  } else if (kind == KIND_GAUGE12) {  // slot = mu*6 + e (rows 0,1)
+    m.n = 24;
+    for (int p = 0; p < 2; p++)
+      for (int mu = 0; mu < 4; mu++)
+        for (int e = 0; e < 6; e++) {
+          const int k = mu * 6 + e;
+          m.step[k] = 16;
+          if (prec == QDP_F64) m.off[p][k] = (long long)(((mu * 2 + p) * 6 + e) * S * 16);
+          else m.off[p][k] = (long long)(((mu * 2 + p) * 3 + e / 2) * S * 16 + (e & 1) * 8);
+        }
   } else {  // gauge: slot = mu*9 + e
     m.n = 36;
     for (int p = 0; p < 2; p++)
@@ -127,6 +138,42 @@ __global__ void clover_kernel(const Geom g, int subset, long nrec, char *data, s
   }
 }
 
+// QDP_GAUGE12: import keeps rows 0,1 of every link and flags links whose row 2 is not
+// conj(row0 x row1) within tol (the compressed field would be wrong); export rebuilds row 2.
+template <typename R, bool IMPORT>
+__global__ void gauge12_kernel(const Geom g, const SlotMap m, long nrec, char *data, R *aos, double tol, int *bad) {
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nrec) return;
+  int p, cb;
+  record_site(g, QDP_ALL, i, p, cb);
+  for (int mu = 0; mu < 4; mu++) {
+    R *rec = aos + (i * 4 + mu) * 18;
+    double re[6], im[6];
+    for (int e = 0; e < 6; e++) {
+      R *d = (R *)(data + m.off[p][mu * 6 + e] + (long long)cb * m.step[mu * 6 + e]);
+      if (IMPORT) { d[0] = rec[2 * e]; d[1] = rec[2 * e + 1]; }
+      re[e] = IMPORT ? (double)rec[2 * e] : (double)d[0];
+      im[e] = IMPORT ? (double)rec[2 * e + 1] : (double)d[1];
+    }
+    double dev = 0.0;
+    for (int a = 0; a < 3; a++) {
+      const int b = (a + 1) % 3, c = (a + 2) % 3;
+      // conj(r0[b] r1[c] - r0[c] r1[b])
+      const double tr = re[b] * re[3 + c] - im[b] * im[3 + c] - (re[c] * re[3 + b] - im[c] * im[3 + b]);
+      const double ti = re[b] * im[3 + c] + im[b] * re[3 + c] - (re[c] * im[3 + b] + im[c] * re[3 + b]);
+      if (IMPORT) {
+        dev = fmax(dev, fabs((double)rec[12 + 2 * a] - tr));
+        dev = fmax(dev, fabs((double)rec[13 + 2 * a] + ti));
+      } else {
+        for (int e = 0; e < 6; e++) { rec[2 * e] = (R)re[e]; rec[2 * e + 1] = (R)im[e]; }
+        rec[12 + 2 * a] = (R)tr;
+        rec[13 + 2 * a] = (R)(-ti);
+      }
+    }
+    if (IMPORT && !(dev <= tol)) atomicExch(bad, 1);
+  }
+}
+
 static int layout_run(qdp_field f, void *dev_aos, bool import) {
   qdp_ctx ctx = f->ctx;
   const Geom &g = ctx->geom;
@@ -135,6 +182,26 @@ static int layout_run(qdp_field f, void *dev_aos, bool import) {
   ProfEvent ev;
   prof_begin(ctx, QDP_PK_LAYOUT, &ev);
   prof_work(ctx, QDP_PK_LAYOUT, 0.0, 2.0 * nrec * host_site_reals(f->kind) * (f->prec == QDP_F64 ? 8 : 4));
+  if (f->kind == KIND_GAUGE12) {
+    int *bad = (int *)(ctx->red_result + 60);
+    QDP_CUDA(ctx, cudaMemsetAsync(bad, 0, sizeof(int), ctx->stream));
+    SlotMap m = make_slot_map(f->kind, f->prec, g.stride, QDP_ALL);
+    const double tol = f->prec == QDP_F64 ? 1e-10 : 1e-5;
+    if (f->prec == QDP_F64) {
+      if (import) gauge12_kernel<double, true><<<blocks, 128, 0, ctx->stream>>>(g, m, nrec, (char *)f->data, (double *)dev_aos, tol, bad);
+      else gauge12_kernel<double, false><<<blocks, 128, 0, ctx->stream>>>(g, m, nrec, (char *)f->data, (double *)dev_aos, tol, bad);
+    } else {
+      if (import) gauge12_kernel<float, true><<<blocks, 128, 0, ctx->stream>>>(g, m, nrec, (char *)f->data, (float *)dev_aos, tol, bad);
+      else gauge12_kernel<float, false><<<blocks, 128, 0, ctx->stream>>>(g, m, nrec, (char *)f->data, (float *)dev_aos, tol, bad);
+    }
+    int rc = prof_end(ctx, &ev);
+    if (rc || !import) return rc;
+    int h = 0;
+    QDP_CUDA(ctx, cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    QDP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    if (h) return set_error(ctx, QDP_EINVAL, "import: QDP_GAUGE12 needs SU(3) links (row 2 = conj(row0 x row1))");
+    return QDP_OK;
+  }
   if (f->kind == KIND_CLOVER) {
     const size_t blk = parity_block_bytes(KIND_CLOVER, f->prec, g.stride);
     if (f->prec == QDP_F64) {

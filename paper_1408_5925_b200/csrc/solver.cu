@@ -24,6 +24,7 @@ struct Op {
   qdp_ctx ctx;
   int prec;
   const void *U;
+  bool rec12;          // U is QDP_GAUGE12
   const void *A_o;     // clover A on odd sites (nullptr: Wilson)
   const void *Ainv_e;  // clover A^-1 on even sites
   double diag;         // 4 + m
@@ -35,6 +36,7 @@ int apply_mhat(const Op &op, void *out, const void *v, bool dag, const void *dot
   DslashArgs a = {};
   int rc;
   a.U = op.U;
+  a.rec12 = op.rec12;
   // t_e = [A_ee^-1] H_eo [g5] v
   a.out = op.t;
   a.psi = v;
@@ -51,6 +53,7 @@ int apply_mhat(const Op &op, void *out, const void *v, bool dag, const void *dot
   // out_o = A_oo v - 1/4 [g5] H_oe t   (Wilson: (4+m) v - 1/(4(4+m)) [g5] H_oe t)
   DslashArgs c = {};
   c.U = op.U;
+  c.rec12 = op.rec12;
   c.out = out;
   c.psi = op.t;
   c.x = v;
@@ -85,6 +88,7 @@ int cg_solve(qdp_field x, const qdp_field b, const qdp_field U, const qdp_field 
   op.ctx = ctx;
   op.prec = prec;
   op.U = U->data;
+  op.rec12 = U->kind == QDP_GAUGE12;
   op.A_o = clover ? (const char *)A->data + (A->subset == QDP_ALL ? cbk : 0) : nullptr;
   op.Ainv_e = clover ? Ainv->data : nullptr;
   op.diag = 4.0 + mass;
@@ -117,6 +121,7 @@ int cg_solve(qdp_field x, const qdp_field b, const qdp_field U, const qdp_field 
   {
     DslashArgs a = {};
     a.U = op.U;
+    a.rec12 = op.rec12;
     a.out = bh;
     a.psi = op.t;
     a.x = b_o;
@@ -168,6 +173,7 @@ int cg_solve(qdp_field x, const qdp_field b, const qdp_field U, const qdp_field 
   {
     DslashArgs a = {};
     a.U = op.U;
+    a.rec12 = op.rec12;
     a.out = x_e;
     a.psi = x_o;
     a.x = b_e;
@@ -191,6 +197,7 @@ int cg_solve(qdp_field x, const qdp_field b, const qdp_field U, const qdp_field 
     for (int par = 0; par < 2; par++) {
       DslashArgs a = {};
       a.U = op.U;
+      a.rec12 = op.rec12;
       a.out = tmp + par * blk;
       a.psi = par == 0 ? x_o : x_e;
       a.x = par == 0 ? x_e : x_o;

@@ -18,7 +18,7 @@ LIB_PATH = os.environ.get("QDPB_LIB") or os.path.join(_HERE, "libqdpb.so")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "qdpb.h")
 
 QDP_F64, QDP_F32 = 0, 1
-QDP_FERMION, QDP_GAUGE, QDP_CLOVER = 0, 1, 2
+QDP_FERMION, QDP_GAUGE, QDP_CLOVER, QDP_GAUGE12 = 0, 1, 2, 3
 QDP_ALL, QDP_EVEN, QDP_ODD = -1, 0, 1
 QDP_FORWARD, QDP_BACKWARD = 1, -1
 QDP_OK, QDP_NOT_CONVERGED = 0, 1
@@ -246,7 +246,7 @@ def qdp_field_import(f: Field, host) -> None:
 
 def _host_shape(f: Field):
     hb, _ = qdp_field_bytes(f.ctx, f.kind, f.prec, f.subset)
-    per = {QDP_FERMION: (4, 3, 2), QDP_GAUGE: (4, 3, 3, 2), QDP_CLOVER: (12, 12, 2)}[f.kind]
+    per = {QDP_FERMION: (4, 3, 2), QDP_GAUGE: (4, 3, 3, 2), QDP_CLOVER: (12, 12, 2), QDP_GAUGE12: (4, 3, 3, 2)}[f.kind]
     isz = 8 if f.prec == QDP_F64 else 4
     n = hb // (isz * int(np.prod(per)))
     return (n,) + per, (np.float64 if f.prec == QDP_F64 else np.float32)

@@ -1,4 +1,7 @@
-"""Build tuning variants of libqdpb.so into variants/ (development aid)."""
+"""Build tuning variants of libqdpb.so into variants/ (development aid).
+
+  python tools/build_variants.py [name ...]
+Each variant is the same source compiled with extra -D tuning macros (see internal.h)."""
 import os
 import sys
 
@@ -8,10 +11,11 @@ from paper_1408_5925_b200 import build as b  # noqa: E402
 
 VARIANTS = {
     "base": [],
-    "b128m3": ["-DQDPB_DSLASH_MAXT=128", "-DQDPB_DSLASH_MINB=3"],
-    "b128m4": ["-DQDPB_DSLASH_MAXT=128", "-DQDPB_DSLASH_MINB=4"],
-    "b256m2": ["-DQDPB_DSLASH_MAXT=256", "-DQDPB_DSLASH_MINB=2", "-DQDPB_DSLASH_BLOCK=256"],
-    "b64m6": ["-DQDPB_DSLASH_MAXT=64", "-DQDPB_DSLASH_MINB=6", "-DQDPB_DSLASH_BLOCK=64"],
+    # occupancy sweeps per (precision, gauge storage): min resident 64-thread blocks per SM
+    "occ_a": ["-DQDPB_MINB_D12=7", "-DQDPB_MINB_F18=8", "-DQDPB_MINB_F12=8"],
+    "occ_b": ["-DQDPB_MINB_D12=8", "-DQDPB_MINB_F18=10", "-DQDPB_MINB_F12=10"],
+    "occ_c": ["-DQDPB_MINB_D12=5", "-DQDPB_MINB_F18=12", "-DQDPB_MINB_F12=12"],
+    "occ_d": ["-DQDPB_MINB_D12=4", "-DQDPB_MINB_F18=16", "-DQDPB_MINB_F12=16"],
 }
 names = sys.argv[1:] or list(VARIANTS)
 for n in names:

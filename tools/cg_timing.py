@@ -11,10 +11,11 @@ from paper_1408_5925_b200 import qdpb as q  # noqa: E402
 
 L = tuple(int(v) for v in (sys.argv[1] if len(sys.argv) > 1 else "40,40,40,32").split(","))
 clover = "--wilson" not in sys.argv
+GK = q.QDP_GAUGE12 if "--recon12" in sys.argv else q.QDP_GAUGE
 U = fieldgen.random_gauge(L, 1004)
 b = fieldgen.random_spinor(L, 2005)
 c = q.qdp_init(L)
-fU = q.qdp_field_alloc(c, q.QDP_GAUGE, 0, q.QDP_ALL)
+fU = q.qdp_field_alloc(c, GK, 0, q.QDP_ALL)
 fb = q.qdp_field_alloc(c, q.QDP_FERMION, 0, q.QDP_ALL)
 fx = q.qdp_field_alloc(c, q.QDP_FERMION, 0, q.QDP_ALL)
 q.qdp_field_import(fU, U)

@@ -1,5 +1,5 @@
-for v in base b128m3 b128m4 b256m2 b64m6; do
+for v in base occ_a occ_b occ_c occ_d; do
   echo "=== $v" >> gpurun_out/variants.log
-  QDPB_LIB=variants/libqdpb_$v.so python tools/quick_bench.py >> gpurun_out/variants.log 2>&1
-  QDPB_LIB=variants/libqdpb_$v.so python tools/cg_timing.py >> gpurun_out/variants.log 2>&1
+  for r in 18 12; do QDPB_LIB=variants/libqdpb_$v.so python tools/quick_bench.py --recon $r --iters 30 >> gpurun_out/variants.log 2>&1; done
+  QDPB_LIB=variants/libqdpb_$v.so python tools/cg_timing.py 40,40,40,32 --recon12 >> gpurun_out/variants.log 2>&1
 done
