@@ -270,6 +270,41 @@ def run_native(args, rank, world, local_rank):
     e2e_value = e2e_flops / (ms_e2e * 1e-3) * 1e-9
     bytes_b = hb.numel() * hb.element_size()
 
+    # ---- time to solution at tol 1e-10 (not the step): fp64 CG vs the mixed-precision CG
+    tts = None
+    if args.tts:
+        fU32 = q.qdp_field_alloc(ctx, q.QDP_GAUGE, q.QDP_F32, q.QDP_ALL)
+        fU32r = q.qdp_field_alloc(ctx, q.QDP_GAUGE12, q.QDP_F32, q.QDP_ALL)
+        fA32 = q.qdp_field_alloc(ctx, q.QDP_CLOVER, q.QDP_F32, q.QDP_ODD)
+        fAi32 = q.qdp_field_alloc(ctx, q.QDP_CLOVER, q.QDP_F32, q.QDP_EVEN)
+        U32 = U.astype(np.float32)
+        q.qdp_field_import(fU32, U32)
+        q.qdp_field_import(fU32r, U32)
+        q.qdp_clover_build(fA32, fAi32, fU32, MASS, CSW)
+        q.qdp_field_import(fb, b)
+        solvers = {
+            "fp64": lambda: q.qdp_cg_solve(fx, fb, fU, fA, fAi, mass=MASS, tol=1e-10, maxit=5000),
+            "mixed_fp32": lambda: q.qdp_cg_solve_mixed(fx, fb, fU, fA, fAi, fU32, fA32, fAi32, mass=MASS, tol=1e-10,
+                                                       delta=0.1, maxit=5000),
+            "mixed_fp32_recon12": lambda: q.qdp_cg_solve_mixed(fx, fb, fU, fA, fAi, fU32r, fA32, fAi32, mass=MASS,
+                                                               tol=1e-10, delta=0.1, maxit=5000),
+        }
+        tts = {}
+        for name, fn in solvers.items():
+            fn()  # warm
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            e4, e5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e4.record(stream)
+            r = fn()
+            e5.record(stream)
+            torch.cuda.synchronize()
+            tts[name] = {"ms": qdist.max_over_ranks(e4.elapsed_time(e5)), "iters": r["iters"],
+                         "true_resid": r["true_resid"], "reliable_updates": r.get("reliable")}
+        for f in (fU32, fU32r, fA32, fAi32):
+            q.qdp_field_free(f)
+
     # ---- CPU baseline (oracle, rank 0 at N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -306,6 +341,7 @@ def run_native(args, rank, world, local_rank):
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
         "parity": parity,
+        "time_to_solution_1e-10": tts,
         "overlap": not args.no_overlap,
     }
     if rank == 0:
@@ -336,6 +372,7 @@ def main():
     ap.add_argument("--ref-iters", type=int, default=1)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-overlap", action="store_true")
+    ap.add_argument("--no-tts", dest="tts", action="store_false", help="skip the time-to-solution comparison")
     ap.add_argument("--check", action="store_true", default=True)
     ap.add_argument("--no-check", dest="check", action="store_false")
     args = ap.parse_args()

@@ -190,6 +190,21 @@ int qdp_cg_solve(qdp_field x, const qdp_field b, const qdp_field U, const qdp_fi
                  const qdp_field Ainv, double mass, double tol, int maxit, int *iters,
                  double *resid_hist, int hist_cap, double *true_resid);
 
+/* Mixed-precision variant of qdp_cg_solve (the reliable-update mixed-precision CG of the
+ * paper's ref. [2], Clark et al.): the CGNR iteration runs on the QDP_F32 "sloppy" fields
+ * U_s, A_s, Ainv_s (the same operator stored in single precision, e.g. imported from the
+ * same data and built with qdp_clover_build); x, b, U, A, Ainv are QDP_F64.  When the fp32
+ * residual norm falls below delta times its maximum since the last update (0 < delta < 1,
+ * e.g. 0.1), the fp32 solution is added to the fp64 x and the fp64 residual is recomputed.
+ * Convergence (|r|^2 <= tol^2 |r_0|^2) is tested only on such fp64 residuals.
+ * resid_hist[k] holds the fp32 residual, or the fp64 one after an update; reliable
+ * (nullable) returns the number of updates.  Other arguments and returns as qdp_cg_solve. */
+int qdp_cg_solve_mixed(qdp_field x, const qdp_field b, const qdp_field U, const qdp_field A,
+                       const qdp_field Ainv, const qdp_field U_s, const qdp_field A_s,
+                       const qdp_field Ainv_s, double mass, double tol, double delta, int maxit,
+                       int *iters, int *reliable, double *resid_hist, int hist_cap,
+                       double *true_resid);
+
 /* ---- diagnostics ---------------------------------------------------------------------- */
 
 const char *qdp_strerror(int status);

@@ -222,6 +222,59 @@ __global__ void __launch_bounds__(RB) cg_xp_kernel(const Geom g, typename E<R>::
     }
 }
 
+// p = r + beta p, beta = res[rr] / res[rho]
+template <typename R>
+__global__ void __launch_bounds__(RB) cg_p_kernel(const Geom g, typename E<R>::T *p, const typename E<R>::T *r,
+                                                  const double *res, int rho_slot, int rr_slot) {
+  const R beta = (R)(res[rr_slot] / res[rho_slot]);
+  for (int cb = blockIdx.x * blockDim.x + threadIdx.x; cb < g.Vh; cb += gridDim.x * blockDim.x)
+#pragma unroll
+    for (int k = 0; k < E<R>::NP; k++) {
+      const size_t i = (size_t)k * g.stride + cb;
+      R pv[E<R>::NR], rv[E<R>::NR];
+      E<R>::get(p[i], pv);
+      E<R>::get(r[i], rv);
+#pragma unroll
+      for (int j = 0; j < E<R>::NR; j++) pv[j] = rv[j] + beta * pv[j];
+      p[i] = E<R>::put(pv);
+    }
+}
+
+// Precision conversion of one fermion parity block: fp64 double2[12] <-> fp32 float4[6].
+template <bool TO32>
+__global__ void __launch_bounds__(RB) convert_kernel(const Geom g, double2 *d64, float4 *f32) {
+  for (int cb = blockIdx.x * blockDim.x + threadIdx.x; cb < g.Vh; cb += gridDim.x * blockDim.x)
+#pragma unroll
+    for (int k = 0; k < 6; k++) {
+      double2 *a = d64 + (size_t)(2 * k) * g.stride + cb, *b = d64 + (size_t)(2 * k + 1) * g.stride + cb;
+      float4 *f = f32 + (size_t)k * g.stride + cb;
+      if (TO32) {
+        const double2 u = *a, v = *b;
+        *f = make_float4((float)u.x, (float)u.y, (float)v.x, (float)v.y);
+      } else {
+        const float4 w = *f;
+        *a = make_double2(w.x, w.y);
+        *b = make_double2(w.z, w.w);
+      }
+    }
+}
+
+// y64 += x32 (the reliable update's accumulation of the sloppy solution), then x32 = 0
+__global__ void __launch_bounds__(RB) accum_mixed_kernel(const Geom g, double2 *y64, float4 *x32) {
+  for (int cb = blockIdx.x * blockDim.x + threadIdx.x; cb < g.Vh; cb += gridDim.x * blockDim.x)
+#pragma unroll
+    for (int k = 0; k < 6; k++) {
+      double2 *a = y64 + (size_t)(2 * k) * g.stride + cb, *b = y64 + (size_t)(2 * k + 1) * g.stride + cb;
+      float4 *f = x32 + (size_t)k * g.stride + cb;
+      const float4 w = *f;
+      double2 u = *a, v = *b;
+      u.x += w.x; u.y += w.y; v.x += w.z; v.y += w.w;
+      *a = u;
+      *b = v;
+      *f = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+}
+
 // ------------------------------------------------------------------ host wrappers
 static int red_grid(const Geom &g) {
   int n = grid_for(g.Vh, RB);
@@ -346,6 +399,40 @@ int blas_cg_update_xp(qdp_ctx ctx, int prec, void *x, void *p, const void *r, in
   if (prec == QDP_F64) { if (update_p) QDPB_XP(double, true); else QDPB_XP(double, false); }
   else { if (update_p) QDPB_XP(float, true); else QDPB_XP(float, false); }
 #undef QDPB_XP
+  return prof_end(ctx, &ev);
+}
+
+int blas_cg_update_p(qdp_ctx ctx, int prec, void *p, const void *r, int rho_slot, int rr_slot) {
+  const Geom &g = ctx->geom;
+  ProfEvent ev;
+  prof_begin(ctx, QDP_PK_BLAS, &ev);
+  prof_work(ctx, QDP_PK_BLAS, 48.0 * g.Vh, 72.0 * g.Vh * (prec == QDP_F64 ? 8 : 4));
+  const int nb = grid_for(g.Vh, RB);
+  if (prec == QDP_F64)
+    cg_p_kernel<double><<<nb, RB, 0, ctx->stream>>>(g, (T_<double> *)p, (const T_<double> *)r, ctx->red_result, rho_slot, rr_slot);
+  else
+    cg_p_kernel<float><<<nb, RB, 0, ctx->stream>>>(g, (T_<float> *)p, (const T_<float> *)r, ctx->red_result, rho_slot, rr_slot);
+  return prof_end(ctx, &ev);
+}
+
+int blas_convert(qdp_ctx ctx, void *dst, int dst_prec, const void *src) {
+  const Geom &g = ctx->geom;
+  ProfEvent ev;
+  prof_begin(ctx, QDP_PK_BLAS, &ev);
+  prof_work(ctx, QDP_PK_BLAS, 0.0, 288.0 * g.Vh);  // 24 reals fp64 + 24 reals fp32 per site
+  const int nb = grid_for(g.Vh, RB);
+  if (dst_prec == QDP_F32) convert_kernel<true><<<nb, RB, 0, ctx->stream>>>(g, (double2 *)src, (float4 *)dst);
+  else convert_kernel<false><<<nb, RB, 0, ctx->stream>>>(g, (double2 *)dst, (float4 *)src);
+  return prof_end(ctx, &ev);
+}
+
+int blas_accum_mixed(qdp_ctx ctx, void *y64, void *x32) {
+  const Geom &g = ctx->geom;
+  ProfEvent ev;
+  prof_begin(ctx, QDP_PK_BLAS, &ev);
+  prof_work(ctx, QDP_PK_BLAS, 24.0 * g.Vh, (2.0 * 24 * 8 + 2.0 * 24 * 4) * g.Vh);
+  const int nb = grid_for(g.Vh, RB);
+  accum_mixed_kernel<<<nb, RB, 0, ctx->stream>>>(g, (double2 *)y64, (float4 *)x32);
   return prof_end(ctx, &ev);
 }
 

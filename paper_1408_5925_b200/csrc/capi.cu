@@ -627,6 +627,43 @@ extern "C" int qdp_cg_solve(qdp_field x, const qdp_field b, const qdp_field U, c
   return cg_solve(x, b, U, A, Ainv, mass, tol, maxit, iters, resid_hist, hist_cap, true_resid);
 }
 
+extern "C" int qdp_cg_solve_mixed(qdp_field x, const qdp_field b, const qdp_field U, const qdp_field A,
+                                  const qdp_field Ainv, const qdp_field Us, const qdp_field As, const qdp_field Ainvs,
+                                  double mass, double tol, double delta, int maxit, int *iters, int *reliable,
+                                  double *resid_hist, int hist_cap, double *true_resid) {
+  if (!x || !b || !U || !Us) return QDP_EINVAL;
+  qdp_ctx c = x->ctx;
+  int rc;
+  if (x->prec != QDP_F64 || b->prec != QDP_F64 || U->prec != QDP_F64)
+    return set_error(c, QDP_EPREC, "cg_mixed: x, b, U must be QDP_F64");
+  if (Us->prec != QDP_F32) return set_error(c, QDP_EPREC, "cg_mixed: the sloppy fields must be QDP_F32");
+  if (Us->ctx != c || !is_gauge(Us->kind)) return set_error(c, QDP_EINVAL, "cg_mixed: U_s must be a gauge field");
+  if ((A == nullptr) != (As == nullptr) || (A == nullptr) != (Ainvs == nullptr))
+    return set_error(c, QDP_EINVAL, "cg_mixed: give A, Ainv, A_s, Ainv_s together, or none");
+  if (As) {
+    if (As->prec != QDP_F32 || Ainvs->prec != QDP_F32) return set_error(c, QDP_EPREC, "cg_mixed: A_s, Ainv_s must be F32");
+    if (As->kind != QDP_CLOVER || Ainvs->kind != QDP_CLOVER || !block_of(As, 1) || !block_of(Ainvs, 0))
+      return set_error(c, QDP_EINVAL, "cg_mixed: A_s must cover odd, Ainv_s even sites");
+  }
+  if (!(delta > 0 && delta < 1)) return set_error(c, QDP_EINVAL, "cg_mixed: 0 < delta < 1");
+  // the fp64 fields obey the rules of qdp_cg_solve
+  if ((rc = check_pair(x, b)) || (rc = check_pair(x, U))) return rc;
+  if (x->kind != QDP_FERMION || b->kind != QDP_FERMION || !is_gauge(U->kind))
+    return set_error(c, QDP_EINVAL, "cg_mixed: kinds (fermion, fermion, gauge)");
+  if (x->subset != QDP_ALL || b->subset != QDP_ALL) return set_error(c, QDP_EINVAL, "cg_mixed: x and b must be QDP_ALL");
+  if (x->data == b->data) return set_error(c, QDP_EALIAS, "cg_mixed: x aliases b");
+  if ((A == nullptr) != (Ainv == nullptr)) return set_error(c, QDP_EINVAL, "cg_mixed: give both A and Ainv, or neither");
+  if (A) {
+    if ((rc = check_pair(x, A)) || (rc = check_pair(x, Ainv))) return rc;
+    if (A->kind != QDP_CLOVER || Ainv->kind != QDP_CLOVER || !block_of(A, 1) || !block_of(Ainv, 0))
+      return set_error(c, QDP_EINVAL, "cg_mixed: A must cover odd, Ainv even sites");
+    if (true_resid && A->subset != QDP_ALL) return set_error(c, QDP_EINVAL, "cg_mixed: true_resid needs A on all sites");
+  }
+  if (maxit < 0 || !(tol >= 0)) return set_error(c, QDP_EINVAL, "cg_mixed: bad tol/maxit");
+  return cg_solve_mixed(x, b, U, A, Ainv, Us, As, Ainvs, mass, tol, delta, maxit, iters, reliable, resid_hist, hist_cap,
+                        true_resid);
+}
+
 // ---------------------------------------------------------------------------- diagnostics
 extern "C" const char *qdp_strerror(int s) {
   switch (s) {

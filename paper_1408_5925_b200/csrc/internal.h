@@ -507,6 +507,12 @@ int blas_cg_update_r(qdp_ctx ctx, int prec, void *r, const void *q, int rho_slot
 int blas_cg_update_xp(qdp_ctx ctx, int prec, void *x, void *p, const void *r, int rho_slot, int pq_slot, int rr_slot,
                       bool update_p);
 int blas_xpay(qdp_ctx ctx, int prec, const void *x, double a, void *y, int nblk);  // y = x + a y
+// p = r + beta p with beta = res[rr] / res[rho]
+int blas_cg_update_p(qdp_ctx ctx, int prec, void *p, const void *r, int rho_slot, int rr_slot);
+// one fermion parity block fp64 <-> fp32 (dst_prec = precision of dst)
+int blas_convert(qdp_ctx ctx, void *dst, int dst_prec, const void *src);
+// y64 += x32 ; x32 = 0  (one parity block)
+int blas_accum_mixed(qdp_ctx ctx, void *y64, void *x32);
 int blas_scale_copy(qdp_ctx ctx, int prec, void *dst, const void *src, double a, int nblk);  // dst = a src
 
 // dslash.cu
@@ -539,6 +545,9 @@ int shift_field(qdp_ctx ctx, qdp_field out, const qdp_field in, int mu, int sign
 int cg_solve(qdp_field x, const qdp_field b, const qdp_field U, const qdp_field A,
              const qdp_field Ainv, double mass, double tol, int maxit, int *iters,
              double *hist, int hist_cap, double *true_resid);
+int cg_solve_mixed(qdp_field x, const qdp_field b, const qdp_field U, const qdp_field A, const qdp_field Ainv,
+                   const qdp_field Us, const qdp_field As, const qdp_field Ainvs, double mass, double tol, double delta,
+                   int maxit, int *iters, int *nreliable, double *hist, int hist_cap, double *true_resid);
 
 // comm.cpp
 int comm_get_unique_id(unsigned char id[128]);

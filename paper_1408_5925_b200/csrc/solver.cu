@@ -11,6 +11,12 @@
 //   bhat_o      = b_o + 1/2 H_oe A_ee^-1 b_e
 //   x_e         = A_ee^-1 (b_e + 1/2 H_eo x_o)
 // Wilson: A = (4 + m) 1, applied as scalars inside the dslash epilogues.
+//
+// cg_solve_mixed: the same CGNR iterated in fp32 ("sloppy" copies of U, A, A^-1) with fp64
+// reliable updates (the mixed-precision solvers of the paper's ref. [2]): whenever the fp32
+// residual has dropped by `delta` below its maximum since the last update, the fp32 solution
+// is accumulated into the fp64 x and the fp64 residual c - Mhat^dag Mhat x is recomputed.
+// Convergence is only ever declared on an fp64 residual.
 #include <math.h>
 
 #include "internal.h"
@@ -18,7 +24,7 @@
 namespace qdpb {
 
 namespace {
-enum { S_RHO = 0, S_PQ = 2, S_RR = 4 };
+enum { S_RHO = 0, S_PQ = 2, S_RR = 4, S_TRUE = 6 };
 
 struct Op {
   qdp_ctx ctx;
@@ -31,13 +37,32 @@ struct Op {
   void *t;             // even scratch block
 };
 
-// out_o = Mhat v_o  (dag: Mhat^dag); dot_x: also red_result[dot_slot] = Re<dot_x, out>
-int apply_mhat(const Op &op, void *out, const void *v, bool dag, const void *dot_x = nullptr, int dot_slot = 0) {
+Op make_op(qdp_ctx ctx, const qdp_field U, const qdp_field A, const qdp_field Ainv, double mass, void *t) {
+  const size_t cbk = parity_block_bytes(KIND_CLOVER, U->prec, ctx->geom.stride);
+  Op op;
+  op.ctx = ctx;
+  op.prec = U->prec;
+  op.U = U->data;
+  op.rec12 = U->kind == QDP_GAUGE12;
+  op.A_o = A ? (const char *)A->data + (A->subset == QDP_ALL ? cbk : 0) : nullptr;
+  op.Ainv_e = A ? Ainv->data : nullptr;
+  op.diag = 4.0 + mass;
+  op.t = t;
+  return op;
+}
+
+DslashArgs args(const Op &op) {
   DslashArgs a = {};
-  int rc;
   a.U = op.U;
   a.rec12 = op.rec12;
+  return a;
+}
+
+// out_o = Mhat v_o  (dag: Mhat^dag); dot_x: also red_result[dot_slot] = Re<dot_x, out>
+int apply_mhat(const Op &op, void *out, const void *v, bool dag, const void *dot_x = nullptr, int dot_slot = 0) {
+  int rc;
   // t_e = [A_ee^-1] H_eo [g5] v
+  DslashArgs a = args(op);
   a.out = op.t;
   a.psi = v;
   a.parity = 0;
@@ -51,9 +76,7 @@ int apply_mhat(const Op &op, void *out, const void *v, bool dag, const void *dot
   }
   if ((rc = dslash(op.ctx, op.prec, a))) return rc;
   // out_o = A_oo v - 1/4 [g5] H_oe t   (Wilson: (4+m) v - 1/(4(4+m)) [g5] H_oe t)
-  DslashArgs c = {};
-  c.U = op.U;
-  c.rec12 = op.rec12;
+  DslashArgs c = args(op);
   c.out = out;
   c.psi = op.t;
   c.x = v;
@@ -72,113 +95,56 @@ int apply_mhat(const Op &op, void *out, const void *v, bool dag, const void *dot
   }
   return dslash(op.ctx, op.prec, c);
 }
-}  // namespace
 
-int cg_solve(qdp_field x, const qdp_field b, const qdp_field U, const qdp_field A, const qdp_field Ainv, double mass,
-             double tol, int maxit, int *iters_out, double *hist, int hist_cap, double *true_resid) {
-  qdp_ctx ctx = x->ctx;
-  const Geom &g = ctx->geom;
-  const int prec = x->prec;
-  const size_t blk = fermion_block_bytes(prec, g.stride);
-  const bool clover = A != nullptr;
-  const size_t cbk = parity_block_bytes(KIND_CLOVER, prec, g.stride);
+int read_slot(qdp_ctx ctx, int slot, double *v) {
+  cudaError_t e = cudaMemcpyAsync(ctx->host_pinned, ctx->red_result + slot, sizeof(double), cudaMemcpyDeviceToHost,
+                                  ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) return cuda_check(ctx, e, "cg: read scalar");
+  *v = ctx->host_pinned[0];
+  return QDP_OK;
+}
+
+int copy_slot(qdp_ctx ctx, int dst, int src) {
+  QDP_CUDA(ctx, cudaMemcpyAsync(ctx->red_result + dst, ctx->red_result + src, sizeof(double), cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+  return QDP_OK;
+}
+
+// bhat_o = b_o + 1/2 H_oe A_ee^-1 b_e
+int prepare_source(const Op &op, void *bh, const char *b_e, const char *b_o) {
   int rc;
+  if (op.A_o) rc = clover_apply(op.ctx, op.prec, op.t, op.Ainv_e, b_e, 1);
+  else rc = blas_scale_copy(op.ctx, op.prec, op.t, b_e, 1.0 / op.diag, 1);
+  if (rc) return rc;
+  DslashArgs a = args(op);
+  a.out = bh;
+  a.psi = op.t;
+  a.x = b_o;
+  a.parity = 1;
+  a.epi = EPI_XPAY;
+  a.a = 1.0;
+  a.b = 0.5;
+  return dslash(op.ctx, op.prec, a);
+}
 
-  Op op;
-  op.ctx = ctx;
-  op.prec = prec;
-  op.U = U->data;
-  op.rec12 = U->kind == QDP_GAUGE12;
-  op.A_o = clover ? (const char *)A->data + (A->subset == QDP_ALL ? cbk : 0) : nullptr;
-  op.Ainv_e = clover ? Ainv->data : nullptr;
-  op.diag = 4.0 + mass;
-
-  // work: [t | r | p | q | mp | bh], persistent in the context (every block is fully
-  // written before it is read, so no clearing is needed)
-  if ((rc = ensure_cg_work(ctx, 6 * blk))) return rc;
-  char *work = (char *)ctx->cg_work;
-  op.t = work;
-  void *r = work + blk, *p = work + 2 * blk, *q = work + 3 * blk, *mp = work + 4 * blk, *bh = work + 5 * blk;
-  const char *b_e = (const char *)b->data, *b_o = b_e + blk;
+// x_e = A_ee^-1 (b_e + 1/2 H_eo x_o), then (if asked) |b - M x| / |b| using `tmp2` (2 blocks)
+int finish_solve(const Op &op, const qdp_field x, const qdp_field b, const qdp_field A, void *tmp2,
+                 double *true_resid) {
+  qdp_ctx ctx = op.ctx;
+  const Geom &g = ctx->geom;
+  const size_t blk = fermion_block_bytes(op.prec, g.stride);
+  const size_t cbk = parity_block_bytes(KIND_CLOVER, op.prec, g.stride);
   char *x_e = (char *)x->data, *x_o = x_e + blk;
-  double *h = ctx->host_pinned;
-  int k = 0, status = QDP_NOT_CONVERGED;
-  double rho0 = 0.0, rho = 0.0;
-
-  auto fail = [&](int e) { return e; };
-  auto read_slot = [&](int slot, double *v) -> int {
-    cudaError_t e = cudaMemcpyAsync(h, ctx->red_result + slot, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-    if (e != cudaSuccess) return cuda_check(ctx, e, "cg: read scalar");
-    *v = h[0];
-    return QDP_OK;
-  };
-
-  // bhat_o = b_o + 1/2 H_oe A_ee^-1 b_e
-  if (clover) rc = clover_apply(ctx, prec, op.t, op.Ainv_e, b_e, 1);
-  else rc = blas_scale_copy(ctx, prec, op.t, b_e, 1.0 / op.diag, 1);
-  if (rc) return fail(rc);
+  const char *b_e = (const char *)b->data;
+  int rc;
   {
-    DslashArgs a = {};
-    a.U = op.U;
-    a.rec12 = op.rec12;
-    a.out = bh;
-    a.psi = op.t;
-    a.x = b_o;
-    a.parity = 1;
-    a.epi = EPI_XPAY;
-    a.a = 1.0;
-    a.b = 0.5;
-    if ((rc = dslash(ctx, prec, a))) return fail(rc);
-  }
-  // x_o = 0 ; r = Mhat^dag bhat ; p = r ; rho0 = |r|^2
-  if (cudaMemsetAsync(x_o, 0, blk, ctx->stream) != cudaSuccess) return fail(set_error(ctx, QDP_ECUDA, "cg: memset"));
-  if ((rc = apply_mhat(op, r, bh, true))) return fail(rc);
-  if (cudaMemcpyAsync(p, r, blk, cudaMemcpyDeviceToDevice, ctx->stream) != cudaSuccess)
-    return fail(set_error(ctx, QDP_ECUDA, "cg: copy"));
-  if ((rc = blas_norm2(ctx, prec, r, 1, S_RHO)) || (rc = reduce_global(ctx, S_RHO, 1)) || (rc = read_slot(S_RHO, &rho0)))
-    return fail(rc);
-  rho = rho0;
-  if (hist_cap > 0 && hist) hist[0] = 1.0;
-  if (rho0 == 0.0) status = QDP_OK;
-
-  while (status == QDP_NOT_CONVERGED && k < maxit) {
-    // q = Mhat^dag Mhat p, with Re<p, q> -> S_PQ fused into the last launch
-    if ((rc = apply_mhat(op, mp, p, false))) return fail(rc);
-    if ((rc = apply_mhat(op, q, mp, true, p, S_PQ))) return fail(rc);
-    // r -= alpha q ; rr = |r|^2
-    if ((rc = blas_cg_update_r(ctx, prec, r, q, S_RHO, S_PQ, S_RR))) return fail(rc);
-    double rho_new;
-    if ((rc = read_slot(S_RR, &rho_new))) return fail(rc);
-    k++;
-    if (hist && k < hist_cap) hist[k] = sqrt(rho_new / rho0);
-    const bool done = rho_new <= tol * tol * rho0;
-    // x += alpha p ; p = r + beta p (skipped on the last iteration)
-    const bool last = done || k == maxit;
-    if ((rc = blas_cg_update_xp(ctx, prec, x_o, p, r, S_RHO, S_PQ, S_RR, !last))) return fail(rc);
-    if (done) {
-      status = QDP_OK;
-      rho = rho_new;
-      break;
-    }
-    if (cudaMemcpyAsync(ctx->red_result + S_RHO, ctx->red_result + S_RR, sizeof(double), cudaMemcpyDeviceToDevice,
-                        ctx->stream) != cudaSuccess)
-      return fail(set_error(ctx, QDP_ECUDA, "cg: scalar copy"));
-    rho = rho_new;
-  }
-  (void)rho;
-  if (iters_out) *iters_out = k;
-
-  // x_e = A_ee^-1 (b_e + 1/2 H_eo x_o)
-  {
-    DslashArgs a = {};
-    a.U = op.U;
-    a.rec12 = op.rec12;
+    DslashArgs a = args(op);
     a.out = x_e;
     a.psi = x_o;
     a.x = b_e;
     a.parity = 0;
-    if (clover) {
+    if (op.A_o) {
       a.epi = EPI_CLOVINV;
       a.clov = op.Ainv_e;
       a.a = 1.0;
@@ -188,38 +154,169 @@ int cg_solve(qdp_field x, const qdp_field b, const qdp_field U, const qdp_field 
       a.a = 1.0 / op.diag;
       a.b = 0.5 / op.diag;
     }
-    if ((rc = dslash(ctx, prec, a))) return fail(rc);
+    if ((rc = dslash(ctx, op.prec, a))) return rc;
   }
-
-  if (true_resid) {
-    // tmp = M x = A x - 1/2 H x  (per parity), then tmp = b - tmp ; |tmp| / |b|
-    char *tmp = (char *)r;  // r | p are adjacent: a full two-block vector
-    for (int par = 0; par < 2; par++) {
-      DslashArgs a = {};
-      a.U = op.U;
-      a.rec12 = op.rec12;
-      a.out = tmp + par * blk;
-      a.psi = par == 0 ? x_o : x_e;
-      a.x = par == 0 ? x_e : x_o;
-      a.parity = par;
-      a.b = -0.5;
-      if (clover) {
-        a.epi = EPI_CLOVXPAY;
-        a.clov = (const char *)A->data + par * cbk;  // A covers ALL sites (checked in capi)
-      } else {
-        a.epi = EPI_XPAY;
-        a.a = op.diag;
-      }
-      if ((rc = dslash(ctx, prec, a))) return fail(rc);
+  if (!true_resid) return QDP_OK;
+  // tmp = M x = A x - 1/2 H x  (per parity), then tmp = b - tmp ; |tmp| / |b|
+  char *tmp = (char *)tmp2;
+  for (int par = 0; par < 2; par++) {
+    DslashArgs a = args(op);
+    a.out = tmp + par * blk;
+    a.psi = par == 0 ? x_o : x_e;
+    a.x = par == 0 ? x_e : x_o;
+    a.parity = par;
+    a.b = -0.5;
+    if (op.A_o) {
+      a.epi = EPI_CLOVXPAY;
+      a.clov = (const char *)A->data + par * cbk;  // A covers ALL sites (checked in capi)
+    } else {
+      a.epi = EPI_XPAY;
+      a.a = op.diag;
     }
-    if ((rc = blas_xpay(ctx, prec, b->data, -1.0, tmp, 2))) return fail(rc);
-    double rr, bb;
-    if ((rc = blas_norm2(ctx, prec, tmp, 2, S_RR)) || (rc = reduce_global(ctx, S_RR, 1)) || (rc = read_slot(S_RR, &rr)))
-      return fail(rc);
-    if ((rc = blas_norm2(ctx, prec, b->data, 2, S_RR)) || (rc = reduce_global(ctx, S_RR, 1)) || (rc = read_slot(S_RR, &bb)))
-      return fail(rc);
-    *true_resid = bb > 0 ? sqrt(rr / bb) : 0.0;
+    if ((rc = dslash(ctx, op.prec, a))) return rc;
   }
+  if ((rc = blas_xpay(ctx, op.prec, b->data, -1.0, tmp, 2))) return rc;
+  double rr, bb;
+  if ((rc = blas_norm2(ctx, op.prec, tmp, 2, S_RR)) || (rc = reduce_global(ctx, S_RR, 1)) || (rc = read_slot(ctx, S_RR, &rr)))
+    return rc;
+  if ((rc = blas_norm2(ctx, op.prec, b->data, 2, S_RR)) || (rc = reduce_global(ctx, S_RR, 1)) ||
+      (rc = read_slot(ctx, S_RR, &bb)))
+    return rc;
+  *true_resid = bb > 0 ? sqrt(rr / bb) : 0.0;
+  return QDP_OK;
+}
+}  // namespace
+
+int cg_solve(qdp_field x, const qdp_field b, const qdp_field U, const qdp_field A, const qdp_field Ainv, double mass,
+             double tol, int maxit, int *iters_out, double *hist, int hist_cap, double *true_resid) {
+  qdp_ctx ctx = x->ctx;
+  const Geom &g = ctx->geom;
+  const int prec = x->prec;
+  const size_t blk = fermion_block_bytes(prec, g.stride);
+  int rc;
+
+  // work: [t | r | p | q | mp | bh], persistent in the context (every block is fully
+  // written before it is read, so no clearing is needed)
+  if ((rc = ensure_cg_work(ctx, 6 * blk))) return rc;
+  char *work = (char *)ctx->cg_work;
+  const Op op = make_op(ctx, U, A, Ainv, mass, work);
+  void *r = work + blk, *p = work + 2 * blk, *q = work + 3 * blk, *mp = work + 4 * blk, *bh = work + 5 * blk;
+  const char *b_e = (const char *)b->data, *b_o = b_e + blk;
+  char *x_o = (char *)x->data + blk;
+  int k = 0, status = QDP_NOT_CONVERGED;
+  double rho0 = 0.0;
+
+  if ((rc = prepare_source(op, bh, b_e, b_o))) return rc;
+  // x_o = 0 ; r = Mhat^dag bhat ; p = r ; rho0 = |r|^2
+  QDP_CUDA(ctx, cudaMemsetAsync(x_o, 0, blk, ctx->stream));
+  if ((rc = apply_mhat(op, r, bh, true))) return rc;
+  QDP_CUDA(ctx, cudaMemcpyAsync(p, r, blk, cudaMemcpyDeviceToDevice, ctx->stream));
+  if ((rc = blas_norm2(ctx, prec, r, 1, S_RHO)) || (rc = reduce_global(ctx, S_RHO, 1)) || (rc = read_slot(ctx, S_RHO, &rho0)))
+    return rc;
+  if (hist_cap > 0 && hist) hist[0] = 1.0;
+  if (rho0 == 0.0) status = QDP_OK;
+
+  while (status == QDP_NOT_CONVERGED && k < maxit) {
+    // q = Mhat^dag Mhat p, with Re<p, q> -> S_PQ fused into the last launch
+    if ((rc = apply_mhat(op, mp, p, false))) return rc;
+    if ((rc = apply_mhat(op, q, mp, true, p, S_PQ))) return rc;
+    // r -= alpha q ; rr = |r|^2
+    if ((rc = blas_cg_update_r(ctx, prec, r, q, S_RHO, S_PQ, S_RR))) return rc;
+    double rho_new;
+    if ((rc = read_slot(ctx, S_RR, &rho_new))) return rc;
+    k++;
+    if (hist && k < hist_cap) hist[k] = sqrt(rho_new / rho0);
+    const bool done = rho_new <= tol * tol * rho0;
+    // x += alpha p ; p = r + beta p (skipped on the last iteration)
+    const bool last = done || k == maxit;
+    if ((rc = blas_cg_update_xp(ctx, prec, x_o, p, r, S_RHO, S_PQ, S_RR, !last))) return rc;
+    if (done) {
+      status = QDP_OK;
+      break;
+    }
+    if ((rc = copy_slot(ctx, S_RHO, S_RR))) return rc;
+  }
+  if (iters_out) *iters_out = k;
+  if ((rc = finish_solve(op, x, b, A, r, true_resid))) return rc;  // r | p: a two-block scratch
+  QDP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return status;
+}
+
+int cg_solve_mixed(qdp_field x, const qdp_field b, const qdp_field U, const qdp_field A, const qdp_field Ainv,
+                   const qdp_field Us, const qdp_field As, const qdp_field Ainvs, double mass, double tol, double delta,
+                   int maxit, int *iters_out, int *nreliable_out, double *hist, int hist_cap, double *true_resid) {
+  qdp_ctx ctx = x->ctx;
+  const Geom &g = ctx->geom;
+  const size_t b64 = fermion_block_bytes(QDP_F64, g.stride), b32 = fermion_block_bytes(QDP_F32, g.stride);
+  int rc;
+  // fp64 work: [t | r | c | mp | q | bh] ; fp32 work: [t | r | p | q | mp | x]
+  if ((rc = ensure_cg_work(ctx, 6 * b64 + 6 * b32))) return rc;
+  char *w64 = (char *)ctx->cg_work, *w32 = w64 + 6 * b64;
+  const Op op = make_op(ctx, U, A, Ainv, mass, w64);
+  const Op ops = make_op(ctx, Us, As, Ainvs, mass, w32);
+  void *r = w64 + b64, *c = w64 + 2 * b64, *mp = w64 + 3 * b64, *q = w64 + 4 * b64, *bh = w64 + 5 * b64;
+  void *rs = w32 + b32, *ps = w32 + 2 * b32, *qs = w32 + 3 * b32, *mps = w32 + 4 * b32, *xs = w32 + 5 * b32;
+  const char *b_e = (const char *)b->data, *b_o = b_e + b64;
+  char *x_o = (char *)x->data + b64;
+  int k = 0, nrel = 0, status = QDP_NOT_CONVERGED;
+  double rho0 = 0.0;
+
+  // c = Mhat^dag bhat (fp64); x_o = 0; r = c; sloppy r_s = p_s = (float) r; x_s = 0
+  if ((rc = prepare_source(op, bh, b_e, b_o))) return rc;
+  if ((rc = apply_mhat(op, c, bh, true))) return rc;
+  QDP_CUDA(ctx, cudaMemsetAsync(x_o, 0, b64, ctx->stream));
+  QDP_CUDA(ctx, cudaMemsetAsync(xs, 0, b32, ctx->stream));
+  QDP_CUDA(ctx, cudaMemcpyAsync(r, c, b64, cudaMemcpyDeviceToDevice, ctx->stream));
+  if ((rc = blas_norm2(ctx, QDP_F64, r, 1, S_RHO)) || (rc = reduce_global(ctx, S_RHO, 1)) ||
+      (rc = read_slot(ctx, S_RHO, &rho0)))
+    return rc;
+  if ((rc = blas_convert(ctx, rs, QDP_F32, r))) return rc;
+  QDP_CUDA(ctx, cudaMemcpyAsync(ps, rs, b32, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (hist_cap > 0 && hist) hist[0] = 1.0;
+  if (rho0 == 0.0) status = QDP_OK;
+  double maxr = sqrt(rho0);
+
+  while (status == QDP_NOT_CONVERGED && k < maxit) {
+    if ((rc = apply_mhat(ops, mps, ps, false))) return rc;
+    if ((rc = apply_mhat(ops, qs, mps, true, ps, S_PQ))) return rc;
+    if ((rc = blas_cg_update_r(ctx, QDP_F32, rs, qs, S_RHO, S_PQ, S_RR))) return rc;
+    double rr;
+    if ((rc = read_slot(ctx, S_RR, &rr))) return rc;
+    k++;
+    const bool reliable = sqrt(rr) < delta * maxr || rr <= tol * tol * rho0 || k == maxit;
+    if (!reliable) {
+      if (hist && k < hist_cap) hist[k] = sqrt(rr / rho0);
+      if ((rc = blas_cg_update_xp(ctx, QDP_F32, xs, ps, rs, S_RHO, S_PQ, S_RR, true))) return rc;
+      if ((rc = copy_slot(ctx, S_RHO, S_RR))) return rc;
+      continue;
+    }
+    // reliable update: x += x_s (fp64), r = c - Mhat^dag Mhat x (fp64), r_s = (float) r
+    if ((rc = blas_cg_update_xp(ctx, QDP_F32, xs, ps, rs, S_RHO, S_PQ, S_RR, false))) return rc;
+    if ((rc = blas_accum_mixed(ctx, x_o, xs))) return rc;
+    if ((rc = apply_mhat(op, mp, x_o, false)) || (rc = apply_mhat(op, q, mp, true))) return rc;
+    QDP_CUDA(ctx, cudaMemcpyAsync(r, c, b64, cudaMemcpyDeviceToDevice, ctx->stream));
+    if ((rc = blas_axpy(ctx, QDP_F64, -1.0, 0.0, q, r, 1))) return rc;
+    double rt;
+    if ((rc = blas_norm2(ctx, QDP_F64, r, 1, S_TRUE)) || (rc = reduce_global(ctx, S_TRUE, 1)) ||
+        (rc = read_slot(ctx, S_TRUE, &rt)))
+      return rc;
+    nrel++;
+    if (hist && k < hist_cap) hist[k] = sqrt(rt / rho0);
+    maxr = sqrt(rt);
+    if (rt <= tol * tol * rho0) {
+      status = QDP_OK;
+      break;
+    }
+    if (k == maxit) break;
+    // p_s = r_s + beta p_s with beta = |r|^2 / rho (the fp64 residual norm), rho <- |r|^2
+    if ((rc = blas_convert(ctx, rs, QDP_F32, r))) return rc;
+    if ((rc = copy_slot(ctx, S_RR, S_TRUE))) return rc;
+    if ((rc = blas_cg_update_p(ctx, QDP_F32, ps, rs, S_RHO, S_RR))) return rc;
+    if ((rc = copy_slot(ctx, S_RHO, S_RR))) return rc;
+  }
+  if (iters_out) *iters_out = k;
+  if (nreliable_out) *nreliable_out = nrel;
+  if ((rc = finish_solve(op, x, b, A, mp, true_resid))) return rc;  // mp | q: a two-block scratch
   QDP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   return status;
 }

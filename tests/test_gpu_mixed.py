@@ -1,0 +1,78 @@
+"""Mixed-precision CGNR with reliable updates (qdp_cg_solve_mixed; the paper's ref. [2]).
+The iteration history is not the oracle's (a different algorithm); what is pinned is the
+answer: the solution agrees with the oracle's fp64 even-odd CG solution of the same system
+within the solver tolerance, the true residual meets it, and convergence was declared on an
+fp64 residual (at least one reliable update)."""
+import numpy as np
+import pytest
+
+import fieldgen
+import oracle
+from _physics import rel_site_err
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def q():
+    from paper_1408_5925_b200 import qdpb
+    qdpb.lib()
+    return qdpb
+
+
+def _field(q, c, kind, prec, subset, host):
+    f = q.qdp_field_alloc(c, kind, prec, subset)
+    q.qdp_field_import(f, np.ascontiguousarray(host, dtype=np.float64 if prec == 0 else np.float32))
+    return f
+
+
+@pytest.mark.parametrize("clover,gk", [(False, 1), (True, 1), (True, 3)])
+@pytest.mark.parametrize("L", [(8, 8, 8, 8), (16, 16, 16, 16)])
+def test_mixed_cg_solution(q, clover, gk, L):
+    m = 0.1
+    U = fieldgen.random_gauge(L, 1901)
+    b = fieldgen.random_spinor(L, 2901)
+    A = oracle.clover_build(U, L, m, 1.0) if clover else None
+    ref = oracle.cg_solve(U, b, L, m, A=A, tol=1e-11, maxit=2000)
+    c = q.qdp_init(L)
+    try:
+        fU = _field(q, c, gk, 0, q.QDP_ALL, U)
+        fUs = _field(q, c, gk, 1, q.QDP_ALL, U)
+        fb = _field(q, c, q.QDP_FERMION, 0, q.QDP_ALL, b)
+        fx = q.qdp_field_alloc(c, q.QDP_FERMION, 0, q.QDP_ALL)
+        fA = fAi = fAs = fAis = None
+        if clover:
+            fA = q.qdp_field_alloc(c, q.QDP_CLOVER, 0, q.QDP_ALL)
+            fAi = q.qdp_field_alloc(c, q.QDP_CLOVER, 0, q.QDP_EVEN)
+            fAs = q.qdp_field_alloc(c, q.QDP_CLOVER, 1, q.QDP_ODD)
+            fAis = q.qdp_field_alloc(c, q.QDP_CLOVER, 1, q.QDP_EVEN)
+            q.qdp_clover_build(fA, fAi, fU, m, 1.0)
+            q.qdp_clover_build(fAs, fAis, fUs, m, 1.0)
+        res = q.qdp_cg_solve_mixed(fx, fb, fU, fA, fAi, fUs, fAs, fAis, mass=m, tol=1e-10, delta=0.1, maxit=2000)
+        assert res["status"] == q.QDP_OK
+        assert res["reliable"] >= 1 and res["hist"][-1] <= 1e-10
+        assert res["true_resid"] <= 1e-9
+        assert res["iters"] <= 2 * ref["iters"] + 10
+        assert rel_site_err(q.qdp_field_export(fx), ref["x"]) <= 1e-8
+        # same system in plain fp64: the answers agree with each other too
+        fy = q.qdp_field_alloc(c, q.QDP_FERMION, 0, q.QDP_ALL)
+        r64 = q.qdp_cg_solve(fy, fb, fU, fA, fAi, mass=m, tol=1e-10, maxit=2000)
+        assert r64["iters"] == oracle.cg_solve(U, b, L, m, A=A, tol=1e-10, maxit=2000)["iters"]
+        assert rel_site_err(q.qdp_field_export(fx), q.qdp_field_export(fy)) <= 1e-8
+    finally:
+        q.qdp_finalize(c)
+
+
+def test_mixed_cg_argument_checks(q):
+    L = (4, 4, 4, 4)
+    c = q.qdp_init(L)
+    try:
+        U = q.qdp_field_alloc(c, q.QDP_GAUGE, 0, q.QDP_ALL)
+        x = q.qdp_field_alloc(c, q.QDP_FERMION, 0, q.QDP_ALL)
+        b = q.qdp_field_alloc(c, q.QDP_FERMION, 0, q.QDP_ALL)
+        for Us, delta, st in ((U, 0.1, q.QDP_EPREC), (q.qdp_field_alloc(c, q.QDP_GAUGE, 1, q.QDP_ALL), 1.5, q.QDP_EINVAL)):
+            with pytest.raises(q.QdpError) as e:
+                q.qdp_cg_solve_mixed(x, b, U, U_s=Us, delta=delta)
+            assert e.value.status == st
+    finally:
+        q.qdp_finalize(c)
