@@ -64,7 +64,9 @@ enum { QDP_F64 = 0, QDP_F32 = 1 };                             /* precision */
  * numbers"): same host layout as QDP_GAUGE; import rejects (QDP_EINVAL) links
  * whose third row differs from conj(row0 x row1) by more than 1e-10 (F64) / 1e-5 (F32), and
  * export returns the rebuilt third row.  Accepted wherever a QDP_GAUGE field is. */
-enum { QDP_FERMION = 0, QDP_GAUGE = 1, QDP_CLOVER = 2, QDP_GAUGE12 = 3 };
+enum { QDP_FERMION = 0, QDP_GAUGE = 1, QDP_CLOVER = 2, QDP_GAUGE12 = 3,
+       QDP_COLORMATRIX = 4, /* LatticeColorMatrix (Table I): REAL[sites][3 row][3 col][2] */
+       QDP_SPINMATRIX = 5   /* LatticeSpinMatrix  (Table I): REAL[sites][4 row][4 col][2] */ };
 enum { QDP_ALL = -1, QDP_EVEN = 0, QDP_ODD = 1 };             /* subset / parity */
 enum { QDP_FORWARD = +1, QDP_BACKWARD = -1 };                 /* shift direction */
 
@@ -116,7 +118,7 @@ int qdp_get_geometry(qdp_ctx ctx, int local_dims[4], int proc_coords[4]);
  *                     NCCL cannot be loaded) instead of packing straight into the ghost
  *                     buffers -- the NCCL code path of a multi-GPU run, on one GPU. */
 enum { QDP_OPT_OVERLAP = 0, QDP_OPT_SELF_HALO = 1, QDP_OPT_PROFILE = 2, QDP_OPT_BLOCK = 3,
-       QDP_OPT_DET_REDUCE = 4, QDP_OPT_SELF_NCCL = 5 };
+       QDP_OPT_DET_REDUCE = 4, QDP_OPT_SELF_NCCL = 5, QDP_OPT_AUTOTUNE = 6 /* see qdp_expr */ };
 int qdp_set_option(qdp_ctx ctx, int option, long value);
 int qdp_get_option(qdp_ctx ctx, int option, long *value);
 
@@ -204,6 +206,25 @@ int qdp_cg_solve_mixed(qdp_field x, const qdp_field b, const qdp_field U, const 
                        const qdp_field Ainv_s, double mass, double tol, double delta, int maxit,
                        int *iters, int *reliable, double *resid_hist, int hist_cap,
                        double *true_resid);
+
+/* ---- site-local expressions: the test functions of PAPER.md Table II (section VI) ----------
+ * One fused streaming kernel per expression, evaluated on every site of the output's subset
+ * (all operands share that subset, or are QDP_ALL when the output is a parity):
+ *   QDP_EXPR_LCM     out = a * b            colour matrices                  (Table II "lcm")
+ *   QDP_EXPR_UPSI    out = a * b            colour matrix x fermion          ("upsi")
+ *   QDP_EXPR_SPMAT   out = a * b            spin matrices                    ("spmat")
+ *   QDP_EXPR_MATVEC  out = a * b + a * c    colour matrix x two fermions     ("matvec")
+ *   QDP_EXPR_CLOVER  out = a * b            clover (packed blocks) x fermion ("clover")
+ * c is NULL except for MATVEC.  All operands have the output's precision (QDP_EPREC).
+ * Block size: the paper's autotuner runs on the payload launches -- first
+ * launch at 1024 threads, halved while the launch fails, then each further launch probes the
+ * next smaller size until the time grows by more than 33%; the best size is kept per
+ * (expression, precision, volume).  QDP_OPT_AUTOTUNE = 0 disables it (128 threads). */
+enum { QDP_EXPR_LCM = 0, QDP_EXPR_UPSI = 1, QDP_EXPR_SPMAT = 2, QDP_EXPR_MATVEC = 3, QDP_EXPR_CLOVER = 4 };
+int qdp_expr(int expr, qdp_field out, const qdp_field a, const qdp_field b, const qdp_field c);
+/* block size the autotuner currently uses for (expr, prec) on this context's volume, and
+ * whether its search has finished (1) */
+int qdp_expr_block(qdp_ctx ctx, int expr, int prec, int *block, int *tuned);
 
 /* ---- diagnostics ---------------------------------------------------------------------- */
 

@@ -156,3 +156,39 @@ def cg_solve(U, b, L, mass: float, A=None, tol: float = 1e-10, maxit: int = 1000
         raise ZeroDivisionError("singular clover block")
     n = iters.value
     return dict(x=x, iters=n, hist=hist[:n + 1].copy(), true_resid=tr.value, status=st)
+
+
+def _n(a, per):
+    return int(np.asarray(a).size // per)
+
+
+def lcm(a, b) -> np.ndarray:
+    """Table II lcm: site-wise 3x3 product.  a, b: [n,3,3,2]."""
+    a, b = _f64(a), _f64(b)
+    out = np.empty_like(a)
+    lib().orc_lcm(_p(out), _p(a), _p(b), ctypes.c_long(_n(a, 18)))
+    return out
+
+
+def upsi(u, psi) -> np.ndarray:
+    """Table II upsi: colour matrix times the colour vector of each spin.  u [n,3,3,2], psi [n,4,3,2]."""
+    u, psi = _f64(u), _f64(psi)
+    out = np.empty_like(psi)
+    lib().orc_upsi(_p(out), _p(u), _p(psi), ctypes.c_long(_n(u, 18)))
+    return out
+
+
+def spmat(a, b) -> np.ndarray:
+    """Table II spmat: site-wise 4x4 product.  a, b: [n,4,4,2]."""
+    a, b = _f64(a), _f64(b)
+    out = np.empty_like(a)
+    lib().orc_spmat(_p(out), _p(a), _p(b), ctypes.c_long(_n(a, 32)))
+    return out
+
+
+def matvec(u, p1, p2) -> np.ndarray:
+    """Table II matvec: u psi1 + u psi2."""
+    u, p1, p2 = _f64(u), _f64(p1), _f64(p2)
+    out = np.empty_like(p1)
+    lib().orc_matvec(_p(out), _p(u), _p(p1), _p(p2), ctypes.c_long(_n(u, 18)))
+    return out

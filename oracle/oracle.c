@@ -574,3 +574,58 @@ int orc_cg_solve(double *x, const double *b, const double *U, const double *A, d
     free(Ainv);
     return status;
 }
+
+/* ================= Table II test functions (section VI) ====================
+ * Site-local products on n sites, host layouts: colour matrix [n][3][3][2], spin matrix
+ * [n][4][4][2], fermion [n][4][3][2].  Plain definitions. */
+
+/* lcm: out(x) = a(x) b(x), 3x3 complex */
+void orc_lcm(double *out_, const double *a_, const double *b_, long n) {
+    const cplx *a = (const cplx *)a_, *b = (const cplx *)b_;
+    cplx *out = (cplx *)out_;
+#pragma omp parallel for schedule(static)
+    for (long s = 0; s < n; s++)
+        for (int i = 0; i < 3; i++)
+            for (int j = 0; j < 3; j++) {
+                cplx acc = 0;
+                for (int k = 0; k < 3; k++) acc += a[s * 9 + i * 3 + k] * b[s * 9 + k * 3 + j];
+                out[s * 9 + i * 3 + j] = acc;
+            }
+}
+
+/* upsi: out(x)_{spin,a} = sum_b u(x)_{a,b} psi(x)_{spin,b} */
+void orc_upsi(double *out_, const double *u_, const double *psi_, long n) {
+    const cplx *u = (const cplx *)u_, *psi = (const cplx *)psi_;
+    cplx *out = (cplx *)out_;
+#pragma omp parallel for schedule(static)
+    for (long s = 0; s < n; s++)
+        for (int sp = 0; sp < 4; sp++)
+            for (int a = 0; a < 3; a++) {
+                cplx acc = 0;
+                for (int b = 0; b < 3; b++) acc += u[s * 9 + a * 3 + b] * psi[s * 12 + sp * 3 + b];
+                out[s * 12 + sp * 3 + a] = acc;
+            }
+}
+
+/* spmat: out(x) = a(x) b(x), 4x4 complex */
+void orc_spmat(double *out_, const double *a_, const double *b_, long n) {
+    const cplx *a = (const cplx *)a_, *b = (const cplx *)b_;
+    cplx *out = (cplx *)out_;
+#pragma omp parallel for schedule(static)
+    for (long s = 0; s < n; s++)
+        for (int i = 0; i < 4; i++)
+            for (int j = 0; j < 4; j++) {
+                cplx acc = 0;
+                for (int k = 0; k < 4; k++) acc += a[s * 16 + i * 4 + k] * b[s * 16 + k * 4 + j];
+                out[s * 16 + i * 4 + j] = acc;
+            }
+}
+
+/* matvec: out(x) = u(x) psi1(x) + u(x) psi2(x) */
+void orc_matvec(double *out, const double *u, const double *p1, const double *p2, long n) {
+    double *t = (double *)malloc(sizeof(double) * 24 * (size_t)n);
+    orc_upsi(out, u, p1, n);
+    orc_upsi(t, u, p2, n);
+    for (long k = 0; k < 24 * n; k++) out[k] += t[k];
+    free(t);
+}

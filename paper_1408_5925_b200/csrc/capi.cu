@@ -166,7 +166,7 @@ static size_t field_host_bytes(qdp_ctx ctx, int kind, int prec, int subset) {
 
 }  // namespace qdpb
 
-static bool valid_kind(int k) { return k == QDP_FERMION || k == QDP_GAUGE || k == QDP_CLOVER || k == QDP_GAUGE12; }
+static bool valid_kind(int k) { return k >= QDP_FERMION && k <= QDP_SPINMATRIX; }
 static bool valid_prec(int p) { return p == QDP_F64 || p == QDP_F32; }
 static bool valid_subset(int s) { return s == QDP_ALL || s == QDP_EVEN || s == QDP_ODD; }
 
@@ -254,6 +254,7 @@ extern "C" int qdp_finalize(qdp_ctx c) {
   if (!c) return QDP_EINVAL;
   if (c->stream) cudaStreamSynchronize(c->stream);
   resolve_profile(c);
+  tune_release(c);
   comm_destroy(c);
   for (auto e : c->event_pool) cudaEventDestroy(e);
   if (c->ev_packed) cudaEventDestroy(c->ev_packed);
@@ -324,6 +325,7 @@ extern "C" int qdp_set_option(qdp_ctx c, int opt, long v) {
       c->block = (int)v;
       return QDP_OK;
     case QDP_OPT_DET_REDUCE: c->det_reduce = v ? 1 : 0; return QDP_OK;
+    case QDP_OPT_AUTOTUNE: c->autotune = v ? 1 : 0; return QDP_OK;
     case QDP_OPT_SELF_NCCL: {
       if (v) {
         int rc = comm_ensure_self(c);
@@ -345,6 +347,7 @@ extern "C" int qdp_get_option(qdp_ctx c, int opt, long *v) {
     case QDP_OPT_BLOCK: *v = c->block; return QDP_OK;
     case QDP_OPT_DET_REDUCE: *v = c->det_reduce; return QDP_OK;
     case QDP_OPT_SELF_NCCL: *v = c->self_nccl; return QDP_OK;
+    case QDP_OPT_AUTOTUNE: *v = c->autotune; return QDP_OK;
   }
   return set_error(c, QDP_EINVAL, "unknown option %d", opt);
 }
@@ -490,9 +493,10 @@ extern "C" int qdp_shift(qdp_field out, const qdp_field in, int mu, int sign) {
   if ((rc = check_pair(out, in))) return rc;
   qdp_ctx c = out->ctx;
   if (mu < 0 || mu > 3 || (sign != 1 && sign != -1)) return set_error(c, QDP_EINVAL, "shift: bad mu/sign");
-  if (out->kind != in->kind || in->kind == QDP_CLOVER) return set_error(c, QDP_EINVAL, "shift: fermion or gauge fields");
+  if (out->kind != in->kind || in->kind == QDP_CLOVER)
+    return set_error(c, QDP_EINVAL, "shift: fermion, gauge, colour- or spin-matrix fields of one kind");
   if (out == in || out->data == in->data) return set_error(c, QDP_EALIAS, "shift: out aliases in");
-  if (in->kind == QDP_FERMION) {
+  if (!is_gauge(in->kind)) {
     const bool ok = (in->subset == QDP_ALL && out->subset == QDP_ALL) ||
                     (in->subset != QDP_ALL && out->subset == 1 - in->subset);
     if (!ok) return set_error(c, QDP_EINVAL, "shift: parity p input needs a parity 1-p output");
@@ -662,6 +666,43 @@ extern "C" int qdp_cg_solve_mixed(qdp_field x, const qdp_field b, const qdp_fiel
   if (maxit < 0 || !(tol >= 0)) return set_error(c, QDP_EINVAL, "cg_mixed: bad tol/maxit");
   return cg_solve_mixed(x, b, U, A, Ainv, Us, As, Ainvs, mass, tol, delta, maxit, iters, reliable, resid_hist, hist_cap,
                         true_resid);
+}
+
+// ---------------------------------------------------------------------------- Table II expressions
+extern "C" int qdp_expr(int expr, qdp_field out, const qdp_field a, const qdp_field b, const qdp_field c) {
+  if (!out || !a || !b) return QDP_EINVAL;
+  qdp_ctx ctx = out->ctx;
+  int rc;
+  if (expr < QDP_EXPR_LCM || expr > QDP_EXPR_CLOVER) return set_error(ctx, QDP_EINVAL, "expr: unknown expression %d", expr);
+  if ((expr == QDP_EXPR_MATVEC) != (c != nullptr)) return set_error(ctx, QDP_EINVAL, "expr: c is used by MATVEC only");
+  static const int kinds[5][4] = {{QDP_COLORMATRIX, QDP_COLORMATRIX, QDP_COLORMATRIX, -1},
+                                  {QDP_FERMION, QDP_COLORMATRIX, QDP_FERMION, -1},
+                                  {QDP_SPINMATRIX, QDP_SPINMATRIX, QDP_SPINMATRIX, -1},
+                                  {QDP_FERMION, QDP_COLORMATRIX, QDP_FERMION, QDP_FERMION},
+                                  {QDP_FERMION, QDP_CLOVER, QDP_FERMION, -1}};
+  const qdp_field f[4] = {out, a, b, c};
+  for (int k = 0; k < 4; k++) {
+    if (!f[k]) continue;
+    if ((rc = check_pair(out, f[k]))) return rc;
+    if (f[k]->kind != kinds[expr][k]) return set_error(ctx, QDP_EINVAL, "expr: operand %d has the wrong kind", k);
+    if (k && !(f[k]->subset == out->subset || f[k]->subset == QDP_ALL))
+      return set_error(ctx, QDP_EINVAL, "expr: operand %d does not cover the output's subset", k);
+    if (k && f[k]->data == out->data) return set_error(ctx, QDP_EALIAS, "expr: out aliases operand %d", k);
+  }
+  return expr_eval(ctx, expr, out, a, b, c);
+}
+
+extern "C" int qdp_expr_block(qdp_ctx c, int expr, int prec, int *block, int *tuned) {
+  if (!c || expr < QDP_EXPR_LCM || expr > QDP_EXPR_CLOVER || !valid_prec(prec)) return QDP_EINVAL;
+  int bl = c->autotune ? 0 : 128, done = c->autotune ? 0 : 1;
+  for (const auto &kv : c->tune) {
+    if (kv.first / (1L << 40) != (long)expr * 2 + prec) continue;
+    bl = kv.second.state == 2 ? kv.second.best_block : kv.second.block;
+    done = kv.second.state == 2;
+  }
+  if (block) *block = bl;
+  if (tuned) *tuned = done;
+  return QDP_OK;
 }
 
 // ---------------------------------------------------------------------------- diagnostics

@@ -14,6 +14,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -403,7 +404,17 @@ __device__ __forceinline__ Spinor<R> clover_mul(const CloverView<R> &A, int cb, 
 #endif  // __CUDACC__
 
 // ------------------------------------------------------------------ host-side objects
-enum { KIND_FERMION = QDP_FERMION, KIND_GAUGE = QDP_GAUGE, KIND_CLOVER = QDP_CLOVER, KIND_GAUGE12 = QDP_GAUGE12 };
+enum { KIND_FERMION = QDP_FERMION, KIND_GAUGE = QDP_GAUGE, KIND_CLOVER = QDP_CLOVER, KIND_GAUGE12 = QDP_GAUGE12,
+       KIND_CMAT = QDP_COLORMATRIX, KIND_SMAT = QDP_SPINMATRIX };
+
+// Block-size autotuner state of one (expression, precision, volume).
+struct Tune {
+  int state = 0;           // 0 untouched, 1 probing, 2 done
+  int block = 1024, best_block = 0;
+  float best_ms = 0.f;
+  bool pending = false;    // an event pair of the last payload launch awaits reading
+  cudaEvent_t a = nullptr, b = nullptr;
+};
 inline bool is_gauge(int kind) { return kind == KIND_GAUGE || kind == KIND_GAUGE12; }
 
 size_t parity_block_bytes(int kind, int prec, int stride);  // bytes of one parity block
@@ -456,6 +467,8 @@ struct qdp_ctx_s {
   double work_flops[QDP_PK_COUNT] = {}, work_bytes[QDP_PK_COUNT] = {};
   double prof_ms[QDP_PK_COUNT] = {};
   std::vector<qdpb::ProfEvent> pending;
+  int autotune = 1;
+  std::map<long, qdpb::Tune> tune;
   std::vector<cudaEvent_t> event_pool;
   std::string last_error;
 };
@@ -537,6 +550,10 @@ int dslash(qdp_ctx ctx, int prec, const DslashArgs &a);
 int clover_build(qdp_ctx ctx, const qdp_field U, void *A, int A_subset, void *Ainv, int Ainv_subset,
                  double mass, double csw, int *singular_flag_host);
 int clover_apply(qdp_ctx ctx, int prec, void *out, const void *A, const void *in, int nblk);
+
+// expr.cu (Table II site expressions)
+int expr_eval(qdp_ctx ctx, int expr, qdp_field out, const qdp_field a, const qdp_field b, const qdp_field c);
+void tune_release(qdp_ctx ctx);
 
 // shift.cu
 int shift_field(qdp_ctx ctx, qdp_field out, const qdp_field in, int mu, int sign);

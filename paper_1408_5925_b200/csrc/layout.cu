@@ -7,12 +7,22 @@
 
 namespace qdpb {
 
-size_t host_site_reals(int kind) { return kind == KIND_FERMION ? 24 : is_gauge(kind) ? 72 : 288; }
+size_t host_site_reals(int kind) {
+  switch (kind) {
+    case KIND_FERMION: return 24;
+    case KIND_CMAT: return 18;
+    case KIND_SMAT: return 32;
+    case KIND_CLOVER: return 288;
+    default: return 72;  // gauge
+  }
+}
 
 size_t parity_block_bytes(int kind, int prec, int stride) {
   if (kind == KIND_FERMION) return fermion_block_bytes(prec, stride);
   if (kind == KIND_GAUGE) return (size_t)4 * stride * (prec == QDP_F64 ? 9 * 16 : 72);  // 4 mu per parity
   if (kind == KIND_GAUGE12) return (size_t)4 * stride * (prec == QDP_F64 ? 6 * 16 : 3 * 16);
+  if (kind == KIND_CMAT) return (size_t)stride * (prec == QDP_F64 ? 9 * 16 : 72);
+  if (kind == KIND_SMAT) return (size_t)stride * (prec == QDP_F64 ? 16 * 16 : 8 * 16);
   return (size_t)stride * (prec == QDP_F64 ? 36 * 16 : 18 * 16);
 }
 
@@ -27,6 +37,22 @@ SlotMap make_slot_map(int kind, int prec, int stride, int subset) {
       for (int k = 0; k < 12; k++) {
         if (prec == QDP_F64) { m.off[p][k] = base < 0 ? -1 : base + (long long)(k * S * 16); m.step[k] = 16; }
         else { m.off[p][k] = base < 0 ? -1 : base + (long long)((k / 2) * S * 16 + (k & 1) * 8); m.step[k] = 16; }
+      }
+    }
+  } else if (kind == KIND_CMAT || kind == KIND_SMAT) {
+    // colour matrix: fp64 double2[9], fp32 float4[4] + float2[1]; spin matrix: double2[16] / float4[8]
+    m.n = kind == KIND_CMAT ? 9 : 16;
+    const size_t blk = parity_block_bytes(kind, prec, stride);
+    for (int p = 0; p < 2; p++) {
+      const long long base = subset == QDP_ALL ? (long long)(p * blk) : (p == subset ? 0 : -1);
+      for (int k = 0; k < m.n; k++) {
+        long long o;
+        int st = 16;
+        if (prec == QDP_F64) o = (long long)(k * S * 16);
+        else if (kind == KIND_CMAT && k == 8) { o = (long long)(S * 64); st = 8; }
+        else o = (long long)((k / 2) * S * 16 + (k & 1) * 8);
+        m.off[p][k] = base < 0 ? -1 : base + o;
+        m.step[k] = st;
       }
     }
   } else if (kind == KIND_GAUGE12) {  // slot = mu*6 + e (rows 0,1)

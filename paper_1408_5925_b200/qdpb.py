@@ -18,13 +18,15 @@ LIB_PATH = os.environ.get("QDPB_LIB") or os.path.join(_HERE, "libqdpb.so")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "qdpb.h")
 
 QDP_F64, QDP_F32 = 0, 1
-QDP_FERMION, QDP_GAUGE, QDP_CLOVER, QDP_GAUGE12 = 0, 1, 2, 3
+QDP_FERMION, QDP_GAUGE, QDP_CLOVER, QDP_GAUGE12, QDP_COLORMATRIX, QDP_SPINMATRIX = range(6)
+QDP_EXPR_LCM, QDP_EXPR_UPSI, QDP_EXPR_SPMAT, QDP_EXPR_MATVEC, QDP_EXPR_CLOVER = range(5)
 QDP_ALL, QDP_EVEN, QDP_ODD = -1, 0, 1
 QDP_FORWARD, QDP_BACKWARD = 1, -1
 QDP_OK, QDP_NOT_CONVERGED = 0, 1
 QDP_EINVAL, QDP_ESHAPE, QDP_EPREC, QDP_EALIAS, QDP_ENOMEM = -1, -2, -3, -4, -5
 QDP_ECUDA, QDP_ENCCL, QDP_ESINGULAR, QDP_EUNSUPPORTED = -6, -7, -8, -9
-QDP_OPT_OVERLAP, QDP_OPT_SELF_HALO, QDP_OPT_PROFILE, QDP_OPT_BLOCK, QDP_OPT_DET_REDUCE, QDP_OPT_SELF_NCCL = range(6)
+(QDP_OPT_OVERLAP, QDP_OPT_SELF_HALO, QDP_OPT_PROFILE, QDP_OPT_BLOCK, QDP_OPT_DET_REDUCE, QDP_OPT_SELF_NCCL,
+ QDP_OPT_AUTOTUNE) = range(7)
 (QDP_PK_DSLASH, QDP_PK_DSLASH_EXT, QDP_PK_PACK, QDP_PK_BLAS, QDP_PK_REDUCE, QDP_PK_CLOVER,
  QDP_PK_SHIFT, QDP_PK_LAYOUT, QDP_PK_COUNT) = range(9)
 PK_NAMES = ["dslash", "dslash_ext", "pack", "blas", "reduce", "clover", "shift", "layout"]
@@ -63,6 +65,8 @@ _SIGS = {
                      ctypes.c_int, _dp],
     "qdp_cg_solve_mixed": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                            ctypes.c_int, _ip, _ip, _dp, ctypes.c_int, _dp],
+    "qdp_expr": [ctypes.c_int, _vp, _vp, _vp, _vp],
+    "qdp_expr_block": [_vp, ctypes.c_int, ctypes.c_int, _ip, _ip],
     "qdp_strerror": [ctypes.c_int],
     "qdp_last_error": [_vp],
     "qdp_profile_query": [_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_long), _dp],
@@ -248,7 +252,8 @@ def qdp_field_import(f: Field, host) -> None:
 
 def _host_shape(f: Field):
     hb, _ = qdp_field_bytes(f.ctx, f.kind, f.prec, f.subset)
-    per = {QDP_FERMION: (4, 3, 2), QDP_GAUGE: (4, 3, 3, 2), QDP_CLOVER: (12, 12, 2), QDP_GAUGE12: (4, 3, 3, 2)}[f.kind]
+    per = {QDP_FERMION: (4, 3, 2), QDP_GAUGE: (4, 3, 3, 2), QDP_CLOVER: (12, 12, 2), QDP_GAUGE12: (4, 3, 3, 2),
+           QDP_COLORMATRIX: (3, 3, 2), QDP_SPINMATRIX: (4, 4, 2)}[f.kind]
     isz = 8 if f.prec == QDP_F64 else 4
     n = hb // (isz * int(np.prod(per)))
     return (n,) + per, (np.float64 if f.prec == QDP_F64 else np.float32)
@@ -332,6 +337,18 @@ def qdp_cg_solve_mixed(x: Field, b: Field, U: Field, A=None, Ainv=None, U_s: Fie
     n = iters.value
     return dict(status=st, iters=n, reliable=rel.value, hist=np.array(hist[:min(n + 1, hist_cap)]),
                 true_resid=tr.value if true_resid else None)
+
+
+def qdp_expr(expr: int, out: Field, a: Field, b: Field, c: Field = None) -> None:
+    """Table II site expression on out's subset."""
+    _check(lib().qdp_expr(int(expr), out, a, b, c), out.ctx)
+
+
+def qdp_expr_block(ctx: Ctx, expr: int, prec: int):
+    """(block size, tuned) of the paper's autotuner for (expr, prec)."""
+    b, t = ctypes.c_int(), ctypes.c_int()
+    _check(lib().qdp_expr_block(ctx, int(expr), int(prec), ctypes.byref(b), ctypes.byref(t)), ctx)
+    return b.value, bool(t.value)
 
 
 # ------------------------------------------------------------------ diagnostics

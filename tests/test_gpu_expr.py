@@ -1,0 +1,141 @@
+"""Table II site expressions (qdp_expr) against the oracle, the paper's block-size autotuner
+(PAPER.md:238), and the Table II flop/byte accounting against the values the paper prints
+(tests/golden/table2_flop_byte.json)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import fieldgen
+import oracle
+from _physics import rel_site_err
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+TOL = {0: 1e-14, 1: 2e-6}
+
+
+@pytest.fixture(scope="module")
+def q():
+    from paper_1408_5925_b200 import qdpb
+    qdpb.lib()
+    return qdpb
+
+
+def _host(a, prec):
+    return np.ascontiguousarray(a, dtype=np.float64 if prec == 0 else np.float32)
+
+
+def _round(a, prec):
+    return a if prec == 0 else a.astype(np.float32).astype(np.float64)
+
+
+def _field(q, c, kind, prec, subset, host):
+    f = q.qdp_field_alloc(c, kind, prec, subset)
+    q.qdp_field_import(f, _host(host, prec))
+    return f
+
+
+def _inputs(L, prec):
+    V = fieldgen.volume(L)
+    g = lambda seed, shape: _round(fieldgen.gaussian(seed, int(np.prod(shape))).reshape(shape), prec)
+    return dict(u=g(11, (V, 3, 3, 2)), v=g(12, (V, 3, 3, 2)), s=g(13, (V, 4, 4, 2)), t=g(14, (V, 4, 4, 2)),
+                p1=g(15, (V, 4, 3, 2)), p2=g(16, (V, 4, 3, 2)))
+
+
+def _err(got, ref):
+    return rel_site_err(got.reshape(len(got), -1), ref.reshape(len(ref), -1))
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+@pytest.mark.parametrize("subset", [-1, 0, 1])
+def test_expressions_vs_oracle(q, prec, subset):
+    L = (8, 6, 4, 10)
+    d = _inputs(L, prec)
+    A = _round(oracle.clover_build(fieldgen.random_gauge(L, 17), L, 0.1, 1.2), prec)
+    sites = np.arange(fieldgen.volume(L)) if subset < 0 else fieldgen.cb_sites(L, subset)
+    c = q.qdp_init(L)
+    try:
+        F = lambda kind, arr: _field(q, c, kind, prec, subset, np.ascontiguousarray(arr[sites]))
+        fu, fv = F(q.QDP_COLORMATRIX, d["u"]), F(q.QDP_COLORMATRIX, d["v"])
+        fs, ft = F(q.QDP_SPINMATRIX, d["s"]), F(q.QDP_SPINMATRIX, d["t"])
+        f1, f2 = F(q.QDP_FERMION, d["p1"]), F(q.QDP_FERMION, d["p2"])
+        fA = F(q.QDP_CLOVER, A)
+        om = q.qdp_field_alloc(c, q.QDP_COLORMATRIX, prec, subset)
+        osm = q.qdp_field_alloc(c, q.QDP_SPINMATRIX, prec, subset)
+        of = q.qdp_field_alloc(c, q.QDP_FERMION, prec, subset)
+        for _ in range(8):  # several payload launches: the autotuner walks through block sizes
+            q.qdp_expr(q.QDP_EXPR_LCM, om, fu, fv)
+            assert _err(q.qdp_field_export(om).astype(np.float64), oracle.lcm(d["u"], d["v"])[sites]) <= TOL[prec]
+            q.qdp_expr(q.QDP_EXPR_UPSI, of, fu, f1)
+            assert _err(q.qdp_field_export(of).astype(np.float64), oracle.upsi(d["u"], d["p1"])[sites]) <= TOL[prec]
+            q.qdp_expr(q.QDP_EXPR_SPMAT, osm, fs, ft)
+            assert _err(q.qdp_field_export(osm).astype(np.float64), oracle.spmat(d["s"], d["t"])[sites]) <= TOL[prec]
+            q.qdp_expr(q.QDP_EXPR_MATVEC, of, fu, f1, f2)
+            ref = oracle.matvec(d["u"], d["p1"], d["p2"])[sites]
+            assert _err(q.qdp_field_export(of).astype(np.float64), ref) <= TOL[prec]
+            q.qdp_expr(q.QDP_EXPR_CLOVER, of, fA, f1)
+            ref = oracle.clover_apply(A, d["p1"], L)[sites]
+            assert _err(q.qdp_field_export(of).astype(np.float64), ref) <= TOL[prec]
+        for e in range(5):
+            block, tuned = q.qdp_expr_block(c, e, prec)
+            assert tuned and block in (32, 64, 128, 256, 512, 1024)
+        with pytest.raises(q.QdpError) as err:
+            q.qdp_expr(q.QDP_EXPR_LCM, om, fu, f1)
+        assert err.value.status == q.QDP_EINVAL
+    finally:
+        q.qdp_finalize(c)
+
+
+def test_autotuner_halves_on_failed_launch(q):
+    """fp64 spmat needs more than 64 registers, so its 1024-thread launch fails and the tuner
+    must halve; the tuned size then stays fixed."""
+    L = (8, 8, 8, 8)
+    d = _inputs(L, 0)
+    c = q.qdp_init(L)
+    try:
+        fs = _field(q, c, q.QDP_SPINMATRIX, 0, q.QDP_ALL, d["s"])
+        ft = _field(q, c, q.QDP_SPINMATRIX, 0, q.QDP_ALL, d["t"])
+        o = q.qdp_field_alloc(c, q.QDP_SPINMATRIX, 0, q.QDP_ALL)
+        q.qdp_expr(q.QDP_EXPR_SPMAT, o, fs, ft)
+        b0, tuned = q.qdp_expr_block(c, q.QDP_EXPR_SPMAT, 0)
+        assert b0 <= 512 and not tuned
+        for _ in range(10):
+            q.qdp_expr(q.QDP_EXPR_SPMAT, o, fs, ft)
+        b1, tuned = q.qdp_expr_block(c, q.QDP_EXPR_SPMAT, 0)
+        assert tuned and b1 <= b0
+        for _ in range(3):
+            q.qdp_expr(q.QDP_EXPR_SPMAT, o, fs, ft)
+        assert q.qdp_expr_block(c, q.QDP_EXPR_SPMAT, 0) == (b1, True)
+    finally:
+        q.qdp_finalize(c)
+
+
+def test_table2_accounting_matches_paper(q):
+    """The library's per-site work counters reproduce the flop/byte column of Table II
+    (matvec with U1 counted twice, as the paper does)."""
+    gold = json.load(open(os.path.join(HERE, "golden", "table2_flop_byte.json")))["flop_per_byte_dp"]
+    L = (4, 4, 4, 4)
+    V = fieldgen.volume(L)
+    d = _inputs(L, 0)
+    c = q.qdp_init(L)
+    try:
+        fu, fv = _field(q, c, q.QDP_COLORMATRIX, 0, -1, d["u"]), _field(q, c, q.QDP_COLORMATRIX, 0, -1, d["v"])
+        fs, ft = _field(q, c, q.QDP_SPINMATRIX, 0, -1, d["s"]), _field(q, c, q.QDP_SPINMATRIX, 0, -1, d["t"])
+        f1, f2 = _field(q, c, q.QDP_FERMION, 0, -1, d["p1"]), _field(q, c, q.QDP_FERMION, 0, -1, d["p2"])
+        fA = q.qdp_field_alloc(c, q.QDP_CLOVER, 0, -1)
+        om, osm, of = (q.qdp_field_alloc(c, k, 0, -1) for k in (q.QDP_COLORMATRIX, q.QDP_SPINMATRIX, q.QDP_FERMION))
+        cases = {"lcm": (q.QDP_EXPR_LCM, om, fu, fv, None), "upsi": (q.QDP_EXPR_UPSI, of, fu, f1, None),
+                 "spmat": (q.QDP_EXPR_SPMAT, osm, fs, ft, None), "matvec": (q.QDP_EXPR_MATVEC, of, fu, f1, f2),
+                 "clover": (q.QDP_EXPR_CLOVER, of, fA, f1, None)}
+        for name, (e, o, a, b, cc) in cases.items():
+            q.qdp_profile_reset(c)
+            q.qdp_expr(e, o, a, b, cc)
+            flops, nbytes = q.qdp_profile_work(c, q.QDP_PK_BLAS)
+            if name == "matvec":
+                nbytes += 144 * V  # the paper counts U1 as loaded twice
+            assert round(flops / nbytes, 3) == pytest.approx(gold[name], abs=0.006), name
+            assert flops / V == {"lcm": 198, "upsi": 264, "spmat": 480, "matvec": 552, "clover": 504}[name]
+    finally:
+        q.qdp_finalize(c)
