@@ -184,6 +184,15 @@ template <typename R, int EXPR>
 static cudaError_t launch(qdp_ctx ctx, const ExprArgs &e, int block) {
   const Geom &g = ctx->geom;
   const long n = (long)e.n_blocks * g.Vh;
+  // A launch with more threads than the kernel's register budget allows fails with
+  // cudaErrorLaunchOutOfResources; report that outcome without issuing the failing launch.
+  static int max_threads = 0;
+  if (!max_threads) {
+    cudaFuncAttributes attr;
+    if (cudaFuncGetAttributes(&attr, expr_kernel<R, EXPR>) != cudaSuccess) return cudaGetLastError();
+    max_threads = attr.maxThreadsPerBlock;
+  }
+  if (block > max_threads) return cudaErrorLaunchOutOfResources;
   expr_kernel<R, EXPR><<<(unsigned)((n + block - 1) / block), block, 0, ctx->stream>>>(g, e);
   return cudaGetLastError();
 }
@@ -212,6 +221,7 @@ void tune_release(qdp_ctx ctx) {
 // start at the largest block (1024), halve while the launch fails; once a launch
 // succeeded, every further payload launch probes the next smaller block until its time exceeds
 // the best seen by more than 33%; then the best block is used for good.  Only payload launches.
+// (A launch "fails" when the block exceeds the kernel's maxThreadsPerBlock -- checked up front.)
 int expr_eval(qdp_ctx ctx, int expr, qdp_field out, const qdp_field a, const qdp_field b, const qdp_field c) {
   const Geom &g = ctx->geom;
   const int prec = out->prec;
