@@ -192,6 +192,7 @@ def run_native(args, rank, world, local_rank):
     P = qdist.proc_grid_for(world, gdims, split=(3,))
     ctx = qdist.bootstrap(gdims, P, stream=stream)
     q.qdp_set_option(ctx, q.QDP_OPT_OVERLAP, 0 if args.no_overlap else 1)
+    q.qdp_set_option(ctx, q.QDP_OPT_P2P, 1 if args.p2p else 0)
     L = LOCAL
     Vh = L[0] * L[1] * L[2] * L[3] // 2
 
@@ -343,6 +344,7 @@ def run_native(args, rank, world, local_rank):
         "parity": parity,
         "time_to_solution_1e-10": tts,
         "overlap": not args.no_overlap,
+        "halo": "p2p" if args.p2p else "nccl",
     }
     if rank == 0:
         print(json.dumps(out), flush=True)
@@ -372,6 +374,7 @@ def main():
     ap.add_argument("--ref-iters", type=int, default=1)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-overlap", action="store_true")
+    ap.add_argument("--p2p", action="store_true", help="peer-to-peer (CUDA IPC) halos instead of NCCL")
     ap.add_argument("--no-tts", dest="tts", action="store_false", help="skip the time-to-solution comparison")
     ap.add_argument("--check", action="store_true", default=True)
     ap.add_argument("--no-check", dest="check", action="store_false")

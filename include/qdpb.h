@@ -117,8 +117,17 @@ int qdp_get_geometry(qdp_ctx ctx, int local_dims[4], int proc_coords[4]);
  *                     rank (a one-rank communicator is created on first use; QDP_ENCCL if
  *                     NCCL cannot be loaded) instead of packing straight into the ghost
  *                     buffers -- the NCCL code path of a multi-GPU run, on one GPU. */
+ /*  QDP_OPT_P2P        1: dslash halos go peer to peer instead of through NCCL: every rank
+ *                     maps its neighbours' ghost buffers (CUDA IPC over NVLink / NVSwitch,
+ *                     exchanged collectively at first use), the face-packing kernel stores
+ *                     straight into them and release-signals a flag, the neighbour's stream
+ *                     acquires it before the exterior kernel and acknowledges afterwards
+ *                     (two slots per face).  Self-halo dims use the same protocol on this rank.
+ *                     A flag wait that never completes surfaces as QDP_ECUDA at the next
+ *                     synchronising call. */
 enum { QDP_OPT_OVERLAP = 0, QDP_OPT_SELF_HALO = 1, QDP_OPT_PROFILE = 2, QDP_OPT_BLOCK = 3,
-       QDP_OPT_DET_REDUCE = 4, QDP_OPT_SELF_NCCL = 5, QDP_OPT_AUTOTUNE = 6 /* see qdp_expr */ };
+       QDP_OPT_DET_REDUCE = 4, QDP_OPT_SELF_NCCL = 5, QDP_OPT_AUTOTUNE = 6 /* see qdp_expr */,
+       QDP_OPT_P2P = 7 };
 int qdp_set_option(qdp_ctx ctx, int option, long value);
 int qdp_get_option(qdp_ctx ctx, int option, long *value);
 

@@ -255,6 +255,7 @@ extern "C" int qdp_finalize(qdp_ctx c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   resolve_profile(c);
   tune_release(c);
+  p2p_destroy(c);
   comm_destroy(c);
   for (auto e : c->event_pool) cudaEventDestroy(e);
   if (c->ev_packed) cudaEventDestroy(c->ev_packed);
@@ -296,7 +297,7 @@ extern "C" int qdp_set_stream(qdp_ctx c, void *s) {
 extern "C" int qdp_synchronize(qdp_ctx c) {
   if (!c) return QDP_EINVAL;
   QDP_CUDA(c, cudaStreamSynchronize(c->stream));
-  return QDP_OK;
+  return p2p_check(c);
 }
 
 extern "C" int qdp_get_geometry(qdp_ctx c, int local_dims[4], int proc_coords[4]) {
@@ -326,6 +327,10 @@ extern "C" int qdp_set_option(qdp_ctx c, int opt, long v) {
       return QDP_OK;
     case QDP_OPT_DET_REDUCE: c->det_reduce = v ? 1 : 0; return QDP_OK;
     case QDP_OPT_AUTOTUNE: c->autotune = v ? 1 : 0; return QDP_OK;
+    case QDP_OPT_P2P:
+      if (v && c->nranks > 1 && !c->comm) return set_error(c, QDP_ENCCL, "p2p: needs the NCCL communicator for setup");
+      c->p2p_on = v ? 1 : 0;
+      return QDP_OK;
     case QDP_OPT_SELF_NCCL: {
       if (v) {
         int rc = comm_ensure_self(c);
@@ -348,6 +353,7 @@ extern "C" int qdp_get_option(qdp_ctx c, int opt, long *v) {
     case QDP_OPT_DET_REDUCE: *v = c->det_reduce; return QDP_OK;
     case QDP_OPT_SELF_NCCL: *v = c->self_nccl; return QDP_OK;
     case QDP_OPT_AUTOTUNE: *v = c->autotune; return QDP_OK;
+    case QDP_OPT_P2P: *v = c->p2p_on; return QDP_OK;
   }
   return set_error(c, QDP_EINVAL, "unknown option %d", opt);
 }

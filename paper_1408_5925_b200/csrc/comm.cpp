@@ -156,6 +156,12 @@ int comm_allgather_f64(qdp_ctx ctx, const double *send, double *recv, int count,
   return QDP_OK;
 }
 
+int comm_allgather_bytes(qdp_ctx ctx, const void *send, void *recv, size_t bytes, cudaStream_t stream) {
+  if (!ctx->comm) return set_error(ctx, QDP_ENCCL, "allgather without a communicator");
+  QDPB_NCCL(ctx, g_nccl.AllGather(send, recv, bytes, ncclChar, ctx->comm->comm, stream));
+  return QDP_OK;
+}
+
 int comm_allreduce_f64(qdp_ctx ctx, double *buf, int count, cudaStream_t stream) {
   if (!ctx->comm) return set_error(ctx, QDP_ENCCL, "allreduce without a communicator");
   QDPB_NCCL(ctx, g_nccl.AllReduce(buf, buf, (size_t)count, ncclDouble, ncclSum, ctx->comm->comm, stream));

@@ -155,6 +155,11 @@ template <typename R, int REC = 18> struct KParams {
   // fused Re<dotx, out>: per-block partials
   FermView<R> dotx;
   double *dot_part;
+  // peer-to-peer halo (QDP_OPT_P2P): after its face stores, the last pack block of dim mu
+  // release-stores `seq` into the receivers' ready flags sig[mu][0..1] (pack_counter counts blocks)
+  unsigned *pack_counter[4];
+  unsigned *sig[4][2];
+  unsigned seq;
 };
 
 template <typename R, int MU, typename KP>
@@ -278,33 +283,50 @@ template <typename R, int REC, bool G5IN>
 __global__ void __launch_bounds__(128) pack_kernel(const Geom g, const KParams<R, REC> P, int mu) {
   const int n = g.faceVh[mu];
   int f = blockIdx.x * blockDim.x + threadIdx.x;
-  if (f >= 2 * n) return;
-  const int q = 1 - P.parity;
-  const bool fwd = f >= n;
-  if (fwd) f -= n;
-  int c[4];
-  face_coords(g, mu, fwd ? g.L[mu] - 1 : 0, f, q, c);
-  const int cb = coords_cb(g, c);
-  Spinor<R> s = P.psi.load(cb);
-  if (G5IN) g5(s);
-  Half<R> h;
-  if (!fwd) {
-    switch (mu) {
-      case 0: h = project<0, -1>(s); break;
-      case 1: h = project<1, -1>(s); break;
-      case 2: h = project<2, -1>(s); break;
-      default: h = project<3, -1>(s); break;
+  if (f < 2 * n) {
+    const int q = 1 - P.parity;
+    const bool fwd = f >= n;
+    if (fwd) f -= n;
+    int c[4];
+    face_coords(g, mu, fwd ? g.L[mu] - 1 : 0, f, q, c);
+    const int cb = coords_cb(g, c);
+    Spinor<R> s = P.psi.load(cb);
+    if (G5IN) g5(s);
+    Half<R> h;
+    if (!fwd) {
+      switch (mu) {
+        case 0: h = project<0, -1>(s); break;
+        case 1: h = project<1, -1>(s); break;
+        case 2: h = project<2, -1>(s); break;
+        default: h = project<3, -1>(s); break;
+      }
+      HalfGhost<R>::store(P.dst[mu][0], n, f, h);
+    } else {
+      switch (mu) {
+        case 0: h = project<0, +1>(s); break;
+        case 1: h = project<1, +1>(s); break;
+        case 2: h = project<2, +1>(s); break;
+        default: h = project<3, +1>(s); break;
+      }
+      Link<R> u = P.U.load(mu, q, cb);
+      HalfGhost<R>::store(P.dst[mu][1], n, f, mul_link_dag(u, h));
     }
-    HalfGhost<R>::store(P.dst[mu][0], n, f, h);
-  } else {
-    switch (mu) {
-      case 0: h = project<0, +1>(s); break;
-      case 1: h = project<1, +1>(s); break;
-      case 2: h = project<2, +1>(s); break;
-      default: h = project<3, +1>(s); break;
+  }
+  // Peer-to-peer halo: the face stores above may target a neighbour's memory over NVLink.
+  // Every thread fences them at system scope; the last block to finish publishes `seq` to the
+  // two receivers' ready flags with release semantics (they acquire before reading).
+  if (P.pack_counter[mu]) {
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned prev = atomicAdd(P.pack_counter[mu], 1u);
+      if (prev == gridDim.x - 1) {
+        *P.pack_counter[mu] = 0u;
+        __threadfence_system();
+        st_release_sys(P.sig[mu][0], P.seq);
+        st_release_sys(P.sig[mu][1], P.seq);
+      }
     }
-    Link<R> u = P.U.load(mu, q, cb);
-    HalfGhost<R>::store(P.dst[mu][1], n, f, mul_link_dag(u, h));
   }
 }
 
@@ -471,21 +493,30 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
     P.dot_part = ctx->red_partials;
   }
 
+  unsigned seq = 0;
+  if (halo && ctx->p2p_on) {
+    // peer-to-peer: pack straight into the neighbours' ghost slots, flags instead of NCCL (p2p.cu)
+    seq = p2p_next_seq(ctx, prec);
+    if ((rc = p2p_prepare(ctx, prec, seq, P.dst, P.ghost, P.pack_counter, P.sig))) return rc;
+    P.seq = seq;
+  }
   if (halo) {
-    if ((rc = ensure_halo(ctx, prec))) return rc;
-    // destinations: self-halo dims pack straight into our own ghost buffers (the peer is
-    // this rank); communicated dims pack into send buffers for NCCL.
     bool any_comm = false;
     size_t face_bytes[4] = {0, 0, 0, 0};
-    for (int mu = 0; mu < 4; mu++) {
-      if (!((g.part >> mu) & 1)) continue;
-      const bool self = direct_self(ctx, mu);
-      any_comm |= !self;
-      face_bytes[mu] = (size_t)g.faceVh[mu] * 12 * sizeof(R);
-      P.dst[mu][0] = self ? ctx->halo_recv[prec][mu][1] : ctx->halo_send[prec][mu][0];
-      P.dst[mu][1] = self ? ctx->halo_recv[prec][mu][0] : ctx->halo_send[prec][mu][1];
-      P.ghost[mu][0] = ctx->halo_recv[prec][mu][0];
-      P.ghost[mu][1] = ctx->halo_recv[prec][mu][1];
+    if (!seq) {
+      if ((rc = ensure_halo(ctx, prec))) return rc;
+      // destinations: self-halo dims pack straight into our own ghost buffers (the peer is
+      // this rank); communicated dims pack into send buffers for NCCL.
+      for (int mu = 0; mu < 4; mu++) {
+        if (!((g.part >> mu) & 1)) continue;
+        const bool self = direct_self(ctx, mu);
+        any_comm |= !self;
+        face_bytes[mu] = (size_t)g.faceVh[mu] * 12 * sizeof(R);
+        P.dst[mu][0] = self ? ctx->halo_recv[prec][mu][1] : ctx->halo_send[prec][mu][0];
+        P.dst[mu][1] = self ? ctx->halo_recv[prec][mu][0] : ctx->halo_send[prec][mu][1];
+        P.ghost[mu][0] = ctx->halo_recv[prec][mu][0];
+        P.ghost[mu][1] = ctx->halo_recv[prec][mu][1];
+      }
     }
     for (int mu = 0; mu < 4; mu++) {
       if (!((g.part >> mu) & 1)) continue;
@@ -513,6 +544,7 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
     if (overlap) QDP_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_comm, 0));
     for (int mu = 0; mu < 4; mu++) {
       if (!((g.part >> mu) & 1)) continue;
+      if (seq && (rc = p2p_wait_ready(ctx, prec, mu, seq))) return rc;
       ProfEvent ev;
       prof_begin(ctx, QDP_PK_DSLASH_EXT, &ev);
       // ghost read, forward-face link, output read-modify-write (+ clover on CLOVINV)
@@ -523,6 +555,7 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
       if (a.epi == EPI_CLOVINV) launch_ext<R, REC, EPI_CLOVINV>(ctx, P, mu, a.g5_out, nullptr);
       else launch_ext<R, REC, EPI_PLAIN>(ctx, P, mu, a.g5_out, dp);
       if ((rc = prof_end(ctx, &ev))) return rc;
+      if (seq && (rc = p2p_ack(ctx, prec, mu, seq))) return rc;
     }
   } else {
     if ((rc = launch_main_epi<R, REC>(ctx, a, P, false, block))) return rc;

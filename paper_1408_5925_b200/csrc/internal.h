@@ -163,6 +163,16 @@ __device__ __forceinline__ void st_stream(double2 *p, double2 v) { __stcs(p, v);
 __device__ __forceinline__ void st_stream(float4 *p, float4 v) { __stcs(p, v); }
 __device__ __forceinline__ void st_stream(float2 *p, float2 v) { __stcs(p, v); }
 
+// System-scope release / acquire on 32-bit flags (peer-to-peer halo signalling, p2p.cu).
+__device__ __forceinline__ void st_release_sys(unsigned *p, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // Spinor: 12 complex, index 3*spin + colour.
 template <typename R> struct Spinor { cx<R> c[12]; };
 // Half spinor: 6 complex, index 3*h + colour (h = 0,1).
@@ -421,6 +431,7 @@ size_t parity_block_bytes(int kind, int prec, int stride);  // bytes of one pari
 size_t host_site_reals(int kind);                           // 24 / 72 / 288
 
 struct Comm;  // comm.cpp
+struct P2P;   // p2p.cu
 
 struct ProfEvent {
   int cls;
@@ -461,6 +472,8 @@ struct qdp_ctx_s {
   void *halo_send[2][4][2] = {}, *halo_recv[2][4][2] = {};
   size_t halo_bytes[2] = {0, 0};
   qdpb::Comm *comm = nullptr;
+  qdpb::P2P *p2p = nullptr;  // peer-to-peer halo state (QDP_OPT_P2P)
+  int p2p_on = 0;
   int neighbour[4][2];  // ranks of -mu / +mu neighbours
   // profiling / counting
   long launches[QDP_PK_COUNT] = {};
@@ -551,6 +564,21 @@ int clover_build(qdp_ctx ctx, const qdp_field U, void *A, int A_subset, void *Ai
                  double mass, double csw, int *singular_flag_host);
 int clover_apply(qdp_ctx ctx, int prec, void *out, const void *A, const void *in, int nblk);
 
+// p2p.cu: peer-to-peer halo.  For dslash call `seq` (1, 2, ...; identical on every rank):
+//   p2p_prepare: make sure the buffers exist and are mapped (collective on first use), wait
+//     (on the stream) until the receivers consumed slot seq&1 two calls ago, and return the
+//     pack destinations (the neighbours' ghost slots), this rank's ghost slots to read, the
+//     pack-block counters and the neighbours' ready flags to signal;
+//   p2p_wait_ready: stream-wait until both ghosts of dim mu carry `seq` (before the exterior);
+//   p2p_ack: tell the two senders of dim mu that their slot was consumed (after the exterior).
+int p2p_prepare(qdp_ctx ctx, int prec, unsigned seq, void *dst[4][2], const void *ghost[4][2], unsigned *counter[4],
+                unsigned *sig[4][2]);
+int p2p_wait_ready(qdp_ctx ctx, int prec, int mu, unsigned seq);
+int p2p_ack(qdp_ctx ctx, int prec, int mu, unsigned seq);
+int p2p_check(qdp_ctx ctx);  // QDP_ECUDA if a flag wait timed out
+unsigned p2p_next_seq(qdp_ctx ctx, int prec);
+void p2p_destroy(qdp_ctx ctx);
+
 // expr.cu (Table II site expressions)
 int expr_eval(qdp_ctx ctx, int expr, qdp_field out, const qdp_field a, const qdp_field b, const qdp_field c);
 void tune_release(qdp_ctx ctx);
@@ -575,6 +603,7 @@ int comm_exchange(qdp_ctx ctx, int prec, const size_t face_bytes[4], cudaStream_
 int comm_sendrecv(qdp_ctx ctx, const void *send, size_t bytes, int to, void *recv, int from, cudaStream_t stream);
 int comm_allgather_f64(qdp_ctx ctx, const double *send, double *recv, int count, cudaStream_t stream);
 int comm_allreduce_f64(qdp_ctx ctx, double *buf, int count, cudaStream_t stream);
+int comm_allgather_bytes(qdp_ctx ctx, const void *send, void *recv, size_t bytes, cudaStream_t stream);
 
 // A partitioned dim whose neighbour is this rank and whose faces are written straight into
 // the local ghost buffers (self-halo without NCCL).

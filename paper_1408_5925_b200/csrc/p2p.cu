@@ -1,0 +1,217 @@
+// p2p.cu -- peer-to-peer halo exchange over NVLink / NVSwitch ("B200-native
+// upgrade"; the face exchange of PAPER.md:208-214 without a separate communication call).
+//
+// Every rank exports its ghost buffers (two slots per face, alternating by call) and a small
+// flag block through CUDA IPC; the neighbours map them.  Per EO dslash call `seq`:
+//   sender : stream-wait until the receiver acknowledged slot seq&1 of call seq-2 (WAR), then
+//            the pack kernel stores the projected faces straight into the receiver's ghost slot
+//            and its last block release-stores seq into the receiver's ready flag;
+//   receiver: interior kernel runs meanwhile; stream-wait (acquire) for ready == seq, exterior
+//            kernel, then release-store seq into the sender's ack flag.
+// A dim with one rank (self-halo) maps "the neighbour" to this rank, so the whole protocol runs
+// and is tested on one GPU.  Waits are 1-thread kernels that poll with a bounded budget and
+// raise an error flag instead of hanging (checked by p2p_check).
+#include <string.h>
+
+#include <algorithm>
+#include <map>
+
+#include "internal.h"
+
+namespace qdpb {
+
+enum { F_READY = 0, F_ACK = 1, F_COUNT = 2 };
+// flag block of one rank: unsigned [2 prec][3 kinds][4 mu][2 dir], then the error word
+constexpr int NFLAGS = 2 * 3 * 4 * 2;
+inline size_t fidx(int prec, int kind, int mu, int d) { return ((size_t)(prec * 3 + kind) * 4 + mu) * 2 + d; }
+
+struct P2P {
+  unsigned *flags = nullptr;  // this rank's flag block (+ error word at NFLAGS)
+  size_t slot_bytes[2] = {0, 0};
+  void *recv[2][4][2] = {};           // this rank's ghost buffers (2 slots each)
+  void *peer_recv[2][4][2] = {};      // [prec][mu][d]: ghost slots channel d writes into
+  unsigned *peer_flags[4][2] = {};    // flag block of the -mu (d = 0) / +mu (d = 1) neighbour
+  unsigned seq[2] = {0, 0};
+  std::vector<void *> opened;         // IPC mappings
+  std::map<int, unsigned *> flag_map;  // rank -> mapped flag block
+};
+
+struct HandleMsg {
+  cudaIpcMemHandle_t recv[4][2];
+  cudaIpcMemHandle_t flags;
+};
+
+constexpr long WAIT_POLLS = 1L << 26;  // ~ 10 s of 128 ns sleeps before declaring a timeout
+
+__global__ void p2p_wait_kernel(const unsigned *f0, const unsigned *f1, unsigned expect, unsigned *err) {
+  if (threadIdx.x) return;
+  long n = 0;
+  while ((int)(ld_acquire_sys(f0) - expect) < 0 || (int)(ld_acquire_sys(f1) - expect) < 0) {
+    if (++n > WAIT_POLLS) {
+      atomicExch(err, 1u);
+      return;
+    }
+    __nanosleep(128);
+  }
+}
+
+__global__ void p2p_signal_kernel(unsigned *f0, unsigned *f1, unsigned v) {
+  if (threadIdx.x) return;
+  st_release_sys(f0, v);
+  st_release_sys(f1, v);
+}
+
+static bool remote_dim(qdp_ctx ctx, int mu) { return ((ctx->geom.part >> mu) & 1) && ctx->pgrid[mu] > 1; }
+
+static int p2p_setup(qdp_ctx ctx, int prec) {
+  const Geom &g = ctx->geom;
+  if (!ctx->p2p) {
+    P2P *p = new P2P();
+    if (cudaMalloc((void **)&p->flags, sizeof(unsigned) * (NFLAGS + 1)) != cudaSuccess) {
+      cudaGetLastError();
+      delete p;
+      return set_error(ctx, QDP_ENOMEM, "p2p flags");
+    }
+    QDP_CUDA(ctx, cudaMemset(p->flags, 0, sizeof(unsigned) * (NFLAGS + 1)));
+    ctx->p2p = p;
+  }
+  P2P *p = ctx->p2p;
+  size_t need = 0;
+  bool any_remote = false;
+  for (int mu = 0; mu < 4; mu++)
+    if ((g.part >> mu) & 1) {
+      need = std::max(need, (size_t)g.faceVh[mu] * 12 * (prec == QDP_F64 ? 8 : 4));  // half spinors
+      any_remote |= remote_dim(ctx, mu);
+    }
+  if (p->slot_bytes[prec] >= need) return QDP_OK;
+  if (p->slot_bytes[prec]) return set_error(ctx, QDP_EUNSUPPORTED, "p2p: the partition changed after first use");
+  QDP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  for (int mu = 0; mu < 4; mu++)
+    if ((g.part >> mu) & 1)
+      for (int d = 0; d < 2; d++) {
+        if (cudaMalloc(&p->recv[prec][mu][d], 2 * need) != cudaSuccess) {
+          cudaGetLastError();
+          return set_error(ctx, QDP_ENOMEM, "p2p ghost buffers");
+        }
+        QDP_CUDA(ctx, cudaMemset(p->recv[prec][mu][d], 0, 2 * need));
+      }
+  // self dims: "the neighbour" is this rank
+  for (int mu = 0; mu < 4; mu++)
+    if (((g.part >> mu) & 1) && !remote_dim(ctx, mu)) {
+      p->peer_recv[prec][mu][0] = p->recv[prec][mu][1];
+      p->peer_recv[prec][mu][1] = p->recv[prec][mu][0];
+      p->peer_flags[mu][0] = p->peer_flags[mu][1] = p->flags;
+    }
+  if (any_remote) {
+    // exchange IPC handles of every rank's ghost buffers and flag block (allgather over NCCL)
+    HandleMsg mine;
+    memset(&mine, 0, sizeof(mine));
+    for (int mu = 0; mu < 4; mu++)
+      if ((g.part >> mu) & 1)
+        for (int d = 0; d < 2; d++) QDP_CUDA(ctx, cudaIpcGetMemHandle(&mine.recv[mu][d], p->recv[prec][mu][d]));
+    QDP_CUDA(ctx, cudaIpcGetMemHandle(&mine.flags, p->flags));
+    std::vector<HandleMsg> all(ctx->nranks);
+    char *dev = nullptr;
+    QDP_CUDA(ctx, cudaMalloc(&dev, sizeof(HandleMsg) * (ctx->nranks + 1)));
+    QDP_CUDA(ctx, cudaMemcpy(dev, &mine, sizeof(HandleMsg), cudaMemcpyHostToDevice));
+    int rc = comm_allgather_bytes(ctx, dev, dev + sizeof(HandleMsg), sizeof(HandleMsg), ctx->stream);
+    if (!rc) {
+      QDP_CUDA(ctx, cudaMemcpyAsync(all.data(), dev + sizeof(HandleMsg), sizeof(HandleMsg) * ctx->nranks,
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+      QDP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    }
+    cudaFree(dev);
+    if (rc) return rc;
+    auto open = [&](const cudaIpcMemHandle_t &h, void **out) -> int {
+      cudaError_t e = cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) return cuda_check(ctx, e, "p2p: cudaIpcOpenMemHandle (peer not reachable?)");
+      p->opened.push_back(*out);
+      return QDP_OK;
+    };
+    for (int mu = 0; mu < 4; mu++) {
+      if (!remote_dim(ctx, mu)) continue;
+      const int nm = ctx->neighbour[mu][0], np = ctx->neighbour[mu][1];
+      // channel 0 writes the -mu neighbour's forward ghost, channel 1 the +mu neighbour's backward ghost
+      if ((rc = open(all[nm].recv[mu][1], &p->peer_recv[prec][mu][0]))) return rc;
+      if ((rc = open(all[np].recv[mu][0], &p->peer_recv[prec][mu][1]))) return rc;
+      for (int d = 0; d < 2; d++) {
+        const int r = d ? np : nm;
+        if (!p->flag_map.count(r)) {
+          void *fp = nullptr;
+          if ((rc = open(all[r].flags, &fp))) return rc;
+          p->flag_map[r] = (unsigned *)fp;
+        }
+        p->peer_flags[mu][d] = p->flag_map[r];
+      }
+    }
+  }
+  p->slot_bytes[prec] = need;
+  return QDP_OK;
+}
+
+unsigned p2p_next_seq(qdp_ctx ctx, int prec) { return ctx->p2p ? ++ctx->p2p->seq[prec] : 1u; }
+
+int p2p_prepare(qdp_ctx ctx, int prec, unsigned seq, void *dst[4][2], const void *ghost[4][2], unsigned *counter[4],
+                unsigned *sig[4][2]) {
+  int rc;
+  if ((rc = p2p_setup(ctx, prec))) return rc;
+  P2P *p = ctx->p2p;
+  const Geom &g = ctx->geom;
+  const size_t off = (seq & 1u) * p->slot_bytes[prec];
+  for (int mu = 0; mu < 4; mu++) {
+    if (!((g.part >> mu) & 1)) continue;
+    for (int d = 0; d < 2; d++) {
+      dst[mu][d] = (char *)p->peer_recv[prec][mu][d] + off;
+      ghost[mu][d] = (const char *)p->recv[prec][mu][d] + off;
+    }
+    counter[mu] = p->flags + fidx(prec, F_COUNT, mu, 0);
+    sig[mu][0] = p->peer_flags[mu][0] + fidx(prec, F_READY, mu, 1);  // -mu neighbour's forward ghost
+    sig[mu][1] = p->peer_flags[mu][1] + fidx(prec, F_READY, mu, 0);  // +mu neighbour's backward ghost
+    // WAR: slot seq&1 was last read by the receivers in call seq-2
+    p2p_wait_kernel<<<1, 32, 0, ctx->stream>>>(p->flags + fidx(prec, F_ACK, mu, 0), p->flags + fidx(prec, F_ACK, mu, 1),
+                                               seq - 2u, p->flags + NFLAGS);
+  }
+  QDP_CUDA(ctx, cudaGetLastError());
+  return QDP_OK;
+}
+
+int p2p_wait_ready(qdp_ctx ctx, int prec, int mu, unsigned seq) {
+  P2P *p = ctx->p2p;
+  p2p_wait_kernel<<<1, 32, 0, ctx->stream>>>(p->flags + fidx(prec, F_READY, mu, 0), p->flags + fidx(prec, F_READY, mu, 1),
+                                             seq, p->flags + NFLAGS);
+  QDP_CUDA(ctx, cudaGetLastError());
+  return QDP_OK;
+}
+
+int p2p_ack(qdp_ctx ctx, int prec, int mu, unsigned seq) {
+  P2P *p = ctx->p2p;
+  // ghost 0 came from the -mu neighbour's channel 1, ghost 1 from the +mu neighbour's channel 0
+  p2p_signal_kernel<<<1, 32, 0, ctx->stream>>>(p->peer_flags[mu][0] + fidx(prec, F_ACK, mu, 1),
+                                               p->peer_flags[mu][1] + fidx(prec, F_ACK, mu, 0), seq);
+  QDP_CUDA(ctx, cudaGetLastError());
+  return QDP_OK;
+}
+
+int p2p_check(qdp_ctx ctx) {
+  if (!ctx->p2p) return QDP_OK;
+  unsigned e = 0;
+  QDP_CUDA(ctx, cudaMemcpyAsync(&e, ctx->p2p->flags + NFLAGS, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
+  QDP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  if (e) return set_error(ctx, QDP_ECUDA, "p2p halo: a flag wait timed out (a neighbour stopped calling dslash?)");
+  return QDP_OK;
+}
+
+void p2p_destroy(qdp_ctx ctx) {
+  P2P *p = ctx->p2p;
+  if (!p) return;
+  for (void *ptr : p->opened) cudaIpcCloseMemHandle(ptr);
+  for (int pr = 0; pr < 2; pr++)
+    for (int mu = 0; mu < 4; mu++)
+      for (int d = 0; d < 2; d++)
+        if (p->recv[pr][mu][d]) cudaFree(p->recv[pr][mu][d]);
+  if (p->flags) cudaFree(p->flags);
+  delete p;
+  ctx->p2p = nullptr;
+}
+
+}  // namespace qdpb

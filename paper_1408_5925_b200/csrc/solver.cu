@@ -239,6 +239,7 @@ int cg_solve(qdp_field x, const qdp_field b, const qdp_field U, const qdp_field 
   if (iters_out) *iters_out = k;
   if ((rc = finish_solve(op, x, b, A, r, true_resid))) return rc;  // r | p: a two-block scratch
   QDP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  if ((rc = p2p_check(ctx))) return rc;
   return status;
 }
 
@@ -318,6 +319,7 @@ int cg_solve_mixed(qdp_field x, const qdp_field b, const qdp_field U, const qdp_
   if (nreliable_out) *nreliable_out = nrel;
   if ((rc = finish_solve(op, x, b, A, mp, true_resid))) return rc;  // mp | q: a two-block scratch
   QDP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  if ((rc = p2p_check(ctx))) return rc;
   return status;
 }
 
