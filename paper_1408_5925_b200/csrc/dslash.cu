@@ -155,10 +155,13 @@ template <typename R, int REC = 18> struct KParams {
   // fused Re<dotx, out>: per-block partials
   FermView<R> dotx;
   double *dot_part;
-  // peer-to-peer halo (QDP_OPT_P2P): after its face stores, the last pack block of dim mu
-  // release-stores `seq` into the receivers' ready flags sig[mu][0..1] (pack_counter counts blocks)
-  unsigned *pack_counter[4];
-  unsigned *sig[4][2];
+  // peer-to-peer halo (QDP_OPT_P2P; p2p.cu): pack waits war >= seq-2, stores, and its last
+  // block release-stores seq into sig; the exterior waits ready >= seq and its last block
+  // release-stores seq into ack_to.  pack_counter == nullptr: NCCL / direct halo.
+  unsigned *pack_counter[4], *ext_counter[4];
+  unsigned *sig[4][2], *ack_to[4][2];
+  const unsigned *war[4][2], *ready[4][2];
+  unsigned *err;
   unsigned seq;
 };
 
@@ -283,6 +286,8 @@ template <typename R, int REC, bool G5IN>
 __global__ void __launch_bounds__(128) pack_kernel(const Geom g, const KParams<R, REC> P, int mu) {
   const int n = g.faceVh[mu];
   int f = blockIdx.x * blockDim.x + threadIdx.x;
+  // peer-to-peer: the receivers must have consumed this slot (written two calls ago)
+  if (P.pack_counter[mu]) block_wait_flags(P.war[mu][0], P.war[mu][1], P.seq - 2u, P.err);
   if (f < 2 * n) {
     const int q = 1 - P.parity;
     const bool fwd = f >= n;
@@ -315,19 +320,7 @@ __global__ void __launch_bounds__(128) pack_kernel(const Geom g, const KParams<R
   // Peer-to-peer halo: the face stores above may target a neighbour's memory over NVLink.
   // Every thread fences them at system scope; the last block to finish publishes `seq` to the
   // two receivers' ready flags with release semantics (they acquire before reading).
-  if (P.pack_counter[mu]) {
-    __threadfence_system();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const unsigned prev = atomicAdd(P.pack_counter[mu], 1u);
-      if (prev == gridDim.x - 1) {
-        *P.pack_counter[mu] = 0u;
-        __threadfence_system();
-        st_release_sys(P.sig[mu][0], P.seq);
-        st_release_sys(P.sig[mu][1], P.seq);
-      }
-    }
-  }
+  if (P.pack_counter[mu]) grid_signal_last(P.pack_counter[mu], P.sig[mu][0], P.sig[mu][1], P.seq);
 }
 
 // Exterior: add the remote hops of dim mu for the output sites on its two faces.  With DOT,
@@ -338,6 +331,8 @@ __global__ void __launch_bounds__(128) exterior_kernel(const Geom g, const KPara
   const int n = g.faceVh[mu];
   int f = blockIdx.x * blockDim.x + threadIdx.x;
   double dot = 0.0;
+  // peer-to-peer: acquire both ghosts of this call before reading them
+  if (P.pack_counter[mu]) block_wait_flags(P.ready[mu][0], P.ready[mu][1], P.seq, P.err);
   if (f < 2 * n) {
     const int p = P.parity;
     const bool fwd = f >= n;  // fwd: site at x_mu = L-1 needs psi(x+mu) from the +mu neighbour
@@ -378,6 +373,8 @@ __global__ void __launch_bounds__(128) exterior_kernel(const Geom g, const KPara
     if (DOT) dot = re_dot(P.dotx.load_stream(cb), acc);
   }
   if (DOT) dot_block_partial(dot, dot_part);
+  // peer-to-peer: the last block tells both senders their slot has been consumed
+  if (P.pack_counter[mu]) grid_signal_last(P.ext_counter[mu], P.ack_to[mu][0], P.ack_to[mu][1], P.seq);
 }
 
 // ------------------------------------------------------------------ host side
@@ -497,7 +494,21 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
   if (halo && ctx->p2p_on) {
     // peer-to-peer: pack straight into the neighbours' ghost slots, flags instead of NCCL (p2p.cu)
     seq = p2p_next_seq(ctx, prec);
-    if ((rc = p2p_prepare(ctx, prec, seq, P.dst, P.ghost, P.pack_counter, P.sig))) return rc;
+    P2PLaunch L;
+    if ((rc = p2p_prepare(ctx, prec, seq, &L))) return rc;
+    for (int mu = 0; mu < 4; mu++) {
+      P.pack_counter[mu] = L.pack_counter[mu];
+      P.ext_counter[mu] = L.ext_counter[mu];
+      for (int d = 0; d < 2; d++) {
+        P.dst[mu][d] = L.dst[mu][d];
+        P.ghost[mu][d] = L.ghost[mu][d];
+        P.sig[mu][d] = L.sig[mu][d];
+        P.ack_to[mu][d] = L.ack_to[mu][d];
+        P.war[mu][d] = L.war[mu][d];
+        P.ready[mu][d] = L.ready[mu][d];
+      }
+    }
+    P.err = L.err;
     P.seq = seq;
   }
   if (halo) {
@@ -544,7 +555,6 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
     if (overlap) QDP_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_comm, 0));
     for (int mu = 0; mu < 4; mu++) {
       if (!((g.part >> mu) & 1)) continue;
-      if (seq && (rc = p2p_wait_ready(ctx, prec, mu, seq))) return rc;
       ProfEvent ev;
       prof_begin(ctx, QDP_PK_DSLASH_EXT, &ev);
       // ghost read, forward-face link, output read-modify-write (+ clover on CLOVINV)
@@ -555,7 +565,6 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
       if (a.epi == EPI_CLOVINV) launch_ext<R, REC, EPI_CLOVINV>(ctx, P, mu, a.g5_out, nullptr);
       else launch_ext<R, REC, EPI_PLAIN>(ctx, P, mu, a.g5_out, dp);
       if ((rc = prof_end(ctx, &ev))) return rc;
-      if (seq && (rc = p2p_ack(ctx, prec, mu, seq))) return rc;
     }
   } else {
     if ((rc = launch_main_epi<R, REC>(ctx, a, P, false, block))) return rc;

@@ -173,6 +173,39 @@ __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned *p) {
   return v;
 }
 
+// Block-wide wait until both flags reach `expect` (wrap-safe); thread 0 polls with a bounded
+// budget (~10 s) and raises *err instead of hanging.  All threads of the block must call it.
+__device__ __forceinline__ void block_wait_flags(const unsigned *f0, const unsigned *f1, unsigned expect, unsigned *err) {
+  if (threadIdx.x == 0) {
+    long n = 0;
+    while ((int)(ld_acquire_sys(f0) - expect) < 0 || (int)(ld_acquire_sys(f1) - expect) < 0) {
+      if (++n > (1L << 26)) {
+        atomicExch(err, 1u);
+        break;
+      }
+      __nanosleep(128);
+    }
+  }
+  __syncthreads();
+}
+// Called by every thread after its stores: the last block of the grid to get here release-
+// stores v into f0 and f1 (system scope) and resets the block counter.  The barrier orders the
+// block's stores before thread 0's system-scope fence (fences are cumulative), and the fence /
+// counter-RMW chain orders every block's stores before the last block's release.
+__device__ __forceinline__ void grid_signal_last(unsigned *counter, unsigned *f0, unsigned *f1, unsigned v) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    const unsigned prev = atomicAdd(counter, 1u);
+    if (prev == gridDim.x - 1) {
+      *counter = 0u;
+      __threadfence_system();
+      st_release_sys(f0, v);
+      st_release_sys(f1, v);
+    }
+  }
+}
+
 // Spinor: 12 complex, index 3*spin + colour.
 template <typename R> struct Spinor { cx<R> c[12]; };
 // Half spinor: 6 complex, index 3*h + colour (h = 0,1).
@@ -564,17 +597,22 @@ int clover_build(qdp_ctx ctx, const qdp_field U, void *A, int A_subset, void *Ai
                  double mass, double csw, int *singular_flag_host);
 int clover_apply(qdp_ctx ctx, int prec, void *out, const void *A, const void *in, int nblk);
 
-// p2p.cu: peer-to-peer halo.  For dslash call `seq` (1, 2, ...; identical on every rank):
-//   p2p_prepare: make sure the buffers exist and are mapped (collective on first use), wait
-//     (on the stream) until the receivers consumed slot seq&1 two calls ago, and return the
-//     pack destinations (the neighbours' ghost slots), this rank's ghost slots to read, the
-//     pack-block counters and the neighbours' ready flags to signal;
-//   p2p_wait_ready: stream-wait until both ghosts of dim mu carry `seq` (before the exterior);
-//   p2p_ack: tell the two senders of dim mu that their slot was consumed (after the exterior).
-int p2p_prepare(qdp_ctx ctx, int prec, unsigned seq, void *dst[4][2], const void *ghost[4][2], unsigned *counter[4],
-                unsigned *sig[4][2]);
-int p2p_wait_ready(qdp_ctx ctx, int prec, int mu, unsigned seq);
-int p2p_ack(qdp_ctx ctx, int prec, int mu, unsigned seq);
+// p2p.cu: peer-to-peer halo.  For dslash call `seq` (1, 2, ...; identical on every rank),
+// p2p_prepare makes sure the buffers exist and are mapped (collective on first use) and
+// returns everything the pack and exterior kernels need to run the protocol themselves:
+//   pack     : wait until war[mu][d] >= seq-2 (the receiver consumed this slot two calls ago),
+//              store into dst[mu][d], the last block release-stores seq into sig[mu][d];
+//   exterior : wait until ready[mu][d] >= seq, read ghost[mu][d], the last block release-stores
+//              seq into ack_to[mu][d] (the senders' WAR flags).
+struct P2PLaunch {
+  void *dst[4][2];
+  const void *ghost[4][2];
+  unsigned *pack_counter[4], *ext_counter[4];
+  unsigned *sig[4][2], *ack_to[4][2];
+  const unsigned *war[4][2], *ready[4][2];
+  unsigned *err;
+};
+int p2p_prepare(qdp_ctx ctx, int prec, unsigned seq, P2PLaunch *out);
 int p2p_check(qdp_ctx ctx);  // QDP_ECUDA if a flag wait timed out
 unsigned p2p_next_seq(qdp_ctx ctx, int prec);
 void p2p_destroy(qdp_ctx ctx);

@@ -2,15 +2,16 @@
 // upgrade"; the face exchange of PAPER.md:208-214 without a separate communication call).
 //
 // Every rank exports its ghost buffers (two slots per face, alternating by call) and a small
-// flag block through CUDA IPC; the neighbours map them.  Per EO dslash call `seq`:
-//   sender : stream-wait until the receiver acknowledged slot seq&1 of call seq-2 (WAR), then
-//            the pack kernel stores the projected faces straight into the receiver's ghost slot
-//            and its last block release-stores seq into the receiver's ready flag;
-//   receiver: interior kernel runs meanwhile; stream-wait (acquire) for ready == seq, exterior
-//            kernel, then release-store seq into the sender's ack flag.
+// flag block through CUDA IPC; the neighbours map them.  Per EO dslash call `seq`, inside the
+// dslash's own kernels (no extra launches, no communication library):
+//   sender (pack kernel): wait until the receiver acknowledged slot seq&1 of call seq-2 (WAR),
+//            store the projected faces straight into the receiver's ghost slot over NVLink, the
+//            last block release-stores seq into the receiver's ready flag;
+//   receiver: the interior kernel runs meanwhile; the exterior kernel acquires ready == seq,
+//            reads the ghosts, and its last block release-stores seq into the senders' ack flags.
 // A dim with one rank (self-halo) maps "the neighbour" to this rank, so the whole protocol runs
-// and is tested on one GPU.  Waits are 1-thread kernels that poll with a bounded budget and
-// raise an error flag instead of hanging (checked by p2p_check).
+// and is tested on one GPU.  Waits poll with a bounded budget and raise an error flag instead
+// of hanging (checked by p2p_check).
 #include <string.h>
 
 #include <algorithm>
@@ -40,26 +41,6 @@ struct HandleMsg {
   cudaIpcMemHandle_t recv[4][2];
   cudaIpcMemHandle_t flags;
 };
-
-constexpr long WAIT_POLLS = 1L << 26;  // ~ 10 s of 128 ns sleeps before declaring a timeout
-
-__global__ void p2p_wait_kernel(const unsigned *f0, const unsigned *f1, unsigned expect, unsigned *err) {
-  if (threadIdx.x) return;
-  long n = 0;
-  while ((int)(ld_acquire_sys(f0) - expect) < 0 || (int)(ld_acquire_sys(f1) - expect) < 0) {
-    if (++n > WAIT_POLLS) {
-      atomicExch(err, 1u);
-      return;
-    }
-    __nanosleep(128);
-  }
-}
-
-__global__ void p2p_signal_kernel(unsigned *f0, unsigned *f1, unsigned v) {
-  if (threadIdx.x) return;
-  st_release_sys(f0, v);
-  st_release_sys(f1, v);
-}
 
 static bool remote_dim(qdp_ctx ctx, int mu) { return ((ctx->geom.part >> mu) & 1) && ctx->pgrid[mu] > 1; }
 
@@ -151,44 +132,31 @@ static int p2p_setup(qdp_ctx ctx, int prec) {
 
 unsigned p2p_next_seq(qdp_ctx ctx, int prec) { return ctx->p2p ? ++ctx->p2p->seq[prec] : 1u; }
 
-int p2p_prepare(qdp_ctx ctx, int prec, unsigned seq, void *dst[4][2], const void *ghost[4][2], unsigned *counter[4],
-                unsigned *sig[4][2]) {
+int p2p_prepare(qdp_ctx ctx, int prec, unsigned seq, P2PLaunch *L) {
   int rc;
   if ((rc = p2p_setup(ctx, prec))) return rc;
   P2P *p = ctx->p2p;
   const Geom &g = ctx->geom;
   const size_t off = (seq & 1u) * p->slot_bytes[prec];
+  memset(L, 0, sizeof(*L));
+  L->err = p->flags + NFLAGS;
   for (int mu = 0; mu < 4; mu++) {
     if (!((g.part >> mu) & 1)) continue;
     for (int d = 0; d < 2; d++) {
-      dst[mu][d] = (char *)p->peer_recv[prec][mu][d] + off;
-      ghost[mu][d] = (const char *)p->recv[prec][mu][d] + off;
+      L->dst[mu][d] = (char *)p->peer_recv[prec][mu][d] + off;
+      L->ghost[mu][d] = (const char *)p->recv[prec][mu][d] + off;
+      // WAR: slot seq&1 of channel d was last read by its receiver in call seq-2
+      L->war[mu][d] = p->flags + fidx(prec, F_ACK, mu, d);
+      L->ready[mu][d] = p->flags + fidx(prec, F_READY, mu, d);
     }
-    counter[mu] = p->flags + fidx(prec, F_COUNT, mu, 0);
-    sig[mu][0] = p->peer_flags[mu][0] + fidx(prec, F_READY, mu, 1);  // -mu neighbour's forward ghost
-    sig[mu][1] = p->peer_flags[mu][1] + fidx(prec, F_READY, mu, 0);  // +mu neighbour's backward ghost
-    // WAR: slot seq&1 was last read by the receivers in call seq-2
-    p2p_wait_kernel<<<1, 32, 0, ctx->stream>>>(p->flags + fidx(prec, F_ACK, mu, 0), p->flags + fidx(prec, F_ACK, mu, 1),
-                                               seq - 2u, p->flags + NFLAGS);
+    L->pack_counter[mu] = p->flags + fidx(prec, F_COUNT, mu, 0);
+    L->ext_counter[mu] = p->flags + fidx(prec, F_COUNT, mu, 1);
+    L->sig[mu][0] = p->peer_flags[mu][0] + fidx(prec, F_READY, mu, 1);  // -mu neighbour's forward ghost
+    L->sig[mu][1] = p->peer_flags[mu][1] + fidx(prec, F_READY, mu, 0);  // +mu neighbour's backward ghost
+    // ghost 0 came from the -mu neighbour's channel 1, ghost 1 from the +mu neighbour's channel 0
+    L->ack_to[mu][0] = p->peer_flags[mu][0] + fidx(prec, F_ACK, mu, 1);
+    L->ack_to[mu][1] = p->peer_flags[mu][1] + fidx(prec, F_ACK, mu, 0);
   }
-  QDP_CUDA(ctx, cudaGetLastError());
-  return QDP_OK;
-}
-
-int p2p_wait_ready(qdp_ctx ctx, int prec, int mu, unsigned seq) {
-  P2P *p = ctx->p2p;
-  p2p_wait_kernel<<<1, 32, 0, ctx->stream>>>(p->flags + fidx(prec, F_READY, mu, 0), p->flags + fidx(prec, F_READY, mu, 1),
-                                             seq, p->flags + NFLAGS);
-  QDP_CUDA(ctx, cudaGetLastError());
-  return QDP_OK;
-}
-
-int p2p_ack(qdp_ctx ctx, int prec, int mu, unsigned seq) {
-  P2P *p = ctx->p2p;
-  // ghost 0 came from the -mu neighbour's channel 1, ghost 1 from the +mu neighbour's channel 0
-  p2p_signal_kernel<<<1, 32, 0, ctx->stream>>>(p->peer_flags[mu][0] + fidx(prec, F_ACK, mu, 1),
-                                               p->peer_flags[mu][1] + fidx(prec, F_ACK, mu, 0), seq);
-  QDP_CUDA(ctx, cudaGetLastError());
   return QDP_OK;
 }
 
