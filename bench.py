@@ -170,6 +170,7 @@ def config_dict(args, world):
                         "t-split; even-odd Wilson-clover CGNR solve, fixed iterations",
             "global_lattice": "x".join(map(str, gl)), "local_lattice": "x".join(map(str, LOCAL)),
             "operator": f"Wilson-clover m={MASS} c_SW={CSW}, hot random SU(3) gauge field",
+            "gauge_storage": "reconstruct-12" if getattr(args, "recon", 18) == 12 else "full 3x3 (18 reals)",
             "cg_iters_per_step": args.iters, "parallelism": f"t-split x{world}" if world > 1 else "single GPU",
             "l2": "inputs larger than L2 (gauge 1.18 GB + clover 1.2 GB + 6 fermion vectors per GPU), no flush"}
 
@@ -187,7 +188,10 @@ def run_native(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    stream = torch.cuda.current_stream()
+    # one explicit stream shared by the library (its context stream) and torch's timing events,
+    # so the events are ordered with the kernels they bracket
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     gdims = (LOCAL[0], LOCAL[1], LOCAL[2], LOCAL[3] * world)
     P = qdist.proc_grid_for(world, gdims, split=(3,))
     ctx = qdist.bootstrap(gdims, P, stream=stream)
@@ -197,7 +201,7 @@ def run_native(args, rank, world, local_rank):
     Vh = L[0] * L[1] * L[2] * L[3] // 2
 
     U, b = gen_fields(L, rank)
-    fU = q.qdp_field_alloc(ctx, q.QDP_GAUGE, q.QDP_F64, q.QDP_ALL)
+    fU = q.qdp_field_alloc(ctx, q.QDP_GAUGE12 if args.recon == 12 else q.QDP_GAUGE, q.QDP_F64, q.QDP_ALL)
     fb = q.qdp_field_alloc(ctx, q.QDP_FERMION, q.QDP_F64, q.QDP_ALL)
     fx = q.qdp_field_alloc(ctx, q.QDP_FERMION, q.QDP_F64, q.QDP_ALL)
     fA = q.qdp_field_alloc(ctx, q.QDP_CLOVER, q.QDP_F64, q.QDP_ALL)
@@ -375,6 +379,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-overlap", action="store_true")
     ap.add_argument("--p2p", action="store_true", help="peer-to-peer (CUDA IPC) halos instead of NCCL")
+    ap.add_argument("--recon", type=int, choices=[18, 12], default=18,
+                    help="gauge storage of the solve: 18 (default, uncompressed as in PAPER.md:292) or 12")
     ap.add_argument("--no-tts", dest="tts", action="store_false", help="skip the time-to-solution comparison")
     ap.add_argument("--check", action="store_true", default=True)
     ap.add_argument("--no-check", dest="check", action="store_false")
