@@ -96,7 +96,9 @@ def to_bytes(v, u):
 
 launches()
 cg = full("dslash_cg")
-full("dslash_plain")
+for rep in sorted(os.listdir(OUT)):
+    if rep.startswith("prof_") and rep.endswith(".ncu-rep") and rep != "prof_dslash_cg.ncu-rep":
+        full(rep[len("prof_"):-len(".ncu-rep")])
 if cg:
     per = [to_bytes(*r["dram__bytes_read.sum"]) + to_bytes(*r["dram__bytes_write.sum"]) for r in cg]
     json.dump({"dram_bytes_per_launch": sum(per) / len(per),
