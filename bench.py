@@ -252,30 +252,62 @@ def run_native(args, rank, world, local_rank):
     flops_job = qdist.sum_over_ranks(f_all)
     value = flops_job / (ms_max * 1e-3) * 1e-9
 
-    # ---- e2e: the same solves through the C ABI with host buffers (pinned), copies inside
-    hb = torch.from_numpy(b).pin_memory()
-    hx = torch.empty_like(hb).pin_memory()
-    k2 = max(1, min(args.steps, args.e2e_steps))
-    q.qdp_field_import(fb, hb)
-    step()
-    q.qdp_field_export(fx, hx)
+    # ---- e2e: the same solves through the C ABI from pinned host memory, every step's source
+    # uploaded and every step's solution downloaded inside the timed region.  Pipelined: on a copy
+    # stream the upload of b_{k+1} and the download of x_{k-1} run while solve k runs; the layout
+    # conversions (qdp_field_import_device / export_device) run on the compute stream.
+    k2 = args.e2e_steps if args.e2e_steps > 0 else args.steps
+    hb = [torch.from_numpy(b).pin_memory() for _ in range(2)]          # host sources
+    hx = [torch.empty_like(hb[0]).pin_memory() for _ in range(2)]       # host solutions
+    d_in = [torch.empty_like(hb[0], device="cuda") for _ in range(2)]   # device staging (host layout)
+    d_out = [torch.empty_like(hb[0], device="cuda") for _ in range(2)]
+    fbs, fxs = [fb, q.qdp_field_alloc(ctx, q.QDP_FERMION, q.QDP_F64, q.QDP_ALL)], [fx, fx]
+    fxs[1] = q.qdp_field_alloc(ctx, q.QDP_FERMION, q.QDP_F64, q.QDP_ALL)
+    cs = torch.cuda.Stream()
+    ev_in = [torch.cuda.Event() for _ in range(2)]
+    ev_out = [torch.cuda.Event() for _ in range(2)]
+    ev_dl = [torch.cuda.Event() for _ in range(2)]
+
+    def e2e_run(n):
+        for e in ev_dl:
+            e.record(cs)
+        with torch.cuda.stream(cs):
+            d_in[0].copy_(hb[0], non_blocking=True)
+            ev_in[0].record(cs)
+        for k in range(n):
+            s = k % 2
+            if k + 1 < n:  # upload the next step's source while this step solves
+                with torch.cuda.stream(cs):
+                    d_in[1 - s].copy_(hb[1 - s], non_blocking=True)
+                    ev_in[1 - s].record(cs)
+            stream.wait_event(ev_in[s])
+            q.qdp_field_import_device(fbs[s], d_in[s])
+            q.qdp_cg_solve(fxs[s], fbs[s], fU, fA, fAi, mass=MASS, tol=0.0, maxit=args.iters)
+            stream.wait_event(ev_dl[s])  # d_out[s] was downloaded (step k-2)
+            q.qdp_field_export_device(fxs[s], d_out[s])
+            ev_out[s].record(stream)
+            with torch.cuda.stream(cs):  # download this step's solution during the next solve
+                cs.wait_event(ev_out[s])
+                hx[s].copy_(d_out[s], non_blocking=True)
+                ev_dl[s].record(cs)
+
+    e2e_run(2)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    f0, _ = q.qdp_profile_work(ctx, -1)
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2.record(stream)
-    for _ in range(k2):
-        q.qdp_field_import(fb, hb)
-        step()
-        q.qdp_field_export(fx, hx)
-    e3.record(stream)
+    cs.wait_event(e2)
+    e2e_run(k2)
+    e3.record(cs)  # after the last download (cs is ordered after every compute step)
     torch.cuda.synchronize()
-    f1, _ = q.qdp_profile_work(ctx, -1)
+    assert np.array_equal(hx[(k2 - 1) % 2].numpy(), q.qdp_field_export(fxs[(k2 - 1) % 2]))
     ms_e2e = qdist.max_over_ranks(e2.elapsed_time(e3))
     e2e_flops = qdist.sum_over_ranks(cg_flops(Vh, args.iters) * k2)
     e2e_value = e2e_flops / (ms_e2e * 1e-3) * 1e-9
-    bytes_b = hb.numel() * hb.element_size()
+    bytes_b = hb[0].numel() * hb[0].element_size()
+    q.qdp_field_free(fbs[1])
+    q.qdp_field_free(fxs[1])
 
     # ---- the metric's plain Wilson dslash in both precisions (not the step): one EO application
     # (out_e = H_eo psi_o) on the same lattice, uncompressed links, live CUDA events
@@ -402,7 +434,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["native", "reference"], default="native")
     ap.add_argument("--iters", type=int, default=32, help="CG iterations per step (tol = 0)")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=0, help="e2e steps (0: the same K as the timed region)")
     ap.add_argument("--cpu-iters", type=int, default=2)
     ap.add_argument("--ref-iters", type=int, default=1)
     ap.add_argument("--no-cpu", action="store_true")

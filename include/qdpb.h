@@ -145,6 +145,11 @@ int qdp_field_info(const qdp_field f, int *kind, int *prec, int *subset, void **
  * layout on the device; export is the inverse.  Host memory may be pageable or pinned. */
 int qdp_field_import(qdp_field f, const void *host, size_t bytes);
 int qdp_field_export(const qdp_field f, void *host, size_t bytes);
+/* The same conversions from / to a DEVICE buffer holding the host canonical layout: enqueued
+ * on the context stream, no synchronisation (so the caller can overlap its own host<->device
+ * copies on another stream).  dev_aos must stay valid until the stream reaches the call. */
+int qdp_field_import_device(qdp_field f, const void *dev_aos, size_t bytes);
+int qdp_field_export_device(const qdp_field f, void *dev_aos, size_t bytes);
 int qdp_field_zero(qdp_field f);
 /* dst <- src (same kind/precision; subsets equal, or dst ALL and src a parity, or
  * src ALL and dst a parity: the matching parity is copied). */

@@ -451,6 +451,22 @@ extern "C" int qdp_field_export(const qdp_field f, void *host, size_t bytes) {
   return QDP_OK;
 }
 
+extern "C" int qdp_field_import_device(qdp_field f, const void *dev_aos, size_t bytes) {
+  if (!f || !dev_aos) return QDP_EINVAL;
+  qdp_ctx c = f->ctx;
+  const size_t hb = field_host_bytes(c, f->kind, f->prec, f->subset);
+  if (bytes != hb) return set_error(c, QDP_ESHAPE, "import_device: %zu bytes, expected %zu", bytes, hb);
+  return layout_import(f, dev_aos);
+}
+
+extern "C" int qdp_field_export_device(const qdp_field f, void *dev_aos, size_t bytes) {
+  if (!f || !dev_aos) return QDP_EINVAL;
+  qdp_ctx c = f->ctx;
+  const size_t hb = field_host_bytes(c, f->kind, f->prec, f->subset);
+  if (bytes != hb) return set_error(c, QDP_ESHAPE, "export_device: %zu bytes, expected %zu", bytes, hb);
+  return layout_export(f, dev_aos);
+}
+
 extern "C" int qdp_field_zero(qdp_field f) {
   if (!f) return QDP_EINVAL;
   qdp_ctx c = f->ctx;

@@ -2,6 +2,8 @@
 // device structure-of-arrays conversion (section III-B), done on the
 // device: the host array is copied as-is into a device staging buffer, then one thread per
 // site scatters / gathers its components.  Also the slot maps shared with shift.cu.
+#include <type_traits>
+
 #include "internal.h"
 #include "slots.h"
 
@@ -107,11 +109,13 @@ __global__ void slots_kernel(const Geom g, const SlotMap m, int subset, long nre
   if (i >= nrec) return;
   int p, cb;
   record_site(g, subset, i, p, cb);
-  R *rec = aos + i * m.n * 2;
+  // one complex = one 16-byte (fp64) or 8-byte (fp32) access on both sides
+  using C2 = typename std::conditional<sizeof(R) == 8, double2, float2>::type;
+  C2 *rec = (C2 *)(aos + i * m.n * 2);
   for (int k = 0; k < m.n; k++) {
-    R *d = (R *)(data + m.off[p][k] + (long long)cb * m.step[k]);
-    if (IMPORT) { d[0] = rec[2 * k]; d[1] = rec[2 * k + 1]; }
-    else { rec[2 * k] = d[0]; rec[2 * k + 1] = d[1]; }
+    C2 *d = (C2 *)(data + m.off[p][k] + (long long)cb * m.step[k]);
+    if (IMPORT) *d = rec[k];
+    else rec[k] = *d;
   }
 }
 

@@ -52,6 +52,8 @@ _SIGS = {
     "qdp_field_info": [_vp, _ip, _ip, _ip, ctypes.POINTER(_vp)],
     "qdp_field_import": [_vp, _vp, ctypes.c_size_t],
     "qdp_field_export": [_vp, _vp, ctypes.c_size_t],
+    "qdp_field_import_device": [_vp, _vp, ctypes.c_size_t],
+    "qdp_field_export_device": [_vp, _vp, ctypes.c_size_t],
     "qdp_field_zero": [_vp],
     "qdp_field_copy": [_vp, _vp],
     "qdp_shift": [_vp, _vp, ctypes.c_int, ctypes.c_int],
@@ -266,6 +268,18 @@ def qdp_field_export(f: Field, out=None):
     p, n, _ = _ptr_bytes(out)
     _check(lib().qdp_field_export(f, p, n), f.ctx)
     return out
+
+
+def qdp_field_import_device(f: Field, dev) -> None:
+    """Enqueue the layout conversion from a CUDA tensor holding the host canonical layout."""
+    p, n, _ = _ptr_bytes(dev)
+    _check(lib().qdp_field_import_device(f, p, n), f.ctx)
+
+
+def qdp_field_export_device(f: Field, dev) -> None:
+    """Enqueue the layout conversion into a CUDA tensor (host canonical layout)."""
+    p, n, _ = _ptr_bytes(dev)
+    _check(lib().qdp_field_export_device(f, p, n), f.ctx)
 
 
 def qdp_field_zero(f: Field) -> None:
