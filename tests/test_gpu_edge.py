@@ -117,6 +117,34 @@ def test_config5_rank_sublattice_through_halo_path(q):
         q.qdp_finalize(c)
 
 
+@pytest.mark.parametrize("prec", [0, 1])
+def test_device_buffer_import_export(q, prec):
+    """qdp_field_import_device / export_device: the host canonical layout in a CUDA tensor,
+    converted on the context stream; bit-exact against the host-buffer path."""
+    import torch
+    L = (4, 6, 4, 4)
+    psi = fieldgen.random_spinor(L, 41)
+    U = fieldgen.random_gauge(L, 42)
+    dt = torch.float64 if prec == 0 else torch.float32
+    c = q.qdp_init(L)
+    try:
+        f = q.qdp_field_alloc(c, q.QDP_FERMION, prec, q.QDP_ALL)
+        g = q.qdp_field_alloc(c, q.QDP_GAUGE, prec, q.QDP_ALL)
+        q.qdp_field_import_device(f, torch.tensor(psi, dtype=dt, device="cuda"))
+        q.qdp_field_import_device(g, torch.tensor(U, dtype=dt, device="cuda"))
+        hp = psi.astype(np.float64 if prec == 0 else np.float32)
+        assert np.array_equal(q.qdp_field_export(f), hp)
+        out = torch.empty(psi.shape, dtype=dt, device="cuda")
+        q.qdp_field_export_device(f, out)
+        q.qdp_synchronize(c)
+        assert np.array_equal(out.cpu().numpy(), hp)
+        with pytest.raises(q.QdpError) as e:
+            q.qdp_field_import_device(f, torch.zeros(7, dtype=dt, device="cuda"))
+        assert e.value.status == q.QDP_ESHAPE
+    finally:
+        q.qdp_finalize(c)
+
+
 def test_init_limits(q):
     with pytest.raises(q.QdpError) as e:
         q.qdp_init((2048, 2048, 2048, 2))      # V/2 > 2^30 sites per parity

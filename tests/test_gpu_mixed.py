@@ -63,6 +63,33 @@ def test_mixed_cg_solution(q, clover, gk, L):
         q.qdp_finalize(c)
 
 
+@pytest.mark.parametrize("clover,gk", [(False, 1), (True, 1), (True, 3)])
+def test_fp32_cg_solution(q, clover, gk):
+    """qdp_cg_solve with all-fp32 fields (the sloppy operator on its own) reaches 1e-5 and
+    agrees with the oracle's fp64 solution of the fp32-rounded system to fp32 accuracy."""
+    L = (8, 8, 8, 8)
+    m = 0.1
+    U = fieldgen.random_gauge(L, 1911).astype(np.float32).astype(np.float64)
+    b = fieldgen.random_spinor(L, 2911).astype(np.float32).astype(np.float64)
+    A = oracle.clover_build(U, L, m, 1.0) if clover else None
+    ref = oracle.cg_solve(U, b, L, m, A=A, tol=1e-12, maxit=2000)
+    c = q.qdp_init(L)
+    try:
+        fU = _field(q, c, gk, 1, q.QDP_ALL, U)
+        fb = _field(q, c, q.QDP_FERMION, 1, q.QDP_ALL, b)
+        fx = q.qdp_field_alloc(c, q.QDP_FERMION, 1, q.QDP_ALL)
+        fA = fAi = None
+        if clover:
+            fA = q.qdp_field_alloc(c, q.QDP_CLOVER, 1, q.QDP_ALL)
+            fAi = q.qdp_field_alloc(c, q.QDP_CLOVER, 1, q.QDP_EVEN)
+            q.qdp_clover_build(fA, fAi, fU, m, 1.0)
+        res = q.qdp_cg_solve(fx, fb, fU, fA, fAi, mass=m, tol=1e-5, maxit=2000)
+        assert res["status"] == q.QDP_OK and res["true_resid"] <= 1e-4
+        assert rel_site_err(q.qdp_field_export(fx).astype(np.float64), ref["x"]) <= 1e-4
+    finally:
+        q.qdp_finalize(c)
+
+
 def test_mixed_cg_argument_checks(q):
     L = (4, 4, 4, 4)
     c = q.qdp_init(L)
