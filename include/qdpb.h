@@ -229,12 +229,15 @@ int qdp_cg_solve_mixed(qdp_field x, const qdp_field b, const qdp_field U, const 
  *   QDP_EXPR_SPMAT   out = a * b            spin matrices                    ("spmat")
  *   QDP_EXPR_MATVEC  out = a * b + a * c    colour matrix x two fermions     ("matvec")
  *   QDP_EXPR_CLOVER  out = a * b            clover (packed blocks) x fermion ("clover")
+ *   QDP_EXPR_ADJ_UPSI out = adj(a) * b      colour matrix^dag x fermion (Fig. 1's adj(u[mu])*phi,
+ *                                           PAPER.md:121)
  * c is NULL except for MATVEC.  All operands have the output's precision (QDP_EPREC).
  * Block size: the paper's autotuner runs on the payload launches -- first
  * launch at 1024 threads, halved while the launch fails, then each further launch probes the
  * next smaller size until the time grows by more than 33%; the best size is kept per
  * (expression, precision, volume).  QDP_OPT_AUTOTUNE = 0 disables it (128 threads). */
-enum { QDP_EXPR_LCM = 0, QDP_EXPR_UPSI = 1, QDP_EXPR_SPMAT = 2, QDP_EXPR_MATVEC = 3, QDP_EXPR_CLOVER = 4 };
+enum { QDP_EXPR_LCM = 0, QDP_EXPR_UPSI = 1, QDP_EXPR_SPMAT = 2, QDP_EXPR_MATVEC = 3, QDP_EXPR_CLOVER = 4,
+       QDP_EXPR_ADJ_UPSI = 5 };
 int qdp_expr(int expr, qdp_field out, const qdp_field a, const qdp_field b, const qdp_field c);
 /* block size the autotuner currently uses for (expr, prec) on this context's volume, and
  * whether its search has finished (1) */

@@ -178,6 +178,14 @@ def upsi(u, psi) -> np.ndarray:
     return out
 
 
+def adj_upsi(u, psi) -> np.ndarray:
+    """adj(u) * psi on every spin (Fig. 1's adj(u[mu])*phi)."""
+    u, psi = _f64(u), _f64(psi)
+    out = np.empty_like(psi)
+    lib().orc_adj_upsi(_p(out), _p(u), _p(psi), ctypes.c_long(_n(u, 18)))
+    return out
+
+
 def spmat(a, b) -> np.ndarray:
     """Table II spmat: site-wise 4x4 product.  a, b: [n,4,4,2]."""
     a, b = _f64(a), _f64(b)

@@ -621,6 +621,20 @@ void orc_spmat(double *out_, const double *a_, const double *b_, long n) {
             }
 }
 
+/* adj(u) * psi: out(x)_{spin,a} = sum_b conj(u(x)_{b,a}) psi(x)_{spin,b}  (Fig. 1) */
+void orc_adj_upsi(double *out_, const double *u_, const double *psi_, long n) {
+    const cplx *u = (const cplx *)u_, *psi = (const cplx *)psi_;
+    cplx *out = (cplx *)out_;
+#pragma omp parallel for schedule(static)
+    for (long s = 0; s < n; s++)
+        for (int sp = 0; sp < 4; sp++)
+            for (int a = 0; a < 3; a++) {
+                cplx acc = 0;
+                for (int b = 0; b < 3; b++) acc += conj(u[s * 9 + b * 3 + a]) * psi[s * 12 + sp * 3 + b];
+                out[s * 12 + sp * 3 + a] = acc;
+            }
+}
+
 /* matvec: out(x) = u(x) psi1(x) + u(x) psi2(x) */
 void orc_matvec(double *out, const double *u, const double *p1, const double *p2, long n) {
     double *t = (double *)malloc(sizeof(double) * 24 * (size_t)n);

@@ -695,13 +695,15 @@ extern "C" int qdp_expr(int expr, qdp_field out, const qdp_field a, const qdp_fi
   if (!out || !a || !b) return QDP_EINVAL;
   qdp_ctx ctx = out->ctx;
   int rc;
-  if (expr < QDP_EXPR_LCM || expr > QDP_EXPR_CLOVER) return set_error(ctx, QDP_EINVAL, "expr: unknown expression %d", expr);
+  if (expr < QDP_EXPR_LCM || expr > QDP_EXPR_ADJ_UPSI)
+    return set_error(ctx, QDP_EINVAL, "expr: unknown expression %d", expr);
   if ((expr == QDP_EXPR_MATVEC) != (c != nullptr)) return set_error(ctx, QDP_EINVAL, "expr: c is used by MATVEC only");
-  static const int kinds[5][4] = {{QDP_COLORMATRIX, QDP_COLORMATRIX, QDP_COLORMATRIX, -1},
+  static const int kinds[6][4] = {{QDP_COLORMATRIX, QDP_COLORMATRIX, QDP_COLORMATRIX, -1},
                                   {QDP_FERMION, QDP_COLORMATRIX, QDP_FERMION, -1},
                                   {QDP_SPINMATRIX, QDP_SPINMATRIX, QDP_SPINMATRIX, -1},
                                   {QDP_FERMION, QDP_COLORMATRIX, QDP_FERMION, QDP_FERMION},
-                                  {QDP_FERMION, QDP_CLOVER, QDP_FERMION, -1}};
+                                  {QDP_FERMION, QDP_CLOVER, QDP_FERMION, -1},
+                                  {QDP_FERMION, QDP_COLORMATRIX, QDP_FERMION, -1}};
   const qdp_field f[4] = {out, a, b, c};
   for (int k = 0; k < 4; k++) {
     if (!f[k]) continue;
@@ -715,7 +717,7 @@ extern "C" int qdp_expr(int expr, qdp_field out, const qdp_field a, const qdp_fi
 }
 
 extern "C" int qdp_expr_block(qdp_ctx c, int expr, int prec, int *block, int *tuned) {
-  if (!c || expr < QDP_EXPR_LCM || expr > QDP_EXPR_CLOVER || !valid_prec(prec)) return QDP_EINVAL;
+  if (!c || expr < QDP_EXPR_LCM || expr > QDP_EXPR_ADJ_UPSI || !valid_prec(prec)) return QDP_EINVAL;
   int bl = c->autotune ? 0 : 128, done = c->autotune ? 0 : 1;
   for (const auto &kv : c->tune) {
     if (kv.first / (1L << 40) != (long)expr * 2 + prec) continue;

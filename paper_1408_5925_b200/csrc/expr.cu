@@ -139,8 +139,15 @@ __global__ void expr_kernel(const Geom g, const ExprArgs e) {
         z.m[3 * r + col] = acc;
       }
     CMatView<R>{(decltype(CMatView<R>::p))out, g.stride}.store(cb, z);
-  } else if (EXPR == QDP_EXPR_UPSI || EXPR == QDP_EXPR_MATVEC) {
-    const Link<R> u = CMatView<R>{(decltype(CMatView<R>::p))a, g.stride}.load(cb);
+  } else if (EXPR == QDP_EXPR_UPSI || EXPR == QDP_EXPR_MATVEC || EXPR == QDP_EXPR_ADJ_UPSI) {
+    Link<R> u = CMatView<R>{(decltype(CMatView<R>::p))a, g.stride}.load(cb);
+    if (EXPR == QDP_EXPR_ADJ_UPSI) {  // u <- u^dag
+      Link<R> t = u;
+#pragma unroll
+      for (int r = 0; r < 3; r++)
+#pragma unroll
+        for (int col = 0; col < 3; col++) u.m[3 * r + col] = {t.m[3 * col + r].re, -t.m[3 * col + r].im};
+    }
     Spinor<R> o = mul_spinor(u, FV{(decltype(FV::p))b, g.stride}.load_stream(cb));
     if (EXPR == QDP_EXPR_MATVEC) {
       const char *c = (const char *)e.c + blk * e.c_blk;
@@ -173,7 +180,8 @@ __global__ void expr_kernel(const Geom g, const ExprArgs e) {
 static void expr_work(int expr, double &flops, double &reals) {
   switch (expr) {
     case QDP_EXPR_LCM: flops = 198; reals = 54; break;        // 3 colour matrices
-    case QDP_EXPR_UPSI: flops = 264; reals = 18 + 48; break;  // U, psi, psi
+    case QDP_EXPR_UPSI:
+    case QDP_EXPR_ADJ_UPSI: flops = 264; reals = 18 + 48; break;  // U, psi, psi
     case QDP_EXPR_SPMAT: flops = 480; reals = 96; break;      // 3 spin matrices
     case QDP_EXPR_MATVEC: flops = 552; reals = 18 + 72; break;  // U once (compulsory), 3 fermions
     default: flops = 504; reals = 72 + 48; break;             // clover, 2 fermions
@@ -202,6 +210,7 @@ static cudaError_t launch_expr(qdp_ctx ctx, int expr, const ExprArgs &e, int blo
   switch (expr) {
     case QDP_EXPR_LCM: return launch<R, QDP_EXPR_LCM>(ctx, e, block);
     case QDP_EXPR_UPSI: return launch<R, QDP_EXPR_UPSI>(ctx, e, block);
+    case QDP_EXPR_ADJ_UPSI: return launch<R, QDP_EXPR_ADJ_UPSI>(ctx, e, block);
     case QDP_EXPR_SPMAT: return launch<R, QDP_EXPR_SPMAT>(ctx, e, block);
     case QDP_EXPR_MATVEC: return launch<R, QDP_EXPR_MATVEC>(ctx, e, block);
     default: return launch<R, QDP_EXPR_CLOVER>(ctx, e, block);

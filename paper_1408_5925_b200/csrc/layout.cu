@@ -83,6 +83,13 @@ SlotMap make_slot_map(int kind, int prec, int stride, int subset) {
           }
         }
   }
+  // fp32: an even slot whose successor fills the other half of the same 16-byte element can be
+  // moved together with it in one 16-byte access (both parities share the pattern)
+  for (int k = 0; k + 1 < m.n; k++) {
+    const int p = m.off[0][k] >= 0 ? 0 : 1;
+    m.pair[k] = prec == QDP_F32 && m.step[k] == 16 && m.step[k + 1] == 16 && m.off[p][k] >= 0 &&
+                m.off[p][k] % 16 == 0 && m.off[p][k + 1] == m.off[p][k] + 8;
+  }
   return m;
 }
 

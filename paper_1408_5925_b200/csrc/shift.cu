@@ -50,8 +50,16 @@ __global__ void shift_kernel(const Geom g, const SlotMap mo, const SlotMap mi, c
       *(T *)(out + mo.off[p][k] + (long long)cb * mo.step[k]) = ghost[((size_t)q * mo.n + k) * nf + f];
   } else {
     const int scb = coords_cb(g, c);
-    for (int k = 0; k < mo.n; k++)
-      *(T *)(out + mo.off[p][k] + (long long)cb * mo.step[k]) = *(const T *)(in + mi.off[q][k] + (long long)scb * mi.step[k]);
+    for (int k = 0; k < mo.n; k++) {
+      char *d = out + mo.off[p][k] + (long long)cb * mo.step[k];
+      const char *s = in + mi.off[q][k] + (long long)scb * mi.step[k];
+      if (sizeof(R) == 4 && mo.pair[k]) {  // two fp32 complex in one 16-byte access
+        *(float4 *)d = *(const float4 *)s;
+        k++;
+      } else {
+        *(T *)d = *(const T *)s;
+      }
+    }
   }
 }
 

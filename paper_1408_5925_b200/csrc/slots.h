@@ -9,6 +9,7 @@ struct SlotMap {
   int n;                  // 12 (fermion) or 36 (gauge: mu*9 + 3*row + col)
   long long off[2][36];   // -1: parity not present in the field
   int step[36];
+  unsigned char pair[36]; // 1: slots k, k+1 are the two halves of one 16-byte element (fp32)
 };
 SlotMap make_slot_map(int kind, int prec, int stride, int subset);
 }  // namespace qdpb

@@ -19,7 +19,7 @@ HEADER = os.path.join(os.path.dirname(_HERE), "include", "qdpb.h")
 
 QDP_F64, QDP_F32 = 0, 1
 QDP_FERMION, QDP_GAUGE, QDP_CLOVER, QDP_GAUGE12, QDP_COLORMATRIX, QDP_SPINMATRIX = range(6)
-QDP_EXPR_LCM, QDP_EXPR_UPSI, QDP_EXPR_SPMAT, QDP_EXPR_MATVEC, QDP_EXPR_CLOVER = range(5)
+QDP_EXPR_LCM, QDP_EXPR_UPSI, QDP_EXPR_SPMAT, QDP_EXPR_MATVEC, QDP_EXPR_CLOVER, QDP_EXPR_ADJ_UPSI = range(6)
 QDP_ALL, QDP_EVEN, QDP_ODD = -1, 0, 1
 QDP_FORWARD, QDP_BACKWARD = 1, -1
 QDP_OK, QDP_NOT_CONVERGED = 0, 1

@@ -57,6 +57,20 @@ def test_upsi_norm_and_consistency():
     assert got[0, 2, 1] == 2 - 1j and np.count_nonzero(got) == 1
 
 
+def test_adj_upsi_inverts_upsi():
+    """For SU(3) u: adj(u) (u psi) = psi; and adj(u) differs from u (a transposition bug would not)."""
+    n = 30
+    u = fieldgen.random_su3(n, 10)
+    psi = fieldgen.random_spinor((n, 1, 1, 1), 11)
+    assert np.max(np.abs(oracle.adj_upsi(u, oracle.upsi(u, psi)) - psi)) < 1e-14
+    assert np.max(np.abs(oracle.adj_upsi(u, psi) - oracle.upsi(u, psi))) > 0.1
+    # hand case: u = i * identity -> adj(u) psi = -i psi
+    ui = np.zeros((1, 3, 3), dtype=complex)
+    ui[0] = 1j * np.eye(3)
+    p = c(fieldgen.random_spinor((1, 1, 1, 1), 12))
+    assert np.allclose(c(oracle.adj_upsi(r(ui), r(p))), -1j * p, atol=0, rtol=1e-15)
+
+
 def test_matvec_linearity():
     n = 40
     u = fieldgen.random_su3(n, 7)
