@@ -145,6 +145,27 @@ def test_device_buffer_import_export(q, prec):
         q.qdp_finalize(c)
 
 
+def test_dslash_production_lattice(q):
+    """The paper's production lattice 40^3 x 256 (16.4M sites, 9.4 GB of links) on
+    one GPU: every output site of one EO dslash (fp64) against the oracle -- 64-bit offsets and
+    large-grid indexing at the largest size in BASELINE.json."""
+    L = (40, 40, 40, 256)
+    U = fieldgen.random_gauge(L, 1004)
+    psi = fieldgen.random_spinor(L, 2005)
+    ref = oracle.hopping(U, psi, L, 1)
+    odd = fieldgen.cb_sites(L, 1)
+    c = q.qdp_init(L)
+    try:
+        fU = _field(q, c, q.QDP_GAUGE, 0, q.QDP_ALL, U)
+        del U
+        fp = _field(q, c, q.QDP_FERMION, 0, 0, np.ascontiguousarray(psi[fieldgen.cb_sites(L, 0)]))
+        fo = q.qdp_field_alloc(c, q.QDP_FERMION, 0, 1)
+        q.qdp_dslash(fo, fU, fp, 1)
+        assert rel_site_err(q.qdp_field_export(fo), ref[odd]) <= 1e-13
+    finally:
+        q.qdp_finalize(c)
+
+
 def test_init_limits(q):
     with pytest.raises(q.QdpError) as e:
         q.qdp_init((2048, 2048, 2048, 2))      # V/2 > 2^30 sites per parity
