@@ -41,6 +41,7 @@ def lib():
         ip = ctypes.POINTER(ctypes.c_int)
         _lib.orc_norm2.restype = ctypes.c_double
         _lib.orc_cg_solve.restype = ctypes.c_int
+        _lib.orc_cg_multishift.restype = ctypes.c_int
         _lib.orc_clover_invert.restype = ctypes.c_int
         _lib.orc_max_threads.restype = ctypes.c_int
         del dp, ip
@@ -156,6 +157,38 @@ def cg_solve(U, b, L, mass: float, A=None, tol: float = 1e-10, maxit: int = 1000
         raise ZeroDivisionError("singular clover block")
     n = iters.value
     return dict(x=x, iters=n, hist=hist[:n + 1].copy(), true_resid=tr.value, status=st)
+
+
+def mhat_apply(U, A, mass: float, v, L, dagger: bool = False) -> np.ndarray:
+    """Mhat v (or Mhat^dag v) on the odd sites, Mhat = A_oo - 1/4 H_oe A_ee^-1 H_eo; even sites 0."""
+    v = _f64(v)
+    out = np.zeros_like(v)
+    Ap = _p(_f64(A)) if A is not None else None
+    lib().orc_mhat_apply(_p(out), _p(_f64(U)), Ap, ctypes.c_double(mass), _p(v), _L(L), int(bool(dagger)))
+    return out
+
+
+def cg_multishift(U, phi, L, mass: float, sigma, A=None, tol: float = 1e-10, maxit: int = 10000):
+    """Multi-shift CG for (Mhat^dag Mhat + sigma_i) x_i = phi_o (oracle.c orc_cg_multishift).
+    Returns dict(x [n,V,4,3,2], iters, conv_iter [n], hist, true_resid [n], status)."""
+    phi = _f64(phi)
+    sigma = np.ascontiguousarray(sigma, dtype=np.float64)
+    n = len(sigma)
+    x = np.zeros((n,) + phi.shape)
+    hist = np.zeros(maxit + 1)
+    conv = (ctypes.c_int * n)()
+    tr = np.zeros(n)
+    iters = ctypes.c_int(0)
+    Ap = _p(_f64(A)) if A is not None else None
+    st = lib().orc_cg_multishift(_p(x), _p(phi), _p(_f64(U)), Ap, ctypes.c_double(mass), _L(L), int(n), _p(sigma),
+                                 ctypes.c_double(tol), int(maxit), ctypes.byref(iters), conv, _p(hist),
+                                 int(maxit + 1), _p(tr))
+    if st == -1:
+        raise ZeroDivisionError("singular clover block")
+    if st == -2:
+        raise ValueError("shifts: sigma[0] must be the smallest")
+    k = iters.value
+    return dict(x=x, iters=k, conv_iter=np.array(conv[:]), hist=hist[:k + 1].copy(), true_resid=tr, status=st)
 
 
 def _n(a, per):

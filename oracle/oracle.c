@@ -575,6 +575,139 @@ int orc_cg_solve(double *x, const double *b, const double *U, const double *A, d
     return status;
 }
 
+/* out_o = Mhat v_o (dagger = 0) or Mhat^dag v_o (dagger = 1); even sites of out zero.
+ * Exposed so tests can assemble the dense even-odd operator column by column. */
+void orc_mhat_apply(double *out, const double *U, const double *A, double mass, const double *v,
+                    const int L[4], int dagger) {
+    long V = vol(L);
+    size_t nb = sizeof(double) * 24 * (size_t)V;
+    double *Ainv = NULL;
+    if (A) {
+        Ainv = (double *)malloc(sizeof(double) * 288 * (size_t)V);
+        orc_clover_invert(Ainv, A, L, 0);
+    }
+    double *t1 = calloc(1, nb), *t2 = calloc(1, nb), *g = calloc(1, nb), *vo = calloc(1, nb);
+    op_t op = {L, U, A, Ainv, 4.0 + mass, V, t1, t2};
+    for (long s = 0; s < V; s++)
+        if (in_subset(s, L, 1)) memcpy(vo + s * 24, v + s * 24, sizeof(double) * 24);
+    if (dagger) apply_Mhat_dag(&op, out, vo, g);
+    else apply_Mhat(&op, out, vo);
+    free(t1); free(t2); free(g); free(vo); free(Ainv);
+}
+
+/* Multi-shift CG (the solver of the paper's RHMC production runs, ref. [14];
+ * reading R25): solves (Mhat^dag Mhat + sigma_i) x_i = phi on the odd sites for all i at once,
+ * from ONE Krylov space: plain CG on the base system sigma_0 (sigma_0 <= sigma_i), the shifted
+ * residuals collinear, r_i = zeta_i r, with (s_i = sigma_i - sigma_0, x_i = 0, p_i = phi):
+ *   zeta_i(k+1) = zeta_i(k) zeta_i(k-1) alpha(k-1) /
+ *                 [alpha(k) beta(k-1) (zeta_i(k-1) - zeta_i(k)) + zeta_i(k-1) alpha(k-1) (1 + s_i alpha(k))]
+ *   alpha_i(k) = alpha(k) zeta_i(k+1) / zeta_i(k),   beta_i(k) = beta(k) (zeta_i(k+1) / zeta_i(k))^2
+ *   x_i += alpha_i(k) p_i ;  p_i = zeta_i(k+1) r(k+1) + beta_i(k) p_i
+ * with zeta(-1) = zeta(0) = 1, alpha(-1) = 1, beta(-1) = 0.  Shift i stops being updated once
+ * zeta_i(k+1)^2 rho(k+1) <= tol^2 rho(0) (its own relative residual); iterations stop when the
+ * base system (the slowest) converges.  Step by step, each line of the recurrence one C line.
+ * hist[k] = sqrt(rho_k / rho_0) of the base system; conv_iter[i] = iteration at which shift i
+ * stopped; true_resid[i] = |phi - (Mhat^dag Mhat + sigma_i) x_i| / |phi|.
+ * x: nshift consecutive fermion arrays [nshift][V][24]; only odd sites are written.
+ * Returns 0 converged, 1 not converged, -1 singular clover, -2 bad shifts. */
+int orc_cg_multishift(double *x, const double *phi, const double *U, const double *A, double mass,
+                      const int L[4], int nshift, const double *sigma, double tol, int maxit,
+                      int *iters, int *conv_iter, double *hist, int hist_cap, double *true_resid) {
+    if (nshift < 1) return -2;
+    for (int i = 1; i < nshift; i++)
+        if (sigma[i] < sigma[0]) return -2;
+    long V = vol(L);
+    size_t nb = sizeof(double) * 24 * (size_t)V;
+    double *Ainv = NULL;
+    if (A) {
+        Ainv = (double *)malloc(sizeof(double) * 288 * (size_t)V);
+        if (orc_clover_invert(Ainv, A, L, 0)) { free(Ainv); return -1; }
+    }
+    double *t1 = calloc(1, nb), *t2 = calloc(1, nb), *g = calloc(1, nb), *mp = calloc(1, nb);
+    double *r = calloc(1, nb), *q = calloc(1, nb), *p = calloc(1, nb * nshift);
+    op_t op = {L, U, A, Ainv, 4.0 + mass, V, t1, t2};
+    double *zeta = malloc(sizeof(double) * nshift), *zeta_old = malloc(sizeof(double) * nshift);
+    double *zeta_new = malloc(sizeof(double) * nshift);
+    int *active = malloc(sizeof(int) * nshift);
+
+    memset(x, 0, nb * nshift);
+    for (long s = 0; s < V; s++)
+        if (in_subset(s, L, 1)) {
+            memcpy(r + s * 24, phi + s * 24, sizeof(double) * 24);
+            for (int i = 0; i < nshift; i++) memcpy(p + i * 24 * V + s * 24, phi + s * 24, sizeof(double) * 24);
+        }
+    for (int i = 0; i < nshift; i++) { zeta[i] = zeta_old[i] = 1.0; active[i] = 1; conv_iter[i] = 0; }
+    double alpha_old = 1.0, beta_old = 0.0;
+    double rho0 = orc_norm2(r, L, 1), rho = rho0;
+    int k = 0, status = 1;
+    if (hist_cap > 0) hist[0] = 1.0;
+    if (rho0 == 0.0) status = 0;
+    while (status == 1 && k < maxit) {
+        /* q = (Mhat^dag Mhat + sigma_0) p_0 */
+        apply_Mhat(&op, mp, p);
+        apply_Mhat_dag(&op, q, mp, g);
+        orc_axpy(sigma[0], 0.0, p, q, L, 1);
+        double pq[2];
+        orc_inner(p, q, L, 1, pq);
+        double alpha = rho / pq[0];
+        /* shifted coefficients and solution updates */
+        for (int i = 0; i < nshift; i++) {
+            if (!active[i]) continue;
+            double a_i = alpha;
+            if (i == 0) zeta_new[i] = 1.0;
+            else {
+                double si = sigma[i] - sigma[0];
+                zeta_new[i] = zeta[i] * zeta_old[i] * alpha_old /
+                              (alpha * beta_old * (zeta_old[i] - zeta[i]) + zeta_old[i] * alpha_old * (1.0 + si * alpha));
+                a_i = alpha * zeta_new[i] / zeta[i];
+            }
+            orc_axpy(a_i, 0.0, p + i * 24 * V, x + i * 24 * V, L, 1);
+        }
+        orc_axpy(-alpha, 0.0, q, r, L, 1);
+        double rho_new = orc_norm2(r, L, 1);
+        k++;
+        if (k < hist_cap) hist[k] = sqrt(rho_new / rho0);
+        double beta = rho_new / rho;
+        for (int i = 0; i < nshift; i++) {
+            if (!active[i]) continue;
+            if (zeta_new[i] * zeta_new[i] * rho_new <= tol * tol * rho0) {  /* shift i converged */
+                active[i] = 0;
+                conv_iter[i] = k;
+                continue;
+            }
+            double b_i = beta * (zeta_new[i] / zeta[i]) * (zeta_new[i] / zeta[i]);
+            double *pi = p + i * 24 * V;
+            for (long s = 0; s < V; s++)
+                if (in_subset(s, L, 1))
+                    for (int c = 0; c < 24; c++) pi[s * 24 + c] = zeta_new[i] * r[s * 24 + c] + b_i * pi[s * 24 + c];
+            zeta_old[i] = zeta[i];
+            zeta[i] = zeta_new[i];
+        }
+        if (!active[0]) status = 0;
+        alpha_old = alpha;
+        beta_old = beta;
+        rho = rho_new;
+    }
+    for (int i = 0; i < nshift; i++)
+        if (active[i]) conv_iter[i] = k;
+    *iters = k;
+
+    /* true residuals */
+    for (int i = 0; i < nshift; i++) {
+        double *xi = x + i * 24 * V;
+        apply_Mhat(&op, mp, xi);
+        apply_Mhat_dag(&op, q, mp, g);
+        orc_axpy(sigma[i], 0.0, xi, q, L, 1);
+        for (long s = 0; s < V; s++)
+            if (in_subset(s, L, 1))
+                for (int c = 0; c < 24; c++) q[s * 24 + c] = phi[s * 24 + c] - q[s * 24 + c];
+        true_resid[i] = sqrt(orc_norm2(q, L, 1) / rho0);
+    }
+    free(t1); free(t2); free(g); free(mp); free(r); free(q); free(p);
+    free(zeta); free(zeta_old); free(zeta_new); free(active); free(Ainv);
+    return status;
+}
+
 /* ================= Table II test functions (section VI) ====================
  * Site-local products on n sites, host layouts: colour matrix [n][3][3][2], spin matrix
  * [n][4][4][2], fermion [n][4][3][2].  Plain definitions. */
