@@ -96,6 +96,28 @@ int qdp_get_unique_id(unsigned char id[128]);
  * The current CUDA device at the time of the call is the context's device. */
 int qdp_init(const int global_dims[4], const int proc_grid[4], int rank, int nranks,
              const unsigned char *id, void *cuda_stream, qdp_ctx *out);
+/* Host allgather supplied by the caller for qdp_init_peer: every rank passes `bytes` bytes
+ * in `send`; `recv` (nranks * bytes) receives all ranks' blocks in rank order.  Return 0 on
+ * success.  Called collectively, only from inside qdp_init_peer. */
+typedef int (*qdp_allgather_fn)(const void *send, void *recv, size_t bytes, void *user);
+
+/* Create a context whose inter-rank communication uses peer memory only, no NCCL
+ * (SURVEY.md 8(e) "B200-native upgrade"; the sub-grid decomposition of PAPER.md:93-95,
+ * 208-214).  Every rank's GPU must be able to map every other rank's memory through CUDA IPC
+ * (GPUs of one NVLink / NVSwitch node, or several processes sharing one GPU).  Arguments as
+ * qdp_init; `allgather` (with `user`) exchanges the IPC handles during this call and is not
+ * used afterwards.  Then:
+ *  - dslash halos always use the peer-to-peer protocol of QDP_OPT_P2P (it cannot be turned off);
+ *  - global sums (norm2, inner_product, the CG's) are one kernel per sum: each rank stores its
+ *    partial into every rank's mapped board and release-signals a flag, then acquires all
+ *    flags and sums in rank order (deterministic, identical on every rank);
+ *  - shift faces are copied into the receiving rank's mapped mailbox by a kernel, with
+ *    release/acquire flags (the mailbox holds the largest face of a fp64 gauge field).
+ * At most 16 ranks (QDP_EUNSUPPORTED).  QDP_OPT_SELF_NCCL returns QDP_EUNSUPPORTED.  A flag
+ * wait that exceeds ~10 s sets an error word reported as QDP_ECUDA by the next synchronising
+ * call (no hang). */
+int qdp_init_peer(const int global_dims[4], const int proc_grid[4], int rank, int nranks,
+                  qdp_allgather_fn allgather, void *user, void *cuda_stream, qdp_ctx *out);
 int qdp_finalize(qdp_ctx ctx);
 int qdp_set_stream(qdp_ctx ctx, void *cuda_stream);
 int qdp_synchronize(qdp_ctx ctx);

@@ -322,6 +322,7 @@ int blas_inner(qdp_ctx ctx, int prec, const void *a, const void *b, int nblk, in
 
 int reduce_global(qdp_ctx ctx, int slot, int n) {
   if (ctx->nranks == 1) return QDP_OK;
+  if (ctx->peer) return peer_allreduce(ctx, slot, n);  // one kernel, deterministic (peer.cu)
   int rc;
   if (ctx->det_reduce) {
     if ((rc = comm_allgather_f64(ctx, ctx->red_result + slot, ctx->red_gather, n, ctx->stream))) return rc;

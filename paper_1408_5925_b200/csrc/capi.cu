@@ -176,8 +176,9 @@ extern "C" int qdp_get_unique_id(unsigned char id[128]) {
   return comm_get_unique_id(id);
 }
 
-extern "C" int qdp_init(const int global_dims[4], const int proc_grid[4], int rank, int nranks, const unsigned char *id,
-                        void *cuda_stream, qdp_ctx *out) {
+// Everything of a context but its communicator.
+static int ctx_create(const int global_dims[4], const int proc_grid[4], int rank, int nranks, void *cuda_stream,
+                      qdp_ctx *out) {
   if (!global_dims || !proc_grid || !out) return QDP_EINVAL;
   *out = nullptr;
   if (nranks < 1 || rank < 0 || rank >= nranks) return QDP_EINVAL;
@@ -241,7 +242,42 @@ extern "C" int qdp_init(const int global_dims[4], const int proc_grid[4], int ra
   if (!rc && (e = cudaMemset(c->red_result, 0, 64 * sizeof(double))) != cudaSuccess) rc = cuda_check(c, e, "scalars");
   if (!rc && (e = cudaMalloc((void **)&c->red_gather, 8 * sizeof(double) * nranks)) != cudaSuccess) rc = cuda_check(c, e, "gather");
   if (!rc && (e = cudaMallocHost((void **)&c->host_pinned, 64 * sizeof(double))) != cudaSuccess) rc = cuda_check(c, e, "pinned");
-  if (!rc) rc = comm_init(c, id);
+  if (rc) {
+    qdp_finalize(c);
+    return rc;
+  }
+  *out = c;
+  return QDP_OK;
+}
+
+extern "C" int qdp_init(const int global_dims[4], const int proc_grid[4], int rank, int nranks, const unsigned char *id,
+                        void *cuda_stream, qdp_ctx *out) {
+  if (!out) return QDP_EINVAL;
+  qdp_ctx c = nullptr;
+  int rc = ctx_create(global_dims, proc_grid, rank, nranks, cuda_stream, &c);
+  if (rc) return rc;
+  if ((rc = comm_init(c, id))) {
+    qdp_finalize(c);
+    return rc;
+  }
+  *out = c;
+  return QDP_OK;
+}
+
+extern "C" int qdp_init_peer(const int global_dims[4], const int proc_grid[4], int rank, int nranks,
+                             qdp_allgather_fn allgather, void *user, void *cuda_stream, qdp_ctx *out) {
+  if (!out || !allgather) return QDP_EINVAL;
+  *out = nullptr;
+  qdp_ctx c = nullptr;
+  int rc = ctx_create(global_dims, proc_grid, rank, nranks, cuda_stream, &c);
+  if (rc) return rc;
+  c->allgather = allgather;
+  c->allgather_user = user;
+  c->p2p_on = 1;
+  if (!rc) rc = peer_init(c);
+  if (!rc) rc = p2p_setup_all(c);
+  c->allgather = nullptr;  // set-up done: the callback is never called again
+  c->allgather_user = nullptr;
   if (rc) {
     qdp_finalize(c);
     return rc;
@@ -256,6 +292,7 @@ extern "C" int qdp_finalize(qdp_ctx c) {
   resolve_profile(c);
   tune_release(c);
   p2p_destroy(c);
+  peer_destroy(c);
   comm_destroy(c);
   for (auto e : c->event_pool) cudaEventDestroy(e);
   if (c->ev_packed) cudaEventDestroy(c->ev_packed);
@@ -328,10 +365,15 @@ extern "C" int qdp_set_option(qdp_ctx c, int opt, long v) {
     case QDP_OPT_DET_REDUCE: c->det_reduce = v ? 1 : 0; return QDP_OK;
     case QDP_OPT_AUTOTUNE: c->autotune = v ? 1 : 0; return QDP_OK;
     case QDP_OPT_P2P:
+      if (c->peer) {
+        if (!v) return set_error(c, QDP_EUNSUPPORTED, "p2p: always on in a peer-memory context");
+        return QDP_OK;
+      }
       if (v && c->nranks > 1 && !c->comm) return set_error(c, QDP_ENCCL, "p2p: needs the NCCL communicator for setup");
       c->p2p_on = v ? 1 : 0;
       return QDP_OK;
     case QDP_OPT_SELF_NCCL: {
+      if (v && c->peer) return set_error(c, QDP_EUNSUPPORTED, "no NCCL in a peer-memory context");
       if (v) {
         int rc = comm_ensure_self(c);
         if (rc) return rc;
@@ -558,7 +600,7 @@ static int read_result(qdp_ctx c, int slot, int n, double *out) {
   QDP_CUDA(c, cudaMemcpyAsync(c->host_pinned, c->red_result + slot, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   QDP_CUDA(c, cudaStreamSynchronize(c->stream));
   memcpy(out, c->host_pinned, n * sizeof(double));
-  return QDP_OK;
+  return c->peer ? peer_check(c) : QDP_OK;
 }
 
 extern "C" int qdp_norm2(const qdp_field a, double *out) {

@@ -92,6 +92,10 @@ static int p2p_setup(qdp_ctx ctx, int prec) {
         for (int d = 0; d < 2; d++) QDP_CUDA(ctx, cudaIpcGetMemHandle(&mine.recv[mu][d], p->recv[prec][mu][d]));
     QDP_CUDA(ctx, cudaIpcGetMemHandle(&mine.flags, p->flags));
     std::vector<HandleMsg> all(ctx->nranks);
+    if (ctx->peer) {
+      int rc = host_allgather(ctx, &mine, all.data(), sizeof(HandleMsg));
+      if (rc) return rc;
+    } else {
     char *dev = nullptr;
     QDP_CUDA(ctx, cudaMalloc(&dev, sizeof(HandleMsg) * (ctx->nranks + 1)));
     QDP_CUDA(ctx, cudaMemcpy(dev, &mine, sizeof(HandleMsg), cudaMemcpyHostToDevice));
@@ -103,6 +107,8 @@ static int p2p_setup(qdp_ctx ctx, int prec) {
     }
     cudaFree(dev);
     if (rc) return rc;
+    }
+    int rc;
     auto open = [&](const cudaIpcMemHandle_t &h, void **out) -> int {
       cudaError_t e = cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess);
       if (e != cudaSuccess) return cuda_check(ctx, e, "p2p: cudaIpcOpenMemHandle (peer not reachable?)");
@@ -128,6 +134,12 @@ static int p2p_setup(qdp_ctx ctx, int prec) {
   }
   p->slot_bytes[prec] = need;
   return QDP_OK;
+}
+
+int p2p_setup_all(qdp_ctx ctx) {
+  int rc;
+  if ((rc = p2p_setup(ctx, QDP_F64))) return rc;
+  return p2p_setup(ctx, QDP_F32);
 }
 
 unsigned p2p_next_seq(qdp_ctx ctx, int prec) { return ctx->p2p ? ++ctx->p2p->seq[prec] : 1u; }
@@ -161,6 +173,10 @@ int p2p_prepare(qdp_ctx ctx, int prec, unsigned seq, P2PLaunch *L) {
 }
 
 int p2p_check(qdp_ctx ctx) {
+  if (ctx->peer) {
+    int rc = peer_check(ctx);
+    if (rc) return rc;
+  }
   if (!ctx->p2p) return QDP_OK;
   unsigned e = 0;
   QDP_CUDA(ctx, cudaMemcpyAsync(&e, ctx->p2p->flags + NFLAGS, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));

@@ -75,6 +75,7 @@ int shift_field(qdp_ctx ctx, qdp_field out, const qdp_field in, int mu, int sign
   const bool remote = (g.part >> mu) & 1;
   const size_t cbytes = in->prec == QDP_F64 ? 16 : 8;
   void *ghost = nullptr;
+  unsigned peer_seq = 0;
   int rc;
   if (remote) {
     const size_t bytes = (size_t)2 * mi.n * g.faceVh[mu] * cbytes;
@@ -94,11 +95,15 @@ int shift_field(qdp_ctx ctx, qdp_field out, const qdp_field in, int mu, int sign
     else
       shift_pack_kernel<float><<<grid_for(nth, 128), 128, 0, ctx->stream>>>(g, mi, (const char *)in->data, mu, xmu, nq, q0, (float2 *)dst);
     if ((rc = prof_end(ctx, &ev))) return rc;
+    ghost = recv;
     if (!self) {
       const int to = ctx->neighbour[mu][sign > 0 ? 0 : 1], from = ctx->neighbour[mu][sign > 0 ? 1 : 0];
-      if ((rc = comm_sendrecv(ctx, send, bytes, to, recv, from, ctx->stream))) return rc;
+      if (ctx->peer) {  // into the receiver's mapped mailbox (peer.cu); ghost = our own mailbox
+        if ((rc = peer_sendrecv(ctx, send, bytes, to, &ghost, &peer_seq))) return rc;
+      } else if ((rc = comm_sendrecv(ctx, send, bytes, to, recv, from, ctx->stream))) {
+        return rc;
+      }
     }
-    ghost = recv;
   }
   ProfEvent ev;
   prof_begin(ctx, QDP_PK_SHIFT, &ev);
@@ -110,7 +115,8 @@ int shift_field(qdp_ctx ctx, qdp_field out, const qdp_field in, int mu, int sign
   else
     shift_kernel<float><<<grid_for(nth, 128), 128, 0, ctx->stream>>>(g, mo, mi, (char *)out->data, (const char *)in->data, mu, sign,
                                                                       np, p0, remote, (const float2 *)ghost);
-  return prof_end(ctx, &ev);
+  if ((rc = prof_end(ctx, &ev))) return rc;
+  return peer_seq ? peer_release_mailbox(ctx, peer_seq) : QDP_OK;
 }
 
 }  // namespace qdpb

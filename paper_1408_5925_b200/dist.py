@@ -88,6 +88,27 @@ def bootstrap(global_dims, P, stream=None):
     return q.qdp_init(global_dims, P, 0, 1, None, stream)
 
 
+def torch_allgather_bytes(blob: bytes) -> bytes:
+    """Host allgather of equal-sized byte blocks over the default torch.distributed group
+    (gloo or nccl), concatenated in rank order: the set-up callback of qdp_init_peer."""
+    import torch.distributed as dist
+    out = [None] * dist.get_world_size()
+    dist.all_gather_object(out, bytes(blob))
+    return b"".join(out)
+
+
+def bootstrap_peer(global_dims, P, stream=None):
+    """Create this rank's peer-memory context (qdp_init_peer: halos, shift faces and global
+    sums through IPC-mapped device memory, no NCCL); IPC handles travel over the default
+    torch.distributed group, which may be gloo."""
+    import torch.distributed as dist
+
+    from . import qdpb as q
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        return q.qdp_init_peer(global_dims, P, dist.get_rank(), dist.get_world_size(), torch_allgather_bytes, stream)
+    return q.qdp_init(global_dims, P, 0, 1, None, stream)
+
+
 def max_over_ranks(value: float) -> float:
     import torch
     import torch.distributed as dist

@@ -33,11 +33,14 @@ PK_NAMES = ["dslash", "dslash_ext", "pack", "blas", "reduce", "clover", "shift",
 
 _lib = None
 _vp = ctypes.c_void_p
+# int (*qdp_allgather_fn)(const void *send, void *recv, size_t bytes, void *user)
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
 _ip = ctypes.POINTER(ctypes.c_int)
 _dp = ctypes.POINTER(ctypes.c_double)
 _SIGS = {
     "qdp_get_unique_id": [ctypes.c_char_p],
     "qdp_init": [_ip, _ip, ctypes.c_int, ctypes.c_int, ctypes.c_char_p, _vp, ctypes.POINTER(_vp)],
+    "qdp_init_peer": [_ip, _ip, ctypes.c_int, ctypes.c_int, ALLGATHER_FN, _vp, _vp, ctypes.POINTER(_vp)],
     "qdp_finalize": [_vp],
     "qdp_set_stream": [_vp, _vp],
     "qdp_synchronize": [_vp],
@@ -179,6 +182,32 @@ def qdp_init(global_dims, proc_grid=(1, 1, 1, 1), rank=0, nranks=1, nccl_id=None
     idb = None if nccl_id is None else ctypes.create_string_buffer(bytes(nccl_id), 128)
     st = lib().qdp_init(_i4(global_dims), _i4(proc_grid), int(rank), int(nranks), idb, _stream_ptr(stream),
                         ctypes.byref(out))
+    _check(st)
+    return Ctx(out.value, global_dims, proc_grid, rank, nranks)
+
+
+def qdp_init_peer(global_dims, proc_grid, rank, nranks, allgather, stream=None) -> Ctx:
+    """Peer-memory context (no NCCL).  `allgather(bytes) -> bytes` is the caller's host
+    allgather (all ranks' blocks concatenated in rank order); it runs only inside this call."""
+    err = []
+
+    def _cb(send, recv, nbytes, _user):
+        try:
+            out = allgather(ctypes.string_at(send, nbytes))
+            if len(out) != nbytes * int(nranks):
+                raise ValueError(f"allgather returned {len(out)} bytes, expected {nbytes * nranks}")
+            ctypes.memmove(recv, out, len(out))
+            return 0
+        except Exception as e:  # reported after the call; the C side sees a failure status
+            err.append(e)
+            return 1
+
+    fn = ALLGATHER_FN(_cb)
+    out = _vp()
+    st = lib().qdp_init_peer(_i4(global_dims), _i4(proc_grid), int(rank), int(nranks), fn, None,
+                             _stream_ptr(stream), ctypes.byref(out))
+    if err:
+        raise err[0]
     _check(st)
     return Ctx(out.value, global_dims, proc_grid, rank, nranks)
 
