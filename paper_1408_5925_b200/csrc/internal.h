@@ -463,8 +463,10 @@ inline bool is_gauge(int kind) { return kind == KIND_GAUGE || kind == KIND_GAUGE
 size_t parity_block_bytes(int kind, int prec, int stride);  // bytes of one parity block
 size_t host_site_reals(int kind);                           // 24 / 72 / 288
 
-struct Comm;  // comm.cpp
-struct P2P;   // p2p.cu
+struct Comm;      // comm.cpp
+struct P2P;       // p2p.cu
+struct PeerComm;  // peer.cu
+#define PEER_MAX_RANKS 16
 
 struct ProfEvent {
   int cls;
@@ -507,6 +509,11 @@ struct qdp_ctx_s {
   qdpb::Comm *comm = nullptr;
   qdpb::P2P *p2p = nullptr;  // peer-to-peer halo state (QDP_OPT_P2P)
   int p2p_on = 0;
+  // peer-memory communicator (qdp_init_peer; peer.cu): no NCCL; the host allgather callback
+  // exchanges IPC handles at set-up time only
+  qdpb::PeerComm *peer = nullptr;
+  qdp_allgather_fn allgather = nullptr;
+  void *allgather_user = nullptr;
   int neighbour[4][2];  // ranks of -mu / +mu neighbours
   // profiling / counting
   long launches[QDP_PK_COUNT] = {};
@@ -588,6 +595,7 @@ struct DslashArgs {
   bool g5_in, g5_out;
   const void *dot_x;      // if set: red_result[dot_slot] = Re<dot_x, out> (global), [dot_slot+1] = 0
   int dot_slot;
+  double dot_shift;       // with dot_x: out += dot_shift * dot_x before the dot (multi-shift CG base shift)
   bool rec12;             // U is a QDP_GAUGE12 field
 };
 int dslash(qdp_ctx ctx, int prec, const DslashArgs &a);
@@ -628,9 +636,24 @@ int shift_field(qdp_ctx ctx, qdp_field out, const qdp_field in, int mu, int sign
 int cg_solve(qdp_field x, const qdp_field b, const qdp_field U, const qdp_field A,
              const qdp_field Ainv, double mass, double tol, int maxit, int *iters,
              double *hist, int hist_cap, double *true_resid);
+int cg_solve_multishift(qdp_field *x, int nshift, const double *sigma, const qdp_field phi, const qdp_field U,
+                        const qdp_field A, const qdp_field Ainv, double mass, double tol, int maxit, int *iters,
+                        int *conv_iter, double *hist, int hist_cap, double *true_resid);
 int cg_solve_mixed(qdp_field x, const qdp_field b, const qdp_field U, const qdp_field A, const qdp_field Ainv,
                    const qdp_field Us, const qdp_field As, const qdp_field Ainvs, double mass, double tol, double delta,
                    int maxit, int *iters, int *nreliable, double *hist, int hist_cap, double *true_resid);
+
+// peer.cu: the peer-memory communicator of qdp_init_peer
+int peer_init(qdp_ctx ctx);
+void peer_destroy(qdp_ctx ctx);
+int host_allgather(qdp_ctx ctx, const void *send, void *recv, size_t bytes);  // set-up only
+int peer_allreduce(qdp_ctx ctx, int slot, int n);  // red_result[slot..slot+n) summed over ranks, rank order
+// copy `bytes` of a packed face into rank `to`'s mailbox and wait for this rank's own
+// mailbox to receive the face of the same call; *ghost = the mailbox, *seq for release
+int peer_sendrecv(qdp_ctx ctx, const void *send, size_t bytes, int to, void **ghost, unsigned *seq);
+int peer_release_mailbox(qdp_ctx ctx, unsigned seq);  // after the mailbox has been read
+int peer_check(qdp_ctx ctx);                          // QDP_ECUDA if a flag wait timed out
+int p2p_setup_all(qdp_ctx ctx);                       // eager p2p halo set-up, both precisions
 
 // comm.cpp
 int comm_get_unique_id(unsigned char id[128]);
