@@ -228,6 +228,26 @@ int qdp_cg_solve(qdp_field x, const qdp_field b, const qdp_field U, const qdp_fi
                  const qdp_field Ainv, double mass, double tol, int maxit, int *iters,
                  double *resid_hist, int hist_cap, double *true_resid);
 
+/* Multi-shift CG (the solver of RHMC gauge generation, ref. [14]; reading
+ * R25): solves (Mhat^dag Mhat + sigma_i) x_i = phi on the odd sites for i = 0..nshift-1 from
+ * ONE Krylov space (Mhat as in qdp_cg_solve).  CG runs on the base shift sigma_0; the shifted
+ * residuals are collinear, r_i = zeta_i r, and
+ *   zeta_i' = zeta_i zeta_i^old a^old / [a b^old (zeta_i^old - zeta_i) + zeta_i^old a^old (1 + (sigma_i - sigma_0) a)],
+ *   x_i += a zeta_i'/zeta_i p_i,  p_i = zeta_i' r + b (zeta_i'/zeta_i)^2 p_i.
+ * Shift i stops being updated once zeta_i'^2 |r|^2 <= tol^2 |phi|^2; the solve ends when the
+ * base system converges (status QDP_OK) or after maxit iterations (QDP_NOT_CONVERGED).
+ * x[i]: nshift distinct fermions covering the odd sites (QDP_ODD or QDP_ALL; only the odd block is
+ * written); phi: fermion covering the odd sites (its odd block is the source); U, A, Ainv, mass as
+ * qdp_cg_solve (A covering the odd, Ainv the even sites); all one precision.  Requires
+ * 1 <= nshift <= 32 and 0 <= sigma[0] <= sigma[i] (QDP_EINVAL).
+ * iters: iterations; conv_iter[i] (nullable): the iteration at which shift i stopped;
+ * resid_hist[k] (nullable) = |r_k| / |phi| of the base system; true_resid[i] (nullable) =
+ * |phi - (Mhat^dag Mhat + sigma_i) x_i| / |phi| (two more operator applications per shift). */
+int qdp_cg_solve_multishift(qdp_field *x, int nshift, const double *sigma, const qdp_field phi,
+                            const qdp_field U, const qdp_field A, const qdp_field Ainv, double mass,
+                            double tol, int maxit, int *iters, int *conv_iter, double *resid_hist,
+                            int hist_cap, double *true_resid);
+
 /* Mixed-precision variant of qdp_cg_solve (the reliable-update mixed-precision CG of the
  * paper's ref. [2], Clark et al.): the CGNR iteration runs on the QDP_F32 "sloppy" fields
  * U_s, A_s, Ainv_s (the same operator stored in single precision, e.g. imported from the

@@ -695,6 +695,40 @@ extern "C" int qdp_cg_solve(qdp_field x, const qdp_field b, const qdp_field U, c
   return cg_solve(x, b, U, A, Ainv, mass, tol, maxit, iters, resid_hist, hist_cap, true_resid);
 }
 
+extern "C" int qdp_cg_solve_multishift(qdp_field *x, int nshift, const double *sigma, const qdp_field phi,
+                                       const qdp_field U, const qdp_field A, const qdp_field Ainv, double mass,
+                                       double tol, int maxit, int *iters, int *conv_iter, double *resid_hist,
+                                       int hist_cap, double *true_resid) {
+  if (!x || !sigma || !phi || !U) return QDP_EINVAL;
+  qdp_ctx c = phi->ctx;
+  int rc;
+  if (nshift < 1 || nshift > QDPB_MAX_SHIFTS)
+    return set_error(c, QDP_EINVAL, "multishift: 1 <= nshift <= %d", QDPB_MAX_SHIFTS);
+  if ((rc = check_pair(phi, U))) return rc;
+  if (phi->kind != QDP_FERMION || !is_gauge(U->kind)) return set_error(c, QDP_EINVAL, "multishift: kinds (fermion, gauge)");
+  if (!block_of(phi, 1)) return set_error(c, QDP_EINVAL, "multishift: phi must cover the odd sites");
+  for (int i = 0; i < nshift; i++) {
+    if (!x[i]) return QDP_EINVAL;
+    if ((rc = check_pair(phi, x[i]))) return rc;
+    if (x[i]->kind != QDP_FERMION || !block_of(x[i], 1))
+      return set_error(c, QDP_EINVAL, "multishift: x[%d] must be a fermion covering the odd sites", i);
+    if (x[i]->data == phi->data) return set_error(c, QDP_EALIAS, "multishift: x[%d] aliases phi", i);
+    for (int j = 0; j < i; j++)
+      if (x[j]->data == x[i]->data) return set_error(c, QDP_EALIAS, "multishift: x[%d] aliases x[%d]", i, j);
+    if (!(sigma[i] >= 0.0) || sigma[i] < sigma[0])
+      return set_error(c, QDP_EINVAL, "multishift: need 0 <= sigma[0] <= sigma[i]");
+  }
+  if ((A == nullptr) != (Ainv == nullptr)) return set_error(c, QDP_EINVAL, "multishift: give both A and Ainv, or neither");
+  if (A) {
+    if ((rc = check_pair(phi, A)) || (rc = check_pair(phi, Ainv))) return rc;
+    if (A->kind != QDP_CLOVER || Ainv->kind != QDP_CLOVER) return set_error(c, QDP_EINVAL, "multishift: A, Ainv clover");
+    if (!block_of(A, 1) || !block_of(Ainv, 0)) return set_error(c, QDP_EINVAL, "multishift: A odd, Ainv even sites");
+  }
+  if (maxit < 0 || !(tol >= 0)) return set_error(c, QDP_EINVAL, "multishift: bad tol/maxit");
+  return cg_solve_multishift(x, nshift, sigma, phi, U, A, Ainv, mass, tol, maxit, iters, conv_iter, resid_hist,
+                             hist_cap, true_resid);
+}
+
 extern "C" int qdp_cg_solve_mixed(qdp_field x, const qdp_field b, const qdp_field U, const qdp_field A,
                                   const qdp_field Ainv, const qdp_field Us, const qdp_field As, const qdp_field Ainvs,
                                   double mass, double tol, double delta, int maxit, int *iters, int *reliable,

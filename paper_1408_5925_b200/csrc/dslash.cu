@@ -155,6 +155,7 @@ template <typename R, int REC = 18> struct KParams {
   // fused Re<dotx, out>: per-block partials
   FermView<R> dotx;
   double *dot_part;
+  R dot_shift;  // with a fused dot: out += dot_shift * dotx first
   // peer-to-peer halo (QDP_OPT_P2P; p2p.cu): pack waits war >= seq-2, stores, and its last
   // block release-stores seq into sig; the exterior waits ready >= seq and its last block
   // release-stores seq into ack_to.  pack_counter == nullptr: NCCL / direct halo.
@@ -273,8 +274,18 @@ __global__ void __launch_bounds__(QDPB_DSLASH_MAXT, (dslash_minb<R, REC>())) dsl
     hop_dir<R, 2>(g, P, c, cb, p, G5IN, HALO, acc);
     hop_dir<R, 3>(g, P, c, cb, p, G5IN, HALO, acc);
     Spinor<R> o = epilogue<R, EPI>(P, cb, acc, G5OUT);
-    P.out.store(cb, o);
-    if (DOT) dot = re_dot(P.dotx.load_stream(cb), o);
+    if (DOT) {
+      // fused Re<d, out> (and out += dot_shift d: the base shift of the multi-shift CG)
+      const Spinor<R> d = P.dotx.load_stream(cb);
+      if (P.dot_shift != R(0)) {
+#pragma unroll
+        for (int k = 0; k < 12; k++) o.c[k] = o.c[k] + P.dot_shift * d.c[k];
+      }
+      P.out.store(cb, o);
+      dot = re_dot(d, o);
+    } else {
+      P.out.store(cb, o);
+    }
   }
   if (DOT) dot_block_partial(dot, P.dot_part);
 }
@@ -437,7 +448,7 @@ static void dslash_work(qdp_ctx ctx, const DslashArgs &a) {
     case EPI_CLOVINV: f += 504 + 24 + (a.x ? 48 : 0); r += 72 + (a.x ? 24 : 0); break;
     default: f += 504 + 48; r += 72 + 24; break;
   }
-  if (a.dot_x) { f += 96; r += 24; }
+  if (a.dot_x) { f += 96 + (a.dot_shift != 0.0 ? 48 : 0); r += 24; }
   const double vh = ctx->geom.Vh;
   prof_work(ctx, QDP_PK_DSLASH, f * vh, r * vh * sizeof(R));
 }
@@ -488,6 +499,7 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
     if ((rc = ensure_reduce(ctx, nparts))) return rc;
     P.dotx = fview<R>(a.dot_x, g.stride);
     P.dot_part = ctx->red_partials;
+    P.dot_shift = (R)a.dot_shift;
   }
 
   unsigned seq = 0;

@@ -44,6 +44,9 @@
 template <typename R, int REC> constexpr int dslash_minb() {
   return sizeof(R) == 8 ? (REC == 18 ? QDPB_MINB_D18 : QDPB_MINB_D12) : (REC == 18 ? QDPB_MINB_F18 : QDPB_MINB_F12);
 }
+#ifndef QDPB_MAX_SHIFTS
+#define QDPB_MAX_SHIFTS 32  // qdp_cg_solve_multishift
+#endif
 #ifndef QDPB_DSLASH_BLOCK
 #define QDPB_DSLASH_BLOCK 64
 #endif

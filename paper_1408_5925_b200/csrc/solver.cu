@@ -59,7 +59,8 @@ DslashArgs args(const Op &op) {
 }
 
 // out_o = Mhat v_o  (dag: Mhat^dag); dot_x: also red_result[dot_slot] = Re<dot_x, out>
-int apply_mhat(const Op &op, void *out, const void *v, bool dag, const void *dot_x = nullptr, int dot_slot = 0) {
+int apply_mhat(const Op &op, void *out, const void *v, bool dag, const void *dot_x = nullptr, int dot_slot = 0,
+               double dot_shift = 0.0) {
   int rc;
   // t_e = [A_ee^-1] H_eo [g5] v
   DslashArgs a = args(op);
@@ -84,6 +85,7 @@ int apply_mhat(const Op &op, void *out, const void *v, bool dag, const void *dot
   c.g5_out = dag;
   c.dot_x = dot_x;
   c.dot_slot = dot_slot;
+  c.dot_shift = dot_shift;
   if (op.A_o) {
     c.epi = EPI_CLOVXPAY;
     c.clov = op.A_o;
@@ -186,6 +188,13 @@ int finish_solve(const Op &op, const qdp_field x, const qdp_field b, const qdp_f
   return QDP_OK;
 }
 }  // namespace
+
+// out_o = Mhat v_o (dag: Mhat^dag v_o) for the multi-shift solver (multishift.cu); with dot_x:
+// out += dot_shift * dot_x and red_result[dot_slot] = Re<dot_x, out>.  t: an even scratch block.
+int mhat_apply(qdp_ctx ctx, const qdp_field U, const qdp_field A, const qdp_field Ainv, double mass, void *t, void *out,
+               const void *v, bool dag, const void *dot_x, int dot_slot, double dot_shift) {
+  return apply_mhat(make_op(ctx, U, A, Ainv, mass, t), out, v, dag, dot_x, dot_slot, dot_shift);
+}
 
 int cg_solve(qdp_field x, const qdp_field b, const qdp_field U, const qdp_field A, const qdp_field Ainv, double mass,
              double tol, int maxit, int *iters_out, double *hist, int hist_cap, double *true_resid) {

@@ -70,6 +70,8 @@ _SIGS = {
                      ctypes.c_int, _dp],
     "qdp_cg_solve_mixed": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                            ctypes.c_int, _ip, _ip, _dp, ctypes.c_int, _dp],
+    "qdp_cg_solve_multishift": [ctypes.POINTER(_vp), ctypes.c_int, _dp, _vp, _vp, _vp, _vp, ctypes.c_double,
+                                ctypes.c_double, ctypes.c_int, _ip, _ip, _dp, ctypes.c_int, _dp],
     "qdp_expr": [ctypes.c_int, _vp, _vp, _vp, _vp],
     "qdp_expr_block": [_vp, ctypes.c_int, ctypes.c_int, _ip, _ip],
     "qdp_strerror": [ctypes.c_int],
@@ -380,6 +382,27 @@ def qdp_cg_solve_mixed(x: Field, b: Field, U: Field, A=None, Ainv=None, U_s: Fie
     n = iters.value
     return dict(status=st, iters=n, reliable=rel.value, hist=np.array(hist[:min(n + 1, hist_cap)]),
                 true_resid=tr.value if true_resid else None)
+
+
+def qdp_cg_solve_multishift(x, sigma, phi: Field, U: Field, A=None, Ainv=None, mass=0.1, tol=1e-10, maxit=10000,
+                            hist_cap=None, true_resid=True):
+    """(Mhat^dag Mhat + sigma_i) x_i = phi_o for every shift (x: list of fields, one per shift)."""
+    n = len(sigma)
+    if len(x) != n:
+        raise ValueError("one solution field per shift")
+    hist_cap = maxit + 1 if hist_cap is None else hist_cap
+    hist = (ctypes.c_double * max(hist_cap, 1))()
+    xs = (_vp * n)(*[f.ptr for f in x])
+    sg = (ctypes.c_double * n)(*[float(v) for v in sigma])
+    conv = (ctypes.c_int * n)()
+    tr = (ctypes.c_double * n)()
+    iters = ctypes.c_int()
+    st = lib().qdp_cg_solve_multishift(xs, n, sg, phi, U, A, Ainv, float(mass), float(tol), int(maxit),
+                                       ctypes.byref(iters), conv, hist, int(hist_cap), tr if true_resid else None)
+    _check(st, phi.ctx)
+    k = iters.value
+    return dict(status=st, iters=k, conv_iter=np.array(conv[:]), hist=np.array(hist[:min(k + 1, hist_cap)]),
+                true_resid=np.array(tr[:]) if true_resid else None)
 
 
 def qdp_expr(expr: int, out: Field, a: Field, b: Field, c: Field = None) -> None:

@@ -143,6 +143,25 @@ def _run(rank, world, case, G, P):
                 assert np.max(np.abs(res["hist"] - ref["hist"]) / ref["hist"]) <= 1e-10
                 assert res["true_resid"] <= 5e-10
                 assert rel_site_err(x, ref["x"]) <= 1e-9
+        elif case == "multishift":
+            m, sigma = 0.1, [0.0, 0.02, 0.5, 3.0]
+            fU = field(q.QDP_GAUGE, 0, q.QDP_ALL, Ul)
+            fphi = field(q.QDP_FERMION, 0, q.QDP_ALL, pl)
+            xs = [q.qdp_field_alloc(c, q.QDP_FERMION, 0, q.QDP_ALL) for _ in sigma]
+            fA = q.qdp_field_alloc(c, q.QDP_CLOVER, 0, q.QDP_ALL)
+            fAi = q.qdp_field_alloc(c, q.QDP_CLOVER, 0, q.QDP_EVEN)
+            q.qdp_clover_build(fA, fAi, fU, m, 1.0)
+            res = q.qdp_cg_solve_multishift(xs, sigma, fphi, fU, fA, fAi, mass=m, tol=1e-10, maxit=1000)
+            _same_on_all_ranks((res["iters"], tuple(res["hist"]), tuple(res["conv_iter"])))
+            got = [_gather(q.qdp_field_export(x), G, P, (4, 3, 2)) for x in xs]
+            if rank == 0:
+                ref = oracle.cg_multishift(U, psi, G, m, sigma, A=oracle.clover_build(U, G, m, 1.0), tol=1e-10,
+                                           maxit=1000)
+                odd = fieldgen.parity(G) == 1
+                assert res["iters"] == ref["iters"] and np.array_equal(res["conv_iter"], ref["conv_iter"])
+                assert np.max(np.abs(res["hist"] - ref["hist"]) / ref["hist"]) <= 1e-10
+                for i in range(len(sigma)):
+                    assert rel_site_err(got[i][odd], ref["x"][i][odd]) <= 1e-9
         else:
             raise ValueError(case)
     finally:

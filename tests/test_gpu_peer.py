@@ -40,6 +40,6 @@ def test_peer_shift():
 
 
 @pytest.mark.timeout(600)
-@pytest.mark.parametrize("case", ["cg", "cg_clover"])
+@pytest.mark.parametrize("case", ["cg", "cg_clover", "multishift"])
 def test_peer_cg(case):
     _spawn(case, (4, 4, 4, 8), (1, 1, 1, 2))
