@@ -196,9 +196,12 @@ def run_native(args, rank, world, local_rank):
     torch.cuda.set_stream(stream)
     gdims = (LOCAL[0], LOCAL[1], LOCAL[2], LOCAL[3] * world)
     P = qdist.proc_grid_for(world, gdims, split=(3,))
-    ctx = qdist.bootstrap(gdims, P, stream=stream)
+    if args.comm == "peer":  # no NCCL on the data path: halos, sums, shifts through peer memory
+        ctx = qdist.bootstrap_peer(gdims, P, stream=stream)
+    else:
+        ctx = qdist.bootstrap(gdims, P, stream=stream)
+        q.qdp_set_option(ctx, q.QDP_OPT_P2P, 1 if args.p2p else 0)
     q.qdp_set_option(ctx, q.QDP_OPT_OVERLAP, 0 if args.no_overlap else 1)
-    q.qdp_set_option(ctx, q.QDP_OPT_P2P, 1 if args.p2p else 0)
     L = LOCAL
     Vh = L[0] * L[1] * L[2] * L[3] // 2
 
@@ -370,6 +373,39 @@ def run_native(args, rank, world, local_rank):
         for f in (fU32, fU32r, fA32, fAi32):
             q.qdp_field_free(f)
 
+    # ---- multi-shift CG (the RHMC solver; not the step): all shifts kept active (tol = 0)
+    msh = None
+    if args.ms_shifts > 0:
+        sig = [0.0] + [0.002 * 4.0 ** i for i in range(args.ms_shifts - 1)]
+        fphi = q.qdp_field_alloc(ctx, q.QDP_FERMION, q.QDP_F64, q.QDP_ODD)
+        q.qdp_field_import(fphi, np.ascontiguousarray(b[fieldgen.parity(L) == 1]))
+        xs = [q.qdp_field_alloc(ctx, q.QDP_FERMION, q.QDP_F64, q.QDP_ODD) for _ in sig]
+        q.qdp_cg_solve_multishift(xs, sig, fphi, fU, fA, fAi, mass=MASS, tol=0.0, maxit=2, true_resid=False)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        q.qdp_profile_reset(ctx)
+        q.qdp_set_option(ctx, q.QDP_OPT_PROFILE, 1)
+        e6, e7 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e6.record(stream)
+        r = q.qdp_cg_solve_multishift(xs, sig, fphi, fU, fA, fAi, mass=MASS, tol=0.0, maxit=args.ms_iters,
+                                      true_resid=False)
+        e7.record(stream)
+        torch.cuda.synchronize()
+        n_u, ms_u = q.qdp_profile_query(ctx, q.QDP_PK_MSHIFT)
+        _, b_u = q.qdp_profile_work(ctx, q.QDP_PK_MSHIFT)
+        f_t, _ = q.qdp_profile_work(ctx, -1)
+        q.qdp_set_option(ctx, q.QDP_OPT_PROFILE, 0)
+        t_ms = qdist.max_over_ranks(e6.elapsed_time(e7))
+        msh = {"shifts": len(sig), "sigma": sig, "iters": r["iters"], "ms_per_iter": t_ms / r["iters"],
+               "gflops_per_gpu": f_t / (t_ms * 1e-3) * 1e-9,
+               "update_pass": {"us_per_launch": ms_u / n_u * 1e3, "bytes_per_site": b_u / n_u / Vh,
+                               "gbs": b_u / (ms_u * 1e-3) * 1e-9,
+                               "frac_of_measured_hbm": b_u / (ms_u * 1e-3) * 1e-9 / measured_peak()[0],
+                               "share_of_solve": ms_u / t_ms}}
+        for f in xs + [fphi]:
+            q.qdp_field_free(f)
+
     # ---- CPU baseline (oracle, rank 0 at N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -407,9 +443,11 @@ def run_native(args, rank, world, local_rank):
         "cpu_baseline": cpu,
         "parity": parity,
         "time_to_solution_1e-10": tts,
+        "multishift_cg": msh,
         "eo_dslash_plain": dsl,
         "overlap": not args.no_overlap,
-        "halo": "p2p" if args.p2p else "nccl",
+        "halo": ("peer (IPC ghost slots + flags, no NCCL)" if args.comm == "peer" else
+                 "p2p" if args.p2p else "nccl") if world > 1 else "none (one GPU, periodic wrap in-kernel)",
     }
     if rank == 0:
         print(json.dumps(out), flush=True)
@@ -439,7 +477,11 @@ def main():
     ap.add_argument("--ref-iters", type=int, default=1)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-overlap", action="store_true")
-    ap.add_argument("--p2p", action="store_true", help="peer-to-peer (CUDA IPC) halos instead of NCCL")
+    ap.add_argument("--p2p", action="store_true", help="with --comm nccl: peer-to-peer (CUDA IPC) halos")
+    ap.add_argument("--comm", choices=["peer", "nccl"], default="peer",
+                    help="N > 1: peer-memory communicator (qdp_init_peer, default) or NCCL")
+    ap.add_argument("--ms-shifts", type=int, default=12, help="multi-shift CG measurement: shifts (0: skip)")
+    ap.add_argument("--ms-iters", type=int, default=20)
     ap.add_argument("--recon", type=int, choices=[18, 12], default=18,
                     help="gauge storage of the solve: 18 (default, uncompressed as in PAPER.md:292) or 12")
     ap.add_argument("--no-tts", dest="tts", action="store_false", help="skip the time-to-solution comparison")

@@ -299,6 +299,7 @@ enum { QDP_PK_DSLASH = 0,  /* interior / whole-lattice dslash */
        QDP_PK_CLOVER,      /* clover apply / build */
        QDP_PK_SHIFT,       /* shift */
        QDP_PK_LAYOUT,      /* import / export / copy / zero */
+       QDP_PK_MSHIFT,      /* multi-shift CG: the update pass over all shifts */
        QDP_PK_COUNT };
 /* launches: kernels launched in this class since the last reset (always counted);
  * total_ms: sum of their CUDA-event durations (only while QDP_OPT_PROFILE = 1; resolving

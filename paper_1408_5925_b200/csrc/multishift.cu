@@ -208,7 +208,7 @@ int cg_solve_multishift(qdp_field *x, int n, const double *sigma, const qdp_fiel
     ms_coeff_kernel<<<1, 32, 0, ctx->stream>>>(st, ctx->red_result, n, k, tol2rho0, k == maxit ? 1 : 0);
     QDP_CUDA(ctx, cudaGetLastError());
     ProfEvent ev;
-    prof_begin(ctx, QDP_PK_BLAS, &ev);
+    prof_begin(ctx, QDP_PK_MSHIFT, &ev);
     if (prec == QDP_F64)
       ms_update_kernel<double><<<grid_for(g.Vh, 256), 256, 0, ctx->stream>>>(g, P, (const double2 *)r, st, n);
     else
@@ -218,7 +218,7 @@ int cg_solve_multishift(qdp_field *x, int n, const double *sigma, const qdp_fiel
     if ((rc = read_slots(ctx, S_RR, S_NP - S_RR + 1, s))) return rc;
     const double rho_new = s[0], nx = s[S_NX - S_RR], np = s[S_NP - S_RR];
     // algorithmic work of the update pass: r once, x_i read + write, p_i read (+ write)
-    prof_work(ctx, QDP_PK_BLAS, (48.0 * nx + 72.0 * np) * g.Vh, (24.0 + 72.0 * nx + 24.0 * np) * g.Vh * fb);
+    prof_work(ctx, QDP_PK_MSHIFT, (48.0 * nx + 72.0 * np) * g.Vh, (24.0 + 72.0 * nx + 24.0 * np) * g.Vh * fb);
     if (hist && k < hist_cap) hist[k] = sqrt(rho_new / rho0);
     if (rho_new <= tol2rho0) status = QDP_OK;
     QDP_CUDA(ctx, cudaMemcpyAsync(ctx->red_result + S_RHO, ctx->red_result + S_RR, sizeof(double),
