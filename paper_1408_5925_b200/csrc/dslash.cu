@@ -266,6 +266,16 @@ __global__ void __launch_bounds__(QDPB_DSLASH_MAXT, (dslash_minb<R, REC>())) dsl
     const int p = P.parity;
     int c[4];
     cb_coords(g, cb, p, c);
+    if constexpr (sizeof(R) == 4 && REC == 12 && QDPB_PF_F12) {
+      // the site's 8 links towards L2 before their first use, without holding registers
+#pragma unroll
+      for (int mu = 0; mu < 4; mu++) {
+        P.U.prefetch(mu, p, cb);
+        int n[4] = {c[0], c[1], c[2], c[3]};
+        n[mu] = (c[mu] == 0) ? g.L[mu] - 1 : c[mu] - 1;
+        P.U.prefetch(mu, 1 - p, coords_cb(g, n));
+      }
+    }
     Spinor<R> acc;
 #pragma unroll
     for (int k = 0; k < 12; k++) acc.c[k] = {R(0), R(0)};

@@ -47,6 +47,12 @@ template <typename R, int REC> constexpr int dslash_minb() {
 #ifndef QDPB_MAX_SHIFTS
 #define QDPB_MAX_SHIFTS 32  // qdp_cg_solve_multishift
 #endif
+// fp32 reconstruct-12 dslash: per-thread L2 prefetch of the site's 8 links at kernel entry
+// (measured 100.7 -> 97.0 us at 40^3x32; the same prefetch slows every fp64 variant, and
+// block-wide bulk prefetch or cp.async staging of the links did not pay either: DESIGN.md §6)
+#ifndef QDPB_PF_F12
+#define QDPB_PF_F12 1
+#endif
 #ifndef QDPB_DSLASH_BLOCK
 #define QDPB_DSLASH_BLOCK 64
 #endif
@@ -158,6 +164,8 @@ __device__ __forceinline__ float2 ld_stream(const float2 *p) {
   asm("ld.global.nc.L1::no_allocate.v2.f32 {%0,%1}, [%2];" : "=f"(r.x), "=f"(r.y) : "l"(p));
   return r;
 }
+// L2 prefetch of one element (no register, no dependency).
+__device__ __forceinline__ void prefetch_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 // Re-used loads (neighbour spinors: 8 readers per site) go through the normal path.
 __device__ __forceinline__ double2 ld_reuse(const double2 *p) { return __ldg(p); }
 __device__ __forceinline__ float4 ld_reuse(const float4 *p) { return __ldg(p); }
@@ -337,6 +345,11 @@ template <> struct GaugeView<double, 12> {
 template <> struct GaugeView<float, 12> {
   const float4 *p;  // float4 [mu][parity][3][stride]
   int stride;
+  __device__ __forceinline__ void prefetch(int mu, int par, int cb) const {
+    const float4 *b = p + (size_t)(mu * 2 + par) * 3 * stride + cb;
+#pragma unroll
+    for (int k = 0; k < 3; k++) prefetch_l2(b + (size_t)k * stride);
+  }
   __device__ __forceinline__ Link<float> load(int mu, int par, int cb) const {
     const float4 *b = p + (size_t)(mu * 2 + par) * 3 * stride;
     Link<float> u;

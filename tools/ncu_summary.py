@@ -21,6 +21,11 @@ want = sys.argv[2:] or [
     "smsp__warp_issue_stalled_mio_throttle_per_warp_active.pct", "smsp__warp_issue_stalled_barrier_per_warp_active.pct",
     "smsp__warps_issue_stalled_drain_per_warp_active.pct",
 ]
+STALLS = ["long_scoreboard", "short_scoreboard", "wait", "math_pipe_throttle", "lg_throttle", "mio_throttle",
+          "barrier", "no_instruction", "not_selected", "selected", "dispatch_stall", "branch_resolving", "tex_throttle",
+          "drain", "membar", "sleeping", "misc"]
+if not sys.argv[2:]:
+    want += [f"smsp__average_warps_issue_stalled_{x}_per_issue_active.ratio" for x in STALLS]
 idx = {h: i for i, h in enumerate(hdr)}
 for d in data:
     print("----")
