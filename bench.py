@@ -187,9 +187,18 @@ def run_native(args, rank, world, local_rank):
     from paper_1408_5925_b200 import dist as qdist
     from paper_1408_5925_b200 import qdpb as q
 
-    torch.cuda.set_device(local_rank)
+    # QDPB_BENCH_ONE_GPU=1: every rank on cuda:0 (functional test of the N > 1 path on a one-GPU
+    # box; peer communicator only, torch.distributed over gloo -- the timings mean nothing)
+    one_gpu = os.environ.get("QDPB_BENCH_ONE_GPU") == "1"
+    dev = 0 if one_gpu else local_rank
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if one_gpu:
+            if args.comm != "peer":
+                raise SystemExit("QDPB_BENCH_ONE_GPU needs --comm peer (NCCL refuses two ranks on one GPU)")
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     # one explicit stream shared by the library (its context stream) and torch's timing events,
     # so the events are ordered with the kernels they bracket
     stream = torch.cuda.Stream()
@@ -236,7 +245,7 @@ def run_native(args, rank, world, local_rank):
     q.qdp_profile_reset(ctx)
     q.qdp_set_option(ctx, q.QDP_OPT_PROFILE, 1)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with Clocks(local_rank) as clk:
+    with Clocks(dev) as clk:
         e0.record(stream)
         for _ in range(args.steps):
             r = step()
@@ -356,6 +365,11 @@ def run_native(args, rank, world, local_rank):
                                                        delta=0.1, maxit=5000),
             "mixed_fp32_recon12": lambda: q.qdp_cg_solve_mixed(fx, fb, fU, fA, fAi, fU32r, fA32, fAi32, mass=MASS,
                                                                tol=1e-10, delta=0.1, maxit=5000),
+            # fewer reliable updates: each costs an fp64 Mhat^dag Mhat (4 fp64 dslash launches)
+            "mixed_fp32_recon12_delta1e-2": lambda: q.qdp_cg_solve_mixed(fx, fb, fU, fA, fAi, fU32r, fA32, fAi32,
+                                                                         mass=MASS, tol=1e-10, delta=1e-2, maxit=5000),
+            "mixed_fp32_recon12_delta1e-3": lambda: q.qdp_cg_solve_mixed(fx, fb, fU, fA, fAi, fU32r, fA32, fAi32,
+                                                                         mass=MASS, tol=1e-10, delta=1e-3, maxit=5000),
         }
         tts = {}
         for name, fn in solvers.items():

@@ -334,6 +334,47 @@ int reduce_global(qdp_ctx ctx, int slot, int n) {
   return comm_allreduce_f64(ctx, ctx->red_result + slot, n, ctx->stream);
 }
 
+__global__ void scalars_kernel(double *dst, const double *src, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+template <typename R>
+__global__ void __launch_bounds__(RB) copy_kernel(const Geom g, typename E<R>::T *d, const typename E<R>::T *s, int nblk) {
+  const size_t bs = (size_t)E<R>::NP * g.stride;
+  for (int cb = blockIdx.x * blockDim.x + threadIdx.x; cb < g.Vh; cb += gridDim.x * blockDim.x)
+    for (int b = 0; b < nblk; b++)
+#pragma unroll
+      for (int k = 0; k < E<R>::NP; k++) {
+        const size_t i = b * bs + (size_t)k * g.stride + cb;
+        d[i] = s[i];
+      }
+}
+
+int read_scalars(qdp_ctx ctx, int slot, int n, double *out) {
+  // host_pinned comes from cudaMallocHost: mapped, the same address on the device (UVA)
+  scalars_kernel<<<1, 64, 0, ctx->stream>>>(ctx->host_pinned, ctx->red_result + slot, n);
+  QDP_CUDA(ctx, cudaGetLastError());
+  QDP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  for (int i = 0; i < n; i++) out[i] = ((volatile double *)ctx->host_pinned)[i];
+  return QDP_OK;
+}
+
+int copy_scalars(qdp_ctx ctx, int dst, int src, int n) {
+  scalars_kernel<<<1, 64, 0, ctx->stream>>>(ctx->red_result + dst, ctx->red_result + src, n);
+  QDP_CUDA(ctx, cudaGetLastError());
+  return QDP_OK;
+}
+
+int copy_blocks(qdp_ctx ctx, int prec, void *dst, const void *src, int nblk) {
+  const Geom &g = ctx->geom;
+  ProfEvent ev;
+  prof_begin(ctx, QDP_PK_BLAS, &ev);
+  prof_work(ctx, QDP_PK_BLAS, 0.0, 48.0 * g.Vh * nblk * (prec == QDP_F64 ? 8 : 4));
+  const int nb = grid_for(g.Vh, RB);
+  if (prec == QDP_F64) copy_kernel<double><<<nb, RB, 0, ctx->stream>>>(g, (T_<double> *)dst, (const T_<double> *)src, nblk);
+  else copy_kernel<float><<<nb, RB, 0, ctx->stream>>>(g, (T_<float> *)dst, (const T_<float> *)src, nblk);
+  return prof_end(ctx, &ev);
+}
+
 int blas_axpy(qdp_ctx ctx, int prec, double ar, double ai, const void *x, void *y, int nblk) {
   const Geom &g = ctx->geom;
   ProfEvent ev;

@@ -597,9 +597,8 @@ extern "C" int qdp_dslash(qdp_field out, const qdp_field U, const qdp_field psi,
 }
 
 static int read_result(qdp_ctx c, int slot, int n, double *out) {
-  QDP_CUDA(c, cudaMemcpyAsync(c->host_pinned, c->red_result + slot, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  QDP_CUDA(c, cudaStreamSynchronize(c->stream));
-  memcpy(out, c->host_pinned, n * sizeof(double));
+  int rc = read_scalars(c, slot, n, out);
+  if (rc) return rc;
   return c->peer ? peer_check(c) : QDP_OK;
 }
 

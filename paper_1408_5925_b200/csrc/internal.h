@@ -596,6 +596,15 @@ int blas_convert(qdp_ctx ctx, void *dst, int dst_prec, const void *src);
 // y64 += x32 ; x32 = 0  (one parity block)
 int blas_accum_mixed(qdp_ctx ctx, void *y64, void *x32);
 int blas_scale_copy(qdp_ctx ctx, int prec, void *dst, const void *src, double a, int nblk);  // dst = a src
+// Copy-engine-free scalar traffic of the solvers: a copy engine busy with a caller's large
+// host<->device transfer would otherwise delay every per-iteration scalar readback (e2e).
+//   read_scalars: red_result[slot .. slot+n) -> out via a kernel store into the mapped pinned
+//                 host buffer, then a stream synchronisation (n <= 64)
+//   copy_scalars: red_result[dst .. dst+n) = red_result[src .. src+n) by a kernel
+//   copy_blocks:  nblk fermion parity blocks dst = src by a kernel
+int read_scalars(qdp_ctx ctx, int slot, int n, double *out);
+int copy_scalars(qdp_ctx ctx, int dst, int src, int n);
+int copy_blocks(qdp_ctx ctx, int prec, void *dst, const void *src, int nblk);
 
 // dslash.cu
 enum Epi { EPI_PLAIN = 0, EPI_XPAY = 1, EPI_CLOVINV = 2, EPI_CLOVXPAY = 3 };

@@ -139,14 +139,7 @@ __global__ void __launch_bounds__(256) ms_update_kernel(const Geom g, const MsPt
   }
 }
 
-int read_slots(qdp_ctx ctx, int slot, int n, double *v) {
-  cudaError_t e = cudaMemcpyAsync(ctx->host_pinned, ctx->red_result + slot, n * sizeof(double), cudaMemcpyDeviceToHost,
-                                  ctx->stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-  if (e != cudaSuccess) return cuda_check(ctx, e, "multishift: read scalars");
-  memcpy(v, ctx->host_pinned, n * sizeof(double));
-  return QDP_OK;
-}
+int read_slots(qdp_ctx ctx, int slot, int n, double *v) { return read_scalars(ctx, slot, n, v); }
 }  // namespace
 
 // Mhat_op: the even-odd operator pieces of solver.cu
@@ -188,9 +181,9 @@ int cg_solve_multishift(qdp_field *x, int n, const double *sigma, const qdp_fiel
   // x_i = 0 ; r = p_i = phi_o ; rho0 = |r|^2
   for (int i = 0; i < n; i++) {
     QDP_CUDA(ctx, cudaMemsetAsync(P.x[i], 0, blk, ctx->stream));
-    QDP_CUDA(ctx, cudaMemcpyAsync(P.p[i], phi_o, blk, cudaMemcpyDeviceToDevice, ctx->stream));
+    if ((rc = copy_blocks(ctx, prec, P.p[i], phi_o, 1))) return rc;
   }
-  QDP_CUDA(ctx, cudaMemcpyAsync(r, phi_o, blk, cudaMemcpyDeviceToDevice, ctx->stream));
+  if ((rc = copy_blocks(ctx, prec, r, phi_o, 1))) return rc;
   double rho0 = 0.0;
   if ((rc = blas_norm2(ctx, prec, r, 1, S_RHO)) || (rc = reduce_global(ctx, S_RHO, 1)) ||
       (rc = read_slots(ctx, S_RHO, 1, &rho0)))
@@ -221,8 +214,7 @@ int cg_solve_multishift(qdp_field *x, int n, const double *sigma, const qdp_fiel
     prof_work(ctx, QDP_PK_MSHIFT, (48.0 * nx + 72.0 * np) * g.Vh, (24.0 + 72.0 * nx + 24.0 * np) * g.Vh * fb);
     if (hist && k < hist_cap) hist[k] = sqrt(rho_new / rho0);
     if (rho_new <= tol2rho0) status = QDP_OK;
-    QDP_CUDA(ctx, cudaMemcpyAsync(ctx->red_result + S_RHO, ctx->red_result + S_RR, sizeof(double),
-                                  cudaMemcpyDeviceToDevice, ctx->stream));
+    if ((rc = copy_scalars(ctx, S_RHO, S_RR, 1))) return rc;
   }
   if (iters_out) *iters_out = k;
   QDP_CUDA(ctx, cudaMemcpyAsync(&h, st, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));

@@ -98,20 +98,8 @@ int apply_mhat(const Op &op, void *out, const void *v, bool dag, const void *dot
   return dslash(op.ctx, op.prec, c);
 }
 
-int read_slot(qdp_ctx ctx, int slot, double *v) {
-  cudaError_t e = cudaMemcpyAsync(ctx->host_pinned, ctx->red_result + slot, sizeof(double), cudaMemcpyDeviceToHost,
-                                  ctx->stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-  if (e != cudaSuccess) return cuda_check(ctx, e, "cg: read scalar");
-  *v = ctx->host_pinned[0];
-  return QDP_OK;
-}
-
-int copy_slot(qdp_ctx ctx, int dst, int src) {
-  QDP_CUDA(ctx, cudaMemcpyAsync(ctx->red_result + dst, ctx->red_result + src, sizeof(double), cudaMemcpyDeviceToDevice,
-                                ctx->stream));
-  return QDP_OK;
-}
+int read_slot(qdp_ctx ctx, int slot, double *v) { return read_scalars(ctx, slot, 1, v); }
+int copy_slot(qdp_ctx ctx, int dst, int src) { return copy_scalars(ctx, dst, src, 1); }
 
 // bhat_o = b_o + 1/2 H_oe A_ee^-1 b_e
 int prepare_source(const Op &op, void *bh, const char *b_e, const char *b_o) {
@@ -219,7 +207,7 @@ int cg_solve(qdp_field x, const qdp_field b, const qdp_field U, const qdp_field 
   // x_o = 0 ; r = Mhat^dag bhat ; p = r ; rho0 = |r|^2
   QDP_CUDA(ctx, cudaMemsetAsync(x_o, 0, blk, ctx->stream));
   if ((rc = apply_mhat(op, r, bh, true))) return rc;
-  QDP_CUDA(ctx, cudaMemcpyAsync(p, r, blk, cudaMemcpyDeviceToDevice, ctx->stream));
+  if ((rc = copy_blocks(ctx, prec, p, r, 1))) return rc;
   if ((rc = blas_norm2(ctx, prec, r, 1, S_RHO)) || (rc = reduce_global(ctx, S_RHO, 1)) || (rc = read_slot(ctx, S_RHO, &rho0)))
     return rc;
   if (hist_cap > 0 && hist) hist[0] = 1.0;
@@ -276,12 +264,12 @@ int cg_solve_mixed(qdp_field x, const qdp_field b, const qdp_field U, const qdp_
   if ((rc = apply_mhat(op, c, bh, true))) return rc;
   QDP_CUDA(ctx, cudaMemsetAsync(x_o, 0, b64, ctx->stream));
   QDP_CUDA(ctx, cudaMemsetAsync(xs, 0, b32, ctx->stream));
-  QDP_CUDA(ctx, cudaMemcpyAsync(r, c, b64, cudaMemcpyDeviceToDevice, ctx->stream));
+  if ((rc = copy_blocks(ctx, QDP_F64, r, c, 1))) return rc;
   if ((rc = blas_norm2(ctx, QDP_F64, r, 1, S_RHO)) || (rc = reduce_global(ctx, S_RHO, 1)) ||
       (rc = read_slot(ctx, S_RHO, &rho0)))
     return rc;
   if ((rc = blas_convert(ctx, rs, QDP_F32, r))) return rc;
-  QDP_CUDA(ctx, cudaMemcpyAsync(ps, rs, b32, cudaMemcpyDeviceToDevice, ctx->stream));
+  if ((rc = copy_blocks(ctx, QDP_F32, ps, rs, 1))) return rc;
   if (hist_cap > 0 && hist) hist[0] = 1.0;
   if (rho0 == 0.0) status = QDP_OK;
   double maxr = sqrt(rho0);
@@ -304,7 +292,7 @@ int cg_solve_mixed(qdp_field x, const qdp_field b, const qdp_field U, const qdp_
     if ((rc = blas_cg_update_xp(ctx, QDP_F32, xs, ps, rs, S_RHO, S_PQ, S_RR, false))) return rc;
     if ((rc = blas_accum_mixed(ctx, x_o, xs))) return rc;
     if ((rc = apply_mhat(op, mp, x_o, false)) || (rc = apply_mhat(op, q, mp, true))) return rc;
-    QDP_CUDA(ctx, cudaMemcpyAsync(r, c, b64, cudaMemcpyDeviceToDevice, ctx->stream));
+    if ((rc = copy_blocks(ctx, QDP_F64, r, c, 1))) return rc;
     if ((rc = blas_axpy(ctx, QDP_F64, -1.0, 0.0, q, r, 1))) return rc;
     double rt;
     if ((rc = blas_norm2(ctx, QDP_F64, r, 1, S_TRUE)) || (rc = reduce_global(ctx, S_TRUE, 1)) ||

@@ -160,3 +160,59 @@ def _reductions(rank, world):
 
 def test_rank_reductions():
     _run("_reductions")
+
+
+def _allgather_bytes(rank, world):
+    # the set-up callback of qdp_init_peer: equal-sized blocks, concatenated in rank order
+    blob = bytes([rank]) * 64 + rank.to_bytes(4, "little") * 16
+    out = qd.torch_allgather_bytes(blob)
+    assert len(out) == world * len(blob)
+    for r in range(world):
+        assert out[r * len(blob):(r + 1) * len(blob)] == bytes([r]) * 64 + r.to_bytes(4, "little") * 16
+
+
+def test_peer_bootstrap_allgather():
+    _run("_allgather_bytes", world=3)
+
+
+def test_peer_ctypes_callback_marshalling():
+    """qdp_init_peer's ctypes trampoline: the C side's (send, recv, bytes) buffers round-trip
+    through the Python allgather (called here directly, no GPU needed)."""
+    import ctypes
+
+    from paper_1408_5925_b200 import qdpb as q
+    calls = []
+
+    def fake_allgather(blob):
+        calls.append(blob)
+        return blob + bytes(reversed(blob))
+
+    captured = {}
+
+    def fake_init(gd, pg, rank, nranks, fn, user, stream, out):
+        send = (ctypes.c_ubyte * 8)(*range(8))
+        recv = (ctypes.c_ubyte * 16)()
+        captured["rc"] = fn(ctypes.addressof(send), ctypes.addressof(recv), 8, None)
+        captured["recv"] = bytes(recv)
+        return -1  # pretend the device part failed afterwards
+
+    class FakeLib:
+        qdp_init_peer = staticmethod(fake_init)
+
+        @staticmethod
+        def qdp_strerror(st):
+            return b"fake"
+
+        @staticmethod
+        def qdp_last_error(c):
+            return b""
+
+    real = q._lib
+    q._lib = FakeLib()
+    try:
+        with pytest.raises(q.QdpError):
+            q.qdp_init_peer((4, 4, 4, 8), (1, 1, 1, 2), 0, 2, fake_allgather)
+    finally:
+        q._lib = real
+    assert captured["rc"] == 0 and calls == [bytes(range(8))]
+    assert captured["recv"] == bytes(range(8)) + bytes(reversed(range(8)))

@@ -119,3 +119,24 @@ def test_multishift_argument_errors(q):
             assert e.value.status == st
     finally:
         q.qdp_finalize(c)
+
+
+def test_multishift_zero_source_and_positive_base(q):
+    """phi = 0: converged at iteration 0 with x_i = 0; a positive base shift (sigma_0 > 0)."""
+    L = (4, 4, 4, 4)
+    c = q.qdp_init(L)
+    try:
+        fU = q.qdp_field_alloc(c, q.QDP_GAUGE, 0, q.QDP_ALL)
+        q.qdp_field_import(fU, fieldgen.random_gauge(L, 1902))
+        fphi = q.qdp_field_alloc(c, q.QDP_FERMION, 0, q.QDP_ODD)
+        q.qdp_field_zero(fphi)
+        xs = [q.qdp_field_alloc(c, q.QDP_FERMION, 0, q.QDP_ODD) for _ in range(2)]
+        res = q.qdp_cg_solve_multishift(xs, [0.0, 1.0], fphi, fU)
+        assert res["status"] == q.QDP_OK and res["iters"] == 0
+        assert all(np.max(np.abs(q.qdp_field_export(x))) == 0.0 for x in xs)
+    finally:
+        q.qdp_finalize(c)
+    res, got, ref = _run(q, L, True, sigma=[0.3, 0.7, 5.0])
+    assert res["iters"] == ref["iters"] and np.array_equal(res["conv_iter"], ref["conv_iter"])
+    for i in range(3):
+        assert rel_site_err(_odd(got[i], L), _odd(ref["x"][i], L)) <= 1e-9
