@@ -285,6 +285,52 @@ int qdp_expr(int expr, qdp_field out, const qdp_field a, const qdp_field b, cons
  * whether its search has finished (1) */
 int qdp_expr_block(qdp_ctx ctx, int expr, int prec, int *block, int *tuned);
 
+/* ---- run-time generated site expressions (PAPER.md sections III-IV, 148-206; Figs. 1-3) ------
+ * The paper's data-parallel expression evaluation: an expression over lattice fields becomes
+ * ONE kernel, one thread per site, generated at run time from the expression's
+ * tree, compiled (here by NVRTC to an sm_100a cubin), cached per context and
+ * launched with the paper's block-size autotuner (as qdp_expr).
+ *
+ * Grammar (whitespace free-form):
+ *   e := e + e | e - e | e * e | -e | (e) | number | $k | $k[mu]
+ *      | adj(e) | timesI(e) | gamma(mu) | gamma5 | shift(e, mu, s)
+ *   $k       operands[k]: QDP_FERMION -> spinor, QDP_COLORMATRIX -> colour matrix,
+ *            QDP_SPINMATRIX -> spin matrix; QDP_GAUGE / QDP_GAUGE12 only as $k[mu] = U_mu
+ *   adj      hermitian conjugate of a colour or spin matrix; timesI: i * e
+ *   gamma    gamma_mu in the DeGrand-Rossi basis (reading R1), gamma5 = diag(1,1,-1,-1);
+ *            only as a left factor of a spinor or spin matrix
+ *   shift    e(x + s mu^), s = +1 (FORWARD) / -1 (BACKWARD) (reading R4),
+ *            evaluated at the neighbouring site inside the same kernel (no temporary; shifts of
+ *            shifts reach diagonal neighbours); periodic on the local lattice
+ *   products: colour x colour, colour x spinor, spin x spin, spin x spinor, real x any
+ * Identical subexpressions at the same site are computed once.  Example, Fig. 1:
+ *   "$0[0]*shift($1,0,+1) + shift(adj($0[0])*$1,0,-1)"  with $0 a gauge field, $1 a fermion.
+ *
+ * qdp_jit_eval: out = expr(operands) on every site of out's subset.  All operands have out's
+ * precision (QDP_EPREC); a one-parity operand must hold the parity it is read at (out's parity,
+ * flipped by each odd shift displacement) and gauge operands must be QDP_ALL (QDP_EINVAL);
+ * out must not alias an operand (QDP_EALIAS).  Parse and type errors: QDP_EINVAL with the
+ * reason in qdp_last_error.  A shift along a dimension reached through the halo path (P_mu > 1
+ * or self-halo) returns QDP_EUNSUPPORTED: use qdp_shift, which exchanges the faces.  The first
+ * call for an (expression, operand kinds, precision) compiles (~0.1-0.5 s); NVRTC missing:
+ * QDP_EUNSUPPORTED.  Work counters (qdp_profile_work, class QDP_PK_BLAS): flops by the Table II
+ * convention for the operations executed, compulsory bytes (each distinct field once + store).
+ *
+ * qdp_jit_source: the same front end without a context or GPU: writes the generated CUDA
+ * source (NUL-terminated, truncated to src_cap; *src_len = bytes needed; on an error the reason
+ * is written there instead) and the work per output site of an output of subset out_subset:
+ * work[0] flops, work[1] compulsory bytes (each distinct field -- for a one-parity output each
+ * distinct parity block of a field -- read once, plus the store), work[2] bytes by Table II's
+ * convention (every leaf occurrence + the store).  compile = 1 also runs NVRTC
+ * (no GPU needed).
+ * qdp_jit_stats: kernels compiled on this context and the seconds spent generating, compiling
+ * and loading them (the paper's JIT overhead). */
+#define QDP_JIT_MAX_OPERANDS 8
+int qdp_jit_eval(qdp_field out, const char *expr, const qdp_field *operands, int n_operands);
+int qdp_jit_source(const char *expr, int out_kind, int out_subset, int prec, const int *operand_kinds,
+                   int n_operands, char *src, size_t src_cap, size_t *src_len, double work[3], int compile);
+int qdp_jit_stats(qdp_ctx ctx, int *kernels, double *seconds);
+
 /* ---- diagnostics ---------------------------------------------------------------------- */
 
 const char *qdp_strerror(int status);

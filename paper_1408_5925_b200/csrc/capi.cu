@@ -290,6 +290,7 @@ extern "C" int qdp_finalize(qdp_ctx c) {
   if (!c) return QDP_EINVAL;
   if (c->stream) cudaStreamSynchronize(c->stream);
   resolve_profile(c);
+  jit_release(c);
   tune_release(c);
   p2p_destroy(c);
   peer_destroy(c);
@@ -789,6 +790,42 @@ extern "C" int qdp_expr(int expr, qdp_field out, const qdp_field a, const qdp_fi
     if (k && f[k]->data == out->data) return set_error(ctx, QDP_EALIAS, "expr: out aliases operand %d", k);
   }
   return expr_eval(ctx, expr, out, a, b, c);
+}
+
+extern "C" int qdp_jit_eval(qdp_field out, const char *expr, const qdp_field *operands, int n_operands) {
+  if (!out || !expr || n_operands < 0 || n_operands > QDP_JIT_MAX_OPERANDS || (n_operands && !operands))
+    return QDP_EINVAL;
+  qdp_ctx ctx = out->ctx;
+  int rc;
+  for (int k = 0; k < n_operands; k++) {
+    if (!operands[k]) return set_error(ctx, QDP_EINVAL, "jit: operand %d is NULL", k);
+    if ((rc = check_pair(out, operands[k]))) return rc;
+    if (operands[k]->data == out->data) return set_error(ctx, QDP_EALIAS, "jit: out aliases operand %d", k);
+  }
+  return jit_eval(out, expr, operands, n_operands);
+}
+
+extern "C" int qdp_jit_source(const char *expr, int out_kind, int out_subset, int prec, const int *operand_kinds,
+                              int n_operands, char *src, size_t src_cap, size_t *src_len, double work[3], int compile) {
+  if (!expr || n_operands < 0 || n_operands > QDP_JIT_MAX_OPERANDS || (n_operands && !operand_kinds)) return QDP_EINVAL;
+  std::string err;
+  const int rc =
+      jit_source(expr, out_kind, out_subset, prec, operand_kinds, n_operands, src, src_cap, src_len, work, compile, err);
+  if (rc < 0) {  // the reason goes where the source would have
+    if (src_len) *src_len = err.size() + 1;
+    if (src && src_cap) {
+      strncpy(src, err.c_str(), src_cap - 1);
+      src[src_cap - 1] = '\0';
+    }
+  }
+  return rc;
+}
+
+extern "C" int qdp_jit_stats(qdp_ctx ctx, int *kernels, double *seconds) {
+  if (!ctx) return QDP_EINVAL;
+  if (kernels) *kernels = ctx->jit_compiled;
+  if (seconds) *seconds = ctx->jit_seconds;
+  return QDP_OK;
 }
 
 extern "C" int qdp_expr_block(qdp_ctx c, int expr, int prec, int *block, int *tuned) {

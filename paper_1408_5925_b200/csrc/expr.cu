@@ -7,6 +7,8 @@
 //   matvec psi0 = U1 psi1 + U1 psi2  552 flop, 864 B by the paper's count (U1 "loaded twice"), 720 compulsory
 //   clover psi0 = A * psi1         504 flop, 960 B
 // Flops and bytes follow Table II's convention (cmul 6, cadd 2; every leaf + the store).
+#include <functional>
+
 #include "internal.h"
 
 namespace qdpb {
@@ -230,7 +232,51 @@ void tune_release(qdp_ctx ctx) {
 // start at the largest block (1024), halve while the launch fails; once a launch
 // succeeded, every further payload launch probes the next smaller block until its time exceeds
 // the best seen by more than 33%; then the best block is used for good.  Only payload launches.
-// (A launch "fails" when the block exceeds the kernel's maxThreadsPerBlock -- checked up front.)
+// (A launch "fails" when the block exceeds the kernel's maxThreadsPerBlock -- checked up front
+// by `go`, which returns cudaErrorLaunchOutOfResources without launching.)
+int tuned_launch(qdp_ctx ctx, long key, const std::function<cudaError_t(int)> &go) {
+  if (!ctx->autotune) {
+    cudaError_t err = go(128);
+    return err != cudaSuccess ? cuda_check(ctx, err, "tuned launch") : QDP_OK;
+  }
+  Tune &t = ctx->tune[key];
+  if (!t.a) {
+    cudaEventCreate(&t.a);
+    cudaEventCreate(&t.b);
+  }
+  if (t.pending) {  // time of the previous payload launch at t.block
+    float ms = 0.f;
+    QDP_CUDA(ctx, cudaEventSynchronize(t.b));
+    QDP_CUDA(ctx, cudaEventElapsedTime(&ms, t.a, t.b));
+    t.pending = false;
+    if (t.best_block == 0 || ms < t.best_ms) {
+      t.best_ms = ms;
+      t.best_block = t.block;
+    }
+    if (ms > 1.33f * t.best_ms || t.block <= 32) {
+      t.state = 2;
+      t.block = t.best_block;
+    } else {
+      t.block /= 2;
+    }
+  }
+  cudaError_t err = cudaSuccess;
+  if (t.state != 2) QDP_CUDA(ctx, cudaEventRecord(t.a, ctx->stream));
+  for (;;) {
+    err = go(t.block);
+    if (err == cudaSuccess || t.state != 0 || t.block <= 32) break;
+    t.block /= 2;  // launch failed (too many resources at this block size): halve and retry
+  }
+  if (err != cudaSuccess) return cuda_check(ctx, err, "tuned launch");
+  if (t.state != 2) {
+    QDP_CUDA(ctx, cudaEventRecord(t.b, ctx->stream));
+    t.pending = true;
+    t.state = 1;
+  }
+  return QDP_OK;
+}
+
+// One Table II expression: the paper's autotuner on its payload launches.
 int expr_eval(qdp_ctx ctx, int expr, qdp_field out, const qdp_field a, const qdp_field b, const qdp_field c) {
   const Geom &g = ctx->geom;
   const int prec = out->prec;
@@ -266,47 +312,10 @@ int expr_eval(qdp_ctx ctx, int expr, qdp_field out, const qdp_field a, const qdp
   ProfEvent ev;
   prof_begin(ctx, QDP_PK_BLAS, &ev);
   prof_work(ctx, QDP_PK_BLAS, flops * sites, reals * sites * (prec == QDP_F64 ? 8 : 4));
-  if (!ctx->autotune) {
-    cudaError_t err = go(128);
-    int rc = prof_end(ctx, &ev);
-    return err != cudaSuccess ? cuda_check(ctx, err, "expr launch") : rc;
-  }
-  Tune &t = ctx->tune[tune_key(expr, prec, sites)];
-  if (!t.a) {
-    cudaEventCreate(&t.a);
-    cudaEventCreate(&t.b);
-  }
-  if (t.pending) {  // time of the previous payload launch at t.block
-    float ms = 0.f;
-    QDP_CUDA(ctx, cudaEventSynchronize(t.b));
-    QDP_CUDA(ctx, cudaEventElapsedTime(&ms, t.a, t.b));
-    t.pending = false;
-    if (t.best_block == 0 || ms < t.best_ms) {
-      t.best_ms = ms;
-      t.best_block = t.block;
-    }
-    if (ms > 1.33f * t.best_ms || t.block <= 32) {
-      t.state = 2;
-      t.block = t.best_block;
-    } else {
-      t.block /= 2;
-    }
-  }
-  cudaError_t err = cudaSuccess;
-  if (t.state != 2) QDP_CUDA(ctx, cudaEventRecord(t.a, ctx->stream));
-  for (;;) {
-    err = go(t.block);
-    if (err == cudaSuccess || t.state != 0 || t.block <= 32) break;
-    t.block /= 2;  // launch failed (too many resources at this block size): halve and retry
-  }
-  if (err != cudaSuccess) {
+  const int rc = tuned_launch(ctx, tune_key(expr, prec, sites), go);
+  if (rc) {
     prof_end(ctx, &ev);
-    return cuda_check(ctx, err, "expr launch");
-  }
-  if (t.state != 2) {
-    QDP_CUDA(ctx, cudaEventRecord(t.b, ctx->stream));
-    t.pending = true;
-    t.state = 1;
+    return rc;
   }
   return prof_end(ctx, &ev);
 }

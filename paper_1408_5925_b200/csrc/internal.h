@@ -14,6 +14,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <functional>
 #include <map>
 #include <string>
 #include <vector>
@@ -474,6 +475,7 @@ struct Tune {
   bool pending = false;    // an event pair of the last payload launch awaits reading
   cudaEvent_t a = nullptr, b = nullptr;
 };
+struct JitKernel;  // jit.cu
 inline bool is_gauge(int kind) { return kind == KIND_GAUGE || kind == KIND_GAUGE12; }
 
 size_t parity_block_bytes(int kind, int prec, int stride);  // bytes of one parity block
@@ -538,6 +540,10 @@ struct qdp_ctx_s {
   std::vector<qdpb::ProfEvent> pending;
   int autotune = 1;
   std::map<long, qdpb::Tune> tune;
+  // run-time generated site-expression kernels (jit.cu), keyed by expression + kinds + precision
+  std::map<std::string, qdpb::JitKernel *> jit;
+  int jit_compiled = 0;
+  double jit_seconds = 0.0;
   std::vector<cudaEvent_t> event_pool;
   std::string last_error;
 };
@@ -653,6 +659,15 @@ void p2p_destroy(qdp_ctx ctx);
 // expr.cu (Table II site expressions)
 int expr_eval(qdp_ctx ctx, int expr, qdp_field out, const qdp_field a, const qdp_field b, const qdp_field c);
 void tune_release(qdp_ctx ctx);
+// the paper's block-size autotuner around go(block), per key (expr.cu)
+int tuned_launch(qdp_ctx ctx, long key, const std::function<cudaError_t(int)> &go);
+
+// jit.cu: run-time generated site-expression kernels (qdp_jit_eval)
+struct JitKernel;
+void jit_release(qdp_ctx ctx);
+int jit_eval(qdp_field out, const char *expr, const qdp_field *ops, int nops);
+int jit_source(const char *expr, int out_kind, int out_subset, int prec, const int *kinds, int nops, char *src,
+               size_t cap, size_t *src_len, double work[3], int compile, std::string &err);
 
 // shift.cu
 int shift_field(qdp_ctx ctx, qdp_field out, const qdp_field in, int mu, int sign);

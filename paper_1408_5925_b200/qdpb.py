@@ -74,6 +74,10 @@ _SIGS = {
                                 ctypes.c_double, ctypes.c_int, _ip, _ip, _dp, ctypes.c_int, _dp],
     "qdp_expr": [ctypes.c_int, _vp, _vp, _vp, _vp],
     "qdp_expr_block": [_vp, ctypes.c_int, ctypes.c_int, _ip, _ip],
+    "qdp_jit_eval": [_vp, ctypes.c_char_p, ctypes.POINTER(_vp), ctypes.c_int],
+    "qdp_jit_source": [ctypes.c_char_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, _ip, ctypes.c_int, ctypes.c_char_p,
+                       ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t), _dp, ctypes.c_int],
+    "qdp_jit_stats": [_vp, _ip, _dp],
     "qdp_strerror": [ctypes.c_int],
     "qdp_last_error": [_vp],
     "qdp_profile_query": [_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_long), _dp],
@@ -415,6 +419,37 @@ def qdp_expr_block(ctx: Ctx, expr: int, prec: int):
     b, t = ctypes.c_int(), ctypes.c_int()
     _check(lib().qdp_expr_block(ctx, int(expr), int(prec), ctypes.byref(b), ctypes.byref(t)), ctx)
     return b.value, bool(t.value)
+
+
+# ------------------------------------------------------------------ run-time generated expressions
+def qdp_jit_eval(out: Field, expr: str, *operands: Field) -> None:
+    """out = expr($0, $1, ...) on out's subset: one generated kernel (include/qdpb.h, PAPER.md III-IV)."""
+    arr = (_vp * max(1, len(operands)))(*[f.ptr for f in operands])
+    _check(lib().qdp_jit_eval(out, expr.encode(), arr, len(operands)), out.ctx)
+
+
+def qdp_jit_source(expr: str, out_kind: int, prec: int, operand_kinds, compile: bool = False, out_subset: int = -1):
+    """(generated CUDA source, {flops, bytes, table2_bytes} per site) -- no context or GPU needed."""
+    kinds = (ctypes.c_int * max(1, len(operand_kinds)))(*[int(k) for k in operand_kinds])
+    need = ctypes.c_size_t()
+    work = (ctypes.c_double * 3)()
+    L = lib()
+    for attempt in range(2):
+        buf = ctypes.create_string_buffer(max(1, need.value))
+        st = L.qdp_jit_source(expr.encode(), int(out_kind), int(out_subset), int(prec), kinds, len(operand_kinds), buf, len(buf),
+                              ctypes.byref(need), work, 1 if (compile and attempt) else 0)
+        if st < 0:  # the reason is in buf (once it is large enough)
+            if need.value > len(buf):
+                continue
+            raise QdpError(st, L.qdp_strerror(st).decode() + f": {buf.value.decode()} in {expr!r}")
+    return buf.value.decode(), dict(flops=work[0], bytes=work[1], table2_bytes=work[2])
+
+
+def qdp_jit_stats(ctx: Ctx):
+    """(kernels compiled on ctx, seconds spent generating + compiling + loading them)."""
+    n, s = ctypes.c_int(), ctypes.c_double()
+    _check(lib().qdp_jit_stats(ctx, ctypes.byref(n), ctypes.byref(s)), ctx)
+    return n.value, s.value
 
 
 # ------------------------------------------------------------------ diagnostics
