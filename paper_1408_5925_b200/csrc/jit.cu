@@ -324,7 +324,10 @@ struct Gen {
       const int parity_flip = (std::abs(d[0]) + std::abs(d[1]) + std::abs(d[2]) + std::abs(d[3])) & 1;
       body << "  int cb" << v << ";\n  {\n    int n[4] = {c[0], c[1], c[2], c[3]};\n";
       for (int m = 0; m < 4; m++)
-        if (d[m]) body << "    n[" << m << "] = wrap(n[" << m << "] + (" << d[m] << "), a.L[" << m << "]);\n";
+        if (d[m] == 1 || d[m] == -1)  // every extent is even and >= 2 (reading R6): one compare
+          body << "    n[" << m << "] = " << (d[m] > 0 ? "wrap_up" : "wrap_down") << "(n[" << m << "], a.L[" << m << "]);\n";
+        else if (d[m])
+          body << "    n[" << m << "] = wrap(n[" << m << "] + (" << d[m] << "), a.L[" << m << "]);\n";
       body << "    cb" << v << " = (n[0] >> 1) + a.Lh0 * (n[1] + a.L[1] * (n[2] + a.L[2] * n[3]));\n  }\n";
       body << "  const int p" << v << " = p ^ " << parity_flip << ";\n";
     }
@@ -361,6 +364,34 @@ struct Gen {
     for (auto &k : n->kid) count_leaves(k.get());
   }
 
+  // cache policy: a field block (operand, mu, parity flip) read at two or more displacements is
+  // reused by neighbouring threads; every other leaf is streamed
+  std::map<std::vector<int>, std::set<std::string>> disp;
+  std::set<std::vector<int>> reuse;
+  static int flip(const int d[4]) { return (std::abs(d[0]) + std::abs(d[1]) + std::abs(d[2]) + std::abs(d[3])) & 1; }
+  void collect(const Node *n, const int d[4]) {
+    if (n->op == N_SHIFT) {
+      int e[4] = {d[0], d[1], d[2], d[3]};
+      e[n->mu] += n->sign;
+      collect(n->kid[0].get(), e);
+      return;
+    }
+    if (n->op == N_LEAF) {
+      auto &ds = disp[{n->leaf, n->mu, flip(d)}];
+      ds.insert(dkey(d));
+      if (ds.size() > 1) reuse.insert({n->leaf, n->mu, flip(d)});
+    }
+    for (auto &k : n->kid) collect(k.get(), d);
+  }
+
+  // n = A - gamma(mu)*A or A + gamma(mu)*A with A a spinor (same text at the same site)
+  static bool is_projector(const Node *n, const int d[4]) {
+    if ((n->op != N_ADD && n->op != N_SUB) || n->type != T_SP) return false;
+    const Node *g = n->kid[1].get();
+    if (g->op != N_MUL || g->kid[0]->op != N_GAMMA || g->kid[0]->mu > 3) return false;
+    return key(n->kid[0].get(), d) == key(g->kid[1].get(), d);
+  }
+
   // emit n at displacement d; returns the C++ expression naming its value
   std::string emit(const Node *n, const int d[4]) {
     if (n->op == N_NUM) {
@@ -386,7 +417,32 @@ struct Gen {
       v = fresh();
       const std::string base = "base(a, " + std::to_string(n->leaf) + ", p" + s + ", " + std::to_string(n->mu) + ")";
       const char *ld = kind == QDP_FERMION ? "ld_sp" : kind == QDP_SPINMATRIX ? "ld_sm" : kind == QDP_GAUGE12 ? "ld_g12" : "ld_cm";
-      body << "  const " << ctype(n->type) << " " << v << " = " << ld << "(" << base << ", a.stride, cb" << s << ");\n";
+      const bool stream = reuse.count({n->leaf, n->mu, flip(d)}) == 0;
+      body << "  const " << ctype(n->type) << " " << v << " = " << ld << (stream ? "<true>(" : "<false>(") << base
+           << ", a.stride, cb" << s << ");\n";
+    } else if (is_projector(n, d)) {
+      // A -/+ gamma(mu)*A = (1 -/+ gamma_mu) A: spin projection.  When A is (after
+      // shifts) a colour matrix times a spinor, the projector commutes with the colour product, so
+      // it is applied first and U multiplies a half spinor: 12 + 132 flop instead of 264 + 24.
+      const int mu = n->kid[1]->kid[0]->mu, S = n->op == N_ADD ? 1 : -1;
+      const Node *x = n->kid[0].get();
+      int e[4] = {d[0], d[1], d[2], d[3]};
+      while (x->op == N_SHIFT) {
+        e[x->mu] += x->sign;
+        shift_dims.insert(x->mu);
+        x = x->kid[0].get();
+      }
+      const std::string tmpl = "<" + std::to_string(mu) + ", " + std::to_string(S) + ">";
+      v = fresh();
+      if (x->op == N_MUL && x->kid[0]->type == T_CM && x->kid[1]->type == T_SP) {
+        const std::string u = emit(x->kid[0].get(), e), sp = emit(x->kid[1].get(), e);
+        body << "  const SP " << v << " = recon" << tmpl << "(mul(" << u << ", proj" << tmpl << "(" << sp << ")));\n";
+        flops += 12 + 2 * (9 * 6 + 6 * 2);
+      } else {
+        const std::string a = emit(n->kid[0].get(), d);
+        body << "  const SP " << v << " = recon" << tmpl << "(proj" << tmpl << "(" << a << "));\n";
+        flops += 12;
+      }
     } else if (n->op == N_MUL && n->kid[0]->op == N_GAMMA) {
       const std::string x = emit(n->kid[1].get(), d);
       v = fresh();
@@ -555,7 +611,49 @@ template <int MU> __device__ __forceinline__ SM gam(const SM &x) {
   }
   return r;
 }
+// half spinor: rows 0, 1 of (1 + S gamma_mu) psi (S = +1 / -1); rows 2, 3 follow from them
+// (DeGrand-Rossi, SURVEY Appendix A): index 3 * h + colour
+struct HS { cx c[6]; };
+template <int MU, int S> __device__ __forceinline__ HS proj(const SP &p) {
+  HS h;
+#pragma unroll
+  for (int c = 0; c < 3; c++) {
+    const cx p0 = p.c[c], p1 = p.c[3 + c], p2 = p.c[6 + c], p3 = p.c[9 + c];
+    if (MU == 0) { h.c[c] = S > 0 ? p0 + ti(p3) : p0 - ti(p3); h.c[3 + c] = S > 0 ? p1 + ti(p2) : p1 - ti(p2); }
+    else if (MU == 1) { h.c[c] = S > 0 ? p0 - p3 : p0 + p3; h.c[3 + c] = S > 0 ? p1 + p2 : p1 - p2; }
+    else if (MU == 2) { h.c[c] = S > 0 ? p0 + ti(p2) : p0 - ti(p2); h.c[3 + c] = S > 0 ? p1 - ti(p3) : p1 + ti(p3); }
+    else { h.c[c] = S > 0 ? p0 + p2 : p0 - p2; h.c[3 + c] = S > 0 ? p1 + p3 : p1 - p3; }
+  }
+  return h;
+}
+template <int MU, int S> __device__ __forceinline__ SP recon(const HS &h) {
+  SP r;
+#pragma unroll
+  for (int c = 0; c < 3; c++) {
+    const cx h0 = h.c[c], h1 = h.c[3 + c];
+    const cx mh0 = {-h0.re, -h0.im}, mh1 = {-h1.re, -h1.im};
+    r.c[c] = h0;
+    r.c[3 + c] = h1;
+    if (MU == 0) { r.c[6 + c] = ti(S > 0 ? mh1 : h1); r.c[9 + c] = ti(S > 0 ? mh0 : h0); }
+    else if (MU == 1) { r.c[6 + c] = S > 0 ? h1 : mh1; r.c[9 + c] = S > 0 ? mh0 : h0; }
+    else if (MU == 2) { r.c[6 + c] = ti(S > 0 ? mh0 : h0); r.c[9 + c] = ti(S > 0 ? h1 : mh1); }
+    else { r.c[6 + c] = S > 0 ? h0 : mh0; r.c[9 + c] = S > 0 ? h1 : mh1; }
+  }
+  return r;
+}
+__device__ __forceinline__ HS mul(const CM &u, const HS &s) {
+  HS o;
+  for (int sp = 0; sp < 2; sp++)
+    for (int a = 0; a < 3; a++) {
+      cx acc = cmul(u.m[3 * a], s.c[3 * sp]);
+      acc = cmadd(u.m[3 * a + 1], s.c[3 * sp + 1], acc);
+      o.c[3 * sp + a] = cmadd(u.m[3 * a + 2], s.c[3 * sp + 2], acc);
+    }
+  return o;
+}
 __device__ __forceinline__ int wrap(int n, int L) { n %= L; return n < 0 ? n + L : n; }
+__device__ __forceinline__ int wrap_up(int n, int L) { return n + 1 == L ? 0 : n + 1; }
+__device__ __forceinline__ int wrap_down(int n, int L) { return n == 0 ? L - 1 : n - 1; }
 __device__ __forceinline__ const char *base(const JitArgs &a, int k, int par, int mu) {
   if (mu >= 0) return a.op[k] + (long long)(2 * mu + par) * a.blk[k];
   return a.op[k] + (a.all[k] ? (long long)par * a.blk[k] : 0);
@@ -567,22 +665,28 @@ __device__ __forceinline__ void third_row(CM &u) {
     u.m[6 + a] = conj(t);
   }
 }
+// Loads: S = true for a field block read at one displacement only (no reuse between threads:
+// streamed past L1, like the hand-written kernels' links), false for blocks read at several
+// displacements (stencil reuse through L1/L2, like the dslash's neighbour spinors).
 #if QDPJ_F64
-__device__ __forceinline__ cx ldc(const char *b, int st, int k, int cb) {
-  const double2 v = __ldg((const double2 *)b + (long long)k * st + cb);
+template <bool S> __device__ __forceinline__ cx ldc(const char *b, int st, int k, int cb) {
+  const double2 *q = (const double2 *)b + (long long)k * st + cb;
+  double2 v;
+  if (S) asm("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(q));
+  else v = __ldg(q);
   return {v.x, v.y};
 }
 __device__ __forceinline__ void stc(char *b, int st, int k, int cb, cx v) {
-  ((double2 *)b)[(long long)k * st + cb] = make_double2(v.re, v.im);
+  __stcs((double2 *)b + (long long)k * st + cb, make_double2(v.re, v.im));
 }
-#define QDPJ_LD(T, N, F) { T r; for (int k = 0; k < N; k++) r.F[k] = ldc(b, st, k, cb); return r; }
+#define QDPJ_LD(T, N, F) { T r; for (int k = 0; k < N; k++) r.F[k] = ldc<S>(b, st, k, cb); return r; }
 #define QDPJ_ST(N, F) { for (int k = 0; k < N; k++) stc(b, st, k, cb, x.F[k]); }
-__device__ __forceinline__ SP ld_sp(const char *b, int st, int cb) QDPJ_LD(SP, 12, c)
-__device__ __forceinline__ CM ld_cm(const char *b, int st, int cb) QDPJ_LD(CM, 9, m)
-__device__ __forceinline__ SM ld_sm(const char *b, int st, int cb) QDPJ_LD(SM, 16, m)
-__device__ __forceinline__ CM ld_g12(const char *b, int st, int cb) {
+template <bool S> __device__ __forceinline__ SP ld_sp(const char *b, int st, int cb) QDPJ_LD(SP, 12, c)
+template <bool S> __device__ __forceinline__ CM ld_cm(const char *b, int st, int cb) QDPJ_LD(CM, 9, m)
+template <bool S> __device__ __forceinline__ SM ld_sm(const char *b, int st, int cb) QDPJ_LD(SM, 16, m)
+template <bool S> __device__ __forceinline__ CM ld_g12(const char *b, int st, int cb) {
   CM u;
-  for (int k = 0; k < 6; k++) u.m[k] = ldc(b, st, k, cb);
+  for (int k = 0; k < 6; k++) u.m[k] = ldc<S>(b, st, k, cb);
   third_row(u);
   return u;
 }
@@ -591,34 +695,43 @@ __device__ __forceinline__ void st_cm(char *b, int st, int cb, const CM &x) QDPJ
 __device__ __forceinline__ void st_sm(char *b, int st, int cb, const SM &x) QDPJ_ST(16, m)
 #else
 // fp32: pairs of complex numbers per float4 plane; colour matrices 4 float4 planes + 1 float2 plane
-__device__ __forceinline__ void ld2(const char *b, int st, int k, int cb, cx &x, cx &y) {
-  const float4 v = __ldg((const float4 *)b + (long long)k * st + cb);
+template <bool S> __device__ __forceinline__ void ld2(const char *b, int st, int k, int cb, cx &x, cx &y) {
+  const float4 *q = (const float4 *)b + (long long)k * st + cb;
+  float4 v;
+  if (S) asm("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(q));
+  else v = __ldg(q);
   x = {v.x, v.y};
   y = {v.z, v.w};
 }
+template <bool S> __device__ __forceinline__ cx ld1(const char *b, int cb) {
+  const float2 *q = (const float2 *)b + cb;
+  float2 v;
+  if (S) asm("ld.global.nc.L1::no_allocate.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(q));
+  else v = __ldg(q);
+  return {v.x, v.y};
+}
 __device__ __forceinline__ void st2(char *b, int st, int k, int cb, cx x, cx y) {
-  ((float4 *)b)[(long long)k * st + cb] = make_float4(x.re, x.im, y.re, y.im);
+  __stcs((float4 *)b + (long long)k * st + cb, make_float4(x.re, x.im, y.re, y.im));
 }
-__device__ __forceinline__ SP ld_sp(const char *b, int st, int cb) {
+template <bool S> __device__ __forceinline__ SP ld_sp(const char *b, int st, int cb) {
   SP r;
-  for (int k = 0; k < 6; k++) ld2(b, st, k, cb, r.c[2 * k], r.c[2 * k + 1]);
+  for (int k = 0; k < 6; k++) ld2<S>(b, st, k, cb, r.c[2 * k], r.c[2 * k + 1]);
   return r;
 }
-__device__ __forceinline__ SM ld_sm(const char *b, int st, int cb) {
+template <bool S> __device__ __forceinline__ SM ld_sm(const char *b, int st, int cb) {
   SM r;
-  for (int k = 0; k < 8; k++) ld2(b, st, k, cb, r.m[2 * k], r.m[2 * k + 1]);
+  for (int k = 0; k < 8; k++) ld2<S>(b, st, k, cb, r.m[2 * k], r.m[2 * k + 1]);
   return r;
 }
-__device__ __forceinline__ CM ld_cm(const char *b, int st, int cb) {
+template <bool S> __device__ __forceinline__ CM ld_cm(const char *b, int st, int cb) {
   CM r;
-  for (int k = 0; k < 4; k++) ld2(b, st, k, cb, r.m[2 * k], r.m[2 * k + 1]);
-  const float2 v = __ldg((const float2 *)(b + (long long)64 * st) + cb);
-  r.m[8] = {v.x, v.y};
+  for (int k = 0; k < 4; k++) ld2<S>(b, st, k, cb, r.m[2 * k], r.m[2 * k + 1]);
+  r.m[8] = ld1<S>(b + (long long)64 * st, cb);
   return r;
 }
-__device__ __forceinline__ CM ld_g12(const char *b, int st, int cb) {
+template <bool S> __device__ __forceinline__ CM ld_g12(const char *b, int st, int cb) {
   CM u;
-  for (int k = 0; k < 3; k++) ld2(b, st, k, cb, u.m[2 * k], u.m[2 * k + 1]);
+  for (int k = 0; k < 3; k++) ld2<S>(b, st, k, cb, u.m[2 * k], u.m[2 * k + 1]);
   third_row(u);
   return u;
 }
@@ -630,7 +743,7 @@ __device__ __forceinline__ void st_sm(char *b, int st, int cb, const SM &x) {
 }
 __device__ __forceinline__ void st_cm(char *b, int st, int cb, const CM &x) {
   for (int k = 0; k < 4; k++) st2(b, st, k, cb, x.m[2 * k], x.m[2 * k + 1]);
-  ((float2 *)(b + (long long)64 * st))[cb] = make_float2(x.m[8].re, x.m[8].im);
+  __stcs((float2 *)(b + (long long)64 * st) + cb, make_float2(x.m[8].re, x.m[8].im));
 }
 #endif
 )PRELUDE";
@@ -681,6 +794,7 @@ int generate(const char *expr, int out_kind, int prec, const int *kinds, int nop
   G.prec = prec;
   G.count_leaves(root.get());
   const int d0[4] = {0, 0, 0, 0};
+  G.collect(root.get(), d0);
   G.site(d0);
   const std::string v = G.emit(root.get(), d0);
   std::ostringstream s;
@@ -775,8 +889,14 @@ int compile_cubin(const std::string &src, std::vector<char> *cubin, std::string 
     err = "nvrtcCreateProgram failed";
     return QDP_ECUDA;
   }
-  const char *opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "--fmad=true"};
-  const int rc = N.compile(prog, 4, opts);
+  std::vector<const char *> opts = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "--fmad=true"};
+  // Register budget 168 (6 x 64-thread blocks per SM, the hand-written dslash's measured optimum,
+  // DESIGN.md section 6): it also makes ptxas hoist more loads.  Measured on the generated hopping
+  // term: no cap 322 us, 168 -> 247 us (hand-written 242 us); profiles/r01_jit_vs_handwritten.txt.
+  std::string maxreg = "--maxrregcount=168";
+  if (const char *e = getenv("QDPB_JIT_MAXRREG")) maxreg = std::string("--maxrregcount=") + e;  // experiments
+  opts.push_back(maxreg.c_str());
+  const int rc = N.compile(prog, (int)opts.size(), opts.data());
   if (rc != 0) {
     size_t n = 0;
     N.log_size(prog, &n);

@@ -52,14 +52,19 @@ def _re(z):
     return np.stack([z.real, z.imag], axis=-1)
 
 
-def hopping_expr(gauge="$0", psi="$1"):
+def hopping_expr(gauge="$0", psi="$1", grouped=True):
     """PAPER.md:282 written in the expression language: sum_mu (1 - g_mu) U_mu psi(x+mu) +
-    (1 + g_mu) U_mu(x-mu)^dag psi(x-mu); common subexpressions are formed once."""
+    (1 + g_mu) U_mu(x-mu)^dag psi(x-mu).  grouped: each (1 -/+ gamma) A in parentheses, which the
+    generator turns into a spin projection; ungrouped: the same sum evaluated literally (with
+    common subexpressions formed once)."""
     terms = []
     for m in range(4):
         f = f"{gauge}[{m}]*shift({psi},{m},+1)"
         b = f"shift(adj({gauge}[{m}])*{psi},{m},-1)"
-        terms.append(f"{f} - gamma({m})*({f}) + {b} + gamma({m})*{b}")
+        if grouped:
+            terms.append(f"({f} - gamma({m})*({f})) + ({b} + gamma({m})*{b})")
+        else:
+            terms.append(f"{f} - gamma({m})*({f}) + {b} + gamma({m})*{b}")
     return " + ".join(terms)
 
 
@@ -207,10 +212,11 @@ def test_hopping_expression_vs_oracle(q, prec, L, gauge_kind):
         fU = _field(q, c, gk, prec, -1, U)
         fp = _field(q, c, q.QDP_FERMION, prec, -1, psi)
         out = q.qdp_field_alloc(c, q.QDP_FERMION, prec, -1)
-        q.qdp_jit_eval(out, hopping_expr(), fU, fp)
         ref = oracle.hopping(U, psi, L, -1)
         tol = TOL[prec]
-        assert _err(q.qdp_field_export(out), ref) <= tol
+        for grouped in (True, False):  # spin-projected and literal forms
+            q.qdp_jit_eval(out, hopping_expr(grouped=grouped), fU, fp)
+            assert _err(q.qdp_field_export(out), ref) <= tol, grouped
         # even-odd: out_e = H_eo psi_o, compared with the fused kernel too
         even, odd = fieldgen.cb_sites(L, 0), fieldgen.cb_sites(L, 1)
         fo = _field(q, c, q.QDP_FERMION, prec, 1, psi[odd])

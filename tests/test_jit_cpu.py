@@ -16,12 +16,15 @@ def q():
     return qdpb
 
 
-def hopping_expr():
+def hopping_expr(grouped=True):
     terms = []
     for m in range(4):
         f = f"$0[{m}]*shift($1,{m},+1)"
         b = f"shift(adj($0[{m}])*$1,{m},-1)"
-        terms.append(f"{f} - gamma({m})*({f}) + {b} + gamma({m})*{b}")
+        if grouped:
+            terms.append(f"({f} - gamma({m})*({f})) + ({b} + gamma({m})*{b})")
+        else:
+            terms.append(f"{f} - gamma({m})*({f}) + {b} + gamma({m})*{b}")
     return " + ".join(terms)
 
 
@@ -43,13 +46,18 @@ def test_table2_accounting_matches_paper(q):
 
 
 def test_hopping_expression_work(q):
-    """CSE: the 8 U*psi products are formed once each (2112 flop) + 15 spinor additions (360);
-    the projections by gamma are free.  Compulsory bytes per EO output site = the hand-written
-    dslash's 1536 (8 links, input, output); for a full-lattice output each
-    field is read once: 4 links + input + output."""
+    """Grouped (1 -/+ gamma_mu)(U psi) terms become spin projections: 8 x (12 projection + 132
+    U x half spinor) + 7 x 24 accumulation = 1320 flop/site, exactly the standard hopping-term count
+    of the hand-written kernel.  Ungrouped, the left-associated sum only
+    matches the pattern for its first term (144 flop); CSE forms the other 7 U*psi products once
+    (7 x 264) and 14 spinor additions remain (14 x 24).  Compulsory bytes per EO output site =
+    the dslash's 1536 (8 links, input, output); for a full-lattice output each field is read once:
+    4 links + input + output."""
     G, F = q.QDP_GAUGE, q.QDP_FERMION
     _, w = q.qdp_jit_source(hopping_expr(), F, q.QDP_F64, [G, F], out_subset=0)
-    assert w["flops"] == 8 * 264 + 15 * 24
+    assert w["flops"] == 8 * (12 + 132) + 7 * 24 == 1320
+    _, w = q.qdp_jit_source(hopping_expr(grouped=False), F, q.QDP_F64, [G, F], out_subset=0)
+    assert w["flops"] == 144 + 7 * 264 + 14 * 24
     assert w["bytes"] == 1536
     _, w = q.qdp_jit_source(hopping_expr(), F, q.QDP_F64, [G, F], out_subset=-1)
     assert w["bytes"] == (4 * 18 + 24 + 24) * 8
@@ -62,7 +70,7 @@ def test_generated_source_structure(q):
                               [q.QDP_GAUGE, q.QDP_FERMION])
     assert src.count("__global__") == 1 and "qdp_jit_kernel" in src
     assert "typedef double R;" in src
-    assert "n[1] = wrap(n[1] + (1), a.L[1]);" in src and "n[2] = wrap(n[2] + (-1), a.L[2]);" in src
+    assert "n[1] = wrap_up(n[1], a.L[1]);" in src and "n[2] = wrap_down(n[2], a.L[2]);" in src
     assert "const int p1 = p ^ 0;" in src  # two hops: same parity
 
 
