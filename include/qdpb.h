@@ -310,8 +310,11 @@ int qdp_expr_block(qdp_ctx ctx, int expr, int prec, int *block, int *tuned);
  * precision (QDP_EPREC); a one-parity operand must hold the parity it is read at (out's parity,
  * flipped by each odd shift displacement) and gauge operands must be QDP_ALL (QDP_EINVAL);
  * out must not alias an operand (QDP_EALIAS).  Parse and type errors: QDP_EINVAL with the
- * reason in qdp_last_error.  A shift along a dimension reached through the halo path (P_mu > 1
- * or self-halo) returns QDP_EUNSUPPORTED: use qdp_shift, which exchanges the faces.  The first
+ * reason in qdp_last_error.  Shifts along dimensions reached through the halo path (P_mu > 1 or
+ * self-halo): every operand read at a displacement with such components is
+ * first shifted by those components with qdp_shift (faces exchanged; collective, so every rank
+ * must make the same call), into temporaries kept with the cached kernel; more than 16 such
+ * (operand, displacement) pairs: QDP_EUNSUPPORTED.  The first
  * call for an (expression, operand kinds, precision) compiles (~0.1-0.5 s); NVRTC missing:
  * QDP_EUNSUPPORTED.  Work counters (qdp_profile_work, class QDP_PK_BLAS): flops by the Table II
  * convention for the operations executed, compulsory bytes (each distinct field once + store).

@@ -22,9 +22,10 @@
 //   shift(a, mu, s)  a(x + s mu^), s = +1 (FORWARD) or -1 (BACKWARD): PAPER.md:111-126 (R4).
 //               Evaluated in place: the subexpression is computed at the neighbouring site, so a
 //               shift costs no temporary and "shifts of shifts" are just diagonal
-//               neighbours.  Periodic on the local lattice: a shift along a dimension reached
-//               through the halo path (multi-rank or self-halo) is QDP_EUNSUPPORTED (use
-//               qdp_shift, which runs the face exchange).
+//               neighbours, periodic on the local lattice.  Along dimensions reached through
+//               the halo path (multi-rank or self-halo) the displaced operand is first
+//               materialised with qdp_shift, which exchanges the faces, and the
+//               kernel reads that temporary (section V's face communication, not overlapped here).
 // Products: colour x colour, colour x spinor, spin x spin, spin x spinor, real x anything,
 // gamma x spinor / spin matrix.  Common subexpressions (same text at the same site) are
 // computed once, so e.g. the hopping term can be written as
@@ -38,6 +39,7 @@
 // the library's roofline numerator) and Table II's (every leaf occurrence + the store).
 #include <dlfcn.h>
 
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -53,6 +55,12 @@ struct qdpb::JitKernel {
   int max_threads = 1024;
   double flops = 0, bytes_all = 0, bytes_parity = 0;  // per output site (out QDP_ALL / one parity)
   long key = 0;                 // autotuner key
+  // halo'd temporaries: operand temp_leaf[j] shifted by temp_dp[j] (qdp_shift chain through
+  // temp_steps[j]; the last step writes temp_field[j]), allocated on first use, kept for reuse
+  std::vector<int> temp_leaf;
+  std::vector<std::array<int, 4>> temp_dp;
+  std::vector<qdp_field> temp_field;
+  std::vector<std::vector<qdp_field>> temp_steps;
 };
 
 namespace qdpb {
@@ -298,9 +306,20 @@ int type_reals(Type t, int kind = -1) {
 }
 const char *ctype(Type t) { return t == T_CM ? "CM" : t == T_SP ? "SP" : t == T_SM ? "SM" : "R"; }
 
+// A leaf read at a displacement with components along dimensions reached through the halo path:
+// the host materialises operand `leaf` shifted by `dp` (those components) with qdp_shift, which
+// exchanges the faces (shifts of shifts for diagonal displacements),
+// and the kernel reads that temporary at the remaining (in-kernel, periodic) displacement.
+struct Temp {
+  int leaf;
+  int dp[4];
+};
+
 struct Gen {
   const int *kinds;
   int prec;
+  int part = 0;              // dims reached through the halo path
+  std::vector<Temp> temps;   // operand slots QDP_JIT_MAX_OPERANDS + j
   std::ostringstream body;
   int nv = 0;
   std::map<std::string, std::string> cse;    // canonical key -> variable
@@ -410,12 +429,25 @@ struct Gen {
     if (it != cse.end()) return it->second;
     std::string v;
     if (n->op == N_LEAF) {
-      const std::string s = site(d);
+      int slot = n->leaf, r[4] = {d[0], d[1], d[2], d[3]};
+      Temp t = {n->leaf, {0, 0, 0, 0}};
+      for (int m = 0; m < 4; m++)
+        if (((part >> m) & 1) && d[m]) {
+          t.dp[m] = d[m];
+          r[m] = 0;
+        }
+      if (t.dp[0] || t.dp[1] || t.dp[2] || t.dp[3]) {
+        size_t j = 0;
+        while (j < temps.size() && !(temps[j].leaf == t.leaf && !memcmp(temps[j].dp, t.dp, sizeof t.dp))) j++;
+        if (j == temps.size()) temps.push_back(t);
+        slot = QDP_JIT_MAX_OPERANDS + (int)j;
+      }
+      const std::string s = site(r);
       const int kind = kinds[n->leaf];
       distinct.insert({n->leaf, n->mu});
       distinct_par.insert({n->leaf, n->mu, (std::abs(d[0]) + std::abs(d[1]) + std::abs(d[2]) + std::abs(d[3])) & 1});
       v = fresh();
-      const std::string base = "base(a, " + std::to_string(n->leaf) + ", p" + s + ", " + std::to_string(n->mu) + ")";
+      const std::string base = "base(a, " + std::to_string(slot) + ", p" + s + ", " + std::to_string(n->mu) + ")";
       const char *ld = kind == QDP_FERMION ? "ld_sp" : kind == QDP_SPINMATRIX ? "ld_sm" : kind == QDP_GAUGE12 ? "ld_g12" : "ld_cm";
       const bool stream = reuse.count({n->leaf, n->mu, flip(d)}) == 0;
       body << "  const " << ctype(n->type) << " " << v << " = " << ld << (stream ? "<true>(" : "<false>(") << base
@@ -489,11 +521,11 @@ struct Gen {
 // device-side prelude: types, algebra and the library's SoA layouts (internal.h), per precision
 const char *kPrelude = R"PRELUDE(
 struct JitArgs {
-  const char *op[8];
+  const char *op[24]; // 8 operands, then up to 16 halo'd temporaries
   char *out;
-  long long blk[8];   // bytes between parity blocks (gauge: between (mu, parity) blocks)
+  long long blk[24];  // bytes between parity blocks (gauge: between (mu, parity) blocks)
   long long out_blk;
-  int all[8];         // operand covers both parities
+  int all[24];        // operand covers both parities
   int L[4];
   int Lh0, Vh, stride, parity, nblk;
 };
@@ -749,6 +781,7 @@ __device__ __forceinline__ void st_cm(char *b, int st, int cb, const CM &x) {
 )PRELUDE";
 
 struct Generated {
+  std::vector<Temp> temps;
   std::string src;
   double flops = 0, table2_reals = 0;
   // compulsory reals per output site: out QDP_ALL -> each distinct field once; out one parity ->
@@ -758,7 +791,8 @@ struct Generated {
   std::vector<std::pair<int, int>> leaf_disp_parity;  // (operand, parity flip) of every leaf load
 };
 
-int generate(const char *expr, int out_kind, int prec, const int *kinds, int nops, Generated *g, std::string &err) {
+int generate(const char *expr, int out_kind, int prec, const int *kinds, int nops, int part, Generated *g,
+             std::string &err) {
   if (!expr) {
     err = "null expression";
     return QDP_EINVAL;
@@ -792,6 +826,7 @@ int generate(const char *expr, int out_kind, int prec, const int *kinds, int nop
   Gen G;
   G.kinds = kinds;
   G.prec = prec;
+  G.part = part;
   G.count_leaves(root.get());
   const int d0[4] = {0, 0, 0, 0};
   G.collect(root.get(), d0);
@@ -819,6 +854,11 @@ int generate(const char *expr, int out_kind, int prec, const int *kinds, int nop
   s << G.body.str();
   const char *st = want == T_SP ? "st_sp" : want == T_CM ? "st_cm" : "st_sm";
   s << "  " << st << "(a.out + (long long)bi * a.out_blk, a.stride, cb, " << v << ");\n}\n";
+  if (G.temps.size() > 16) {
+    err = "more than 16 distinct operand displacements across the halo path";
+    return QDP_EUNSUPPORTED;
+  }
+  g->temps = G.temps;
   g->src = s.str();
   g->flops = G.flops;
   g->shift_dims = G.shift_dims;
@@ -918,6 +958,9 @@ int compile_cubin(const std::string &src, std::vector<char> *cubin, std::string 
 
 void jit_release(qdp_ctx ctx) {
   for (auto &kv : ctx->jit) {
+    for (qdp_field f : kv.second->temp_field) qdp_field_free(f);
+    for (auto &v : kv.second->temp_steps)
+      for (qdp_field f : v) qdp_field_free(f);
     if (kv.second->lib) cudaLibraryUnload(kv.second->lib);
     delete kv.second;
   }
@@ -930,17 +973,15 @@ int jit_eval(qdp_field out, const char *expr, const qdp_field *ops, int nops) {
   const int prec = out->prec;
   int kinds[QDP_JIT_MAX_OPERANDS];
   for (int k = 0; k < nops; k++) kinds[k] = ops[k]->kind;
-  // cache key: expression text, operand kinds, output kind, precision
-  std::string key = std::string(expr) + "|" + std::to_string(out->kind) + "|" + std::to_string(prec);
-  for (int k = 0; k < nops; k++) key += "|" + std::to_string(kinds[k]);
+  // cache key: expression text, operand kinds and subsets, output kind and subset, precision,
+  // and the dims reached through the halo path (they decide which leaves become temporaries)
+  std::string key = std::string(expr) + "|" + std::to_string(out->kind) + "|" + std::to_string(out->subset) + "|" +
+                    std::to_string(prec) + "|" + std::to_string(g.part);
+  for (int k = 0; k < nops; k++) key += "|" + std::to_string(kinds[k]) + "/" + std::to_string(ops[k]->subset);
   Generated gen;
   std::string err;
-  int rc = generate(expr, out->kind, prec, kinds, nops, &gen, err);
+  int rc = generate(expr, out->kind, prec, kinds, nops, g.part, &gen, err);
   if (rc) return set_error(ctx, rc, "jit: %s", err.c_str());
-  for (int mu : gen.shift_dims)
-    if ((g.part >> mu) & 1)
-      return set_error(ctx, QDP_EUNSUPPORTED,
-                       "jit: shift along dim %d, which is reached through the halo path (use qdp_shift)", mu);
   // operand subsets: each leaf is read at parity out_parity ^ flip; a one-parity operand must match
   for (const auto &lp : gen.leaf_disp_parity) {
     const qdp_field f = ops[lp.first];
@@ -966,6 +1007,12 @@ int jit_eval(qdp_field out, const char *expr, const qdp_field *ops, int nops) {
     k->bytes_all = gen.compulsory_all * (prec == QDP_F64 ? 8 : 4);
     k->bytes_parity = gen.compulsory_parity * (prec == QDP_F64 ? 8 : 4);
     k->key = (1L << 62) | (long)(std::hash<std::string>()(key) & ((1L << 61) - 1));
+    for (const Temp &t : gen.temps) {
+      k->temp_leaf.push_back(t.leaf);
+      k->temp_dp.push_back({t.dp[0], t.dp[1], t.dp[2], t.dp[3]});
+    }
+    k->temp_field.assign(gen.temps.size(), nullptr);
+    k->temp_steps.assign(gen.temps.size(), {});
     ctx->jit_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     ctx->jit_compiled++;
     K = k.release();
@@ -975,11 +1022,11 @@ int jit_eval(qdp_field out, const char *expr, const qdp_field *ops, int nops) {
   }
 
   struct Args {  // mirrors JitArgs of the generated prelude
-    const char *op[8];
+    const char *op[24];
     char *out;
-    long long blk[8];
+    long long blk[24];
     long long out_blk;
-    int all[8];
+    int all[24];
     int L[4];
     int Lh0, Vh, stride, parity, nblk;
   } a;
@@ -991,6 +1038,33 @@ int jit_eval(qdp_field out, const char *expr, const qdp_field *ops, int nops) {
       a.blk[k] = (long long)parity_block_bytes(ops[k]->kind, prec, g.stride) / 4;
     else
       a.blk[k] = (long long)parity_block_bytes(ops[k]->kind, prec, g.stride);
+  }
+  // halo'd temporaries: operand shifted by dp, one qdp_shift per unit step (faces exchanged there)
+  for (size_t j = 0; j < K->temp_leaf.size(); j++) {
+    const qdp_field src = ops[K->temp_leaf[j]];
+    std::vector<std::pair<int, int>> steps;  // (mu, sign)
+    for (int m = 0; m < 4; m++)
+      for (int i = 0; i < std::abs(K->temp_dp[j][m]); i++) steps.push_back({m, K->temp_dp[j][m] > 0 ? 1 : -1});
+    auto subset_after = [&](size_t n) { return src->subset == QDP_ALL ? QDP_ALL : src->subset ^ (int)(n & 1); };
+    if (!K->temp_field[j]) {
+      if ((rc = qdp_field_alloc(ctx, src->kind, prec, subset_after(steps.size()), &K->temp_field[j]))) return rc;
+      for (size_t i = 0; i + 1 < steps.size(); i++) {
+        qdp_field f;
+        if ((rc = qdp_field_alloc(ctx, src->kind, prec, subset_after(i + 1), &f))) return rc;
+        K->temp_steps[j].push_back(f);
+      }
+    }
+    qdp_field in = src;
+    for (size_t i = 0; i < steps.size(); i++) {
+      qdp_field o = i + 1 == steps.size() ? K->temp_field[j] : K->temp_steps[j][i];
+      if ((rc = qdp_shift(o, in, steps[i].first, steps[i].second))) return rc;
+      in = o;
+    }
+    const int slot = QDP_JIT_MAX_OPERANDS + (int)j;
+    const qdp_field t = K->temp_field[j];
+    a.op[slot] = (const char *)t->data;
+    a.all[slot] = t->subset == QDP_ALL;
+    a.blk[slot] = (long long)parity_block_bytes(t->kind, prec, g.stride) / (is_gauge(t->kind) ? 4 : 1);
   }
   a.out = (char *)out->data;
   a.out_blk = (long long)parity_block_bytes(out->kind, prec, g.stride);
@@ -1020,7 +1094,7 @@ int jit_eval(qdp_field out, const char *expr, const qdp_field *ops, int nops) {
 int jit_source(const char *expr, int out_kind, int out_subset, int prec, const int *kinds, int nops, char *src,
                size_t cap, size_t *src_len, double work[3], int compile, std::string &err) {
   Generated gen;
-  int rc = generate(expr, out_kind, prec, kinds, nops, &gen, err);
+  int rc = generate(expr, out_kind, prec, kinds, nops, 0, &gen, err);
   if (rc) return rc;
   if (work) {
     work[0] = gen.flops;

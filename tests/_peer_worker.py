@@ -162,6 +162,27 @@ def _run(rank, world, case, G, P):
                 assert np.max(np.abs(res["hist"] - ref["hist"]) / ref["hist"]) <= 1e-10
                 for i in range(len(sigma)):
                     assert rel_site_err(got[i][odd], ref["x"][i][odd]) <= 1e-9
+        elif case == "jit":
+            # run-time generated expressions whose shifts cross rank boundaries: the halo'd leaves are
+            # materialised through qdp_shift (faces via the peer mailbox), the rest is in-kernel
+            from test_gpu_jit import hopping_expr
+            fU = field(q.QDP_GAUGE, 0, q.QDP_ALL, Ul)
+            fp = field(q.QDP_FERMION, 0, q.QDP_ALL, pl)
+            fo = q.qdp_field_alloc(c, q.QDP_FERMION, 0, q.QDP_ALL)
+            for _ in range(2):  # second call: cached kernel and temporaries
+                q.qdp_jit_eval(fo, hopping_expr(), fU, fp)
+            got = _gather(q.qdp_field_export(fo), G, P, (4, 3, 2))
+            # Fig. 1 along t and a diagonal shift of a shift
+            q.qdp_jit_eval(fo, "$0[3]*shift($1,3,+1) + shift(adj($0[3])*$1,3,-1)", fU, fp)
+            fig1 = _gather(q.qdp_field_export(fo), G, P, (4, 3, 2))
+            q.qdp_jit_eval(fo, "shift(shift($0,2,-1),3,+1)", fp)
+            diag = _gather(q.qdp_field_export(fo), G, P, (4, 3, 2))
+            if rank == 0:
+                assert rel_site_err(got, oracle.hopping(U, psi, G, -1)) <= 1e-13
+                ref = (oracle.upsi(U[:, 3], oracle.shift(psi, G, 3, 1))
+                       + oracle.shift(oracle.adj_upsi(U[:, 3], psi), G, 3, -1))
+                assert rel_site_err(fig1, ref) <= 1e-13
+                assert np.array_equal(diag, oracle.shift(oracle.shift(psi, G, 2, -1), G, 3, 1))
         else:
             raise ValueError(case)
     finally:

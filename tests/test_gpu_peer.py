@@ -40,6 +40,12 @@ def test_peer_shift():
 
 
 @pytest.mark.timeout(600)
+@pytest.mark.parametrize("G, P", [((4, 4, 4, 8), (1, 1, 1, 2)), ((4, 4, 4, 8), (1, 1, 2, 2))])
+def test_peer_jit(G, P):
+    _spawn("jit", G, P)
+
+
+@pytest.mark.timeout(600)
 @pytest.mark.parametrize("case", ["cg", "cg_clover", "multishift"])
 def test_peer_cg(case):
     _spawn(case, (4, 4, 4, 8), (1, 1, 1, 2))
