@@ -185,6 +185,7 @@ def run_native(args, rank, world, local_rank):
 
     import fieldgen
     from paper_1408_5925_b200 import dist as qdist
+    from paper_1408_5925_b200 import exprs as qexprs
     from paper_1408_5925_b200 import qdpb as q
 
     # QDPB_BENCH_ONE_GPU=1: every rank on cuda:0 (functional test of the N > 1 path on a one-GPU
@@ -344,6 +345,24 @@ def run_native(args, rank, world, local_rank):
         dsl[tag] = {"us_per_launch": t_d * 1e6, "gflops_per_gpu": f_d / n_d / t_d * 1e-9,
                     "gbs_compulsory_per_gpu": b_d / n_d / t_d * 1e-9, "bytes_per_site": b_d / n_d / Vh,
                     "frac_of_measured_hbm": b_d / n_d / t_d * 1e-9 / measured_peak()[0]}
+        # the same operator generated at run time from its expression (qdp_jit_eval; PAPER.md
+        # sections III-IV): the paper's generated-vs-hand-tuned comparison
+        if world == 1:
+            expr = qexprs.hopping()
+            for _ in range(12):  # compile once, then let the paper's autotuner settle
+                q.qdp_jit_eval(fo, expr, fUp, fi)
+            q.qdp_synchronize(ctx)
+            q.qdp_profile_reset(ctx)
+            q.qdp_set_option(ctx, q.QDP_OPT_PROFILE, 1)
+            for _ in range(20):
+                q.qdp_jit_eval(fo, expr, fUp, fi)
+            n_j, ms_j = q.qdp_profile_query(ctx, q.QDP_PK_BLAS)
+            f_j, b_j = q.qdp_profile_work(ctx, q.QDP_PK_BLAS)
+            q.qdp_set_option(ctx, q.QDP_OPT_PROFILE, 0)
+            t_j = ms_j / n_j * 1e-3
+            dsl[tag]["generated"] = {"us_per_launch": t_j * 1e6, "flop_per_site": f_j / n_j / Vh,
+                                     "gbs_compulsory_per_gpu": b_j / n_j / t_j * 1e-9,
+                                     "speed_vs_handwritten": t_d / t_j}
         for f in (fi, fo) + (() if fUp is fU else (fUp,)):
             q.qdp_field_free(f)
 

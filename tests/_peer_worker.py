@@ -165,7 +165,7 @@ def _run(rank, world, case, G, P):
         elif case == "jit":
             # run-time generated expressions whose shifts cross rank boundaries: the halo'd leaves are
             # materialised through qdp_shift (faces via the peer mailbox), the rest is in-kernel
-            from test_gpu_jit import hopping_expr
+            from paper_1408_5925_b200.exprs import hopping as hopping_expr
             fU = field(q.QDP_GAUGE, 0, q.QDP_ALL, Ul)
             fp = field(q.QDP_FERMION, 0, q.QDP_ALL, pl)
             fo = q.qdp_field_alloc(c, q.QDP_FERMION, 0, q.QDP_ALL)

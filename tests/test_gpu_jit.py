@@ -53,19 +53,9 @@ def _re(z):
 
 
 def hopping_expr(gauge="$0", psi="$1", grouped=True):
-    """PAPER.md:282 written in the expression language: sum_mu (1 - g_mu) U_mu psi(x+mu) +
-    (1 + g_mu) U_mu(x-mu)^dag psi(x-mu).  grouped: each (1 -/+ gamma) A in parentheses, which the
-    generator turns into a spin projection; ungrouped: the same sum evaluated literally (with
-    common subexpressions formed once)."""
-    terms = []
-    for m in range(4):
-        f = f"{gauge}[{m}]*shift({psi},{m},+1)"
-        b = f"shift(adj({gauge}[{m}])*{psi},{m},-1)"
-        if grouped:
-            terms.append(f"({f} - gamma({m})*({f})) + ({b} + gamma({m})*{b})")
-        else:
-            terms.append(f"{f} - gamma({m})*({f}) + {b} + gamma({m})*{b}")
-    return " + ".join(terms)
+    """PAPER.md:282 in the expression language (paper_1408_5925_b200/exprs.py)."""
+    from paper_1408_5925_b200 import exprs
+    return exprs.hopping(gauge, psi, grouped)
 
 
 @pytest.mark.parametrize("prec", [0, 1])

@@ -17,15 +17,8 @@ def q():
 
 
 def hopping_expr(grouped=True):
-    terms = []
-    for m in range(4):
-        f = f"$0[{m}]*shift($1,{m},+1)"
-        b = f"shift(adj($0[{m}])*$1,{m},-1)"
-        if grouped:
-            terms.append(f"({f} - gamma({m})*({f})) + ({b} + gamma({m})*{b})")
-        else:
-            terms.append(f"{f} - gamma({m})*({f}) + {b} + gamma({m})*{b}")
-    return " + ".join(terms)
+    from paper_1408_5925_b200 import exprs
+    return exprs.hopping(grouped=grouped)
 
 
 def test_table2_accounting_matches_paper(q):

@@ -22,7 +22,7 @@ import torch  # noqa: E402
 
 import fieldgen  # noqa: E402
 from paper_1408_5925_b200 import qdpb as q  # noqa: E402
-from test_gpu_jit import hopping_expr  # noqa: E402  (grouped: spin-projected form)
+from paper_1408_5925_b200.exprs import hopping as hopping_expr  # noqa: E402  (grouped: spin-projected)
 
 
 def timed(stream, fn, n=30, warm=5):
