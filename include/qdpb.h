@@ -321,7 +321,8 @@ int qdp_expr_block(qdp_ctx ctx, int expr, int prec, int *block, int *tuned);
  *
  * qdp_jit_source: the same front end without a context or GPU: writes the generated CUDA
  * source (NUL-terminated, truncated to src_cap; *src_len = bytes needed; on an error the reason
- * is written there instead) and the work per output site of an output of subset out_subset:
+ * is written there instead; out_kind = QDP_JIT_SUM for a qdp_jit_sum expression) and the work
+ * per output site of an output of subset out_subset:
  * work[0] flops, work[1] compulsory bytes (each distinct field -- for a one-parity output each
  * distinct parity block of a field -- read once, plus the store), work[2] bytes by Table II's
  * convention (every leaf occurrence + the store).  compile = 1 also runs NVRTC
@@ -329,10 +330,24 @@ int qdp_expr_block(qdp_ctx ctx, int expr, int prec, int *block, int *tuned);
  * qdp_jit_stats: kernels compiled on this context and the seconds spent generating, compiling
  * and loading them (the paper's JIT overhead). */
 #define QDP_JIT_MAX_OPERANDS 8
+#define QDP_JIT_SUM (-1) /* qdp_jit_source out_kind of a qdp_jit_sum expression */
 int qdp_jit_eval(qdp_field out, const char *expr, const qdp_field *operands, int n_operands);
 int qdp_jit_source(const char *expr, int out_kind, int out_subset, int prec, const int *operand_kinds,
                    int n_operands, char *src, size_t src_cap, size_t *src_len, double work[3], int compile);
 int qdp_jit_stats(qdp_ctx ctx, int *kernels, double *seconds);
+/* Global sums of site expressions (QDP++'s sum(), PAPER.md:95 global sums): out[0] + i out[1] =
+ * sum over the sites of `subset` (QDP_ALL / QDP_EVEN / QDP_ODD) of a complex-scalar expression,
+ * built with
+ *   trace(e)                  trace of a colour or spin matrix
+ *   localNorm2(e)             sum of |component|^2 of a field (a complex scalar with zero imaginary part)
+ *   localInnerProduct(a, b)   sum of conj(a_i) b_i over the components (conjugate-linear in a)
+ *   real(z)                   z with its imaginary part dropped
+ * and the operators above (complex scalars add, subtract, multiply, scale, timesI).  E.g. the
+ * plaquette: "real(trace($0[0]*shift($0[1],0,+1)*adj(shift($0[0],1,+1))*adj($0[1])))".
+ * Accumulated in fp64 (per-thread, block partials, one fixed-order final pass, rank-ordered
+ * cross-rank sum: deterministic for a fixed rank count), 256-thread blocks.  Collective across
+ * ranks.  Errors as qdp_jit_eval; the output-parity rule applies with out's parity = subset. */
+int qdp_jit_sum(qdp_ctx ctx, const char *expr, const qdp_field *operands, int n_operands, int subset, double out[2]);
 
 /* ---- diagnostics ---------------------------------------------------------------------- */
 

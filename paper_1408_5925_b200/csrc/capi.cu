@@ -805,6 +805,20 @@ extern "C" int qdp_jit_eval(qdp_field out, const char *expr, const qdp_field *op
   return jit_eval(out, expr, operands, n_operands);
 }
 
+extern "C" int qdp_jit_sum(qdp_ctx ctx, const char *expr, const qdp_field *operands, int n_operands, int subset,
+                           double out[2]) {
+  if (!ctx || !expr || !out || n_operands < 1 || n_operands > QDP_JIT_MAX_OPERANDS || !operands) return QDP_EINVAL;
+  if (subset != QDP_ALL && subset != QDP_EVEN && subset != QDP_ODD) return set_error(ctx, QDP_EINVAL, "jit sum: subset");
+  int rc;
+  for (int k = 0; k < n_operands; k++) {
+    if (!operands[k]) return set_error(ctx, QDP_EINVAL, "jit: operand %d is NULL", k);
+    if (operands[k]->ctx != ctx) return set_error(ctx, QDP_ESHAPE, "jit: operand %d on another context", k);
+    if ((rc = check_pair(operands[0], operands[k]))) return rc;
+  }
+  if ((rc = jit_sum(ctx, expr, operands, n_operands, subset, operands[0]->prec, 12))) return rc;
+  return read_result(ctx, 12, 2, out);
+}
+
 extern "C" int qdp_jit_source(const char *expr, int out_kind, int out_subset, int prec, const int *operand_kinds,
                               int n_operands, char *src, size_t src_cap, size_t *src_len, double work[3], int compile) {
   if (!expr || n_operands < 0 || n_operands > QDP_JIT_MAX_OPERANDS || (n_operands && !operand_kinds)) return QDP_EINVAL;

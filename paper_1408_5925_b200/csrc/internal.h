@@ -666,6 +666,8 @@ int tuned_launch(qdp_ctx ctx, long key, const std::function<cudaError_t(int)> &g
 struct JitKernel;
 void jit_release(qdp_ctx ctx);
 int jit_eval(qdp_field out, const char *expr, const qdp_field *ops, int nops);
+// red_result[slot], [slot+1] = global sum of a complex-scalar expression over `subset`
+int jit_sum(qdp_ctx ctx, const char *expr, const qdp_field *ops, int nops, int subset, int prec, int slot);
 int jit_source(const char *expr, int out_kind, int out_subset, int prec, const int *kinds, int nops, char *src,
                size_t cap, size_t *src_len, double work[3], int compile, std::string &err);
 

@@ -66,8 +66,9 @@ struct qdpb::JitKernel {
 namespace qdpb {
 namespace {
 
-enum Type { T_REAL, T_CM, T_SP, T_SM, T_GAMMA };
-enum NodeOp { N_NUM, N_LEAF, N_ADD, N_SUB, N_NEG, N_MUL, N_ADJ, N_SHIFT, N_GAMMA, N_TIMESI };
+enum Type { T_REAL, T_CM, T_SP, T_SM, T_GAMMA, T_CPLX };
+enum NodeOp { N_NUM, N_LEAF, N_ADD, N_SUB, N_NEG, N_MUL, N_ADJ, N_SHIFT, N_GAMMA, N_TIMESI, N_TRACE, N_LNORM2, N_LINNER,
+              N_REAL };
 
 struct Node {
   NodeOp op;
@@ -79,7 +80,7 @@ struct Node {
 using NodeP = std::unique_ptr<Node>;
 
 const char *type_name(Type t) {
-  static const char *n[] = {"real", "colour matrix", "spinor", "spin matrix", "gamma"};
+  static const char *n[] = {"real", "colour matrix", "spinor", "spin matrix", "gamma", "complex scalar"};
   return n[t];
 }
 
@@ -212,11 +213,20 @@ struct Parser {
     if (id == "gamma") {
       n = make(N_GAMMA);
       if (!integer(&n->mu) || n->mu < 0 || n->mu > 3) return fail("gamma index must be 0..3");
-    } else if (id == "adj" || id == "timesI") {
-      n = make(id == "adj" ? N_ADJ : N_TIMESI);
+    } else if (id == "adj" || id == "timesI" || id == "trace" || id == "localNorm2" || id == "real") {
+      n = make(id == "adj" ? N_ADJ : id == "timesI" ? N_TIMESI : id == "trace" ? N_TRACE : id == "real" ? N_REAL : N_LNORM2);
       NodeP a = expr();
       if (!a) return nullptr;
       n->kid.push_back(std::move(a));
+    } else if (id == "localInnerProduct") {
+      n = make(N_LINNER);
+      NodeP a = expr();
+      if (!a) return nullptr;
+      n->kid.push_back(std::move(a));
+      if (!eat(',')) return fail("localInnerProduct needs two arguments");
+      NodeP b = expr();
+      if (!b) return nullptr;
+      n->kid.push_back(std::move(b));
     } else if (id == "shift") {
       n = make(N_SHIFT);
       NodeP a = expr();
@@ -274,7 +284,7 @@ bool typecheck(Node *n, const int *kinds, int nops, std::string &err) {
       n->type = a;
       return true;
     case N_TIMESI:
-      if (a == T_GAMMA || a == T_REAL) return bad("timesI needs a field");
+      if (a == T_GAMMA || a == T_REAL) return bad("timesI needs a field or complex scalar");
       n->type = a;
       return true;
     case N_ADJ:
@@ -285,6 +295,23 @@ bool typecheck(Node *n, const int *kinds, int nops, std::string &err) {
       if (a == T_GAMMA || a == T_REAL) return bad("shift needs a field");
       n->type = a;
       return true;
+    case N_TRACE:
+      if (a != T_CM && a != T_SM) return bad("trace needs a colour or spin matrix");
+      n->type = T_CPLX;
+      return true;
+    case N_LNORM2:
+      if (a != T_CM && a != T_SP && a != T_SM && a != T_CPLX) return bad("localNorm2 needs a field");
+      n->type = T_CPLX;
+      return true;
+    case N_LINNER:
+      if (a != b || (a != T_CM && a != T_SP && a != T_SM && a != T_CPLX))
+        return bad("localInnerProduct needs two fields of one type");
+      n->type = T_CPLX;
+      return true;
+    case N_REAL:
+      if (a != T_CPLX) return bad("real needs a complex scalar");
+      n->type = T_CPLX;
+      return true;
     case N_MUL:
       if (a == T_REAL && b != T_GAMMA) n->type = b;
       else if (b == T_REAL && a != T_GAMMA) n->type = a;
@@ -293,6 +320,7 @@ bool typecheck(Node *n, const int *kinds, int nops, std::string &err) {
       else if (a == T_SM && b == T_SM) n->type = T_SM;
       else if (a == T_SM && b == T_SP) n->type = T_SP;
       else if (a == T_GAMMA && (b == T_SP || b == T_SM)) n->type = b;
+      else if (a == T_CPLX && b == T_CPLX) n->type = T_CPLX;
       else return bad(std::string("cannot multiply ") + type_name(a) + " by " + type_name(b));
       return true;
   }
@@ -302,9 +330,10 @@ bool typecheck(Node *n, const int *kinds, int nops, std::string &err) {
 // ------------------------------------------------------------------ code generation
 int type_reals(Type t, int kind = -1) {
   if (kind == QDP_GAUGE12) return 12;
-  return t == T_CM ? 18 : t == T_SP ? 24 : t == T_SM ? 32 : 0;
+  return t == T_CM ? 18 : t == T_SP ? 24 : t == T_SM ? 32 : t == T_CPLX ? 2 : 0;
 }
-const char *ctype(Type t) { return t == T_CM ? "CM" : t == T_SP ? "SP" : t == T_SM ? "SM" : "R"; }
+const char *ctype(Type t) { return t == T_CM ? "CM" : t == T_SP ? "SP" : t == T_SM ? "SM" : t == T_CPLX ? "cx" : "R"; }
+int type_complex(Type t) { return t == T_CM ? 9 : t == T_SP ? 12 : t == T_SM ? 16 : t == T_CPLX ? 1 : 0; }
 
 // A leaf read at a displacement with components along dimensions reached through the halo path:
 // the host materialises operand `leaf` shifted by `dp` (those components) with qdp_shift, which
@@ -484,7 +513,7 @@ struct Gen {
       for (auto &kd : n->kid) xs.push_back(emit(kd.get(), d));
       v = fresh();
       const Type t = n->type;
-      const double nc = t == T_CM ? 9 : t == T_SP ? 12 : t == T_SM ? 16 : 0.5;  // complex numbers (real: 1 flop)
+      const double nc = t == T_REAL ? 0.5 : type_complex(t);  // complex numbers (real: 1 flop)
       std::string e;
       switch (n->op) {
         case N_ADD: e = "add(" + xs[0] + ", " + xs[1] + ")"; flops += 2 * nc; break;
@@ -492,11 +521,23 @@ struct Gen {
         case N_NEG: e = "neg(" + xs[0] + ")"; break;
         case N_ADJ: e = "adj(" + xs[0] + ")"; break;
         case N_TIMESI: e = "timesI(" + xs[0] + ")"; break;
+        case N_TRACE: {
+          const int nd = n->kid[0]->type == T_CM ? 3 : 4;
+          e = "trace(" + xs[0] + ")";
+          flops += 2 * (nd - 1);
+          break;
+        }
+        case N_LNORM2: e = "lnorm2(" + xs[0] + ")"; flops += 4 * type_complex(n->kid[0]->type); break;
+        case N_LINNER: e = "linner(" + xs[0] + ", " + xs[1] + ")"; flops += 8 * type_complex(n->kid[0]->type); break;
+        case N_REAL: e = "cx{" + xs[0] + ".re, R(0)}"; break;
         case N_MUL: {
           const Type a = n->kid[0]->type, b = n->kid[1]->type;
           if (a == T_REAL && b == T_REAL) {
             e = "(" + xs[0] + " * " + xs[1] + ")";
             flops += 1;
+          } else if (a == T_CPLX && b == T_CPLX) {
+            e = "cmul(" + xs[0] + ", " + xs[1] + ")";
+            flops += 6;
           } else if (a == T_REAL || b == T_REAL) {
             e = a == T_REAL ? "scale(" + xs[0] + ", " + xs[1] + ")" : "scale(" + xs[1] + ", " + xs[0] + ")";
             flops += 2 * nc;
@@ -606,6 +647,47 @@ __device__ __forceinline__ SM adj(const SM &u) {
   for (int i = 0; i < 4; i++)
     for (int j = 0; j < 4; j++) r.m[4 * i + j] = conj(u.m[4 * j + i]);
   return r;
+}
+// complex scalars per site (trace, local norms and inner products) and their algebra
+__device__ __forceinline__ cx add(cx a, cx b) { return a + b; }
+__device__ __forceinline__ cx sub(cx a, cx b) { return a - b; }
+__device__ __forceinline__ cx neg(cx a) { return {-a.re, -a.im}; }
+__device__ __forceinline__ cx scale(R s, cx a) { return {s * a.re, s * a.im}; }
+__device__ __forceinline__ cx timesI(cx a) { return ti(a); }
+__device__ __forceinline__ cx trace(const CM &u) { return u.m[0] + u.m[4] + u.m[8]; }
+__device__ __forceinline__ cx trace(const SM &u) { return u.m[0] + u.m[5] + u.m[10] + u.m[15]; }
+#define QDPJ_LOCAL(T, N, F)                                                                   \
+  __device__ __forceinline__ cx lnorm2(const T &a) {                                           \
+    R s = 0; for (int k = 0; k < N; k++) s += a.F[k].re * a.F[k].re + a.F[k].im * a.F[k].im;  \
+    return {s, R(0)};                                                                          \
+  }                                                                                            \
+  __device__ __forceinline__ cx linner(const T &a, const T &b) {                               \
+    cx s = {0, 0}; for (int k = 0; k < N; k++) s = s + cmul(conj(a.F[k]), b.F[k]); return s;   \
+  }
+QDPJ_LOCAL(CM, 9, m)
+QDPJ_LOCAL(SP, 12, c)
+QDPJ_LOCAL(SM, 16, m)
+__device__ __forceinline__ cx lnorm2(cx a) { return {a.re * a.re + a.im * a.im, R(0)}; }
+__device__ __forceinline__ cx linner(cx a, cx b) { return cmul(conj(a), b); }
+// block sum of (v0, v1) in fp64 -> partials[2 * blockIdx.x + {0, 1}] (fixed order: deterministic)
+__device__ __forceinline__ void block_partial(double v0, double v1, double *partials) {
+  __shared__ double s0[32], s1[32];
+  for (int o = 16; o > 0; o >>= 1) {
+    v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+    v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) { s0[w] = v0; s1[w] = v1; }
+  __syncthreads();
+  if (w == 0) {
+    v0 = l < (int)(blockDim.x >> 5) ? s0[l] : 0.0;
+    v1 = l < (int)(blockDim.x >> 5) ? s1[l] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) {
+      v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+      v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+    }
+    if (l == 0) { partials[2 * blockIdx.x] = v0; partials[2 * blockIdx.x + 1] = v1; }
+  }
 }
 // DeGrand-Rossi gamma_mu (mu = 0..3) and gamma5 (4): row s has one entry, at column
 // gcol[mu][s] with phase gph[mu][s] (0: +1, 1: +i, 2: -1, 3: -i)
@@ -814,7 +896,10 @@ int generate(const char *expr, int out_kind, int prec, const int *kinds, int nop
     return QDP_EINVAL;
   }
   if (!typecheck(root.get(), kinds, nops, err)) return QDP_EINVAL;
-  const Type want = out_kind == QDP_FERMION ? T_SP : out_kind == QDP_COLORMATRIX ? T_CM : out_kind == QDP_SPINMATRIX ? T_SM : T_GAMMA;
+  const bool sum = out_kind == QDP_JIT_SUM;  // global sum of a complex-scalar expression
+  const Type want = sum ? T_CPLX
+                  : out_kind == QDP_FERMION ? T_SP : out_kind == QDP_COLORMATRIX ? T_CM : out_kind == QDP_SPINMATRIX ? T_SM
+                                                                                                            : T_GAMMA;
   if (want == T_GAMMA) {
     err = "output must be a fermion, colour matrix or spin matrix field";
     return QDP_EINVAL;
@@ -836,10 +921,16 @@ int generate(const char *expr, int out_kind, int prec, const int *kinds, int nop
   s << "// generated by qdpb jit.cu from: " << expr << "\n";
   s << (prec == QDP_F64 ? "typedef double R;\n#define QDPJ_F64 1\n" : "typedef float R;\n#define QDPJ_F64 0\n");
   s << kPrelude;
-  s << "extern \"C\" __global__ void qdp_jit_kernel(const JitArgs a) {\n"
-       "  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;\n"
-       "  if (i >= (long long)a.nblk * a.Vh) return;\n"
-       "  const int bi = (int)(i / a.Vh), cb = (int)(i - (long long)bi * a.Vh);\n"
+  if (sum)  // grid-stride loop, fp64 accumulation, one fixed-order partial per block
+    s << "extern \"C\" __global__ void qdp_jit_kernel(const JitArgs a, double *partials) {\n"
+         "  double acc_re = 0.0, acc_im = 0.0;\n"
+         "  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (long long)a.nblk * a.Vh;\n"
+         "       i += (long long)gridDim.x * blockDim.x) {\n";
+  else
+    s << "extern \"C\" __global__ void qdp_jit_kernel(const JitArgs a) {\n"
+         "  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;\n"
+         "  if (i >= (long long)a.nblk * a.Vh) return;\n";
+  s << "  const int bi = (int)(i / a.Vh), cb = (int)(i - (long long)bi * a.Vh);\n"
        "  const int p = a.nblk == 2 ? bi : a.parity;\n"
        "  int c[4];\n"
        "  {\n"
@@ -852,8 +943,13 @@ int generate(const char *expr, int out_kind, int prec, const int *kinds, int nop
        "  }\n"
        "  (void)c;\n";
   s << G.body.str();
-  const char *st = want == T_SP ? "st_sp" : want == T_CM ? "st_cm" : "st_sm";
-  s << "  " << st << "(a.out + (long long)bi * a.out_blk, a.stride, cb, " << v << ");\n}\n";
+  if (sum) {
+    s << "  acc_re += (double)" << v << ".re;\n  acc_im += (double)" << v << ".im;\n  }\n"
+      << "  block_partial(acc_re, acc_im, partials);\n}\n";
+  } else {
+    const char *st = want == T_SP ? "st_sp" : want == T_CM ? "st_cm" : "st_sm";
+    s << "  " << st << "(a.out + (long long)bi * a.out_blk, a.stride, cb, " << v << ");\n}\n";
+  }
   if (G.temps.size() > 16) {
     err = "more than 16 distinct operand displacements across the halo path";
     return QDP_EUNSUPPORTED;
@@ -862,10 +958,10 @@ int generate(const char *expr, int out_kind, int prec, const int *kinds, int nop
   g->src = s.str();
   g->flops = G.flops;
   g->shift_dims = G.shift_dims;
-  g->compulsory_all = g->compulsory_parity = type_reals(want);
+  g->compulsory_all = g->compulsory_parity = sum ? 0 : type_reals(want);
   for (const auto &f : G.distinct) g->compulsory_all += type_reals(kind_type(kinds[f.first]), kinds[f.first]);
   for (const auto &f : G.distinct_par) g->compulsory_parity += type_reals(kind_type(kinds[f[0]]), kinds[f[0]]);
-  g->table2_reals = G.table2_reals + type_reals(want);
+  g->table2_reals = G.table2_reals + (sum ? 0 : type_reals(want));
   // parity of every leaf load relative to the output site's parity
   for (const auto &kv : G.cse) {
     const std::string &k = kv.first;
@@ -967,20 +1063,32 @@ void jit_release(qdp_ctx ctx) {
   ctx->jit.clear();
 }
 
-int jit_eval(qdp_field out, const char *expr, const qdp_field *ops, int nops) {
-  qdp_ctx ctx = out->ctx;
+namespace {
+struct HostArgs {  // mirrors JitArgs of the generated prelude
+  const char *op[24];
+  char *out;
+  long long blk[24];
+  long long out_blk;
+  int all[24];
+  int L[4];
+  int Lh0, Vh, stride, parity, nblk;
+};
+
+// Generate / look up the kernel of (expr, operands, output kind, subset), materialise its halo'd
+// temporaries and fill the launch arguments (everything but the output).
+int jit_prepare(qdp_ctx ctx, const char *expr, int out_kind, int subset, int prec, const qdp_field *ops, int nops,
+                JitKernel **Kout, HostArgs *a) {
   const Geom &g = ctx->geom;
-  const int prec = out->prec;
   int kinds[QDP_JIT_MAX_OPERANDS];
   for (int k = 0; k < nops; k++) kinds[k] = ops[k]->kind;
   // cache key: expression text, operand kinds and subsets, output kind and subset, precision,
   // and the dims reached through the halo path (they decide which leaves become temporaries)
-  std::string key = std::string(expr) + "|" + std::to_string(out->kind) + "|" + std::to_string(out->subset) + "|" +
+  std::string key = std::string(expr) + "|" + std::to_string(out_kind) + "|" + std::to_string(subset) + "|" +
                     std::to_string(prec) + "|" + std::to_string(g.part);
   for (int k = 0; k < nops; k++) key += "|" + std::to_string(kinds[k]) + "/" + std::to_string(ops[k]->subset);
   Generated gen;
   std::string err;
-  int rc = generate(expr, out->kind, prec, kinds, nops, g.part, &gen, err);
+  int rc = generate(expr, out_kind, prec, kinds, nops, g.part, &gen, err);
   if (rc) return set_error(ctx, rc, "jit: %s", err.c_str());
   // operand subsets: each leaf is read at parity out_parity ^ flip; a one-parity operand must match
   for (const auto &lp : gen.leaf_disp_parity) {
@@ -988,7 +1096,7 @@ int jit_eval(qdp_field out, const char *expr, const qdp_field *ops, int nops) {
     if (is_gauge(f->kind) && f->subset != QDP_ALL)
       return set_error(ctx, QDP_EINVAL, "jit: gauge operand $%d must cover all sites", lp.first);
     if (f->subset == QDP_ALL) continue;
-    if (out->subset == QDP_ALL || (out->subset ^ lp.second) != f->subset)
+    if (subset == QDP_ALL || (subset ^ lp.second) != f->subset)
       return set_error(ctx, QDP_EINVAL, "jit: operand $%d is read on parity it does not hold", lp.first);
   }
   auto it = ctx->jit.find(key);
@@ -1021,23 +1129,12 @@ int jit_eval(qdp_field out, const char *expr, const qdp_field *ops, int nops) {
     K = it->second;
   }
 
-  struct Args {  // mirrors JitArgs of the generated prelude
-    const char *op[24];
-    char *out;
-    long long blk[24];
-    long long out_blk;
-    int all[24];
-    int L[4];
-    int Lh0, Vh, stride, parity, nblk;
-  } a;
-  memset(&a, 0, sizeof a);
+  memset(a, 0, sizeof *a);
   for (int k = 0; k < nops; k++) {
-    a.op[k] = (const char *)ops[k]->data;
-    a.all[k] = ops[k]->subset == QDP_ALL;
-    if (is_gauge(ops[k]->kind))  // one (mu, parity) block
-      a.blk[k] = (long long)parity_block_bytes(ops[k]->kind, prec, g.stride) / 4;
-    else
-      a.blk[k] = (long long)parity_block_bytes(ops[k]->kind, prec, g.stride);
+    a->op[k] = (const char *)ops[k]->data;
+    a->all[k] = ops[k]->subset == QDP_ALL;
+    // gauge: one (mu, parity) block
+    a->blk[k] = (long long)parity_block_bytes(ops[k]->kind, prec, g.stride) / (is_gauge(ops[k]->kind) ? 4 : 1);
   }
   // halo'd temporaries: operand shifted by dp, one qdp_shift per unit step (faces exchanged there)
   for (size_t j = 0; j < K->temp_leaf.size(); j++) {
@@ -1062,19 +1159,30 @@ int jit_eval(qdp_field out, const char *expr, const qdp_field *ops, int nops) {
     }
     const int slot = QDP_JIT_MAX_OPERANDS + (int)j;
     const qdp_field t = K->temp_field[j];
-    a.op[slot] = (const char *)t->data;
-    a.all[slot] = t->subset == QDP_ALL;
-    a.blk[slot] = (long long)parity_block_bytes(t->kind, prec, g.stride) / (is_gauge(t->kind) ? 4 : 1);
+    a->op[slot] = (const char *)t->data;
+    a->all[slot] = t->subset == QDP_ALL;
+    a->blk[slot] = (long long)parity_block_bytes(t->kind, prec, g.stride) / (is_gauge(t->kind) ? 4 : 1);
   }
+  for (int m = 0; m < 4; m++) a->L[m] = g.L[m];
+  a->Lh0 = g.Lh0;
+  a->Vh = g.Vh;
+  a->stride = g.stride;
+  a->nblk = subset == QDP_ALL ? 2 : 1;
+  a->parity = subset == QDP_ALL ? 0 : subset;
+  *Kout = K;
+  return QDP_OK;
+}
+}  // namespace
+
+int jit_eval(qdp_field out, const char *expr, const qdp_field *ops, int nops) {
+  qdp_ctx ctx = out->ctx;
+  JitKernel *K;
+  HostArgs a;
+  int rc = jit_prepare(ctx, expr, out->kind, out->subset, out->prec, ops, nops, &K, &a);
+  if (rc) return rc;
   a.out = (char *)out->data;
-  a.out_blk = (long long)parity_block_bytes(out->kind, prec, g.stride);
-  for (int m = 0; m < 4; m++) a.L[m] = g.L[m];
-  a.Lh0 = g.Lh0;
-  a.Vh = g.Vh;
-  a.stride = g.stride;
-  a.nblk = out->subset == QDP_ALL ? 2 : 1;
-  a.parity = out->subset == QDP_ALL ? 0 : out->subset;
-  const long sites = (long)a.nblk * g.Vh;
+  a.out_blk = (long long)parity_block_bytes(out->kind, out->prec, ctx->geom.stride);
+  const long sites = (long)a.nblk * ctx->geom.Vh;
   auto go = [&](int block) -> cudaError_t {
     if (block > K->max_threads) return cudaErrorLaunchOutOfResources;
     void *args[] = {&a};
@@ -1089,6 +1197,34 @@ int jit_eval(qdp_field out, const char *expr, const qdp_field *ops, int nops) {
     return rc;
   }
   return prof_end(ctx, &ev);
+}
+
+int jit_sum(qdp_ctx ctx, const char *expr, const qdp_field *ops, int nops, int subset, int prec, int slot) {
+  JitKernel *K;
+  HostArgs a;
+  int rc = jit_prepare(ctx, expr, QDP_JIT_SUM, subset, prec, ops, nops, &K, &a);
+  if (rc) return rc;
+  const long sites = (long)a.nblk * ctx->geom.Vh;
+  // fixed launch shape (256 threads, at most 8 blocks per SM, grid-stride): the block partials and
+  // therefore the rounding of the sum do not depend on tuning
+  const int block = 256;
+  const long want = (sites + block - 1) / block;
+  const int nb = (int)(want < 148 * 8 ? want : 148 * 8);
+  if (block > K->max_threads) return set_error(ctx, QDP_EUNSUPPORTED, "jit: sum kernel exceeds its register budget");
+  if ((rc = ensure_reduce(ctx, nb))) return rc;
+  ProfEvent ev;
+  prof_begin(ctx, QDP_PK_REDUCE, &ev);
+  prof_work(ctx, QDP_PK_REDUCE, K->flops * sites, (a.nblk == 2 ? K->bytes_all : K->bytes_parity) * sites);
+  double *partials = ctx->red_partials;
+  void *args[] = {&a, &partials};
+  cudaError_t e = cudaLaunchKernel((const void *)K->kern, dim3(nb), dim3(block), args, 0, ctx->stream);
+  if (e != cudaSuccess) {
+    prof_end(ctx, &ev);
+    return cuda_check(ctx, e, "jit sum launch");
+  }
+  if ((rc = prof_end(ctx, &ev))) return rc;
+  if ((rc = reduce_partials(ctx, nb, slot))) return rc;
+  return reduce_global(ctx, slot, 2);
 }
 
 int jit_source(const char *expr, int out_kind, int out_subset, int prec, const int *kinds, int nops, char *src,

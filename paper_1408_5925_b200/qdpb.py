@@ -78,6 +78,7 @@ _SIGS = {
     "qdp_jit_source": [ctypes.c_char_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, _ip, ctypes.c_int, ctypes.c_char_p,
                        ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t), _dp, ctypes.c_int],
     "qdp_jit_stats": [_vp, _ip, _dp],
+    "qdp_jit_sum": [_vp, ctypes.c_char_p, ctypes.POINTER(_vp), ctypes.c_int, ctypes.c_int, _dp],
     "qdp_strerror": [ctypes.c_int],
     "qdp_last_error": [_vp],
     "qdp_profile_query": [_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_long), _dp],
@@ -426,6 +427,18 @@ def qdp_jit_eval(out: Field, expr: str, *operands: Field) -> None:
     """out = expr($0, $1, ...) on out's subset: one generated kernel (include/qdpb.h, PAPER.md III-IV)."""
     arr = (_vp * max(1, len(operands)))(*[f.ptr for f in operands])
     _check(lib().qdp_jit_eval(out, expr.encode(), arr, len(operands)), out.ctx)
+
+
+def qdp_jit_sum(ctx: Ctx, expr: str, *operands: Field, subset: int = QDP_ALL) -> complex:
+    """Global sum over `subset` of a complex-scalar site expression (trace / localNorm2 /
+    localInnerProduct / real; include/qdpb.h)."""
+    arr = (_vp * max(1, len(operands)))(*[f.ptr for f in operands])
+    v = (ctypes.c_double * 2)()
+    _check(lib().qdp_jit_sum(ctx, expr.encode(), arr, len(operands), int(subset), v), ctx)
+    return complex(v[0], v[1])
+
+
+QDP_JIT_SUM = -1
 
 
 def qdp_jit_source(expr: str, out_kind: int, prec: int, operand_kinds, compile: bool = False, out_subset: int = -1):

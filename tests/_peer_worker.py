@@ -177,7 +177,22 @@ def _run(rank, world, case, G, P):
             fig1 = _gather(q.qdp_field_export(fo), G, P, (4, 3, 2))
             q.qdp_jit_eval(fo, "shift(shift($0,2,-1),3,+1)", fp)
             diag = _gather(q.qdp_field_export(fo), G, P, (4, 3, 2))
+            # global sums of site expressions: the plaquette across rank boundaries, identical on every rank
+            plaq = "real(trace($0[2]*shift($0[3],2,+1)*adj(shift($0[2],3,+1))*adj($0[3])))"
+            pv = q.qdp_jit_sum(c, plaq, fU)
+            nv = q.qdp_jit_sum(c, "localNorm2($0)", fp)
+            _same_on_all_ranks((pv, nv))
             if rank == 0:
+                Uc = U[..., 0] + 1j * U[..., 1]
+                sh = lambda a, mu: oracle.shift(a, G, mu, 1)
+                Un = sh(U, 2)[:, 3]
+                Un = Un[..., 0] + 1j * Un[..., 1]
+                Um = sh(U, 3)[:, 2]
+                Um = Um[..., 0] + 1j * Um[..., 1]
+                H = lambda m: np.conj(np.swapaxes(m, 1, 2))
+                ref = np.sum(np.trace(Uc[:, 2] @ Un @ H(Um) @ H(Uc[:, 3]), axis1=1, axis2=2).real)
+                assert abs(pv.real - ref) <= 1e-12 * 3 * np.prod(G)
+                assert abs(nv.real - oracle.norm2(psi, G)) <= 1e-13 * nv.real
                 assert rel_site_err(got, oracle.hopping(U, psi, G, -1)) <= 1e-13
                 ref = (oracle.upsi(U[:, 3], oracle.shift(psi, G, 3, 1))
                        + oracle.shift(oracle.adj_upsi(U[:, 3], psi), G, 3, -1))

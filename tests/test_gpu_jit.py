@@ -282,3 +282,66 @@ def test_cache_accounting_and_errors(q):
             assert _err(q.qdp_field_export(oe), ref) <= 1e-13, mask
         finally:
             q.qdp_finalize(c)
+
+
+def _plaq_ref(U, L, mu, nu):
+    """sum_x Re tr U_mu(x) U_nu(x+mu) U_mu(x+nu)^dag U_nu(x)^dag from the oracle's products and shifts"""
+    Umu, Unu = U[:, mu], U[:, nu]
+    adj = lambda m: _re(np.conj(np.swapaxes(_cx(m), 1, 2)))
+    t = oracle.lcm(oracle.lcm(Umu, oracle.shift(Unu, L, mu, 1)), adj(oracle.shift(Umu, L, nu, 1)))
+    t = oracle.lcm(t, adj(Unu))
+    return float(np.sum(np.trace(_cx(t), axis1=1, axis2=2).real))
+
+
+def plaq_expr(mu, nu):
+    return f"real(trace($0[{mu}]*shift($0[{nu}],{mu},+1)*adj(shift($0[{mu}],{nu},+1))*adj($0[{nu}])))"
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+def test_sums_plaquette_norms(q, prec):
+    """qdp_jit_sum: the plaquette (QDP++ sum(real(trace(...))) over shifted links) against the
+    oracle's products / shifts, its closed form on the unit gauge field (3 per site) and its gauge
+    invariance; localNorm2 / localInnerProduct sums against the oracle's norm2 / inner, exact on
+    integer-valued inputs; determinism."""
+    from _physics import gauge_transform
+    L = (4, 6, 4, 8)
+    V = fieldgen.volume(L)
+    U = _round(fieldgen.random_gauge(L, 71), prec)
+    c = q.qdp_init(L)
+    try:
+        fU = _field(q, c, q.QDP_GAUGE, prec, -1, U)
+        tol = 1e-12 if prec == 0 else 1e-5
+        for mu, nu in ((0, 1), (2, 3), (1, 3)):
+            got = q.qdp_jit_sum(c, plaq_expr(mu, nu), fU)
+            ref = _plaq_ref(U, L, mu, nu)
+            assert abs(got.real - ref) <= tol * 3 * V and got.imag == 0.0, (mu, nu, got, ref)
+            assert q.qdp_jit_sum(c, plaq_expr(mu, nu), fU) == got  # deterministic
+            # even + odd = all
+            e = q.qdp_jit_sum(c, plaq_expr(mu, nu), fU, subset=0)
+            o = q.qdp_jit_sum(c, plaq_expr(mu, nu), fU, subset=1)
+            assert abs(e.real + o.real - got.real) <= tol * 3 * V
+        # gauge invariance: U_mu(x) -> g(x) U_mu(x) g(x+mu)^dag leaves the plaquette unchanged
+        Ug = _round(gauge_transform(U, fieldgen.random_gauge_transform(L, 72), L), prec)
+        fUg = _field(q, c, q.QDP_GAUGE, prec, -1, Ug)
+        assert abs(q.qdp_jit_sum(c, plaq_expr(0, 3), fUg).real - q.qdp_jit_sum(c, plaq_expr(0, 3), fU).real) \
+            <= (1e-11 if prec == 0 else 1e-4) * 3 * V
+        # unit gauge field: exactly 3 per site
+        f1 = _field(q, c, q.QDP_GAUGE, prec, -1, fieldgen.unit_gauge(L))
+        assert q.qdp_jit_sum(c, plaq_expr(1, 2), f1) == complex(3 * V, 0)
+        # norms and inner products: integer-valued spinors give exact sums
+        a = np.round(4 * fieldgen.random_spinor(L, 73))
+        b = np.round(4 * fieldgen.random_spinor(L, 74))
+        fa, fb = _field(q, c, q.QDP_FERMION, prec, -1, a), _field(q, c, q.QDP_FERMION, prec, -1, b)
+        assert q.qdp_jit_sum(c, "localNorm2($0)", fa) == complex(oracle.norm2(a, L), 0)
+        assert q.qdp_jit_sum(c, "localInnerProduct($0, $1)", fa, fb) == oracle.inner(a, b, L)
+        for sub in (0, 1):
+            assert q.qdp_jit_sum(c, "localNorm2($0)", fa, subset=sub) == complex(oracle.norm2(a, L, sub), 0)
+        # complex-scalar algebra: <a, b> + i |a|^2 - 2 tr(U_0)
+        ref = oracle.inner(a, b, L) + 1j * oracle.norm2(a, L) - 2 * np.sum(np.trace(_cx(U[:, 0]), axis1=1, axis2=2))
+        got = q.qdp_jit_sum(c, "localInnerProduct($0,$1) + timesI(localNorm2($0)) - 2*trace($2[0])", fa, fb, fU)
+        assert abs(got - ref) <= (1e-12 if prec == 0 else 1e-5) * abs(ref)
+        with pytest.raises(q.QdpError) as e:
+            q.qdp_jit_sum(c, "$0", fa)
+        assert e.value.status == q.QDP_EINVAL
+    finally:
+        q.qdp_finalize(c)

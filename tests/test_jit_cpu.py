@@ -92,3 +92,21 @@ def test_nvrtc_compiles_for_sm100a(q, prec):
                             ("gamma5*$0*adj($0)", q.QDP_SPINMATRIX, [q.QDP_SPINMATRIX])]:
         src, _ = q.qdp_jit_source(expr, ok, prec, kinds, compile=True)
         assert "qdp_jit_kernel" in src
+
+
+def test_sum_expressions(q):
+    """Complex-scalar expressions for qdp_jit_sum: the plaquette executes 3 colour products (594)
+    + a trace (4); local norms / inner products count like the BLAS kernels (48 / 96 per spinor)."""
+    G, F = q.QDP_GAUGE, q.QDP_FERMION
+    plaq = "real(trace($0[0]*shift($0[1],0,+1)*adj(shift($0[0],1,+1))*adj($0[1])))"
+    _, w = q.qdp_jit_source(plaq, q.QDP_JIT_SUM, q.QDP_F64, [G])
+    assert w["flops"] == 3 * 198 + 4
+    _, w = q.qdp_jit_source("localNorm2($0)", q.QDP_JIT_SUM, q.QDP_F64, [F])
+    assert w["flops"] == 48 and w["bytes"] == 192
+    _, w = q.qdp_jit_source("localInnerProduct($0,$1)", q.QDP_JIT_SUM, q.QDP_F32, [F, F], compile=True)
+    assert w["flops"] == 96 and w["bytes"] == 192
+    for bad, msg in [("$0", "complex scalar"), ("trace($0)", "trace needs"), ("localInnerProduct($0)", "two arguments"),
+                     ("real($0)", "real needs")]:
+        with pytest.raises(q.QdpError) as e:
+            q.qdp_jit_source(bad, q.QDP_JIT_SUM, q.QDP_F64, [F])
+        assert msg in str(e.value), bad
