@@ -142,6 +142,9 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     import oracle
+    # the other ranks exit without work, so rank 0 has the host's cores (torchrun sets
+    # OMP_NUM_THREADS=1 per rank, which would otherwise pin the oracle to one thread)
+    oracle.set_threads(len(os.sched_getaffinity(0)))
     L = LOCAL
     Vh = L[0] * L[1] * L[2] * L[3] // 2
     U, b = gen_fields(L, 0)
