@@ -345,9 +345,12 @@ def run_native(args, rank, world, local_rank):
         f_d, b_d = q.qdp_profile_work(ctx, q.QDP_PK_DSLASH)
         q.qdp_set_option(ctx, q.QDP_OPT_PROFILE, 0)
         t_d = ms_d / n_d * 1e-3
-        dsl[tag] = {"us_per_launch": t_d * 1e6, "gflops_per_gpu": f_d / n_d / t_d * 1e-9,
+        eff = 2880 if prec == q.QDP_F64 else 1440  # Table II convention: every leaf load, no reuse (R17)
+        dsl[tag] = {"us_per_launch": t_d * 1e6, "gsites_per_s": Vh / t_d * 1e-9, "gflops_per_gpu": f_d / n_d / t_d * 1e-9,
                     "gbs_compulsory_per_gpu": b_d / n_d / t_d * 1e-9, "bytes_per_site": b_d / n_d / Vh,
-                    "frac_of_measured_hbm": b_d / n_d / t_d * 1e-9 / measured_peak()[0]}
+                    "gbs_effective_per_gpu": eff * Vh / t_d * 1e-9,
+                    "frac_of_measured_hbm": b_d / n_d / t_d * 1e-9 / measured_peak()[0],
+                    "frac_of_8TBs": b_d / n_d / t_d * 1e-9 / 8000.0}
         # the same operator generated at run time from its expression (qdp_jit_eval; PAPER.md
         # sections III-IV): the paper's generated-vs-hand-tuned comparison
         if world == 1:
