@@ -150,6 +150,13 @@ struct Parser {
     return a;
   }
   NodeP term() {
+    if (eat('-')) {  // a leading minus negates the whole product: -gamma(mu)*a = -(gamma(mu)*a)
+      NodeP t = term();
+      if (!t) return nullptr;
+      NodeP n = make(N_NEG);
+      n->kid.push_back(std::move(t));
+      return n;
+    }
     NodeP a = unary();
     while (a && eat('*')) {
       NodeP b = unary();
@@ -432,12 +439,93 @@ struct Gen {
     for (auto &k : n->kid) collect(k.get(), d);
   }
 
-  // n = A - gamma(mu)*A or A + gamma(mu)*A with A a spinor (same text at the same site)
-  static bool is_projector(const Node *n, const int d[4]) {
-    if ((n->op != N_ADD && n->op != N_SUB) || n->type != T_SP) return false;
-    const Node *g = n->kid[1].get();
-    if (g->op != N_MUL || g->kid[0]->op != N_GAMMA || g->kid[0]->mu > 3) return false;
-    return key(n->kid[0].get(), d) == key(g->kid[1].get(), d);
+  // A spinor sum is flattened into signed terms; a term A and a term gamma(mu)*A (same text at the
+  // same site, any grouping or order) combine into s (1 + S gamma_mu) A: spin projection.
+  // When A is, after its shifts, a colour matrix times a spinor, the projector commutes with the
+  // colour product, so it is applied first and U multiplies a half spinor: 12 + 132 flop instead of
+  // 264 + 24.  The remaining terms are added in their written order.
+  static void flatten(const Node *n, int sign, std::vector<std::pair<const Node *, int>> &terms) {
+    if ((n->op == N_ADD || n->op == N_SUB) && n->type == T_SP) {
+      flatten(n->kid[0].get(), sign, terms);
+      flatten(n->kid[1].get(), n->op == N_ADD ? sign : -sign, terms);
+    } else if (n->op == N_NEG && n->type == T_SP) {
+      flatten(n->kid[0].get(), -sign, terms);
+    } else {
+      terms.push_back({n, sign});
+    }
+  }
+  static bool gamma_term(const Node *n) {
+    return n->op == N_MUL && n->kid[0]->op == N_GAMMA && n->kid[0]->mu <= 3;
+  }
+  std::string emit_projector(const Node *A, int mu, int S, const int d[4]) {
+    const Node *x = A;
+    int e[4] = {d[0], d[1], d[2], d[3]};
+    while (x->op == N_SHIFT) {
+      e[x->mu] += x->sign;
+      shift_dims.insert(x->mu);
+      x = x->kid[0].get();
+    }
+    const std::string tmpl = "<" + std::to_string(mu) + ", " + std::to_string(S) + ">";
+    const std::string v = fresh();
+    if (x->op == N_MUL && x->kid[0]->type == T_CM && x->kid[1]->type == T_SP) {
+      const std::string u = emit(x->kid[0].get(), e), sp = emit(x->kid[1].get(), e);
+      body << "  const SP " << v << " = recon" << tmpl << "(mul(" << u << ", proj" << tmpl << "(" << sp << ")));\n";
+      flops += 12 + 2 * (9 * 6 + 6 * 2);
+    } else {
+      const std::string a = emit(A, d);
+      body << "  const SP " << v << " = recon" << tmpl << "(proj" << tmpl << "(" << a << "));\n";
+      flops += 12;
+    }
+    return v;
+  }
+  std::string emit_spinor_sum(const Node *n, const int d[4]) {
+    std::vector<std::pair<const Node *, int>> terms;
+    flatten(n, 1, terms);
+    std::vector<int> used(terms.size(), 0);
+    // accumulate as the terms are produced (written order), so only the running sum and the term
+    // at hand are live
+    std::string acc;
+    auto accumulate = [&](const std::string &val, int sign) {
+      if (acc.empty()) {
+        if (sign > 0) {
+          acc = val;
+        } else {
+          acc = fresh();
+          body << "  const SP " << acc << " = neg(" << val << ");\n";
+        }
+        return;
+      }
+      const std::string v = fresh();
+      body << "  const SP " << v << " = " << (sign > 0 ? "add(" : "sub(") << acc << ", " << val << ");\n";
+      flops += 24;
+      acc = v;
+    };
+    for (size_t i = 0; i < terms.size(); i++) {
+      if (used[i]) continue;
+      const Node *t = terms[i].first;
+      // pair this term with a partner: t = A and a later gamma(mu)*A, or t = gamma(mu)*A and a later A
+      size_t j = terms.size();
+      int mu = -1;
+      const Node *A = nullptr;
+      for (size_t k = i + 1; k < terms.size() && j == terms.size(); k++) {
+        if (used[k]) continue;
+        const Node *u = terms[k].first;
+        if (gamma_term(u) && !gamma_term(t) && key(u->kid[1].get(), d) == key(t, d)) {
+          j = k; mu = u->kid[0]->mu; A = t;
+        } else if (gamma_term(t) && !gamma_term(u) && key(t->kid[1].get(), d) == key(u, d)) {
+          j = k; mu = t->kid[0]->mu; A = u;
+        }
+      }
+      if (j < terms.size()) {
+        used[j] = 1;
+        const int sA = A == t ? terms[i].second : terms[j].second;  // sign of A
+        const int sG = A == t ? terms[j].second : terms[i].second;  // sign of gamma(mu)*A
+        accumulate(emit_projector(A, mu, sA * sG, d), sA);
+      } else {
+        accumulate(emit(t, d), terms[i].second);
+      }
+    }
+    return acc;
   }
 
   // emit n at displacement d; returns the C++ expression naming its value
@@ -481,29 +569,8 @@ struct Gen {
       const bool stream = reuse.count({n->leaf, n->mu, flip(d)}) == 0;
       body << "  const " << ctype(n->type) << " " << v << " = " << ld << (stream ? "<true>(" : "<false>(") << base
            << ", a.stride, cb" << s << ");\n";
-    } else if (is_projector(n, d)) {
-      // A -/+ gamma(mu)*A = (1 -/+ gamma_mu) A: spin projection.  When A is (after
-      // shifts) a colour matrix times a spinor, the projector commutes with the colour product, so
-      // it is applied first and U multiplies a half spinor: 12 + 132 flop instead of 264 + 24.
-      const int mu = n->kid[1]->kid[0]->mu, S = n->op == N_ADD ? 1 : -1;
-      const Node *x = n->kid[0].get();
-      int e[4] = {d[0], d[1], d[2], d[3]};
-      while (x->op == N_SHIFT) {
-        e[x->mu] += x->sign;
-        shift_dims.insert(x->mu);
-        x = x->kid[0].get();
-      }
-      const std::string tmpl = "<" + std::to_string(mu) + ", " + std::to_string(S) + ">";
-      v = fresh();
-      if (x->op == N_MUL && x->kid[0]->type == T_CM && x->kid[1]->type == T_SP) {
-        const std::string u = emit(x->kid[0].get(), e), sp = emit(x->kid[1].get(), e);
-        body << "  const SP " << v << " = recon" << tmpl << "(mul(" << u << ", proj" << tmpl << "(" << sp << ")));\n";
-        flops += 12 + 2 * (9 * 6 + 6 * 2);
-      } else {
-        const std::string a = emit(n->kid[0].get(), d);
-        body << "  const SP " << v << " = recon" << tmpl << "(proj" << tmpl << "(" << a << "));\n";
-        flops += 12;
-      }
+    } else if ((n->op == N_ADD || n->op == N_SUB) && n->type == T_SP) {
+      v = emit_spinor_sum(n, d);
     } else if (n->op == N_MUL && n->kid[0]->op == N_GAMMA) {
       const std::string x = emit(n->kid[1].get(), d);
       v = fresh();

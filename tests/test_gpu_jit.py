@@ -204,9 +204,15 @@ def test_hopping_expression_vs_oracle(q, prec, L, gauge_kind):
         out = q.qdp_field_alloc(c, q.QDP_FERMION, prec, -1)
         ref = oracle.hopping(U, psi, L, -1)
         tol = TOL[prec]
-        for grouped in (True, False):  # spin-projected and literal forms
+        for grouped in (True, False):  # grouped and left-associated forms (both spin-projected)
             q.qdp_jit_eval(out, hopping_expr(grouped=grouped), fU, fp)
             assert _err(q.qdp_field_export(out), ref) <= tol, grouped
+        # the literal sum (no projection): "1*(A)" is not the same text as A, so no term pairs up
+        lit = " + ".join(f"(1*($0[{m}]*shift($1,{m},+1)) - gamma({m})*($0[{m}]*shift($1,{m},+1)))"
+                         f" + (1*shift(adj($0[{m}])*$1,{m},-1) + gamma({m})*shift(adj($0[{m}])*$1,{m},-1))"
+                         for m in range(4))
+        q.qdp_jit_eval(out, lit, fU, fp)
+        assert _err(q.qdp_field_export(out), ref) <= tol
         # even-odd: out_e = H_eo psi_o, compared with the fused kernel too
         even, odd = fieldgen.cb_sites(L, 0), fieldgen.cb_sites(L, 1)
         fo = _field(q, c, q.QDP_FERMION, prec, 1, psi[odd])

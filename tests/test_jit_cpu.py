@@ -39,19 +39,28 @@ def test_table2_accounting_matches_paper(q):
 
 
 def test_hopping_expression_work(q):
-    """Grouped (1 -/+ gamma_mu)(U psi) terms become spin projections: 8 x (12 projection + 132
-    U x half spinor) + 7 x 24 accumulation = 1320 flop/site, exactly the standard hopping-term count
-    of the hand-written kernel.  Ungrouped, the left-associated sum only
-    matches the pattern for its first term (144 flop); CSE forms the other 7 U*psi products once
-    (7 x 264) and 14 spinor additions remain (14 x 24).  Compulsory bytes per EO output site =
-    the dslash's 1536 (8 links, input, output); for a full-lattice output each field is read once:
-    4 links + input + output."""
+    """A spinor sum is flattened and every pair of terms A, +-gamma_mu A (any grouping, order or
+    sign) becomes a spin projection: 8 x (12 projection + 132 U x half spinor) + 7 x 24 accumulation
+    = 1320 flop/site, exactly the standard hopping-term count of the hand-written kernel (DESIGN.md
+    section 7).  Compulsory bytes per EO output site = the dslash's 1536 (8 links, input, output);
+    for a full-lattice output each field is read once: 4 links + input + output."""
     G, F = q.QDP_GAUGE, q.QDP_FERMION
-    _, w = q.qdp_jit_source(hopping_expr(), F, q.QDP_F64, [G, F], out_subset=0)
-    assert w["flops"] == 8 * (12 + 132) + 7 * 24 == 1320
-    _, w = q.qdp_jit_source(hopping_expr(grouped=False), F, q.QDP_F64, [G, F], out_subset=0)
-    assert w["flops"] == 144 + 7 * 264 + 14 * 24
-    assert w["bytes"] == 1536
+    for grouped in (True, False):
+        _, w = q.qdp_jit_source(hopping_expr(grouped), F, q.QDP_F64, [G, F], out_subset=0)
+        assert w["flops"] == 8 * (12 + 132) + 7 * 24 == 1320
+        assert w["bytes"] == 1536
+    # order and sign do not matter: gamma term first, negated pairs
+    f = "$0[0]*shift($1,0,+1)"
+    for e, fl in ((f"-gamma(0)*({f}) + {f}", 144), (f"-({f}) + gamma(0)*({f})", 144),
+                  (f"{f} - $1 - gamma(0)*({f})", 144 + 24)):
+        _, w = q.qdp_jit_source(e, F, q.QDP_F64, [G, F])
+        assert w["flops"] == fl, e
+    # any gamma_mu pairs with any A, e.g. (1 - gamma_y) applied to an x-hop
+    _, w = q.qdp_jit_source(f"{f} - gamma(1)*({f})", F, q.QDP_F64, [G, F])
+    assert w["flops"] == 144
+    # no partner (the gamma term's operand is 2A, not A): literal product, scale and subtraction
+    _, w = q.qdp_jit_source(f"{f} - gamma(1)*(2*({f}))", F, q.QDP_F64, [G, F])
+    assert w["flops"] == 264 + 24 + 24
     _, w = q.qdp_jit_source(hopping_expr(), F, q.QDP_F64, [G, F], out_subset=-1)
     assert w["bytes"] == (4 * 18 + 24 + 24) * 8
     _, w = q.qdp_jit_source(hopping_expr(), F, q.QDP_F32, [q.QDP_GAUGE12, F], out_subset=1)
