@@ -164,6 +164,12 @@ template <typename R, int REC = 18> struct KParams {
   const unsigned *war[4][2], *ready[4][2];
   unsigned *err;
   unsigned seq;
+  // fused t boundary (peer-to-peer, only t partitioned): the main kernel visits the interior
+  // sites first and the two t-face slabs last; the blocks holding face sites acquire the ghosts,
+  // add the remote t hops themselves (no exterior kernel, no read-modify-write of the output)
+  // and the last of them acknowledges the senders
+  int fuse_t;
+  int fuse_npack;  // fused t boundary: leading blocks that pack the t faces (64-thread blocks)
 };
 
 template <typename R, int MU, typename KP>
@@ -258,10 +264,90 @@ __device__ __forceinline__ void dot_block_partial(double v, double *part) {
 
 // Whole-lattice (HALO=false) or interior (HALO=true: remote hops skipped) kernel.
 // DOT: also accumulate Re<dot, out> per block into dot_part (fused inner product).
+// Face packing for dim mu: input psi has parity q = 1 - p.
+//   f <  faceVh: my sites at x_mu = 0      -> P^- psi          -> dst[mu][0] (the -mu neighbour's forward ghost)
+//   f >= faceVh: my sites at x_mu = L-1    -> U_mu^dag P^+ psi  -> dst[mu][1] (the +mu neighbour's backward ghost)
+template <typename R, int REC, bool G5IN, typename KP>
+__device__ __forceinline__ void pack_site(const Geom &g, const KP &P, int mu, int f) {
+  const int n = g.faceVh[mu];
+  if (f >= 2 * n) return;
+  const int q = 1 - P.parity;
+  const bool fwd = f >= n;
+  if (fwd) f -= n;
+  int c[4];
+  face_coords(g, mu, fwd ? g.L[mu] - 1 : 0, f, q, c);
+  const int cb = coords_cb(g, c);
+  Spinor<R> s = P.psi.load(cb);
+  if (G5IN) g5(s);
+  Half<R> h;
+  if (!fwd) {
+    switch (mu) {
+      case 0: h = project<0, -1>(s); break;
+      case 1: h = project<1, -1>(s); break;
+      case 2: h = project<2, -1>(s); break;
+      default: h = project<3, -1>(s); break;
+    }
+    HalfGhost<R>::store(P.dst[mu][0], n, f, h);
+  } else {
+    switch (mu) {
+      case 0: h = project<0, +1>(s); break;
+      case 1: h = project<1, +1>(s); break;
+      case 2: h = project<2, +1>(s); break;
+      default: h = project<3, +1>(s); break;
+    }
+    Link<R> u = P.U.load(mu, q, cb);
+    HalfGhost<R>::store(P.dst[mu][1], n, f, mul_link_dag(u, h));
+  }
+}
+
+template <typename R, int REC, bool G5IN>
+__global__ void __launch_bounds__(128) pack_kernel(const Geom g, const KParams<R, REC> P, int mu) {
+  // peer-to-peer: the receivers must have consumed this slot (written two calls ago)
+  if (P.pack_counter[mu]) block_wait_flags(P.war[mu][0], P.war[mu][1], P.seq - 2u, P.err);
+  pack_site<R, REC, G5IN>(g, P, mu, blockIdx.x * blockDim.x + threadIdx.x);
+  // Peer-to-peer halo: the face stores above may target a neighbour's memory over NVLink.
+  // Every thread fences them at system scope; the last block to finish publishes `seq` to the
+  // two receivers' ready flags with release semantics (they acquire before reading).
+  if (P.pack_counter[mu]) grid_signal_last(P.pack_counter[mu], P.sig[mu][0], P.sig[mu][1], P.seq);
+}
+
+// last blocks of a grid segment: the final one to arrive release-stores v into f0 and f1
+__device__ __forceinline__ void blocks_signal_last(unsigned *counter, unsigned nblocks, unsigned *f0, unsigned *f1,
+                                                   unsigned v) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    const unsigned prev = atomicAdd(counter, 1u);
+    if (prev == nblocks - 1) {
+      *counter = 0u;
+      __threadfence_system();
+      st_release_sys(f0, v);
+      st_release_sys(f1, v);
+    }
+  }
+}
+
 template <typename R, int REC, int EPI, bool G5IN, bool G5OUT, bool HALO, bool DOT>
 __global__ void __launch_bounds__(QDPB_DSLASH_MAXT, (dslash_minb<R, REC>())) dslash_kernel(const Geom g, const KParams<R, REC> P) {
-  const int cb = blockIdx.x * blockDim.x + threadIdx.x;
+  int cb = blockIdx.x * blockDim.x + threadIdx.x;
   double dot = 0.0;
+  bool tface = false;  // fused t boundary: this block holds face sites
+  if (HALO && P.fuse_t) {
+    // leading blocks: pack the t faces into the neighbours' ghost slots (as pack_kernel)
+    if ((int)blockIdx.x < P.fuse_npack) {
+      block_wait_flags(P.war[3][0], P.war[3][1], P.seq - 2u, P.err);
+      pack_site<R, REC, G5IN>(g, P, 3, cb);
+      blocks_signal_last(P.pack_counter[3], P.fuse_npack, P.sig[3][0], P.sig[3][1], P.seq);
+      if (DOT) dot_block_partial(0.0, P.dot_part);
+      return;
+    }
+    cb -= P.fuse_npack * blockDim.x;
+    // then the interior sites [F, Vh - F), then the t = 0 slab [0, F) and the t = L-1 slab [Vh - F, Vh)
+    const int F = g.faceVh[3], nin = g.Vh - 2 * F;
+    tface = (int)((blockIdx.x - P.fuse_npack + 1) * blockDim.x) > nin;
+    if (tface) block_wait_flags(P.ready[3][0], P.ready[3][1], P.seq, P.err);
+    cb = cb < nin ? F + cb : (cb - nin < F ? cb - nin : cb);
+  }
   if (cb < g.Vh) {
     const int p = P.parity;
     int c[4];
@@ -283,6 +369,15 @@ __global__ void __launch_bounds__(QDPB_DSLASH_MAXT, (dslash_minb<R, REC>())) dsl
     hop_dir<R, 1>(g, P, c, cb, p, G5IN, HALO, acc);
     hop_dir<R, 2>(g, P, c, cb, p, G5IN, HALO, acc);
     hop_dir<R, 3>(g, P, c, cb, p, G5IN, HALO, acc);
+    if (HALO && P.fuse_t && (c[3] == 0 || c[3] == g.L[3] - 1)) {
+      // the remote t hop from the ghost the neighbour stored (fused exterior)
+      const int n = g.faceVh[3], f = face_index(g, 3, c);
+      if (c[3] == g.L[3] - 1) {
+        const Half<R> h = HalfGhost<R>::load(P.ghost[3][1], n, f);
+        accum_recon<3, -1>(acc, mul_link(P.U.load(3, p, cb), h));
+      }
+      if (c[3] == 0) accum_recon<3, +1>(acc, HalfGhost<R>::load(P.ghost[3][0], n, f));
+    }
     Spinor<R> o = epilogue<R, EPI>(P, cb, acc, G5OUT);
     if (DOT) {
       // fused Re<d, out> (and out += dot_shift d: the base shift of the multi-shift CG)
@@ -298,50 +393,10 @@ __global__ void __launch_bounds__(QDPB_DSLASH_MAXT, (dslash_minb<R, REC>())) dsl
     }
   }
   if (DOT) dot_block_partial(dot, P.dot_part);
-}
-
-// Face packing for dim MU: input psi has parity q = 1 - p.
-//   f <  faceVh: my sites at x_mu = 0      -> P^- psi          -> dst[mu][0] (the -mu neighbour's forward ghost)
-//   f >= faceVh: my sites at x_mu = L-1    -> U_mu^dag P^+ psi  -> dst[mu][1] (the +mu neighbour's backward ghost)
-template <typename R, int REC, bool G5IN>
-__global__ void __launch_bounds__(128) pack_kernel(const Geom g, const KParams<R, REC> P, int mu) {
-  const int n = g.faceVh[mu];
-  int f = blockIdx.x * blockDim.x + threadIdx.x;
-  // peer-to-peer: the receivers must have consumed this slot (written two calls ago)
-  if (P.pack_counter[mu]) block_wait_flags(P.war[mu][0], P.war[mu][1], P.seq - 2u, P.err);
-  if (f < 2 * n) {
-    const int q = 1 - P.parity;
-    const bool fwd = f >= n;
-    if (fwd) f -= n;
-    int c[4];
-    face_coords(g, mu, fwd ? g.L[mu] - 1 : 0, f, q, c);
-    const int cb = coords_cb(g, c);
-    Spinor<R> s = P.psi.load(cb);
-    if (G5IN) g5(s);
-    Half<R> h;
-    if (!fwd) {
-      switch (mu) {
-        case 0: h = project<0, -1>(s); break;
-        case 1: h = project<1, -1>(s); break;
-        case 2: h = project<2, -1>(s); break;
-        default: h = project<3, -1>(s); break;
-      }
-      HalfGhost<R>::store(P.dst[mu][0], n, f, h);
-    } else {
-      switch (mu) {
-        case 0: h = project<0, +1>(s); break;
-        case 1: h = project<1, +1>(s); break;
-        case 2: h = project<2, +1>(s); break;
-        default: h = project<3, +1>(s); break;
-      }
-      Link<R> u = P.U.load(mu, q, cb);
-      HalfGhost<R>::store(P.dst[mu][1], n, f, mul_link_dag(u, h));
-    }
+  if (HALO && P.fuse_t && tface) {  // the last face block tells both senders their slot was consumed
+    const unsigned first = (unsigned)(P.fuse_npack + (g.Vh - 2 * g.faceVh[3]) / (int)blockDim.x);
+    blocks_signal_last(P.ext_counter[3], gridDim.x - first, P.ack_to[3][0], P.ack_to[3][1], P.seq);
   }
-  // Peer-to-peer halo: the face stores above may target a neighbour's memory over NVLink.
-  // Every thread fences them at system scope; the last block to finish publishes `seq` to the
-  // two receivers' ready flags with release semantics (they acquire before reading).
-  if (P.pack_counter[mu]) grid_signal_last(P.pack_counter[mu], P.sig[mu][0], P.sig[mu][1], P.seq);
 }
 
 // Exterior: add the remote hops of dim mu for the output sites on its two faces.  With DOT,
@@ -412,7 +467,8 @@ template <> CloverView<float> cview<float>(const void *p, int stride) { return {
 template <typename R, int REC, int EPI, bool G5IN, bool G5OUT, bool HALO, bool DOT>
 static void launch_main(qdp_ctx ctx, const KParams<R, REC> &P, int block) {
   const Geom &g = ctx->geom;
-  dslash_kernel<R, REC, EPI, G5IN, G5OUT, HALO, DOT><<<grid_for(g.Vh, block), block, 0, ctx->stream>>>(g, P);
+  dslash_kernel<R, REC, EPI, G5IN, G5OUT, HALO, DOT>
+      <<<grid_for(g.Vh, block) + P.fuse_npack, block, 0, ctx->stream>>>(g, P);
 }
 
 template <typename R, int REC, int EPI>
@@ -497,12 +553,17 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
   int rc;
   if (dot && !(a.epi == EPI_XPAY || a.epi == EPI_CLOVXPAY) ) return set_error(ctx, QDP_EINVAL, "fused dot: XPAY epilogues only");
   if (dot && (a.g5_in || !a.g5_out)) return set_error(ctx, QDP_EINVAL, "fused dot: Mhat^dag output step only");
+  // peer-to-peer with only t partitioned: the main kernel adds the remote t hops itself
+  // (KParams::fuse_t); QDPB_FUSE_T=0 restores the separate exterior kernel (comparison)
+  static const bool fuse_env = !(getenv("QDPB_FUSE_T") && atoi(getenv("QDPB_FUSE_T")) == 0);
+  const bool fuse_t = halo && ctx->p2p_on && g.part == 8 && fuse_env;
   // partial-sum layout of the fused inner product: interior blocks, then each exterior's blocks
   int nparts = 0, ext_off[4] = {0, 0, 0, 0};
+  const int npack = fuse_t ? grid_for(2 * g.faceVh[3], block) : 0;
   if (dot) {
-    nparts = grid_for(g.Vh, block);
+    nparts = grid_for(g.Vh, block) + npack;
     for (int mu = 0; mu < 4; mu++)
-      if ((g.part >> mu) & 1) {
+      if (((g.part >> mu) & 1) && !fuse_t) {
         ext_off[mu] = nparts;
         nparts += grid_for(2 * g.faceVh[mu], 128);
       }
@@ -532,6 +593,8 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
     }
     P.err = L.err;
     P.seq = seq;
+    P.fuse_t = fuse_t ? 1 : 0;
+    P.fuse_npack = npack;
   }
   if (halo) {
     bool any_comm = false;
@@ -553,6 +616,10 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
     }
     for (int mu = 0; mu < 4; mu++) {
       if (!((g.part >> mu) & 1)) continue;
+      if (fuse_t) {  // packed by the leading blocks of the main kernel: bytes only, no launch
+        prof_work(ctx, QDP_PK_DSLASH, 0.0, (double)g.faceVh[mu] * (24 + 12 + 24 + REC + 12) * sizeof(R));
+        continue;
+      }
       ProfEvent ev;
       prof_begin(ctx, QDP_PK_PACK, &ev);
       // compulsory: psi read on both faces, the forward face's link, the half spinors written
@@ -576,7 +643,7 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
     if ((rc = launch_main_epi<R, REC>(ctx, a, P, true, block))) return rc;
     if (overlap) QDP_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_comm, 0));
     for (int mu = 0; mu < 4; mu++) {
-      if (!((g.part >> mu) & 1)) continue;
+      if (!((g.part >> mu) & 1) || fuse_t) continue;
       ProfEvent ev;
       prof_begin(ctx, QDP_PK_DSLASH_EXT, &ev);
       // ghost read, forward-face link, output read-modify-write (+ clover on CLOVINV)

@@ -53,7 +53,12 @@ def test_dslash_p2p_self(q, prec, mask):
             got = q.qdp_field_export(fo).astype(np.float64)
             assert rel_site_err(got, ref) <= (1e-13 if prec == 0 else 2e-6)
         n_pack, _ = q.qdp_profile_query(c, q.QDP_PK_PACK)
-        assert n_pack == 10 * bin(mask).count("1")
+        n_ext, _ = q.qdp_profile_query(c, q.QDP_PK_DSLASH_EXT)
+        n_main, _ = q.qdp_profile_query(c, q.QDP_PK_DSLASH)
+        if mask == 8:  # t only: packing, interior and the remote t hops in ONE kernel per EO dslash
+            assert (n_pack, n_ext, n_main) == (0, 0, 10)
+        else:
+            assert n_pack == 10 * bin(mask).count("1") and n_ext == n_pack and n_main == 10
     finally:
         q.qdp_finalize(c)
 
