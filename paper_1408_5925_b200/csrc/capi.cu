@@ -292,6 +292,8 @@ extern "C" int qdp_finalize(qdp_ctx c) {
   resolve_profile(c);
   jit_release(c);
   tune_release(c);
+  for (int q = 0; q < 2; q++)
+    if (c->fuse_perm[q]) cudaFree(c->fuse_perm[q]);
   p2p_destroy(c);
   peer_destroy(c);
   comm_destroy(c);

@@ -164,12 +164,16 @@ template <typename R, int REC = 18> struct KParams {
   const unsigned *war[4][2], *ready[4][2];
   unsigned *err;
   unsigned seq;
-  // fused t boundary (peer-to-peer, only t partitioned): the main kernel visits the interior
-  // sites first and the two t-face slabs last; the blocks holding face sites acquire the ghosts,
-  // add the remote t hops themselves (no exterior kernel, no read-modify-write of the output)
-  // and the last of them acknowledges the senders
-  int fuse_t;
-  int fuse_npack;  // fused t boundary: leading blocks that pack the t faces (64-thread blocks)
+  // fused boundary (peer-to-peer): leading blocks pack every partitioned face into the
+  // neighbours' ghost slots; the rest visit the output sites in the order perm -- interior sites
+  // first, sites on a partitioned face last; the blocks holding face sites acquire the ghosts, add
+  // the remote hops themselves (no exterior kernels, no read-modify-write of the output) and the
+  // last of them acknowledges the senders
+  int fuse;
+  int fuse_npack;   // leading pack blocks
+  int fuse_nin;     // interior sites: perm[0, nin) interior, perm[nin, Vh) on a partitioned face
+  const int *perm;  // visiting order of the output parity's sites (nullptr: only t partitioned)
+  int pack_off[5];  // cumulative pack threads per dim (2 faceVh for a partitioned dim, else 0)
 };
 
 template <typename R, int MU, typename KP>
@@ -311,42 +315,76 @@ __global__ void __launch_bounds__(128) pack_kernel(const Geom g, const KParams<R
   if (P.pack_counter[mu]) grid_signal_last(P.pack_counter[mu], P.sig[mu][0], P.sig[mu][1], P.seq);
 }
 
-// last blocks of a grid segment: the final one to arrive release-stores v into f0 and f1
-__device__ __forceinline__ void blocks_signal_last(unsigned *counter, unsigned nblocks, unsigned *f0, unsigned *f1,
-                                                   unsigned v) {
+// Fused boundary: of `nblocks` blocks, the last to arrive release-stores v into both flags of
+// every partitioned dim (counter: that of the first partitioned dim).
+__device__ __forceinline__ void fused_signal_last(const Geom &g, unsigned *const counters[4], int nblocks,
+                                                  unsigned *const flags[4][2], unsigned v) {
   __syncthreads();
   if (threadIdx.x == 0) {
+    int m0 = 0;
+    while (!((g.part >> m0) & 1)) m0++;
     __threadfence_system();
-    const unsigned prev = atomicAdd(counter, 1u);
-    if (prev == nblocks - 1) {
-      *counter = 0u;
+    const unsigned prev = atomicAdd(counters[m0], 1u);
+    if (prev == (unsigned)nblocks - 1) {
+      *counters[m0] = 0u;
       __threadfence_system();
-      st_release_sys(f0, v);
-      st_release_sys(f1, v);
+      for (int mu = 0; mu < 4; mu++)
+        if ((g.part >> mu) & 1) {
+          st_release_sys(flags[mu][0], v);
+          st_release_sys(flags[mu][1], v);
+        }
     }
   }
+}
+
+// Fused boundary: the remote hop(s) of dim MU for a site on its faces, from the ghost slots
+// (forward: P^- psi(x + mu) from the +mu neighbour, multiplied here by U_mu(x); backward: the
+// neighbour already applied U^dag P^+)
+template <typename R, int MU, typename KP>
+__device__ __forceinline__ void remote_hop(const Geom &g, const KP &P, const int c[4], int cb, int p, Spinor<R> &acc) {
+  if (!((g.part >> MU) & 1)) return;
+  const int n = g.faceVh[MU];
+  if (c[MU] == g.L[MU] - 1) {
+    const Half<R> h = HalfGhost<R>::load(P.ghost[MU][1], n, face_index(g, MU, c));
+    accum_recon<MU, -1>(acc, mul_link(P.U.load(MU, p, cb), h));
+  }
+  if (c[MU] == 0) accum_recon<MU, +1>(acc, HalfGhost<R>::load(P.ghost[MU][0], n, face_index(g, MU, c)));
 }
 
 template <typename R, int REC, int EPI, bool G5IN, bool G5OUT, bool HALO, bool DOT>
 __global__ void __launch_bounds__(QDPB_DSLASH_MAXT, (dslash_minb<R, REC>())) dslash_kernel(const Geom g, const KParams<R, REC> P) {
   int cb = blockIdx.x * blockDim.x + threadIdx.x;
   double dot = 0.0;
-  bool tface = false;  // fused t boundary: this block holds face sites
-  if (HALO && P.fuse_t) {
-    // leading blocks: pack the t faces into the neighbours' ghost slots (as pack_kernel)
+  bool face = false;  // fused boundary: this block holds sites on a partitioned face
+  if (HALO && P.fuse) {
     if ((int)blockIdx.x < P.fuse_npack) {
-      block_wait_flags(P.war[3][0], P.war[3][1], P.seq - 2u, P.err);
-      pack_site<R, REC, G5IN>(g, P, 3, cb);
-      blocks_signal_last(P.pack_counter[3], P.fuse_npack, P.sig[3][0], P.sig[3][1], P.seq);
+      // leading blocks: pack the partitioned faces into the neighbours' ghost slots (as
+      // pack_kernel), once the receivers consumed the slot (written two calls ago)
+#pragma unroll
+      for (int mu = 0; mu < 4; mu++)
+        if ((g.part >> mu) & 1) block_wait_flags(P.war[mu][0], P.war[mu][1], P.seq - 2u, P.err);
+#pragma unroll
+      for (int mu = 0; mu < 4; mu++)
+        if (cb >= P.pack_off[mu] && cb < P.pack_off[mu + 1]) pack_site<R, REC, G5IN>(g, P, mu, cb - P.pack_off[mu]);
+      fused_signal_last(g, P.pack_counter, P.fuse_npack, P.sig, P.seq);
       if (DOT) dot_block_partial(0.0, P.dot_part);
       return;
     }
     cb -= P.fuse_npack * blockDim.x;
-    // then the interior sites [F, Vh - F), then the t = 0 slab [0, F) and the t = L-1 slab [Vh - F, Vh)
-    const int F = g.faceVh[3], nin = g.Vh - 2 * F;
-    tface = (int)((blockIdx.x - P.fuse_npack + 1) * blockDim.x) > nin;
-    if (tface) block_wait_flags(P.ready[3][0], P.ready[3][1], P.seq, P.err);
-    cb = cb < nin ? F + cb : (cb - nin < F ? cb - nin : cb);
+    face = (int)((blockIdx.x - P.fuse_npack + 1) * blockDim.x) > P.fuse_nin;
+    if (face) {
+#pragma unroll
+      for (int mu = 0; mu < 4; mu++)
+        if ((g.part >> mu) & 1) block_wait_flags(P.ready[mu][0], P.ready[mu][1], P.seq, P.err);
+    }
+    if (cb < g.Vh) {
+      if (P.perm) {
+        cb = P.perm[cb];
+      } else {  // only t partitioned: interior [F, Vh - F), then the slabs t = 0 and t = L-1, by arithmetic
+        const int F = g.faceVh[3];
+        cb = cb < P.fuse_nin ? F + cb : (cb - P.fuse_nin < F ? cb - P.fuse_nin : cb);
+      }
+    }
   }
   if (cb < g.Vh) {
     const int p = P.parity;
@@ -369,14 +407,11 @@ __global__ void __launch_bounds__(QDPB_DSLASH_MAXT, (dslash_minb<R, REC>())) dsl
     hop_dir<R, 1>(g, P, c, cb, p, G5IN, HALO, acc);
     hop_dir<R, 2>(g, P, c, cb, p, G5IN, HALO, acc);
     hop_dir<R, 3>(g, P, c, cb, p, G5IN, HALO, acc);
-    if (HALO && P.fuse_t && (c[3] == 0 || c[3] == g.L[3] - 1)) {
-      // the remote t hop from the ghost the neighbour stored (fused exterior)
-      const int n = g.faceVh[3], f = face_index(g, 3, c);
-      if (c[3] == g.L[3] - 1) {
-        const Half<R> h = HalfGhost<R>::load(P.ghost[3][1], n, f);
-        accum_recon<3, -1>(acc, mul_link(P.U.load(3, p, cb), h));
-      }
-      if (c[3] == 0) accum_recon<3, +1>(acc, HalfGhost<R>::load(P.ghost[3][0], n, f));
+    if (HALO && P.fuse) {  // remote hops from the ghosts the neighbours stored
+      remote_hop<R, 0>(g, P, c, cb, p, acc);
+      remote_hop<R, 1>(g, P, c, cb, p, acc);
+      remote_hop<R, 2>(g, P, c, cb, p, acc);
+      remote_hop<R, 3>(g, P, c, cb, p, acc);
     }
     Spinor<R> o = epilogue<R, EPI>(P, cb, acc, G5OUT);
     if (DOT) {
@@ -393,9 +428,9 @@ __global__ void __launch_bounds__(QDPB_DSLASH_MAXT, (dslash_minb<R, REC>())) dsl
     }
   }
   if (DOT) dot_block_partial(dot, P.dot_part);
-  if (HALO && P.fuse_t && tface) {  // the last face block tells both senders their slot was consumed
-    const unsigned first = (unsigned)(P.fuse_npack + (g.Vh - 2 * g.faceVh[3]) / (int)blockDim.x);
-    blocks_signal_last(P.ext_counter[3], gridDim.x - first, P.ack_to[3][0], P.ack_to[3][1], P.seq);
+  if (HALO && P.fuse && face) {  // the last face block tells the senders their slots were consumed
+    const int first = P.fuse_npack + P.fuse_nin / (int)blockDim.x;
+    fused_signal_last(g, P.ext_counter, (int)gridDim.x - first, P.ack_to, P.seq);
   }
 }
 
@@ -534,6 +569,38 @@ static int launch_main_epi(qdp_ctx ctx, const DslashArgs &a, const KParams<R, RE
   return prof_end(ctx, &ev);
 }
 
+// Visiting order of the fused boundary kernel for output parity p: sites on no partitioned face
+// first (nin of them), then the others; built once per (context, partition, parity), on the host.
+static int fuse_order(qdp_ctx ctx, int p, const int **perm, int *nin) {
+  const Geom &g = ctx->geom;
+  if (ctx->fuse_part != g.part) {
+    for (int q = 0; q < 2; q++) {
+      if (ctx->fuse_perm[q]) cudaFree(ctx->fuse_perm[q]);
+      ctx->fuse_perm[q] = nullptr;
+    }
+    ctx->fuse_part = g.part;
+  }
+  if (!ctx->fuse_perm[p]) {
+    std::vector<int> in, out;
+    in.reserve(g.Vh);
+    for (int cb = 0; cb < g.Vh; cb++) {
+      int c[4];
+      cb_coords(g, cb, p, c);
+      bool onface = false;
+      for (int mu = 0; mu < 4; mu++)
+        if (((g.part >> mu) & 1) && (c[mu] == 0 || c[mu] == g.L[mu] - 1)) onface = true;
+      (onface ? out : in).push_back(cb);
+    }
+    ctx->fuse_nin[p] = (int)in.size();
+    in.insert(in.end(), out.begin(), out.end());
+    QDP_CUDA(ctx, cudaMalloc((void **)&ctx->fuse_perm[p], sizeof(int) * g.Vh));
+    QDP_CUDA(ctx, cudaMemcpy(ctx->fuse_perm[p], in.data(), sizeof(int) * g.Vh, cudaMemcpyHostToDevice));
+  }
+  *perm = ctx->fuse_perm[p];
+  *nin = ctx->fuse_nin[p];
+  return QDP_OK;
+}
+
 template <typename R, int REC>
 static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
   const Geom &g = ctx->geom;
@@ -553,17 +620,19 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
   int rc;
   if (dot && !(a.epi == EPI_XPAY || a.epi == EPI_CLOVXPAY) ) return set_error(ctx, QDP_EINVAL, "fused dot: XPAY epilogues only");
   if (dot && (a.g5_in || !a.g5_out)) return set_error(ctx, QDP_EINVAL, "fused dot: Mhat^dag output step only");
-  // peer-to-peer with only t partitioned: the main kernel adds the remote t hops itself
-  // (KParams::fuse_t); QDPB_FUSE_T=0 restores the separate exterior kernel (comparison)
-  static const bool fuse_env = !(getenv("QDPB_FUSE_T") && atoi(getenv("QDPB_FUSE_T")) == 0);
-  const bool fuse_t = halo && ctx->p2p_on && g.part == 8 && fuse_env;
+  // peer-to-peer: packing, interior and remote hops in the one main kernel (KParams::fuse);
+  // QDPB_FUSE=0 restores the separate pack and exterior kernels (comparison)
+  static const bool fuse_env = !(getenv("QDPB_FUSE") && atoi(getenv("QDPB_FUSE")) == 0);
+  const bool fuse = halo && ctx->p2p_on && fuse_env;
   // partial-sum layout of the fused inner product: interior blocks, then each exterior's blocks
   int nparts = 0, ext_off[4] = {0, 0, 0, 0};
-  const int npack = fuse_t ? grid_for(2 * g.faceVh[3], block) : 0;
+  int pack_off[5] = {0, 0, 0, 0, 0};
+  for (int mu = 0; mu < 4; mu++) pack_off[mu + 1] = pack_off[mu] + (((g.part >> mu) & 1) ? 2 * g.faceVh[mu] : 0);
+  const int npack = fuse ? grid_for(pack_off[4], block) : 0;
   if (dot) {
     nparts = grid_for(g.Vh, block) + npack;
     for (int mu = 0; mu < 4; mu++)
-      if (((g.part >> mu) & 1) && !fuse_t) {
+      if (((g.part >> mu) & 1) && !fuse) {
         ext_off[mu] = nparts;
         nparts += grid_for(2 * g.faceVh[mu], 128);
       }
@@ -593,8 +662,17 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
     }
     P.err = L.err;
     P.seq = seq;
-    P.fuse_t = fuse_t ? 1 : 0;
-    P.fuse_npack = npack;
+    if (fuse && g.part == 8) {  // t slabs are contiguous in cb: the order is arithmetic
+      P.perm = nullptr;
+      P.fuse_nin = g.Vh - 2 * g.faceVh[3];
+    } else if (fuse) {
+      if ((rc = fuse_order(ctx, a.parity, &P.perm, &P.fuse_nin))) return rc;
+    }
+    if (fuse) {
+      P.fuse = 1;
+      P.fuse_npack = npack;
+      for (int k = 0; k < 5; k++) P.pack_off[k] = pack_off[k];
+    }
   }
   if (halo) {
     bool any_comm = false;
@@ -616,7 +694,7 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
     }
     for (int mu = 0; mu < 4; mu++) {
       if (!((g.part >> mu) & 1)) continue;
-      if (fuse_t) {  // packed by the leading blocks of the main kernel: bytes only, no launch
+      if (fuse) {  // packed by the leading blocks of the main kernel: bytes only, no launch
         prof_work(ctx, QDP_PK_DSLASH, 0.0, (double)g.faceVh[mu] * (24 + 12 + 24 + REC + 12) * sizeof(R));
         continue;
       }
@@ -643,7 +721,7 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
     if ((rc = launch_main_epi<R, REC>(ctx, a, P, true, block))) return rc;
     if (overlap) QDP_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_comm, 0));
     for (int mu = 0; mu < 4; mu++) {
-      if (!((g.part >> mu) & 1) || fuse_t) continue;
+      if (!((g.part >> mu) & 1) || fuse) continue;
       ProfEvent ev;
       prof_begin(ctx, QDP_PK_DSLASH_EXT, &ev);
       // ghost read, forward-face link, output read-modify-write (+ clover on CLOVINV)

@@ -527,6 +527,10 @@ struct qdp_ctx_s {
   qdpb::Comm *comm = nullptr;
   qdpb::P2P *p2p = nullptr;  // peer-to-peer halo state (QDP_OPT_P2P)
   int p2p_on = 0;
+  // fused peer-to-peer boundary (dslash.cu): per output parity, interior sites first, then face sites
+  int *fuse_perm[2] = {nullptr, nullptr};
+  int fuse_nin[2] = {0, 0};
+  int fuse_part = -1;
   // peer-memory communicator (qdp_init_peer; peer.cu): no NCCL; the host allgather callback
   // exchanges IPC handles at set-up time only
   qdpb::PeerComm *peer = nullptr;

@@ -18,5 +18,5 @@ for mode in ("whole","p2p"):
     for k,name in enumerate(q.PK_NAMES):
         n,ms=q.qdp_profile_query(c,k)
         if n: out.append(f"{name} {ms/n*1e3:.1f}us x{n//30}")
-    print(mode, os.environ.get("QDPB_FUSE_T","1"), " | ".join(out), flush=True)
+    print(mode, os.environ.get("QDPB_FUSE","1"), " | ".join(out), flush=True)
     q.qdp_finalize(c)
