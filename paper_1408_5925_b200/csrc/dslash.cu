@@ -27,12 +27,15 @@ template <> struct HalfGhost<double> {
 #pragma unroll
     for (int k = 0; k < 6; k++) q[(size_t)k * n + f] = make_double2(h.c[k].re, h.c[k].im);
   }
+  // Ghosts may be written by other blocks of the same kernel or by a peer GPU while this kernel
+  // runs (peer-to-peer halo): coherent L2 loads (ld.global.cg) after the acquire, never the
+  // non-coherent read-only path.
   static __device__ __forceinline__ Half<double> load(const void *buf, int n, int f) {
     const double2 *q = (const double2 *)buf;
     Half<double> h;
 #pragma unroll
     for (int k = 0; k < 6; k++) {
-      double2 v = ld_stream(q + (size_t)k * n + f);
+      double2 v = __ldcg(q + (size_t)k * n + f);
       h.c[k] = {v.x, v.y};
     }
     return h;
@@ -50,7 +53,7 @@ template <> struct HalfGhost<float> {
     Half<float> h;
 #pragma unroll
     for (int k = 0; k < 3; k++) {
-      float4 v = ld_stream(q + (size_t)k * n + f);
+      float4 v = __ldcg(q + (size_t)k * n + f);  // coherent: see HalfGhost<double>::load
       h.c[2 * k] = {v.x, v.y};
       h.c[2 * k + 1] = {v.z, v.w};
     }
@@ -594,7 +597,11 @@ static int fuse_order(qdp_ctx ctx, int p, const int **perm, int *nin) {
     ctx->fuse_nin[p] = (int)in.size();
     in.insert(in.end(), out.begin(), out.end());
     QDP_CUDA(ctx, cudaMalloc((void **)&ctx->fuse_perm[p], sizeof(int) * g.Vh));
-    QDP_CUDA(ctx, cudaMemcpy(ctx->fuse_perm[p], in.data(), sizeof(int) * g.Vh, cudaMemcpyHostToDevice));
+    // on the context stream, ordered before the kernels that read it (a pageable cudaMemcpy may
+    // return before its DMA lands, and the context stream need not synchronise with it)
+    QDP_CUDA(ctx, cudaMemcpyAsync(ctx->fuse_perm[p], in.data(), sizeof(int) * g.Vh, cudaMemcpyHostToDevice,
+                                  ctx->stream));
+    QDP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));  // `in` is released on return
   }
   *perm = ctx->fuse_perm[p];
   *nin = ctx->fuse_nin[p];
@@ -620,10 +627,13 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
   int rc;
   if (dot && !(a.epi == EPI_XPAY || a.epi == EPI_CLOVXPAY) ) return set_error(ctx, QDP_EINVAL, "fused dot: XPAY epilogues only");
   if (dot && (a.g5_in || !a.g5_out)) return set_error(ctx, QDP_EINVAL, "fused dot: Mhat^dag output step only");
-  // peer-to-peer: packing, interior and remote hops in the one main kernel (KParams::fuse);
-  // QDPB_FUSE=0 restores the separate pack and exterior kernels (comparison)
-  static const bool fuse_env = !(getenv("QDPB_FUSE") && atoi(getenv("QDPB_FUSE")) == 0);
-  const bool fuse = halo && ctx->p2p_on && fuse_env;
+  // peer-to-peer: packing, interior and remote hops in the one main kernel (KParams::fuse), for
+  // a t split (the weak-scaling bench's).  Other splits keep the separate pack / exterior kernels:
+  // the site-table variant for them (QDPB_FUSE=2, experimental) gave wrong face sites on the first
+  // call under compute-sanitizer racecheck / synccheck scheduling, not yet explained.
+  // QDPB_FUSE=0 restores the separate kernels for the t split too (comparison).
+  static const int fuse_env = getenv("QDPB_FUSE") ? atoi(getenv("QDPB_FUSE")) : 1;
+  const bool fuse = halo && ctx->p2p_on && (fuse_env == 2 || (fuse_env == 1 && g.part == 8));
   // partial-sum layout of the fused inner product: interior blocks, then each exterior's blocks
   int nparts = 0, ext_off[4] = {0, 0, 0, 0};
   int pack_off[5] = {0, 0, 0, 0, 0};

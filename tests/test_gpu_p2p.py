@@ -55,8 +55,10 @@ def test_dslash_p2p_self(q, prec, mask):
         n_pack, _ = q.qdp_profile_query(c, q.QDP_PK_PACK)
         n_ext, _ = q.qdp_profile_query(c, q.QDP_PK_DSLASH_EXT)
         n_main, _ = q.qdp_profile_query(c, q.QDP_PK_DSLASH)
-        # packing, interior and the remote hops in ONE kernel per EO dslash (fused boundary)
-        assert (n_pack, n_ext, n_main) == (0, 0, 10)
+        if mask == 8:  # t split: packing, interior and the remote hops in ONE kernel per EO dslash
+            assert (n_pack, n_ext, n_main) == (0, 0, 10)
+        else:
+            assert n_pack == 10 * bin(mask).count("1") and n_ext == n_pack and n_main == 10
     finally:
         q.qdp_finalize(c)
 

@@ -10,3 +10,6 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
     python bench.py --steps 1 --warmup 3 --iters 8 --no-cpu --no-check --no-tts --ms-shifts 0 > gpurun_out/ncu_launches_bench.log 2>&1; echo ncu_rc=$?
 tail -3 gpurun_out/gpu_tests.log
 cat gpurun_out/smoke.log
+timeout 900 bash tools/sanitize.sh > gpurun_out/sanitize.txt 2>&1; echo san_rc=$?
+QDPB_BENCH_ONE_GPU=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 2 --warmup 3 --iters 4 --ms-iters 3 --no-tts > gpurun_out/bench_2rank_onegpu.json 2> gpurun_out/bench_2rank_onegpu.err; echo b2_rc=$?
+cat gpurun_out/sanitize.txt | grep -E "===|SUMMARY|passed|failed"
