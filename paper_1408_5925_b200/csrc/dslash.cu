@@ -583,23 +583,24 @@ static int fuse_order(qdp_ctx ctx, int p, const int **perm, int *nin) {
     }
     ctx->fuse_part = g.part;
   }
-  if (!ctx->fuse_perm[p]) {
+  for (int pp = 0; pp < 2; pp++) {  // both parities at once (before either kernel runs)
+    if (ctx->fuse_perm[pp]) continue;
     std::vector<int> in, out;
     in.reserve(g.Vh);
     for (int cb = 0; cb < g.Vh; cb++) {
       int c[4];
-      cb_coords(g, cb, p, c);
+      cb_coords(g, cb, pp, c);
       bool onface = false;
       for (int mu = 0; mu < 4; mu++)
         if (((g.part >> mu) & 1) && (c[mu] == 0 || c[mu] == g.L[mu] - 1)) onface = true;
       (onface ? out : in).push_back(cb);
     }
-    ctx->fuse_nin[p] = (int)in.size();
+    ctx->fuse_nin[pp] = (int)in.size();
     in.insert(in.end(), out.begin(), out.end());
-    QDP_CUDA(ctx, cudaMalloc((void **)&ctx->fuse_perm[p], sizeof(int) * g.Vh));
+    QDP_CUDA(ctx, cudaMalloc((void **)&ctx->fuse_perm[pp], sizeof(int) * g.Vh));
     // on the context stream, ordered before the kernels that read it (a pageable cudaMemcpy may
     // return before its DMA lands, and the context stream need not synchronise with it)
-    QDP_CUDA(ctx, cudaMemcpyAsync(ctx->fuse_perm[p], in.data(), sizeof(int) * g.Vh, cudaMemcpyHostToDevice,
+    QDP_CUDA(ctx, cudaMemcpyAsync(ctx->fuse_perm[pp], in.data(), sizeof(int) * g.Vh, cudaMemcpyHostToDevice,
                                   ctx->stream));
     QDP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));  // `in` is released on return
   }
