@@ -366,9 +366,11 @@ __global__ void __launch_bounds__(QDPB_DSLASH_MAXT, (dslash_minb<R, REC>())) dsl
 #pragma unroll
       for (int mu = 0; mu < 4; mu++)
         if ((g.part >> mu) & 1) block_wait_flags(P.war[mu][0], P.war[mu][1], P.seq - 2u, P.err);
+      for (int i = cb; i < P.pack_off[4]; i += P.fuse_npack * blockDim.x) {  // grid-stride over face sites
 #pragma unroll
-      for (int mu = 0; mu < 4; mu++)
-        if (cb >= P.pack_off[mu] && cb < P.pack_off[mu + 1]) pack_site<R, REC, G5IN>(g, P, mu, cb - P.pack_off[mu]);
+        for (int mu = 0; mu < 4; mu++)
+          if (i >= P.pack_off[mu] && i < P.pack_off[mu + 1]) pack_site<R, REC, G5IN>(g, P, mu, i - P.pack_off[mu]);
+      }
       fused_signal_last(g, P.pack_counter, P.fuse_npack, P.sig, P.seq);
       if (DOT) dot_block_partial(0.0, P.dot_part);
       return;
@@ -639,7 +641,9 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
   int nparts = 0, ext_off[4] = {0, 0, 0, 0};
   int pack_off[5] = {0, 0, 0, 0, 0};
   for (int mu = 0; mu < 4; mu++) pack_off[mu + 1] = pack_off[mu] + (((g.part >> mu) & 1) ? 2 * g.faceVh[mu] : 0);
-  const int npack = fuse ? grid_for(pack_off[4], block) : 0;
+  // pack blocks: few enough that their per-block system fences stay cheap (grid-stride loop)
+  static const int pack_cap = getenv("QDPB_PACK_BLOCKS") ? atoi(getenv("QDPB_PACK_BLOCKS")) : 2 * 148;  // measured: 260.0 -> 257.7 us
+  const int npack = fuse ? std::min(grid_for(pack_off[4], block), pack_cap) : 0;
   if (dot) {
     nparts = grid_for(g.Vh, block) + npack;
     for (int mu = 0; mu < 4; mu++)
