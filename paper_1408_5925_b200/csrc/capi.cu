@@ -239,7 +239,7 @@ static int ctx_create(const int global_dims[4], const int proc_grid[4], int rank
               (e = cudaEventCreateWithFlags(&c->ev_comm, cudaEventDisableTiming)) != cudaSuccess))
     rc = cuda_check(c, e, "events");
   if (!rc && (e = cudaMalloc((void **)&c->red_result, 64 * sizeof(double))) != cudaSuccess) rc = cuda_check(c, e, "scalars");
-  if (!rc && (e = cudaMemset(c->red_result, 0, 64 * sizeof(double))) != cudaSuccess) rc = cuda_check(c, e, "scalars");
+  if (!rc && (e = cudaMemsetAsync(c->red_result, 0, 64 * sizeof(double), c->stream)) != cudaSuccess) rc = cuda_check(c, e, "scalars");
   if (!rc && (e = cudaMalloc((void **)&c->red_gather, 8 * sizeof(double) * nranks)) != cudaSuccess) rc = cuda_check(c, e, "gather");
   if (!rc && (e = cudaMallocHost((void **)&c->host_pinned, 64 * sizeof(double))) != cudaSuccess) rc = cuda_check(c, e, "pinned");
   if (rc) {

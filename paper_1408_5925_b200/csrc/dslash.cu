@@ -631,10 +631,12 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
   if (dot && !(a.epi == EPI_XPAY || a.epi == EPI_CLOVXPAY) ) return set_error(ctx, QDP_EINVAL, "fused dot: XPAY epilogues only");
   if (dot && (a.g5_in || !a.g5_out)) return set_error(ctx, QDP_EINVAL, "fused dot: Mhat^dag output step only");
   // peer-to-peer: packing, interior and remote hops in the one main kernel (KParams::fuse), for
-  // a t split (the weak-scaling bench's).  Other splits keep the separate pack / exterior kernels:
-  // the site-table variant for them (QDPB_FUSE=2, experimental) gave wrong face sites on the first
-  // call under compute-sanitizer racecheck / synccheck scheduling, not yet explained.
-  // QDPB_FUSE=0 restores the separate kernels for the t split too (comparison).
+  // a t split (the weak-scaling bench's).  Other splits keep the separate pack / exterior kernels
+  // by default.  The site-table variant for them (QDPB_FUSE=2) matches the oracle in plain runs
+  // since p2p_setup orders its flag reset on the context stream (it used a legacy-stream
+  // cudaMemset, unordered with the non-blocking stream: a reused allocation showed the previous
+  // context's flags to the first call), but still gives wrong face sites under compute-sanitizer
+  // racecheck / synccheck scheduling, so it stays opt-in.  QDPB_FUSE=0: separate kernels always.
   static const int fuse_env = getenv("QDPB_FUSE") ? atoi(getenv("QDPB_FUSE")) : 1;
   const bool fuse = halo && ctx->p2p_on && (fuse_env == 2 || (fuse_env == 1 && g.part == 8));
   // partial-sum layout of the fused inner product: interior blocks, then each exterior's blocks

@@ -53,7 +53,10 @@ static int p2p_setup(qdp_ctx ctx, int prec) {
       delete p;
       return set_error(ctx, QDP_ENOMEM, "p2p flags");
     }
-    QDP_CUDA(ctx, cudaMemset(p->flags, 0, sizeof(unsigned) * (NFLAGS + 1)));
+    // on the context stream (non-blocking: a legacy-stream cudaMemset is not ordered before its
+    // kernels, and a reused allocation would show the previous context's flags to the first call)
+    QDP_CUDA(ctx, cudaMemsetAsync(p->flags, 0, sizeof(unsigned) * (NFLAGS + 1), ctx->stream));
+    QDP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));  // zero before any peer can map and signal it
     ctx->p2p = p;
   }
   P2P *p = ctx->p2p;
@@ -74,8 +77,9 @@ static int p2p_setup(qdp_ctx ctx, int prec) {
           cudaGetLastError();
           return set_error(ctx, QDP_ENOMEM, "p2p ghost buffers");
         }
-        QDP_CUDA(ctx, cudaMemset(p->recv[prec][mu][d], 0, 2 * need));
+        QDP_CUDA(ctx, cudaMemsetAsync(p->recv[prec][mu][d], 0, 2 * need, ctx->stream));
       }
+  QDP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   // self dims: "the neighbour" is this rank
   for (int mu = 0; mu < 4; mu++)
     if (((g.part >> mu) & 1) && !remote_dim(ctx, mu)) {
@@ -98,7 +102,7 @@ static int p2p_setup(qdp_ctx ctx, int prec) {
     } else {
     char *dev = nullptr;
     QDP_CUDA(ctx, cudaMalloc(&dev, sizeof(HandleMsg) * (ctx->nranks + 1)));
-    QDP_CUDA(ctx, cudaMemcpy(dev, &mine, sizeof(HandleMsg), cudaMemcpyHostToDevice));
+    QDP_CUDA(ctx, cudaMemcpyAsync(dev, &mine, sizeof(HandleMsg), cudaMemcpyHostToDevice, ctx->stream));
     int rc = comm_allgather_bytes(ctx, dev, dev + sizeof(HandleMsg), sizeof(HandleMsg), ctx->stream);
     if (!rc) {
       QDP_CUDA(ctx, cudaMemcpyAsync(all.data(), dev + sizeof(HandleMsg), sizeof(HandleMsg) * ctx->nranks,
