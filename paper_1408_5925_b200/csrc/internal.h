@@ -199,6 +199,13 @@ __device__ __forceinline__ void block_wait_flags(const unsigned *f0, const unsig
     }
   }
   __syncthreads();
+  // every thread acquires the flags itself (they only grow, so it reads a value >= expect):
+  // its later ghost loads are then ordered after the sender's release without relying on the
+  // barrier carrying thread 0's acquire to the rest of the block
+  if (threadIdx.x) {
+    (void)ld_acquire_sys(f0);
+    (void)ld_acquire_sys(f1);
+  }
 }
 // Called by every thread after its stores: the last block of the grid to get here release-
 // stores v into f0 and f1 (system scope) and resets the block counter.  The barrier orders the
