@@ -141,12 +141,17 @@ int qdp_get_geometry(qdp_ctx ctx, int local_dims[4], int proc_coords[4]);
  *                     buffers -- the NCCL code path of a multi-GPU run, on one GPU. */
  /*  QDP_OPT_P2P        1: dslash halos go peer to peer instead of through NCCL: every rank
  *                     maps its neighbours' ghost buffers (CUDA IPC over NVLink / NVSwitch,
- *                     exchanged collectively at first use), the face-packing kernel stores
- *                     straight into them and release-signals a flag, the neighbour's stream
- *                     acquires it before the exterior kernel and acknowledges afterwards
- *                     (two slots per face).  Self-halo dims use the same protocol on this rank.
- *                     A flag wait that never completes surfaces as QDP_ECUDA at the next
- *                     synchronising call. */
+ *                     exchanged collectively at first use).  One kernel per EO dslash: its
+ *                     first-started blocks (an atomic start ticket deals out the roles) pack the
+ *                     faces straight into the neighbours' ghost slots and release-signal a
+ *                     flag; the interior blocks run meanwhile; the blocks holding face sites
+ *                     acquire the flags, add the remote hops and acknowledge (two slots per
+ *                     face).  With QDP_OPT_OVERLAP = 0 every block waits for the ghosts first.
+ *                     Self-halo dims use the same protocol on this rank.  Changing
+ *                     QDP_OPT_SELF_HALO after the first dslash rebuilds the slots when every
+ *                     partitioned dim is a self dim, else returns QDP_EUNSUPPORTED from the
+ *                     next dslash.  A flag wait that never completes surfaces as QDP_ECUDA at
+ *                     the next synchronising call. */
 enum { QDP_OPT_OVERLAP = 0, QDP_OPT_SELF_HALO = 1, QDP_OPT_PROFILE = 2, QDP_OPT_BLOCK = 3,
        QDP_OPT_DET_REDUCE = 4, QDP_OPT_SELF_NCCL = 5, QDP_OPT_AUTOTUNE = 6 /* see qdp_expr */,
        QDP_OPT_P2P = 7 };

@@ -177,6 +177,12 @@ template <typename R, int REC = 18> struct KParams {
   int fuse_nin;     // interior sites: perm[0, nin) interior, perm[nin, Vh) on a partitioned face
   const int *perm;  // visiting order of the output parity's sites (nullptr: only t partitioned)
   int pack_off[5];  // cumulative pack threads per dim (2 faceVh for a partitioned dim, else 0)
+  // block roles are dealt out by an atomic ticket taken when a block starts (not by blockIdx:
+  // CUDA does not promise in-order dispatch), so every packing block is already running before
+  // any block that waits for a ghost; ticket - ticket_base is the block's virtual index
+  unsigned *ticket;
+  unsigned ticket_base;
+  int wait_all;     // QDP_OPT_OVERLAP = 0: every block waits for the ghosts (no overlap; Fig. 6)
 };
 
 template <typename R, int MU, typename KP>
@@ -250,8 +256,8 @@ __device__ __forceinline__ double re_dot(const Spinor<R> &d, const Spinor<R> &o)
   return s;
 }
 
-// block sum of v -> part[2 * blockIdx.x] (re), part[2 * blockIdx.x + 1] = 0; blockDim <= 256
-__device__ __forceinline__ void dot_block_partial(double v, double *part) {
+// block sum of v -> part[2 * idx] (re), part[2 * idx + 1] = 0; blockDim <= 256
+__device__ __forceinline__ void dot_block_partial(double v, double *part, int idx) {
   __shared__ double sm[8];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -263,8 +269,8 @@ __device__ __forceinline__ void dot_block_partial(double v, double *part) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     if (l == 0) {
-      part[2 * blockIdx.x] = v;
-      part[2 * blockIdx.x + 1] = 0.0;
+      part[2 * idx] = v;
+      part[2 * idx + 1] = 0.0;
     }
   }
 }
@@ -357,12 +363,18 @@ __device__ __forceinline__ void remote_hop(const Geom &g, const KP &P, const int
 template <typename R, int REC, int EPI, bool G5IN, bool G5OUT, bool HALO, bool DOT>
 __global__ void __launch_bounds__(QDPB_DSLASH_MAXT, (dslash_minb<R, REC>())) dslash_kernel(const Geom g, const KParams<R, REC> P) {
   int cb = blockIdx.x * blockDim.x + threadIdx.x;
+  int vb = blockIdx.x;  // virtual block index (fused boundary: the start ticket)
   double dot = 0.0;
   bool face = false;  // fused boundary: this block holds sites on a partitioned face
   if (HALO && P.fuse) {
-    if ((int)blockIdx.x < P.fuse_npack) {
-      // leading blocks: pack the partitioned faces into the neighbours' ghost slots (as
-      // pack_kernel), once the receivers consumed the slot (written two calls ago)
+    __shared__ unsigned s_ticket;
+    if (threadIdx.x == 0) s_ticket = atomicAdd(P.ticket, 1u) - P.ticket_base;
+    __syncthreads();
+    vb = (int)s_ticket;
+    cb = vb * blockDim.x + threadIdx.x;
+    if (vb < P.fuse_npack) {
+      // the first blocks to start: pack the partitioned faces into the neighbours' ghost slots
+      // (as pack_kernel), once the receivers consumed the slot (written two calls ago)
 #pragma unroll
       for (int mu = 0; mu < 4; mu++)
         if ((g.part >> mu) & 1) block_wait_flags(P.war[mu][0], P.war[mu][1], P.seq - 2u, P.err);
@@ -372,12 +384,12 @@ __global__ void __launch_bounds__(QDPB_DSLASH_MAXT, (dslash_minb<R, REC>())) dsl
           if (i >= P.pack_off[mu] && i < P.pack_off[mu + 1]) pack_site<R, REC, G5IN>(g, P, mu, i - P.pack_off[mu]);
       }
       fused_signal_last(g, P.pack_counter, P.fuse_npack, P.sig, P.seq);
-      if (DOT) dot_block_partial(0.0, P.dot_part);
+      if (DOT) dot_block_partial(0.0, P.dot_part, vb);
       return;
     }
     cb -= P.fuse_npack * blockDim.x;
-    face = (int)((blockIdx.x - P.fuse_npack + 1) * blockDim.x) > P.fuse_nin;
-    if (face) {
+    face = (vb - P.fuse_npack + 1) * (int)blockDim.x > P.fuse_nin;
+    if (face || P.wait_all) {
 #pragma unroll
       for (int mu = 0; mu < 4; mu++)
         if ((g.part >> mu) & 1) block_wait_flags(P.ready[mu][0], P.ready[mu][1], P.seq, P.err);
@@ -432,7 +444,7 @@ __global__ void __launch_bounds__(QDPB_DSLASH_MAXT, (dslash_minb<R, REC>())) dsl
       P.out.store(cb, o);
     }
   }
-  if (DOT) dot_block_partial(dot, P.dot_part);
+  if (DOT) dot_block_partial(dot, P.dot_part, vb);
   if (HALO && P.fuse && face) {  // the last face block tells the senders their slots were consumed
     const int first = P.fuse_npack + P.fuse_nin / (int)blockDim.x;
     fused_signal_last(g, P.ext_counter, (int)gridDim.x - first, P.ack_to, P.seq);
@@ -488,7 +500,7 @@ __global__ void __launch_bounds__(128) exterior_kernel(const Geom g, const KPara
     P.out.store(cb, o);
     if (DOT) dot = re_dot(P.dotx.load_stream(cb), acc);
   }
-  if (DOT) dot_block_partial(dot, dot_part);
+  if (DOT) dot_block_partial(dot, dot_part, blockIdx.x);
   // peer-to-peer: the last block tells both senders their slot has been consumed
   if (P.pack_counter[mu]) grid_signal_last(P.ext_counter[mu], P.ack_to[mu][0], P.ack_to[mu][1], P.seq);
 }
@@ -631,20 +643,18 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
   if (dot && !(a.epi == EPI_XPAY || a.epi == EPI_CLOVXPAY) ) return set_error(ctx, QDP_EINVAL, "fused dot: XPAY epilogues only");
   if (dot && (a.g5_in || !a.g5_out)) return set_error(ctx, QDP_EINVAL, "fused dot: Mhat^dag output step only");
   // peer-to-peer: packing, interior and remote hops in the one main kernel (KParams::fuse), for
-  // a t split (the weak-scaling bench's).  Other splits keep the separate pack / exterior kernels
-  // by default.  The site-table variant for them (QDPB_FUSE=2) matches the oracle in plain runs
-  // since p2p_setup orders its flag reset on the context stream (it used a legacy-stream
-  // cudaMemset, unordered with the non-blocking stream: a reused allocation showed the previous
-  // context's flags to the first call), but still gives wrong face sites under compute-sanitizer
-  // racecheck / synccheck scheduling, so it stays opt-in.  QDPB_FUSE=0: separate kernels always.
+  // every split (t: the face sites are the two end slabs of the cb order, found by arithmetic;
+  // others: a site table, interior sites first).  QDPB_FUSE=0: separate pack / interior /
+  // exterior kernels (kept for comparison).
   static const int fuse_env = getenv("QDPB_FUSE") ? atoi(getenv("QDPB_FUSE")) : 1;
-  const bool fuse = halo && ctx->p2p_on && (fuse_env == 2 || (fuse_env == 1 && g.part == 8));
+  const bool fuse = halo && ctx->p2p_on && fuse_env != 0;
   // partial-sum layout of the fused inner product: interior blocks, then each exterior's blocks
   int nparts = 0, ext_off[4] = {0, 0, 0, 0};
   int pack_off[5] = {0, 0, 0, 0, 0};
   for (int mu = 0; mu < 4; mu++) pack_off[mu + 1] = pack_off[mu] + (((g.part >> mu) & 1) ? 2 * g.faceVh[mu] : 0);
   // pack blocks: few enough that their per-block system fences stay cheap (grid-stride loop)
-  static const int pack_cap = getenv("QDPB_PACK_BLOCKS") ? atoi(getenv("QDPB_PACK_BLOCKS")) : 2 * 148;  // measured: 260.0 -> 257.7 us
+  static const int pack_cap =
+      std::max(1, getenv("QDPB_PACK_BLOCKS") ? atoi(getenv("QDPB_PACK_BLOCKS")) : 2 * 148);  // measured: 260.0 -> 257.7 us
   const int npack = fuse ? std::min(grid_for(pack_off[4], block), pack_cap) : 0;
   if (dot) {
     nparts = grid_for(g.Vh, block) + npack;
@@ -661,10 +671,13 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
 
   unsigned seq = 0;
   if (halo && ctx->p2p_on) {
+    // host-side preparation that can fail comes first; the sequence number is taken last, by
+    // p2p_prepare, so a failure never leaves this rank a call behind its neighbours
+    if (fuse && g.part != 8 && (rc = fuse_order(ctx, a.parity, &P.perm, &P.fuse_nin))) return rc;
     // peer-to-peer: pack straight into the neighbours' ghost slots, flags instead of NCCL (p2p.cu)
-    seq = p2p_next_seq(ctx, prec);
     P2PLaunch L;
-    if ((rc = p2p_prepare(ctx, prec, seq, &L))) return rc;
+    if ((rc = p2p_prepare(ctx, prec, &L))) return rc;
+    seq = L.seq;
     for (int mu = 0; mu < 4; mu++) {
       P.pack_counter[mu] = L.pack_counter[mu];
       P.ext_counter[mu] = L.ext_counter[mu];
@@ -679,16 +692,18 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
     }
     P.err = L.err;
     P.seq = seq;
-    if (fuse && g.part == 8) {  // t slabs are contiguous in cb: the order is arithmetic
-      P.perm = nullptr;
-      P.fuse_nin = g.Vh - 2 * g.faceVh[3];
-    } else if (fuse) {
-      if ((rc = fuse_order(ctx, a.parity, &P.perm, &P.fuse_nin))) return rc;
-    }
     if (fuse) {
+      if (g.part == 8) {  // t slabs are contiguous in cb: the order is arithmetic
+        P.perm = nullptr;
+        P.fuse_nin = g.Vh - 2 * g.faceVh[3];
+      }
       P.fuse = 1;
       P.fuse_npack = npack;
       for (int k = 0; k < 5; k++) P.pack_off[k] = pack_off[k];
+      P.ticket = L.ticket;
+      P.ticket_base = *L.ticket_base;
+      *L.ticket_base += (unsigned)(grid_for(g.Vh, block) + npack);  // the launch below takes them all
+      P.wait_all = ctx->overlap ? 0 : 1;
     }
   }
   if (halo) {

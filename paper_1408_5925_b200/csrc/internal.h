@@ -661,10 +661,13 @@ struct P2PLaunch {
   unsigned *sig[4][2], *ack_to[4][2];
   const unsigned *war[4][2], *ready[4][2];
   unsigned *err;
+  unsigned seq;               // this call's sequence number (taken after every set-up step succeeded)
+  unsigned *ticket;           // block-ticket counter of the fused boundary kernel (device)
+  unsigned *ticket_base;      // host mirror: tickets handed out before this launch
 };
-int p2p_prepare(qdp_ctx ctx, int prec, unsigned seq, P2PLaunch *out);
+// set up (collective on first use), then take the next sequence number and fill *out
+int p2p_prepare(qdp_ctx ctx, int prec, P2PLaunch *out);
 int p2p_check(qdp_ctx ctx);  // QDP_ECUDA if a flag wait timed out
-unsigned p2p_next_seq(qdp_ctx ctx, int prec);
 void p2p_destroy(qdp_ctx ctx);
 
 // expr.cu (Table II site expressions)

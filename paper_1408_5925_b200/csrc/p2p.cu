@@ -26,9 +26,15 @@ enum { F_READY = 0, F_ACK = 1, F_COUNT = 2 };
 constexpr int NFLAGS = 2 * 3 * 4 * 2;
 inline size_t fidx(int prec, int kind, int mu, int d) { return ((size_t)(prec * 3 + kind) * 4 + mu) * 2 + d; }
 
+// words after the flag block: [NFLAGS] error word, [NFLAGS + 1 + prec] block-ticket counter of the
+// fused boundary kernel (local only: never written by a peer)
+constexpr int NWORDS = NFLAGS + 3;
+
 struct P2P {
-  unsigned *flags = nullptr;  // this rank's flag block (+ error word at NFLAGS)
+  unsigned *flags = nullptr;  // this rank's flag block (+ error word and ticket counters)
   size_t slot_bytes[2] = {0, 0};
+  int part[2] = {-1, -1};             // partition mask the slots of each precision were set up for
+  unsigned ticket_base[2] = {0, 0};   // tickets handed out so far (host mirror of the counter)
   void *recv[2][4][2] = {};           // this rank's ghost buffers (2 slots each)
   void *peer_recv[2][4][2] = {};      // [prec][mu][d]: ghost slots channel d writes into
   unsigned *peer_flags[4][2] = {};    // flag block of the -mu (d = 0) / +mu (d = 1) neighbour
@@ -48,14 +54,14 @@ static int p2p_setup(qdp_ctx ctx, int prec) {
   const Geom &g = ctx->geom;
   if (!ctx->p2p) {
     P2P *p = new P2P();
-    if (cudaMalloc((void **)&p->flags, sizeof(unsigned) * (NFLAGS + 1)) != cudaSuccess) {
+    if (cudaMalloc((void **)&p->flags, sizeof(unsigned) * NWORDS) != cudaSuccess) {
       cudaGetLastError();
       delete p;
       return set_error(ctx, QDP_ENOMEM, "p2p flags");
     }
     // on the context stream (non-blocking: a legacy-stream cudaMemset is not ordered before its
     // kernels, and a reused allocation would show the previous context's flags to the first call)
-    QDP_CUDA(ctx, cudaMemsetAsync(p->flags, 0, sizeof(unsigned) * (NFLAGS + 1), ctx->stream));
+    QDP_CUDA(ctx, cudaMemsetAsync(p->flags, 0, sizeof(unsigned) * NWORDS, ctx->stream));
     QDP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));  // zero before any peer can map and signal it
     ctx->p2p = p;
   }
@@ -67,8 +73,29 @@ static int p2p_setup(qdp_ctx ctx, int prec) {
       need = std::max(need, (size_t)g.faceVh[mu] * 12 * (prec == QDP_F64 ? 8 : 4));  // half spinors
       any_remote |= remote_dim(ctx, mu);
     }
-  if (p->slot_bytes[prec] >= need) return QDP_OK;
-  if (p->slot_bytes[prec]) return set_error(ctx, QDP_EUNSUPPORTED, "p2p: the partition changed after first use");
+  if (p->slot_bytes[prec] && p->part[prec] == g.part) return QDP_OK;
+  if (p->slot_bytes[prec]) {
+    // The partition changed after first use (QDP_OPT_SELF_HALO).  Dims reached through a
+    // neighbour's mapped memory cannot be re-negotiated without every rank taking part, so that
+    // is refused; a context whose partitioned dims are all self-halo dims rebuilds its slots and
+    // restarts its sequence with zeroed flags (a newly partitioned dim's WAR flag would otherwise
+    // lag the running sequence and its first pack would wait forever).
+    if (any_remote) return set_error(ctx, QDP_EUNSUPPORTED, "p2p: the partition changed after first use");
+    QDP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    for (int mu = 0; mu < 4; mu++)
+      for (int d = 0; d < 2; d++) {
+        if (p->recv[prec][mu][d]) cudaFree(p->recv[prec][mu][d]);
+        p->recv[prec][mu][d] = p->peer_recv[prec][mu][d] = nullptr;
+      }
+    const size_t f0 = fidx(prec, 0, 0, 0), nf = fidx(prec + 1, 0, 0, 0) - f0;
+    QDP_CUDA(ctx, cudaMemsetAsync(p->flags + f0, 0, sizeof(unsigned) * nf, ctx->stream));
+    QDP_CUDA(ctx, cudaMemsetAsync(p->flags + NFLAGS + 1 + prec, 0, sizeof(unsigned), ctx->stream));
+    p->seq[prec] = 0;
+    p->ticket_base[prec] = 0;
+    p->slot_bytes[prec] = 0;
+    p->part[prec] = -1;
+  }
+  if (need == 0) return QDP_OK;
   QDP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   for (int mu = 0; mu < 4; mu++)
     if ((g.part >> mu) & 1)
@@ -137,6 +164,7 @@ static int p2p_setup(qdp_ctx ctx, int prec) {
     }
   }
   p->slot_bytes[prec] = need;
+  p->part[prec] = g.part;
   return QDP_OK;
 }
 
@@ -146,16 +174,22 @@ int p2p_setup_all(qdp_ctx ctx) {
   return p2p_setup(ctx, QDP_F32);
 }
 
-unsigned p2p_next_seq(qdp_ctx ctx, int prec) { return ctx->p2p ? ++ctx->p2p->seq[prec] : 1u; }
-
-int p2p_prepare(qdp_ctx ctx, int prec, unsigned seq, P2PLaunch *L) {
+// Set-up (collective on first use) happens BEFORE the call's sequence number is taken, so every
+// launch of a call sees a fresh `seq` (a first call that created the state used to get seq 1 and
+// the next call seq 1 again: its face blocks then passed their ready wait on the previous call's
+// flag and could read the ghosts before this call's packers wrote them).
+int p2p_prepare(qdp_ctx ctx, int prec, P2PLaunch *L) {
   int rc;
   if ((rc = p2p_setup(ctx, prec))) return rc;
   P2P *p = ctx->p2p;
   const Geom &g = ctx->geom;
+  const unsigned seq = ++p->seq[prec];
   const size_t off = (seq & 1u) * p->slot_bytes[prec];
   memset(L, 0, sizeof(*L));
+  L->seq = seq;
   L->err = p->flags + NFLAGS;
+  L->ticket = p->flags + NFLAGS + 1 + prec;
+  L->ticket_base = &p->ticket_base[prec];
   for (int mu = 0; mu < 4; mu++) {
     if (!((g.part >> mu) & 1)) continue;
     for (int d = 0; d < 2; d++) {
