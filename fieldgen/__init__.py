@@ -26,7 +26,8 @@ import numpy as np
 __all__ = [
     "volume", "coords", "parity", "gaussian", "uniform", "random_spinor",
     "random_su3", "random_gauge", "warm_gauge", "unit_gauge", "random_gauge_transform",
-    "to_fp32", "cb_sites", "apply_antiperiodic_t",
+    "to_fp32", "cb_sites", "apply_antiperiodic_t", "random_gauge_sites", "random_spinor_sites",
+    "random_gauge_torch", "random_spinor_torch",
 ]
 
 _GAMMA = np.uint64(0x9E3779B97F4A7C15)
@@ -114,12 +115,12 @@ def _su3_from_gaussian(g: np.ndarray) -> np.ndarray:
     return np.stack([r0, r1, r2], axis=1)
 
 
-def random_su3(n: int, seed: int, chunk: int = 1 << 20) -> np.ndarray:
-    """n random SU(3) matrices as float64[n,3,3,2]."""
+def random_su3(n: int, seed: int, chunk: int = 1 << 20, first: int = 0) -> np.ndarray:
+    """n random SU(3) matrices as float64[n,3,3,2]: matrices first .. first+n-1 of stream `seed`."""
     out = np.empty((n, 3, 3, 2), dtype=np.float64)
     for lo in range(0, n, chunk):
         m = min(chunk, n - lo)
-        g = gaussian(seed, m * 18, start=lo * 18).reshape(m, 3, 3, 2)
+        g = gaussian(seed, m * 18, start=(first + lo) * 18).reshape(m, 3, 3, 2)
         c = _su3_from_gaussian(g[..., 0] + 1j * g[..., 1])
         out[lo:lo + m, ..., 0] = c.real
         out[lo:lo + m, ..., 1] = c.imag
@@ -130,6 +131,50 @@ def random_gauge(L, seed: int) -> np.ndarray:
     """Hot random SU(3) gauge field float64[V,4,3,3,2]."""
     V = volume(L)
     return random_su3(V * 4, seed).reshape(V, 4, 3, 3, 2)
+
+
+def random_gauge_sites(seed: int, site_lo: int, n_sites: int) -> np.ndarray:
+    """Sites site_lo .. site_lo+n_sites-1 of random_gauge(L, seed) (the counter-based stream makes
+    any contiguous site range cheap: e.g. one time slice of a neighbouring rank's sub-lattice)."""
+    return random_su3(n_sites * 4, seed, first=site_lo * 4).reshape(n_sites, 4, 3, 3, 2)
+
+
+def random_spinor_sites(seed: int, site_lo: int, n_sites: int) -> np.ndarray:
+    """Sites site_lo .. site_lo+n_sites-1 of random_spinor(L, seed)."""
+    return gaussian(seed, n_sites * 24, start=site_lo * 24).reshape(n_sites, 4, 3, 2)
+
+
+def random_gauge_torch(L, seed: int, device="cuda"):
+    """Hot random SU(3) gauge field generated on `device` with torch's generator (float64 tensor
+    [V,4,3,3,2], host canonical layout).  Same Gram-Schmidt construction as random_gauge, but NOT
+    the same numbers: for timing-only workloads whose fields are too large to generate on the host
+    in reasonable time (no parity claim rests on them)."""
+    import torch
+    V = volume(L)
+    gen = torch.Generator(device=device)
+    gen.manual_seed(int(seed))
+    out = torch.empty((V * 4, 3, 3, 2), dtype=torch.float64, device=device)
+    chunk = 1 << 22
+    for lo in range(0, V * 4, chunk):
+        m = min(chunk, V * 4 - lo)
+        g = torch.randn((m, 3, 3, 2), dtype=torch.float64, device=device, generator=gen)
+        a = torch.complex(g[..., 0], g[..., 1])
+        r0 = a[:, 0, :] / torch.linalg.vector_norm(a[:, 0, :], dim=1, keepdim=True)
+        r1 = a[:, 1, :] - torch.sum(torch.conj(r0) * a[:, 1, :], dim=1, keepdim=True) * r0
+        r1 = r1 / torch.linalg.vector_norm(r1, dim=1, keepdim=True)
+        r2 = torch.conj(torch.linalg.cross(r0, r1, dim=1))
+        c = torch.stack([r0, r1, r2], dim=1)
+        out[lo:lo + m, ..., 0] = c.real
+        out[lo:lo + m, ..., 1] = c.imag
+    return out.reshape(V, 4, 3, 3, 2)
+
+
+def random_spinor_torch(L, seed: int, device="cuda"):
+    """Gaussian fermion generated on `device` (float64 tensor [V,4,3,2]); see random_gauge_torch."""
+    import torch
+    gen = torch.Generator(device=device)
+    gen.manual_seed(int(seed))
+    return torch.randn((volume(L), 4, 3, 2), dtype=torch.float64, device=device, generator=gen)
 
 
 def warm_gauge(L, seed: int, eps: float, chunk: int = 1 << 20) -> np.ndarray:

@@ -151,10 +151,19 @@ int qdp_get_geometry(qdp_ctx ctx, int local_dims[4], int proc_coords[4]);
  *                     QDP_OPT_SELF_HALO after the first dslash rebuilds the slots when every
  *                     partitioned dim is a self dim, else returns QDP_EUNSUPPORTED from the
  *                     next dslash.  A flag wait that never completes surfaces as QDP_ECUDA at
- *                     the next synchronising call. */
+ *                     the next synchronising call.
+ *  QDP_OPT_FUSE       1 (default; environment QDPB_FUSE=0 changes the default): with
+ *                     QDP_OPT_P2P, packing, interior and remote hops in the one kernel above;
+ *                     0: separate pack / interior / exterior kernels (comparison mode).
+ *  QDP_OPT_DSLASH_VARIANT  -1 (default): the whole-lattice EO dslash launch configuration is
+ *                     chosen by the paper's autotuner on the payload
+ *                     launches, per (precision, gauge storage, epilogue, volume), among:
+ *                     0 four threads per site (one per direction, 128-thread blocks; plain
+ *                     and xpay epilogues), 1 one thread per site, 64-thread blocks, 2 one thread
+ *                     per site, 32-thread blocks.  0, 1, 2 force that variant (measurements). */
 enum { QDP_OPT_OVERLAP = 0, QDP_OPT_SELF_HALO = 1, QDP_OPT_PROFILE = 2, QDP_OPT_BLOCK = 3,
        QDP_OPT_DET_REDUCE = 4, QDP_OPT_SELF_NCCL = 5, QDP_OPT_AUTOTUNE = 6 /* see qdp_expr */,
-       QDP_OPT_P2P = 7 };
+       QDP_OPT_P2P = 7, QDP_OPT_FUSE = 8, QDP_OPT_DSLASH_VARIANT = 9 };
 int qdp_set_option(qdp_ctx ctx, int option, long value);
 int qdp_get_option(qdp_ctx ctx, int option, long *value);
 

@@ -6,6 +6,8 @@
 // Every kernel runs one thread per checkerboard site (grid-stride), looping over the
 // site's planes (12 double2 or 6 float4) and over nblk consecutive parity blocks, so the
 // padded tail of each plane (cb >= Vh) is never read or written.
+#include <string.h>
+
 #include "internal.h"
 
 namespace qdpb {
@@ -33,23 +35,6 @@ __device__ __forceinline__ double warp_sum(double v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
-// block sum of (v0, v1); thread 0 writes partials[2*blockIdx.x + {0,1}]
-__device__ __forceinline__ void block_partial(double v0, double v1, double *partials) {
-  __shared__ double s0[RB / 32], s1[RB / 32];
-  v0 = warp_sum(v0);
-  v1 = warp_sum(v1);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0) { s0[w] = v0; s1[w] = v1; }
-  __syncthreads();
-  if (w == 0) {
-    v0 = l < RB / 32 ? s0[l] : 0.0;
-    v1 = l < RB / 32 ? s1[l] : 0.0;
-    v0 = warp_sum(v0);
-    v1 = warp_sum(v1);
-    if (l == 0) { partials[2 * blockIdx.x] = v0; partials[2 * blockIdx.x + 1] = v1; }
-  }
-}
-
 // Final pass: one block sums n partial pairs in a fixed order -> res[slot], res[slot+1].
 __global__ void __launch_bounds__(1024) final_kernel(const double *partials, int n, double *res, int slot) {
   __shared__ double s0[32], s1[32];
@@ -80,7 +65,7 @@ __global__ void rank_sum_kernel(const double *g, int nranks, int n, double *res,
 }
 
 template <typename R>
-__global__ void __launch_bounds__(RB) norm2_kernel(const Geom g, const typename E<R>::T *a, int nblk, double *partials) {
+__global__ void __launch_bounds__(RB) norm2_kernel(const Geom g, const typename E<R>::T *a, int nblk, const __grid_constant__ RedArgs Rd) {
   double acc = 0.0;
   const size_t bs = (size_t)E<R>::NP * g.stride;
   for (int cb = blockIdx.x * blockDim.x + threadIdx.x; cb < g.Vh; cb += gridDim.x * blockDim.x)
@@ -92,12 +77,12 @@ __global__ void __launch_bounds__(RB) norm2_kernel(const Geom g, const typename 
 #pragma unroll
         for (int j = 0; j < E<R>::NR; j++) acc += (double)v[j] * (double)v[j];
       }
-  block_partial(acc, 0.0, partials);
+  red_finish(Rd, gridDim.x, blockIdx.x, acc, 0.0, false);
 }
 
 template <typename R>
 __global__ void __launch_bounds__(RB) inner_kernel(const Geom g, const typename E<R>::T *a, const typename E<R>::T *b_,
-                                                   int nblk, double *partials) {
+                                                   int nblk, const __grid_constant__ RedArgs Rd) {
   double re = 0.0, im = 0.0;
   const size_t bs = (size_t)E<R>::NP * g.stride;
   for (int cb = blockIdx.x * blockDim.x + threadIdx.x; cb < g.Vh; cb += gridDim.x * blockDim.x)
@@ -114,7 +99,7 @@ __global__ void __launch_bounds__(RB) inner_kernel(const Geom g, const typename 
           im += (double)u[j] * v[j + 1] - (double)u[j + 1] * v[j];
         }
       }
-  block_partial(re, im, partials);
+  red_finish(Rd, gridDim.x, blockIdx.x, re, im, false);
 }
 
 template <typename R>
@@ -174,34 +159,46 @@ __global__ void __launch_bounds__(RB) scale_copy_kernel(const Geom g, typename E
       }
 }
 
-// r -= alpha q ; partial |r|^2   with alpha = res[rho] / res[pq]  (CG step 5)
+// r -= alpha q ; |r|^2 (one launch, reduce.cuh)   with alpha = res[rho] / res[pq]  (CG step 5).
+// Rd.has_cg: iteration Rd.cg.k of the device-side CG (no work once *stop < k; records |r_k|^2).
 template <typename R>
 __global__ void __launch_bounds__(RB) cg_r_kernel(const Geom g, typename E<R>::T *r, const typename E<R>::T *q,
-                                                  const double *res, int rho_slot, int pq_slot, double *partials) {
-  const R alpha = (R)(res[rho_slot] / res[pq_slot]);
+                                                  const double *res, int rho_slot, int pq_slot,
+                                                  const __grid_constant__ RedArgs Rd) {
+  const bool skip = Rd.has_cg && cg_skip(Rd.cg.stop, Rd.cg.k);
   double acc = 0.0;
-  for (int cb = blockIdx.x * blockDim.x + threadIdx.x; cb < g.Vh; cb += gridDim.x * blockDim.x)
+  if (!skip) {
+    const R alpha = (R)(res[rho_slot] / res[pq_slot]);
+    for (int cb = blockIdx.x * blockDim.x + threadIdx.x; cb < g.Vh; cb += gridDim.x * blockDim.x)
 #pragma unroll
-    for (int k = 0; k < E<R>::NP; k++) {
-      const size_t i = (size_t)k * g.stride + cb;
-      R rv[E<R>::NR], qv[E<R>::NR];
-      E<R>::get(r[i], rv);
-      E<R>::get(q[i], qv);
+      for (int k = 0; k < E<R>::NP; k++) {
+        const size_t i = (size_t)k * g.stride + cb;
+        R rv[E<R>::NR], qv[E<R>::NR];
+        E<R>::get(r[i], rv);
+        E<R>::get(q[i], qv);
 #pragma unroll
-      for (int j = 0; j < E<R>::NR; j++) {
-        rv[j] = rv[j] - alpha * qv[j];
-        acc += (double)rv[j] * (double)rv[j];
+        for (int j = 0; j < E<R>::NR; j++) {
+          rv[j] = rv[j] - alpha * qv[j];
+          acc += (double)rv[j] * (double)rv[j];
+        }
+        r[i] = E<R>::put(rv);
       }
-      r[i] = E<R>::put(rv);
-    }
-  block_partial(acc, 0.0, partials);
+  }
+  red_finish(Rd, gridDim.x, blockIdx.x, acc, 0.0, skip);
 }
 
-// x += alpha p ; p = r + beta p (UPD_P), alpha = res[rho] / res[pq], beta = res[rr] / res[rho]
+// x += alpha p ; p = r + beta p (UPD_P), alpha = res[rho] / res[pq], beta = res[rr] / res[rho].
+// stop (device-side CG): no work when *stop < iter; x only when *stop == iter (the last iteration)
 template <typename R, bool UPD_P>
 __global__ void __launch_bounds__(RB) cg_xp_kernel(const Geom g, typename E<R>::T *x, typename E<R>::T *p,
                                                    const typename E<R>::T *r, const double *res, int rho_slot,
-                                                   int pq_slot, int rr_slot) {
+                                                   int pq_slot, int rr_slot, const int *stop, int iter) {
+  bool upd_p = UPD_P;
+  if (stop) {
+    const int s = __ldcg(stop);
+    if (s < iter) return;
+    if (s == iter) upd_p = false;
+  }
   const R alpha = (R)(res[rho_slot] / res[pq_slot]);
   const R beta = (R)(res[rr_slot] / res[rho_slot]);
   for (int cb = blockIdx.x * blockDim.x + threadIdx.x; cb < g.Vh; cb += gridDim.x * blockDim.x)
@@ -211,14 +208,14 @@ __global__ void __launch_bounds__(RB) cg_xp_kernel(const Geom g, typename E<R>::
       R xv[E<R>::NR], pv[E<R>::NR], rv[E<R>::NR];
       E<R>::get(x[i], xv);
       E<R>::get(p[i], pv);
-      if (UPD_P) E<R>::get(r[i], rv);
+      if (UPD_P && upd_p) E<R>::get(r[i], rv);
 #pragma unroll
       for (int j = 0; j < E<R>::NR; j++) {
         xv[j] = xv[j] + alpha * pv[j];
-        if (UPD_P) pv[j] = rv[j] + beta * pv[j];
+        if (UPD_P && upd_p) pv[j] = rv[j] + beta * pv[j];
       }
       x[i] = E<R>::put(xv);
-      if (UPD_P) p[i] = E<R>::put(pv);
+      if (UPD_P && upd_p) p[i] = E<R>::put(pv);
     }
 }
 
@@ -290,34 +287,65 @@ int reduce_partials(qdp_ctx ctx, int nparts, int slot) {
   return prof_end(ctx, &ev);
 }
 
-int blas_norm2(qdp_ctx ctx, int prec, const void *a, int nblk, int slot) {
+int red_setup(qdp_ctx ctx, int nblk, int slot, int n, bool global, bool host, RedArgs *R, bool *after) {
+  int rc;
+  if ((rc = ensure_reduce(ctx, nblk))) return rc;
+  memset(R, 0, sizeof(*R));
+  R->part = ctx->red_partials;
+  R->part2 = ctx->red_partials2;
+  R->cnt = ctx->red_cnt;
+  R->res = ctx->red_result;
+  R->slot = slot;
+  R->n = n;
+  const bool multi = global && ctx->nranks > 1;
+  R->peer = multi && ctx->peer;
+  *after = multi && !ctx->peer;  // NCCL: reduce_global after the launch
+  if (host && !*after) R->host = ctx->host_pinned + 32;
+  if (R->peer) {
+    R->pa = peer_args(ctx);
+    R->seq = peer_next_sum_seq(ctx);
+  }
+  return QDP_OK;
+}
+
+int read_red_host(qdp_ctx ctx, int n, double *out) {
+  QDP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  for (int i = 0; i < n; i++) out[i] = ((volatile double *)ctx->host_pinned)[32 + i];
+  return QDP_OK;
+}
+
+int blas_norm2(qdp_ctx ctx, int prec, const void *a, int nblk, int slot, bool host) {
   const Geom &g = ctx->geom;
   const int nb = red_grid(g);
   int rc;
-  if ((rc = ensure_reduce(ctx, nb))) return rc;
+  RedArgs R;
+  bool after;
+  if ((rc = red_setup(ctx, nb, slot, 1, true, host, &R, &after))) return rc;
   ProfEvent ev;
   prof_begin(ctx, QDP_PK_REDUCE, &ev);
   prof_work(ctx, QDP_PK_REDUCE, 48.0 * g.Vh * nblk, 24.0 * g.Vh * nblk * (prec == QDP_F64 ? 8 : 4));
-  if (prec == QDP_F64) norm2_kernel<double><<<nb, RB, 0, ctx->stream>>>(g, (const T_<double> *)a, nblk, ctx->red_partials);
-  else norm2_kernel<float><<<nb, RB, 0, ctx->stream>>>(g, (const T_<float> *)a, nblk, ctx->red_partials);
+  if (prec == QDP_F64) norm2_kernel<double><<<nb, RB, 0, ctx->stream>>>(g, (const T_<double> *)a, nblk, R);
+  else norm2_kernel<float><<<nb, RB, 0, ctx->stream>>>(g, (const T_<float> *)a, nblk, R);
   if ((rc = prof_end(ctx, &ev))) return rc;
-  return reduce_partials(ctx, nb, slot);
+  return after ? reduce_global(ctx, slot, 1) : QDP_OK;
 }
 
-int blas_inner(qdp_ctx ctx, int prec, const void *a, const void *b, int nblk, int slot) {
+int blas_inner(qdp_ctx ctx, int prec, const void *a, const void *b, int nblk, int slot, bool host) {
   const Geom &g = ctx->geom;
   const int nb = red_grid(g);
   int rc;
-  if ((rc = ensure_reduce(ctx, nb))) return rc;
+  RedArgs R;
+  bool after;
+  if ((rc = red_setup(ctx, nb, slot, 2, true, host, &R, &after))) return rc;
   ProfEvent ev;
   prof_begin(ctx, QDP_PK_REDUCE, &ev);
   prof_work(ctx, QDP_PK_REDUCE, 96.0 * g.Vh * nblk, 48.0 * g.Vh * nblk * (prec == QDP_F64 ? 8 : 4));
   if (prec == QDP_F64)
-    inner_kernel<double><<<nb, RB, 0, ctx->stream>>>(g, (const T_<double> *)a, (const T_<double> *)b, nblk, ctx->red_partials);
+    inner_kernel<double><<<nb, RB, 0, ctx->stream>>>(g, (const T_<double> *)a, (const T_<double> *)b, nblk, R);
   else
-    inner_kernel<float><<<nb, RB, 0, ctx->stream>>>(g, (const T_<float> *)a, (const T_<float> *)b, nblk, ctx->red_partials);
+    inner_kernel<float><<<nb, RB, 0, ctx->stream>>>(g, (const T_<float> *)a, (const T_<float> *)b, nblk, R);
   if ((rc = prof_end(ctx, &ev))) return rc;
-  return reduce_partials(ctx, nb, slot);
+  return after ? reduce_global(ctx, slot, 2) : QDP_OK;
 }
 
 int reduce_global(qdp_ctx ctx, int slot, int n) {
@@ -408,27 +436,34 @@ int blas_scale_copy(qdp_ctx ctx, int prec, void *dst, const void *src, double a,
   return prof_end(ctx, &ev);
 }
 
-int blas_cg_update_r(qdp_ctx ctx, int prec, void *r, const void *q, int rho_slot, int pq_slot, int rr_slot) {
+int blas_cg_update_r(qdp_ctx ctx, int prec, void *r, const void *q, int rho_slot, int pq_slot, int rr_slot,
+                     const CgDev *cg) {
   const Geom &g = ctx->geom;
   const int nb = red_grid(g);
   int rc;
-  if ((rc = ensure_reduce(ctx, nb))) return rc;
+  RedArgs R;
+  bool after;
+  if ((rc = red_setup(ctx, nb, rr_slot, 1, true, false, &R, &after))) return rc;
+  if (cg) {
+    if (after) return set_error(ctx, QDP_EINVAL, "device-side CG needs the in-kernel global sum");
+    R.has_cg = 1;
+    R.cg = *cg;
+  }
   ProfEvent ev;
   prof_begin(ctx, QDP_PK_BLAS, &ev);
   prof_work(ctx, QDP_PK_BLAS, 96.0 * g.Vh, 72.0 * g.Vh * (prec == QDP_F64 ? 8 : 4));
   if (prec == QDP_F64)
     cg_r_kernel<double><<<nb, RB, 0, ctx->stream>>>(g, (T_<double> *)r, (const T_<double> *)q, ctx->red_result, rho_slot,
-                                                     pq_slot, ctx->red_partials);
+                                                     pq_slot, R);
   else
     cg_r_kernel<float><<<nb, RB, 0, ctx->stream>>>(g, (T_<float> *)r, (const T_<float> *)q, ctx->red_result, rho_slot,
-                                                    pq_slot, ctx->red_partials);
+                                                    pq_slot, R);
   if ((rc = prof_end(ctx, &ev))) return rc;
-  if ((rc = reduce_partials(ctx, nb, rr_slot))) return rc;
-  return reduce_global(ctx, rr_slot, 1);
+  return after ? reduce_global(ctx, rr_slot, 1) : QDP_OK;
 }
 
 int blas_cg_update_xp(qdp_ctx ctx, int prec, void *x, void *p, const void *r, int rho_slot, int pq_slot, int rr_slot,
-                      bool update_p) {
+                      bool update_p, const int *stop, int iter) {
   const Geom &g = ctx->geom;
   ProfEvent ev;
   prof_begin(ctx, QDP_PK_BLAS, &ev);
@@ -437,7 +472,7 @@ int blas_cg_update_xp(qdp_ctx ctx, int prec, void *x, void *p, const void *r, in
   const int nb = grid_for(g.Vh, RB);
 #define QDPB_XP(Rt, U)                                                                                              \
   cg_xp_kernel<Rt, U><<<nb, RB, 0, ctx->stream>>>(g, (T_<Rt> *)x, (T_<Rt> *)p, (const T_<Rt> *)r, ctx->red_result, \
-                                                  rho_slot, pq_slot, rr_slot)
+                                                  rho_slot, pq_slot, rr_slot, stop, iter)
   if (prec == QDP_F64) { if (update_p) QDPB_XP(double, true); else QDPB_XP(double, false); }
   else { if (update_p) QDPB_XP(float, true); else QDPB_XP(float, false); }
 #undef QDPB_XP

@@ -4,6 +4,8 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
+
 #include "internal.h"
 
 using namespace qdpb;
@@ -89,16 +91,21 @@ int ensure_staging(qdp_ctx ctx, size_t bytes) {
 
 int ensure_reduce(qdp_ctx ctx, int blocks) {
   if (ctx->red_capacity >= blocks) return QDP_OK;
-  if (ctx->red_partials) {
-    QDP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    cudaFree(ctx->red_partials);
-  }
-  ctx->red_partials = nullptr;
+  if (ctx->red_partials) QDP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  cudaFree(ctx->red_partials);
+  cudaFree(ctx->red_partials2);
+  cudaFree(ctx->red_cnt);
+  ctx->red_partials = ctx->red_partials2 = nullptr;
+  ctx->red_cnt = nullptr;
   ctx->red_capacity = 0;
-  if (cudaMalloc((void **)&ctx->red_partials, sizeof(double) * 2 * blocks) != cudaSuccess) {
+  blocks = std::max(blocks, 4096);
+  if (cudaMalloc((void **)&ctx->red_partials, sizeof(double) * 2 * blocks) != cudaSuccess ||
+      cudaMalloc((void **)&ctx->red_partials2, sizeof(double) * 2 * blocks) != cudaSuccess ||
+      cudaMalloc((void **)&ctx->red_cnt, sizeof(unsigned) * (1 + blocks)) != cudaSuccess) {
     cudaGetLastError();
     return set_error(ctx, QDP_ENOMEM, "reduction partials");
   }
+  QDP_CUDA(ctx, cudaMemsetAsync(ctx->red_cnt, 0, sizeof(unsigned) * (1 + blocks), ctx->stream));
   ctx->red_capacity = blocks;
   return QDP_OK;
 }
@@ -220,6 +227,7 @@ static int ctx_create(const int global_dims[4], const int proc_grid[4], int rank
   g.stride = (g.Vh + 63) / 64 * 64;
   for (int mu = 0; mu < 4; mu++) g.faceVh[mu] = (int)(V / g.L[mu] / 2);
   update_partition(c);
+  if (const char *fe = getenv("QDPB_FUSE")) c->fuse = atoi(fe) ? 1 : 0;
 
   int rc = QDP_OK;
   cudaError_t e = cudaGetDevice(&c->device);
@@ -309,6 +317,10 @@ extern "C" int qdp_finalize(qdp_ctx c) {
   if (c->staging) cudaFree(c->staging);
   if (c->cg_work) cudaFree(c->cg_work);
   if (c->red_partials) cudaFree(c->red_partials);
+  if (c->red_partials2) cudaFree(c->red_partials2);
+  if (c->red_cnt) cudaFree(c->red_cnt);
+  if (c->cg_hist) cudaFreeHost(c->cg_hist);
+  if (c->cg_stop) cudaFree(c->cg_stop);
   if (c->red_result) cudaFree(c->red_result);
   if (c->red_gather) cudaFree(c->red_gather);
   if (c->host_pinned) cudaFreeHost(c->host_pinned);
@@ -367,6 +379,11 @@ extern "C" int qdp_set_option(qdp_ctx c, int opt, long v) {
       return QDP_OK;
     case QDP_OPT_DET_REDUCE: c->det_reduce = v ? 1 : 0; return QDP_OK;
     case QDP_OPT_AUTOTUNE: c->autotune = v ? 1 : 0; return QDP_OK;
+    case QDP_OPT_FUSE: c->fuse = v ? 1 : 0; return QDP_OK;
+    case QDP_OPT_DSLASH_VARIANT:
+      if (v < -1 || v > 2) return set_error(c, QDP_EINVAL, "dslash variant must be -1 (tuned), 0, 1 or 2");
+      c->dslash_variant = (int)v;
+      return QDP_OK;
     case QDP_OPT_P2P:
       if (c->peer) {
         if (!v) return set_error(c, QDP_EUNSUPPORTED, "p2p: always on in a peer-memory context");
@@ -399,6 +416,8 @@ extern "C" int qdp_get_option(qdp_ctx c, int opt, long *v) {
     case QDP_OPT_SELF_NCCL: *v = c->self_nccl; return QDP_OK;
     case QDP_OPT_AUTOTUNE: *v = c->autotune; return QDP_OK;
     case QDP_OPT_P2P: *v = c->p2p_on; return QDP_OK;
+    case QDP_OPT_FUSE: *v = c->fuse; return QDP_OK;
+    case QDP_OPT_DSLASH_VARIANT: *v = c->dslash_variant; return QDP_OK;
   }
   return set_error(c, QDP_EINVAL, "unknown option %d", opt);
 }
@@ -610,9 +629,10 @@ extern "C" int qdp_norm2(const qdp_field a, double *out) {
   qdp_ctx c = a->ctx;
   if (a->kind != QDP_FERMION) return set_error(c, QDP_EINVAL, "norm2: fermion fields");
   int rc;
-  if ((rc = blas_norm2(c, a->prec, a->data, a->subset == QDP_ALL ? 2 : 1, 8))) return rc;
-  if ((rc = reduce_global(c, 8, 1))) return rc;
-  return read_result(c, 8, 1, out);
+  if ((rc = blas_norm2(c, a->prec, a->data, a->subset == QDP_ALL ? 2 : 1, 8, true))) return rc;
+  if (c->nranks > 1 && !c->peer) return read_result(c, 8, 1, out);  // NCCL sum after the kernel
+  if ((rc = read_red_host(c, 1, out))) return rc;  // one launch, result in mapped host memory
+  return c->peer ? peer_check(c) : QDP_OK;
 }
 
 extern "C" int qdp_inner_product(const qdp_field a, const qdp_field b, double out[2]) {
@@ -622,9 +642,10 @@ extern "C" int qdp_inner_product(const qdp_field a, const qdp_field b, double ou
   qdp_ctx c = a->ctx;
   if (a->kind != QDP_FERMION || b->kind != QDP_FERMION) return set_error(c, QDP_EINVAL, "inner: fermion fields");
   if (a->subset != b->subset) return set_error(c, QDP_EINVAL, "inner: subsets differ");
-  if ((rc = blas_inner(c, a->prec, a->data, b->data, a->subset == QDP_ALL ? 2 : 1, 10))) return rc;
-  if ((rc = reduce_global(c, 10, 2))) return rc;
-  return read_result(c, 10, 2, out);
+  if ((rc = blas_inner(c, a->prec, a->data, b->data, a->subset == QDP_ALL ? 2 : 1, 10, true))) return rc;
+  if (c->nranks > 1 && !c->peer) return read_result(c, 10, 2, out);
+  if ((rc = read_red_host(c, 2, out))) return rc;
+  return c->peer ? peer_check(c) : QDP_OK;
 }
 
 extern "C" int qdp_axpy(double ar, double ai, const qdp_field x, qdp_field y) {

@@ -183,6 +183,9 @@ template <typename R, int REC = 18> struct KParams {
   unsigned *ticket;
   unsigned ticket_base;
   int wait_all;     // QDP_OPT_OVERLAP = 0: every block waits for the ghosts (no overlap; Fig. 6)
+  // fused inner product finished inside this kernel (reduce.cuh; whole-lattice or fused boundary)
+  int red_fin;
+  RedArgs red;
 };
 
 template <typename R, int MU, typename KP>
@@ -361,7 +364,8 @@ __device__ __forceinline__ void remote_hop(const Geom &g, const KP &P, const int
 }
 
 template <typename R, int REC, int EPI, bool G5IN, bool G5OUT, bool HALO, bool DOT>
-__global__ void __launch_bounds__(QDPB_DSLASH_MAXT, (dslash_minb<R, REC>())) dslash_kernel(const Geom g, const KParams<R, REC> P) {
+__global__ void __launch_bounds__(QDPB_DSLASH_MAXT, (dslash_minb<R, REC>()))
+    dslash_kernel(const Geom g, const __grid_constant__ KParams<R, REC> P) {
   int cb = blockIdx.x * blockDim.x + threadIdx.x;
   int vb = blockIdx.x;  // virtual block index (fused boundary: the start ticket)
   double dot = 0.0;
@@ -384,7 +388,10 @@ __global__ void __launch_bounds__(QDPB_DSLASH_MAXT, (dslash_minb<R, REC>())) dsl
           if (i >= P.pack_off[mu] && i < P.pack_off[mu + 1]) pack_site<R, REC, G5IN>(g, P, mu, i - P.pack_off[mu]);
       }
       fused_signal_last(g, P.pack_counter, P.fuse_npack, P.sig, P.seq);
-      if (DOT) dot_block_partial(0.0, P.dot_part, vb);
+      if (DOT) {
+        if (P.red_fin) red_finish(P.red, gridDim.x, vb, 0.0, 0.0, false);
+        else dot_block_partial(0.0, P.dot_part, vb);
+      }
       return;
     }
     cb -= P.fuse_npack * blockDim.x;
@@ -444,7 +451,10 @@ __global__ void __launch_bounds__(QDPB_DSLASH_MAXT, (dslash_minb<R, REC>())) dsl
       P.out.store(cb, o);
     }
   }
-  if (DOT) dot_block_partial(dot, P.dot_part, vb);
+  if (DOT) {
+    if (P.red_fin) red_finish(P.red, gridDim.x, vb, dot, 0.0, false);
+    else dot_block_partial(dot, P.dot_part, vb);
+  }
   if (HALO && P.fuse && face) {  // the last face block tells the senders their slots were consumed
     const int first = P.fuse_npack + P.fuse_nin / (int)blockDim.x;
     fused_signal_last(g, P.ext_counter, (int)gridDim.x - first, P.ack_to, P.seq);
@@ -505,6 +515,65 @@ __global__ void __launch_bounds__(128) exterior_kernel(const Geom g, const KPara
   if (P.pack_counter[mu]) grid_signal_last(P.ext_counter[mu], P.ack_to[mu][0], P.ack_to[mu][1], P.seq);
 }
 
+// ------------------------------------------------------------------ small-volume variant
+// Below the bandwidth "shoulder" (not enough threads resident to hide the memory
+// latency) one thread per output site leaves the SMs short of independent loads: at 16^3 x 32 the
+// whole lattice is about one wave of the main kernel.  Here FOUR threads share a site, one per
+// direction: warp w of a 128-thread block does the two hops of mu = w for 32 consecutive sites
+// (warp-uniform mu, coalesced 32-site loads), the four partial spinors meet in shared memory, and
+// thread (w, l) finishes components k = w, w + 4, w + 8 of site l (epilogue and store).  Whole
+// lattice, EPI_PLAIN / EPI_XPAY, no fused dot.  Chosen by the tuner below when it is faster.
+__device__ __forceinline__ cx<double> comp_load(const FermView<double> &v, int cb, int k) {
+  const double2 t = ld_stream(v.p + (size_t)k * v.stride + cb);
+  return {t.x, t.y};
+}
+__device__ __forceinline__ void comp_store(const FermView<double> &v, int cb, int k, cx<double> c) {
+  st_stream(v.p + (size_t)k * v.stride + cb, make_double2(c.re, c.im));
+}
+__device__ __forceinline__ cx<float> comp_load(const FermView<float> &v, int cb, int k) {
+  const float2 t = ld_stream((const float2 *)(v.p + (size_t)(k >> 1) * v.stride) + 2 * cb + (k & 1));
+  return {t.x, t.y};
+}
+__device__ __forceinline__ void comp_store(const FermView<float> &v, int cb, int k, cx<float> c) {
+  st_stream((float2 *)(v.p + (size_t)(k >> 1) * v.stride) + 2 * cb + (k & 1), make_float2(c.re, c.im));
+}
+
+template <typename R, int REC, int EPI, bool G5IN, bool G5OUT>
+__global__ void __launch_bounds__(128) dslash4_kernel(const Geom g, const __grid_constant__ KParams<R, REC> P) {
+  __shared__ cx<R> part[4][12][33];
+  const int mu = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int cb = blockIdx.x * 32 + l;
+  const int p = P.parity;
+  Spinor<R> acc;
+#pragma unroll
+  for (int k = 0; k < 12; k++) acc.c[k] = {R(0), R(0)};
+  if (cb < g.Vh) {
+    int c[4];
+    cb_coords(g, cb, p, c);
+    switch (mu) {  // warp-uniform
+      case 0: hop_dir<R, 0>(g, P, c, cb, p, G5IN, false, acc); break;
+      case 1: hop_dir<R, 1>(g, P, c, cb, p, G5IN, false, acc); break;
+      case 2: hop_dir<R, 2>(g, P, c, cb, p, G5IN, false, acc); break;
+      default: hop_dir<R, 3>(g, P, c, cb, p, G5IN, false, acc); break;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 12; k++) part[mu][k][l] = acc.c[k];
+  __syncthreads();
+  if (cb >= g.Vh) return;
+#pragma unroll
+  for (int j = 0; j < 3; j++) {
+    const int k = mu + 4 * j;
+    cx<R> h = part[0][k][l] + part[1][k][l];
+    h = h + part[2][k][l];
+    h = h + part[3][k][l];
+    if (G5OUT && k >= 6) h = -h;
+    cx<R> o = P.b * h;
+    if (EPI == EPI_XPAY) o = P.a * comp_load(P.x, cb, k) + o;
+    comp_store(P.out, cb, k, o);
+  }
+}
+
 // ------------------------------------------------------------------ host side
 template <typename R> static FermView<R> fview(const void *p, int stride);
 template <> FermView<double> fview<double>(const void *p, int stride) { return {(double2 *)p, stride}; }
@@ -521,6 +590,17 @@ static void launch_main(qdp_ctx ctx, const KParams<R, REC> &P, int block) {
   const Geom &g = ctx->geom;
   dslash_kernel<R, REC, EPI, G5IN, G5OUT, HALO, DOT>
       <<<grid_for(g.Vh, block) + P.fuse_npack, block, 0, ctx->stream>>>(g, P);
+}
+
+template <typename R, int REC, int EPI>
+static void launch_four(qdp_ctx ctx, const KParams<R, REC> &P, bool g5i, bool g5o) {
+  if constexpr (EPI == EPI_PLAIN || EPI == EPI_XPAY) {
+    const int grid = grid_for(ctx->geom.Vh, 32);
+#define QDPB_L4(A, B) dslash4_kernel<R, REC, EPI, A, B><<<grid, 128, 0, ctx->stream>>>(ctx->geom, P)
+    if (g5i) { if (g5o) QDPB_L4(true, true); else QDPB_L4(true, false); }
+    else { if (g5o) QDPB_L4(false, true); else QDPB_L4(false, false); }
+#undef QDPB_L4
+  }
 }
 
 template <typename R, int REC, int EPI>
@@ -571,19 +651,57 @@ static void dslash_work(qdp_ctx ctx, const DslashArgs &a) {
   prof_work(ctx, QDP_PK_DSLASH, f * vh, r * vh * sizeof(R));
 }
 
+// The paper's autotuner (section VII) on the launch configuration of the
+// whole-lattice EO dslash, on its payload launches: the candidates in decreasing threads per block
+// -- the four-threads-per-site kernel (128), the main kernel with 64 and with 32 threads -- the
+// first launch takes the largest, later launches probe the next ones until one is 33% slower
+// than the best, and the best is kept for the key (precision, gauge storage, epilogue, volume).
+static int variant_count(int epi, bool dot) { return (!dot && (epi == EPI_PLAIN || epi == EPI_XPAY)) ? 3 : 2; }
+
 template <typename R, int REC>
 static int launch_main_epi(qdp_ctx ctx, const DslashArgs &a, const KParams<R, REC> &P, bool halo, int block) {
   ProfEvent ev;
   prof_begin(ctx, QDP_PK_DSLASH, &ev);
   dslash_work<R, REC>(ctx, a);
   const bool dot = a.dot_x != nullptr;
-  switch (a.epi) {
-    case EPI_PLAIN: launch_main_dispatch<R, REC, EPI_PLAIN>(ctx, P, a.g5_in, a.g5_out, halo, false, block); break;
-    case EPI_XPAY: launch_main_dispatch<R, REC, EPI_XPAY>(ctx, P, a.g5_in, a.g5_out, halo, dot, block); break;
-    case EPI_CLOVINV: launch_main_dispatch<R, REC, EPI_CLOVINV>(ctx, P, a.g5_in, a.g5_out, halo, false, block); break;
-    default: launch_main_dispatch<R, REC, EPI_CLOVXPAY>(ctx, P, a.g5_in, a.g5_out, halo, dot, block); break;
+  auto go = [&](int variant) -> cudaError_t {
+    // variant: 0 = four threads per site (PLAIN / XPAY only), 1 = main kernel with `block`
+    // threads, 2 = main kernel with 32 threads
+    if (variant == 0) {
+      if (a.epi == EPI_PLAIN) launch_four<R, REC, EPI_PLAIN>(ctx, P, a.g5_in, a.g5_out);
+      else launch_four<R, REC, EPI_XPAY>(ctx, P, a.g5_in, a.g5_out);
+      return cudaGetLastError();
+    }
+    const int b = variant == 1 ? block : 32;
+    switch (a.epi) {
+      case EPI_PLAIN: launch_main_dispatch<R, REC, EPI_PLAIN>(ctx, P, a.g5_in, a.g5_out, halo, false, b); break;
+      case EPI_XPAY: launch_main_dispatch<R, REC, EPI_XPAY>(ctx, P, a.g5_in, a.g5_out, halo, dot, b); break;
+      case EPI_CLOVINV: launch_main_dispatch<R, REC, EPI_CLOVINV>(ctx, P, a.g5_in, a.g5_out, halo, false, b); break;
+      default: launch_main_dispatch<R, REC, EPI_CLOVXPAY>(ctx, P, a.g5_in, a.g5_out, halo, dot, b); break;
+    }
+    return cudaGetLastError();
+  };
+  // tuned: whole lattice, no fused reduction (its partial layout follows the block size), no
+  // explicit QDP_OPT_BLOCK
+  if (!halo && !dot && ctx->block == 0 && ctx->dslash_variant >= 0) {  // forced (measurements)
+    const int v = variant_count(a.epi, dot) == 3 ? ctx->dslash_variant : std::max(1, ctx->dslash_variant);
+    const cudaError_t e = go(v);
+    const int rc = prof_end(ctx, &ev);
+    return e != cudaSuccess ? cuda_check(ctx, e, "dslash launch") : rc;
   }
-  return prof_end(ctx, &ev);
+  if (!halo && !dot && ctx->autotune && ctx->block == 0) {
+    const int nv = variant_count(a.epi, dot);
+    const long key = ((((long)(sizeof(R) == 8) * 2 + (REC == 12)) * 4 + a.epi) << 40) + ctx->geom.Vh;
+    int rc = tuned_variant(ctx, key, nv, [&](int v) { return go(nv == 3 ? v : v + 1); });
+    if (rc) {
+      prof_end(ctx, &ev);
+      return rc;
+    }
+    return prof_end(ctx, &ev);
+  }
+  const cudaError_t e = go(1);
+  const int rc = prof_end(ctx, &ev);
+  return e != cudaSuccess ? cuda_check(ctx, e, "dslash launch") : rc;
 }
 
 // Visiting order of the fused boundary kernel for output parity p: sites on no partitioned face
@@ -644,10 +762,9 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
   if (dot && (a.g5_in || !a.g5_out)) return set_error(ctx, QDP_EINVAL, "fused dot: Mhat^dag output step only");
   // peer-to-peer: packing, interior and remote hops in the one main kernel (KParams::fuse), for
   // every split (t: the face sites are the two end slabs of the cb order, found by arithmetic;
-  // others: a site table, interior sites first).  QDPB_FUSE=0: separate pack / interior /
-  // exterior kernels (kept for comparison).
-  static const int fuse_env = getenv("QDPB_FUSE") ? atoi(getenv("QDPB_FUSE")) : 1;
-  const bool fuse = halo && ctx->p2p_on && fuse_env != 0;
+  // others: a site table, interior sites first).  Otherwise separate pack / interior /
+  // exterior kernels (QDP_OPT_FUSE = 0, kept for comparison).
+  const bool fuse = halo && ctx->p2p_on && ctx->fuse;
   // partial-sum layout of the fused inner product: interior blocks, then each exterior's blocks
   int nparts = 0, ext_off[4] = {0, 0, 0, 0};
   int pack_off[5] = {0, 0, 0, 0, 0};
@@ -656,6 +773,9 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
   static const int pack_cap =
       std::max(1, getenv("QDPB_PACK_BLOCKS") ? atoi(getenv("QDPB_PACK_BLOCKS")) : 2 * 148);  // measured: 260.0 -> 257.7 us
   const int npack = fuse ? std::min(grid_for(pack_off[4], block), pack_cap) : 0;
+  // fused inner product: finished inside the main kernel when every partial is produced there
+  // (whole lattice, or the fused boundary); else block partials + a final pass
+  const bool red_fin = dot && (!halo || fuse);
   if (dot) {
     nparts = grid_for(g.Vh, block) + npack;
     for (int mu = 0; mu < 4; mu++)
@@ -750,7 +870,13 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
         if ((rc = comm_exchange(ctx, prec, face_bytes, ctx->stream))) return rc;
       }
     }
+    bool red_after = false;
+    if (red_fin) {  // takes the peer sum's sequence number: right before the launch
+      if ((rc = red_setup(ctx, grid_for(g.Vh, block) + npack, a.dot_slot, 2, true, false, &P.red, &red_after))) return rc;
+      P.red_fin = 1;
+    }
     if ((rc = launch_main_epi<R, REC>(ctx, a, P, true, block))) return rc;
+    if (red_fin) return red_after ? reduce_global(ctx, a.dot_slot, 2) : QDP_OK;
     if (overlap) QDP_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_comm, 0));
     for (int mu = 0; mu < 4; mu++) {
       if (!((g.part >> mu) & 1) || fuse) continue;
@@ -766,7 +892,13 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
       if ((rc = prof_end(ctx, &ev))) return rc;
     }
   } else {
+    bool red_after = false;
+    if (red_fin) {
+      if ((rc = red_setup(ctx, grid_for(g.Vh, block), a.dot_slot, 2, true, false, &P.red, &red_after))) return rc;
+      P.red_fin = 1;
+    }
     if ((rc = launch_main_epi<R, REC>(ctx, a, P, false, block))) return rc;
+    if (red_fin) return red_after ? reduce_global(ctx, a.dot_slot, 2) : QDP_OK;
   }
   if (dot) {
     if ((rc = reduce_partials(ctx, nparts, a.dot_slot))) return rc;

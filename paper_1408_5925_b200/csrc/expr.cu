@@ -276,6 +276,48 @@ int tuned_launch(qdp_ctx ctx, long key, const std::function<cudaError_t(int)> &g
   return QDP_OK;
 }
 
+// The same rule over an ordered list of launch variants (index 0 = the most threads per block):
+// variant 0 first (the next one if it fails to launch), then probe 1, 2, ... on later payload
+// launches until one is 33% slower than the best or the list ends; keep the best.
+int tuned_variant(qdp_ctx ctx, long key, int nvar, const std::function<cudaError_t(int)> &go) {
+  Tune &t = ctx->tune[key ^ (1L << 62)];
+  if (!t.a) {
+    cudaEventCreate(&t.a);
+    cudaEventCreate(&t.b);
+    t.block = 0;
+  }
+  if (t.pending) {
+    float ms = 0.f;
+    QDP_CUDA(ctx, cudaEventSynchronize(t.b));
+    QDP_CUDA(ctx, cudaEventElapsedTime(&ms, t.a, t.b));
+    t.pending = false;
+    if (t.best_ms == 0.f || ms < t.best_ms) {
+      t.best_ms = ms;
+      t.best_block = t.block;
+    }
+    if (ms > 1.33f * t.best_ms || t.block + 1 >= nvar) {
+      t.state = 2;
+      t.block = t.best_block;
+    } else {
+      t.block++;
+    }
+  }
+  if (t.state != 2) QDP_CUDA(ctx, cudaEventRecord(t.a, ctx->stream));
+  cudaError_t err;
+  for (;;) {
+    err = go(t.block);
+    if (err == cudaSuccess || t.state != 0 || t.block + 1 >= nvar) break;
+    t.block++;  // could not launch (resources): the next variant
+  }
+  if (err != cudaSuccess) return cuda_check(ctx, err, "tuned launch");
+  if (t.state != 2) {
+    QDP_CUDA(ctx, cudaEventRecord(t.b, ctx->stream));
+    t.pending = true;
+    t.state = 1;
+  }
+  return QDP_OK;
+}
+
 // One Table II expression: the paper's autotuner on its payload launches.
 int expr_eval(qdp_ctx ctx, int expr, qdp_field out, const qdp_field a, const qdp_field b, const qdp_field c) {
   const Geom &g = ctx->geom;

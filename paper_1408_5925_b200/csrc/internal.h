@@ -57,6 +57,7 @@ template <typename R, int REC> constexpr int dslash_minb() {
 #ifndef QDPB_DSLASH_BLOCK
 #define QDPB_DSLASH_BLOCK 64
 #endif
+#define PEER_MAX_RANKS 16
 
 namespace qdpb {
 
@@ -224,6 +225,10 @@ __device__ __forceinline__ void grid_signal_last(unsigned *counter, unsigned *f0
     }
   }
 }
+
+}  // namespace qdpb
+#include "reduce.cuh"
+namespace qdpb {
 
 // Spinor: 12 complex, index 3*spin + colour.
 template <typename R> struct Spinor { cx<R> c[12]; };
@@ -491,7 +496,6 @@ size_t host_site_reals(int kind);                           // 24 / 72 / 288
 struct Comm;      // comm.cpp
 struct P2P;       // p2p.cu
 struct PeerComm;  // peer.cu
-#define PEER_MAX_RANKS 16
 
 struct ProfEvent {
   int cls;
@@ -518,14 +522,21 @@ struct qdp_ctx_s {
   cudaEvent_t ev_packed = nullptr, ev_comm = nullptr;
   // options
   int overlap = 1, self_halo = 0, profiling = 0, block = 0, det_reduce = 1, self_nccl = 0;
+  int fuse = 1;  // QDP_OPT_FUSE (default: env QDPB_FUSE, else 1)
+  int dslash_variant = -1;  // QDP_OPT_DSLASH_VARIANT: -1 tuned, else the forced launch variant
   // scratch (device)
   void *staging = nullptr;
   size_t staging_bytes = 0;
   double *red_partials = nullptr;  // per-block partial sums (2 doubles per block)
+  double *red_partials2 = nullptr; // per-group partial sums of the one-launch reductions (reduce.cuh)
+  unsigned *red_cnt = nullptr;     // their counters: [0] top, [1 + g] groups (zero between launches)
   int red_capacity = 0;            // number of blocks
   double *red_result = nullptr;    // device scalars: [0..7]
   double *red_gather = nullptr;    // [nranks * 2] gathered per-rank sums
-  double *host_pinned = nullptr;   // pinned host scratch (64 doubles)
+  double *host_pinned = nullptr;   // pinned host scratch (64 doubles; [32..40): reduction results)
+  double *cg_hist = nullptr;       // mapped pinned |r_k|^2 of the device-side CG bookkeeping
+  int cg_hist_cap = 0;
+  int *cg_stop = nullptr;          // device: first iteration that stops the CG (reduce.cuh CgDev)
   void *cg_work = nullptr;         // persistent CG work vectors
   size_t cg_work_bytes = 0;
   // halo buffers: [prec][mu][dir] for send and recv (dir 0 = to/from -mu, 1 = to/from +mu)
@@ -593,18 +604,34 @@ int field_copy_parity(qdp_ctx ctx, int kind, int prec, void *dst, const void *sr
 // y = a x + y
 int blas_axpy(qdp_ctx ctx, int prec, double ar, double ai, const void *x, void *y, int nblk);
 // partial sums -> red_result[slot] (and slot+1 for the imaginary part)
-int blas_norm2(qdp_ctx ctx, int prec, const void *a, int nblk, int slot);
-int blas_inner(qdp_ctx ctx, int prec, const void *a, const void *b, int nblk, int slot);
+// GLOBAL sums (over all ranks), one launch with a peer communicator; host: also into
+// host_pinned + 32 (read_red_host)
+int blas_norm2(qdp_ctx ctx, int prec, const void *a, int nblk, int slot, bool host = false);
+int blas_inner(qdp_ctx ctx, int prec, const void *a, const void *b, int nblk, int slot, bool host = false);
 // sum nparts block partial pairs in red_partials -> red_result[slot], [slot+1]
 int reduce_partials(qdp_ctx ctx, int nparts, int slot);
+#ifdef __CUDACC__
+// Arguments of a reduction that finishes inside its producing kernel of nblk blocks (reduce.cuh):
+// res[slot .. slot+n); global: summed over the ranks -- in the kernel with a peer communicator
+// (*after = false), else by reduce_global after the launch (*after = true); host: also store the
+// values into ctx->host_pinned + 32 (read them with read_red_host).  Takes the peer sum's
+// sequence number: call it right before the launch.
+int red_setup(qdp_ctx ctx, int nblk, int slot, int n, bool global, bool host, RedArgs *R, bool *after);
+#endif
+int read_red_host(qdp_ctx ctx, int n, double *out);  // synchronise, then ctx->host_pinned[32 ..]
 // finish a reduction: cross-rank sum of red_result[slot..slot+n-1]
 int reduce_global(qdp_ctx ctx, int slot, int n);
 // CG helpers (device scalars in red_result)
-// r -= alpha q ; red_result[rr_slot] = |r|^2 (global), alpha = res[rho] / res[pq]
-int blas_cg_update_r(qdp_ctx ctx, int prec, void *r, const void *q, int rho_slot, int pq_slot, int rr_slot);
-// x += alpha p ; if update_p: p = r + beta p with beta = res[rr] / res[rho]
+// r -= alpha q ; red_result[rr_slot] = |r|^2 (global), alpha = res[rho] / res[pq].  cg (optional):
+// the device-side bookkeeping of iteration cg->k (skip when *cg->stop < cg->k; record |r_k|^2)
+#ifdef __CUDACC__
+int blas_cg_update_r(qdp_ctx ctx, int prec, void *r, const void *q, int rho_slot, int pq_slot, int rr_slot,
+                     const CgDev *cg = nullptr);
+#endif
+// x += alpha p ; if update_p: p = r + beta p with beta = res[rr] / res[rho].  stop (optional):
+// skip when *stop < iter, no p update when *stop == iter (iteration `iter` is the last)
 int blas_cg_update_xp(qdp_ctx ctx, int prec, void *x, void *p, const void *r, int rho_slot, int pq_slot, int rr_slot,
-                      bool update_p);
+                      bool update_p, const int *stop = nullptr, int iter = 0);
 int blas_xpay(qdp_ctx ctx, int prec, const void *x, double a, void *y, int nblk);  // y = x + a y
 // p = r + beta p with beta = res[rr] / res[rho]
 int blas_cg_update_p(qdp_ctx ctx, int prec, void *p, const void *r, int rho_slot, int rr_slot);
@@ -675,6 +702,8 @@ int expr_eval(qdp_ctx ctx, int expr, qdp_field out, const qdp_field a, const qdp
 void tune_release(qdp_ctx ctx);
 // the paper's block-size autotuner around go(block), per key (expr.cu)
 int tuned_launch(qdp_ctx ctx, long key, const std::function<cudaError_t(int)> &go);
+// the same rule over nvar launch variants ordered by decreasing threads per block (dslash.cu)
+int tuned_variant(qdp_ctx ctx, long key, int nvar, const std::function<cudaError_t(int)> &go);
 
 // jit.cu: run-time generated site-expression kernels (qdp_jit_eval)
 struct JitKernel;
@@ -704,6 +733,10 @@ int peer_init(qdp_ctx ctx);
 void peer_destroy(qdp_ctx ctx);
 int host_allgather(qdp_ctx ctx, const void *send, void *recv, size_t bytes);  // set-up only
 int peer_allreduce(qdp_ctx ctx, int slot, int n);  // red_result[slot..slot+n) summed over ranks, rank order
+#ifdef __CUDACC__
+PeerArgs peer_args(qdp_ctx ctx);
+#endif
+unsigned peer_next_sum_seq(qdp_ctx ctx);
 // copy `bytes` of a packed face into rank `to`'s mailbox and wait for this rank's own
 // mailbox to receive the face of the same call; *ghost = the mailbox, *seq for release
 int peer_sendrecv(qdp_ctx ctx, const void *send, size_t bytes, int to, void **ghost, unsigned *seq);

@@ -185,7 +185,7 @@ int cg_solve_multishift(qdp_field *x, int n, const double *sigma, const qdp_fiel
   }
   if ((rc = copy_blocks(ctx, prec, r, phi_o, 1))) return rc;
   double rho0 = 0.0;
-  if ((rc = blas_norm2(ctx, prec, r, 1, S_RHO)) || (rc = reduce_global(ctx, S_RHO, 1)) ||
+  if ((rc = blas_norm2(ctx, prec, r, 1, S_RHO)) ||
       (rc = read_slots(ctx, S_RHO, 1, &rho0)))
     return rc;
   if (hist_cap > 0 && hist) hist[0] = 1.0;
@@ -228,7 +228,7 @@ int cg_solve_multishift(qdp_field *x, int n, const double *sigma, const qdp_fiel
       if ((rc = mhat_apply(ctx, U, A, Ainv, mass, t, q, mp, true, P.x[i], S_PQ, sigma[i]))) return rc;
       if ((rc = blas_xpay(ctx, prec, phi_o, -1.0, q, 1))) return rc;
       double rr;
-      if ((rc = blas_norm2(ctx, prec, q, 1, S_RR)) || (rc = reduce_global(ctx, S_RR, 1)) ||
+      if ((rc = blas_norm2(ctx, prec, q, 1, S_RR)) ||
           (rc = read_slots(ctx, S_RR, 1, &rr)))
         return rc;
       true_resid[i] = rho0 > 0 ? sqrt(rr / rho0) : 0.0;

@@ -37,14 +37,9 @@
 namespace qdpb {
 
 constexpr int MAXR = PEER_MAX_RANKS;
-constexpr size_t HDR_BYTES = 4096;
-constexpr size_t VAL_BYTES = sizeof(double) * 2 * MAXR * 8;
+constexpr size_t HDR_BYTES = PEER_HDR_BYTES;
+constexpr size_t VAL_BYTES = PEER_VAL_BYTES;
 static_assert(sizeof(unsigned) * (2 * MAXR + 4) <= HDR_BYTES, "peer board header");
-
-struct BoardHdr {
-  unsigned sum_flag[2][MAXR];
-  unsigned shift_arrived, shift_consumed, put_counter, err;
-};
 
 struct PeerComm {
   char *board = nullptr;        // this rank's board
@@ -54,46 +49,15 @@ struct PeerComm {
   std::vector<void *> opened;
 };
 
-struct PeerArgs {
-  char *board[MAXR];
-  int nranks, me;
-};
+__device__ __forceinline__ BoardHdr *hdr(char *b) { return board_hdr(b); }
 
-__device__ __forceinline__ BoardHdr *hdr(char *b) { return (BoardHdr *)b; }
-__device__ __forceinline__ double *vals(char *b, int slot, int src) {
-  return (double *)(b + HDR_BYTES) + ((size_t)slot * MAXR + src) * 8;
-}
-
-// One thread: the allgather-and-sum of n <= 8 doubles at res[slot ..] (see the header).
+// One thread: the allgather-and-sum of n <= 8 doubles at res[slot ..] (reduce.cuh peer_sum_dev).
 __global__ void peer_sum_kernel(const PeerArgs a, double *res, int slot, int n, unsigned seq) {
   if (threadIdx.x != 0) return;
-  const int s = seq & 1;
   double v[8];
   for (int i = 0; i < n; i++) v[i] = res[slot + i];
-  for (int q = 0; q < a.nranks; q++) {
-    char *b = a.board[q];
-    double *d = vals(b, s, a.me);
-    for (int i = 0; i < n; i++) d[i] = v[i];
-    st_release_sys(&hdr(b)->sum_flag[s][a.me], seq);  // orders this thread's stores above
-  }
-  char *mine = a.board[a.me];
-  BoardHdr *h = hdr(mine);
-  for (int q = 0; q < a.nranks; q++) {
-    long k = 0;
-    while ((int)(ld_acquire_sys(&h->sum_flag[s][q]) - seq) < 0) {
-      if (++k > (1L << 26)) {
-        atomicExch(&h->err, 1u);
-        break;
-      }
-      __nanosleep(64);
-    }
-  }
-  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int q = 0; q < a.nranks; q++) {
-    const volatile double *src = vals(mine, s, q);
-    for (int i = 0; i < n; i++) acc[i] += src[i];
-  }
-  for (int i = 0; i < n; i++) res[slot + i] = acc[i];
+  peer_sum_dev(a, v, n, seq);
+  for (int i = 0; i < n; i++) res[slot + i] = v[i];
 }
 
 // Sender side of a shift face: wait for the receiver's mailbox, copy, publish.
@@ -116,7 +80,9 @@ __global__ void peer_mark_consumed_kernel(char *board, unsigned seq) {
   if (threadIdx.x == 0) st_release_sys(&hdr(board)->shift_consumed, seq);
 }
 
-static PeerArgs peer_args(qdp_ctx ctx) {
+unsigned peer_next_sum_seq(qdp_ctx ctx) { return ++ctx->peer->sum_seq; }
+
+PeerArgs peer_args(qdp_ctx ctx) {
   PeerArgs a;
   memset(&a, 0, sizeof(a));
   for (int q = 0; q < ctx->nranks; q++) a.board[q] = ctx->peer->peer[q];
@@ -178,7 +144,7 @@ int peer_allreduce(qdp_ctx ctx, int slot, int n) {
   if (n > 8) return set_error(ctx, QDP_EINVAL, "peer sum: at most 8 scalars");
   ProfEvent ev;
   prof_begin(ctx, QDP_PK_REDUCE, &ev);
-  peer_sum_kernel<<<1, 32, 0, ctx->stream>>>(peer_args(ctx), ctx->red_result, slot, n, ++ctx->peer->sum_seq);
+  peer_sum_kernel<<<1, 32, 0, ctx->stream>>>(peer_args(ctx), ctx->red_result, slot, n, peer_next_sum_seq(ctx));
   return prof_end(ctx, &ev);
 }
 

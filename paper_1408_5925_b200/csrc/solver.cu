@@ -18,13 +18,18 @@
 // is accumulated into the fp64 x and the fp64 residual c - Mhat^dag Mhat x is recomputed.
 // Convergence is only ever declared on an fp64 residual.
 #include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
 
 #include "internal.h"
 
 namespace qdpb {
 
 namespace {
-enum { S_RHO = 0, S_PQ = 2, S_RR = 4, S_TRUE = 6 };
+enum { S_RHO = 0, S_PQ = 2, S_RR = 4, S_TRUE = 6, S_RHO0 = 14 };
 
 struct Op {
   qdp_ctx ctx;
@@ -167,9 +172,9 @@ int finish_solve(const Op &op, const qdp_field x, const qdp_field b, const qdp_f
   }
   if ((rc = blas_xpay(ctx, op.prec, b->data, -1.0, tmp, 2))) return rc;
   double rr, bb;
-  if ((rc = blas_norm2(ctx, op.prec, tmp, 2, S_RR)) || (rc = reduce_global(ctx, S_RR, 1)) || (rc = read_slot(ctx, S_RR, &rr)))
+  if ((rc = blas_norm2(ctx, op.prec, tmp, 2, S_RR)) || (rc = read_slot(ctx, S_RR, &rr)))
     return rc;
-  if ((rc = blas_norm2(ctx, op.prec, b->data, 2, S_RR)) || (rc = reduce_global(ctx, S_RR, 1)) ||
+  if ((rc = blas_norm2(ctx, op.prec, b->data, 2, S_RR)) ||
       (rc = read_slot(ctx, S_RR, &bb)))
     return rc;
   *true_resid = bb > 0 ? sqrt(rr / bb) : 0.0;
@@ -184,6 +189,26 @@ int mhat_apply(qdp_ctx ctx, const qdp_field U, const qdp_field A, const qdp_fiel
   return apply_mhat(make_op(ctx, U, A, Ainv, mass, t), out, v, dag, dot_x, dot_slot, dot_shift);
 }
 
+// Iterations per host round trip of cg_solve: all of them up to QDPB_CG_CHUNK (default 16) while
+// the residual history says convergence is further away; fewer near the end (so few iterations
+// are enqueued past the stopping one -- they run as no-ops); 1 = a host read every iteration.
+static int cg_chunk(const double *hist_raw, int k, int maxit, double tol2rho0) {
+  static const int cmax = getenv("QDPB_CG_CHUNK") ? std::max(1, atoi(getenv("QDPB_CG_CHUNK"))) : 16;
+  int c = std::min(cmax, maxit - k);
+  if (tol2rho0 > 0.0) {
+    if (k < 2) return std::min(c, 2);
+    const int m = std::min(k, 4);
+    const double rate = pow(hist_raw[k] / hist_raw[k - m], 1.0 / m);  // per-iteration factor of |r|^2
+    if (rate < 1.0 && rate > 0.0) {
+      const double left = log(tol2rho0 / hist_raw[k]) / log(rate);
+      c = std::min(c, std::max(1, (int)(0.75 * left)));
+    } else {
+      c = std::min(c, 2);
+    }
+  }
+  return std::max(1, c);
+}
+
 int cg_solve(qdp_field x, const qdp_field b, const qdp_field U, const qdp_field A, const qdp_field Ainv, double mass,
              double tol, int maxit, int *iters_out, double *hist, int hist_cap, double *true_resid) {
   qdp_ctx ctx = x->ctx;
@@ -195,6 +220,19 @@ int cg_solve(qdp_field x, const qdp_field b, const qdp_field U, const qdp_field 
   // work: [t | r | p | q | mp | bh], persistent in the context (every block is fully
   // written before it is read, so no clearing is needed)
   if ((rc = ensure_cg_work(ctx, 6 * blk))) return rc;
+  // device-side bookkeeping: |r_k|^2 history in mapped pinned memory, the stop word on the device
+  if (ctx->cg_hist_cap < maxit + 1) {
+    if (ctx->cg_hist) {
+      QDP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+      cudaFreeHost(ctx->cg_hist);
+      ctx->cg_hist = nullptr;
+      ctx->cg_hist_cap = 0;
+    }
+    const int cap = std::max(maxit + 1, 1024);
+    QDP_CUDA(ctx, cudaHostAlloc((void **)&ctx->cg_hist, sizeof(double) * cap, cudaHostAllocMapped));
+    ctx->cg_hist_cap = cap;
+  }
+  if (!ctx->cg_stop) QDP_CUDA(ctx, cudaMalloc((void **)&ctx->cg_stop, sizeof(int)));
   char *work = (char *)ctx->cg_work;
   const Op op = make_op(ctx, U, A, Ainv, mass, work);
   void *r = work + blk, *p = work + 2 * blk, *q = work + 3 * blk, *mp = work + 4 * blk, *bh = work + 5 * blk;
@@ -208,30 +246,56 @@ int cg_solve(qdp_field x, const qdp_field b, const qdp_field U, const qdp_field 
   QDP_CUDA(ctx, cudaMemsetAsync(x_o, 0, blk, ctx->stream));
   if ((rc = apply_mhat(op, r, bh, true))) return rc;
   if ((rc = copy_blocks(ctx, prec, p, r, 1))) return rc;
-  if ((rc = blas_norm2(ctx, prec, r, 1, S_RHO)) || (rc = reduce_global(ctx, S_RHO, 1)) || (rc = read_slot(ctx, S_RHO, &rho0)))
+  if ((rc = blas_norm2(ctx, prec, r, 1, S_RHO)) || (rc = copy_scalars(ctx, S_RHO0, S_RHO, 1)) ||
+      (rc = read_slot(ctx, S_RHO, &rho0)))
     return rc;
   if (hist_cap > 0 && hist) hist[0] = 1.0;
   if (rho0 == 0.0) status = QDP_OK;
 
+  // Iterations run in chunks without host round trips: alpha, beta and |r|^2 stay on the device
+  // (rho of iteration k in slot S_RHO / S_RR alternately), the final block of the r update
+  // records |r_k|^2 and the stopping iteration (reduce.cuh CgDev), and the vector updates of a
+  // later iteration do nothing.  The history and the stop are read once per chunk.
+  volatile int *stop_host = (volatile int *)(ctx->host_pinned + 40);
+  *stop_host = 0x7f7f7f7f;
+  QDP_CUDA(ctx, cudaMemsetAsync(ctx->cg_stop, 0x7f, sizeof(int), ctx->stream));
+  const double tol2 = tol * tol;
+  const int rs[2] = {S_RHO, S_RR};
+  std::vector<double> snap_f((size_t)QDP_PK_COUNT * 17), snap_b((size_t)QDP_PK_COUNT * 17);
   while (status == QDP_NOT_CONVERGED && k < maxit) {
-    // q = Mhat^dag Mhat p, with Re<p, q> -> S_PQ fused into the last launch
-    if ((rc = apply_mhat(op, mp, p, false))) return rc;
-    if ((rc = apply_mhat(op, q, mp, true, p, S_PQ))) return rc;
-    // r -= alpha q ; rr = |r|^2
-    if ((rc = blas_cg_update_r(ctx, prec, r, q, S_RHO, S_PQ, S_RR))) return rc;
-    double rho_new;
-    if ((rc = read_slot(ctx, S_RR, &rho_new))) return rc;
-    k++;
-    if (hist && k < hist_cap) hist[k] = sqrt(rho_new / rho0);
-    const bool done = rho_new <= tol * tol * rho0;
-    // x += alpha p ; p = r + beta p (skipped on the last iteration)
-    const bool last = done || k == maxit;
-    if ((rc = blas_cg_update_xp(ctx, prec, x_o, p, r, S_RHO, S_PQ, S_RR, !last))) return rc;
-    if (done) {
-      status = QDP_OK;
+    const int c = cg_chunk(ctx->cg_hist, k, maxit, tol2 * rho0);
+    snap_f.resize((size_t)QDP_PK_COUNT * (c + 1));
+    snap_b.resize((size_t)QDP_PK_COUNT * (c + 1));
+    for (int j = 1; j <= c; j++) {
+      const int it = k + j;
+      const int rho = rs[(it - 1) & 1], rr = rs[it & 1];
+      // q = Mhat^dag Mhat p, with Re<p, q> -> S_PQ fused into the last launch
+      // (after the stopping iteration these still run -- the predictor keeps that rare -- but the
+      // two updates below do nothing, so x, r and the history stay those of the stopping one)
+      if ((rc = apply_mhat(op, mp, p, false))) return rc;
+      if ((rc = apply_mhat(op, q, mp, true, p, S_PQ))) return rc;
+      // r -= alpha q ; |r|^2 ; records |r_it|^2 and whether it stops here
+      const CgDev cg = {ctx->cg_hist, ctx->cg_stop, (int *)stop_host, ctx->red_result + S_RHO0, it, maxit, tol2};
+      if ((rc = blas_cg_update_r(ctx, prec, r, q, rho, S_PQ, rr, &cg))) return rc;
+      // x += alpha p ; p = r + beta p (not on the stopping iteration)
+      if ((rc = blas_cg_update_xp(ctx, prec, x_o, p, r, rho, S_PQ, rr, it < maxit, ctx->cg_stop, it))) return rc;
+      memcpy(&snap_f[(size_t)QDP_PK_COUNT * j], ctx->work_flops, sizeof(double) * QDP_PK_COUNT);
+      memcpy(&snap_b[(size_t)QDP_PK_COUNT * j], ctx->work_bytes, sizeof(double) * QDP_PK_COUNT);
+    }
+    QDP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    const int s = *stop_host;
+    const int last = std::min(s, k + c);
+    for (int it = k + 1; it <= last; it++)
+      if (hist && it < hist_cap) hist[it] = sqrt(ctx->cg_hist[it] / rho0);
+    if (s <= k + c) {  // stopped inside this chunk: the iterations after s did no work
+      memcpy(ctx->work_flops, &snap_f[(size_t)QDP_PK_COUNT * (s - k)], sizeof(double) * QDP_PK_COUNT);
+      memcpy(ctx->work_bytes, &snap_b[(size_t)QDP_PK_COUNT * (s - k)], sizeof(double) * QDP_PK_COUNT);
+      if (s < maxit) prof_work(ctx, QDP_PK_BLAS, -48.0 * g.Vh, -48.0 * g.Vh * (prec == QDP_F64 ? 8 : 4));
+      k = s;
+      if (ctx->cg_hist[s] <= tol2 * rho0) status = QDP_OK;
       break;
     }
-    if ((rc = copy_slot(ctx, S_RHO, S_RR))) return rc;
+    k += c;
   }
   if (iters_out) *iters_out = k;
   if ((rc = finish_solve(op, x, b, A, r, true_resid))) return rc;  // r | p: a two-block scratch
@@ -265,7 +329,7 @@ int cg_solve_mixed(qdp_field x, const qdp_field b, const qdp_field U, const qdp_
   QDP_CUDA(ctx, cudaMemsetAsync(x_o, 0, b64, ctx->stream));
   QDP_CUDA(ctx, cudaMemsetAsync(xs, 0, b32, ctx->stream));
   if ((rc = copy_blocks(ctx, QDP_F64, r, c, 1))) return rc;
-  if ((rc = blas_norm2(ctx, QDP_F64, r, 1, S_RHO)) || (rc = reduce_global(ctx, S_RHO, 1)) ||
+  if ((rc = blas_norm2(ctx, QDP_F64, r, 1, S_RHO)) ||
       (rc = read_slot(ctx, S_RHO, &rho0)))
     return rc;
   if ((rc = blas_convert(ctx, rs, QDP_F32, r))) return rc;
@@ -295,7 +359,7 @@ int cg_solve_mixed(qdp_field x, const qdp_field b, const qdp_field U, const qdp_
     if ((rc = copy_blocks(ctx, QDP_F64, r, c, 1))) return rc;
     if ((rc = blas_axpy(ctx, QDP_F64, -1.0, 0.0, q, r, 1))) return rc;
     double rt;
-    if ((rc = blas_norm2(ctx, QDP_F64, r, 1, S_TRUE)) || (rc = reduce_global(ctx, S_TRUE, 1)) ||
+    if ((rc = blas_norm2(ctx, QDP_F64, r, 1, S_TRUE)) ||
         (rc = read_slot(ctx, S_TRUE, &rt)))
       return rc;
     nrel++;

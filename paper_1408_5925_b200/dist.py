@@ -8,22 +8,34 @@ from __future__ import annotations
 import numpy as np
 
 
-def proc_grid_for(n: int, global_dims, split=(3, 2)):
+def proc_grid_for(n: int, global_dims, split=(3, 2), caps=None):
     """Rank grid P (P0,P1,P2,P3) for n ranks: factor n over the dims in `split` order
-    (t first, then z), keeping every local extent even.  Raises if impossible."""
+    (t first, then z), keeping every local extent even and P[mu] <= caps[mu] where given.
+    Raises if impossible."""
     P = [1, 1, 1, 1]
     rem = n
+    caps = caps or {}
     for mu in split:
         while rem > 1:
             f = next((k for k in range(2, rem + 1) if rem % k == 0), rem)
             loc = global_dims[mu] // (P[mu] * f)
-            if global_dims[mu] % (P[mu] * f) or loc < 2 or loc % 2:
+            if global_dims[mu] % (P[mu] * f) or loc < 2 or loc % 2 or P[mu] * f > caps.get(mu, n):
                 break
             P[mu] *= f
             rem //= f
     if rem != 1:
         raise ValueError(f"cannot split {global_dims} over {n} ranks along dims {split}")
     return tuple(P)
+
+
+CONFIG5_DIMS = (48, 48, 48, 96)
+
+
+def config5_grid(n: int):
+    """Rank grid of BASELINE.json config 5 (48^3 x 96 even-odd CG, "t x z decomposition"):
+    t first, at most 4 ranks along t, then z -- so 8 ranks give P = (1,1,2,4) (local
+    48 x 48 x 24 x 24); 2 and 4 ranks split t only."""
+    return proc_grid_for(n, CONFIG5_DIMS, split=(3, 2), caps={3: 4})
 
 
 def rank_coords(rank: int, P):

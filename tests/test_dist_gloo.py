@@ -56,6 +56,9 @@ def test_proc_grid_and_neighbours():
     assert qd.proc_grid_for(8, (40, 40, 40, 256)) == (1, 1, 1, 8)
     assert qd.proc_grid_for(8, (48, 48, 48, 96)) == (1, 1, 1, 8)
     assert qd.proc_grid_for(4, (8, 8, 8, 4)) == (1, 1, 2, 2)   # t runs out (local t must stay even)
+    # config 5: the t x z decomposition of BASELINE.json (at most 4 ranks along t)
+    assert [qd.config5_grid(n) for n in (1, 2, 4, 8)] == [(1, 1, 1, 1), (1, 1, 1, 2), (1, 1, 1, 4), (1, 1, 2, 4)]
+    assert qd.proc_grid_for(8, (48, 48, 48, 96), caps={3: 2}) == (1, 1, 4, 2)
     with pytest.raises(ValueError):
         qd.proc_grid_for(3, (4, 4, 4, 4))
     P = (1, 1, 2, 4)

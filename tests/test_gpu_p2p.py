@@ -64,25 +64,31 @@ def test_dslash_p2p_self(q, prec, mask, overlap):
 
 
 @pytest.mark.timeout(120)
-def test_dslash_p2p_separate_kernels_env(q):
-    """QDPB_FUSE=0 (separate pack / interior / exterior kernels) in a subprocess: same result."""
-    import os
-    import subprocess
-    import sys
-    code = ("import sys; sys.path[:0] = ['.', 'tests']; import numpy as np, fieldgen, oracle; "
-            "from _physics import rel_site_err; from paper_1408_5925_b200 import qdpb as q; "
-            "L = (4, 6, 4, 8); U = fieldgen.random_gauge(L, 2101); psi = fieldgen.random_spinor(L, 3101); "
-            "c = q.qdp_init(L); q.qdp_set_option(c, q.QDP_OPT_SELF_HALO, 12); q.qdp_set_option(c, q.QDP_OPT_P2P, 1); "
-            "fU = q.qdp_field_alloc(c, q.QDP_GAUGE, 0, q.QDP_ALL); q.qdp_field_import(fU, U); "
-            "fp = q.qdp_field_alloc(c, q.QDP_FERMION, 0, q.QDP_ALL); q.qdp_field_import(fp, psi); "
-            "fo = q.qdp_field_alloc(c, q.QDP_FERMION, 0, q.QDP_ALL); ref = oracle.hopping(U, psi, L, -1); "
-            "[q.qdp_dslash(fo, fU, fp, q.QDP_ALL) for _ in range(3)]; q.qdp_synchronize(c); "
-            "e = rel_site_err(q.qdp_field_export(fo), ref); n = q.qdp_profile_query(c, q.QDP_PK_PACK)[0]; "
-            "print(e, n); assert e <= 1e-13 and n == 12")
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, QDPB_FUSE="0"),
-                       capture_output=True, text=True, timeout=100)
-    assert r.returncode == 0, r.stdout + r.stderr
+@pytest.mark.parametrize("mask", [8, 12])
+def test_dslash_p2p_separate_kernels(q, mask):
+    """QDP_OPT_FUSE = 0: separate pack / interior / exterior kernels, same result."""
+    L = (4, 6, 4, 8)
+    U = fieldgen.random_gauge(L, 2101)
+    psi = fieldgen.random_spinor(L, 3101)
+    ref = oracle.hopping(U, psi, L, -1)
+    c = _ctx(q, L, mask)
+    q.qdp_set_option(c, q.QDP_OPT_FUSE, 0)
+    try:
+        fU = _field(q, c, q.QDP_GAUGE, 0, q.QDP_ALL, U)
+        fp = _field(q, c, q.QDP_FERMION, 0, q.QDP_ALL, psi)
+        fo = q.qdp_field_alloc(c, q.QDP_FERMION, 0, q.QDP_ALL)
+        for _ in range(3):
+            q.qdp_dslash(fo, fU, fp, q.QDP_ALL)
+            q.qdp_synchronize(c)
+            assert rel_site_err(q.qdp_field_export(fo), ref) <= 1e-13
+        n_pack, _ = q.qdp_profile_query(c, q.QDP_PK_PACK)
+        assert n_pack == 6 * bin(mask).count("1")
+        q.qdp_set_option(c, q.QDP_OPT_FUSE, 1)  # switching back mid-sequence keeps the protocol
+        q.qdp_dslash(fo, fU, fp, q.QDP_ALL)
+        q.qdp_synchronize(c)
+        assert rel_site_err(q.qdp_field_export(fo), ref) <= 1e-13
+    finally:
+        q.qdp_finalize(c)
 
 
 @pytest.mark.timeout(120)
