@@ -938,6 +938,11 @@ def measure_tts(b, ctx, fU, fA, fAi, fb, fx, U, bsrc):
                                                                          mass=MASS, tol=1e-10, delta=1e-2, maxit=5000),
             "mixed_fp32_recon12_delta1e-3": lambda: q.qdp_cg_solve_mixed(fx, fb, fU, fA, fAi, fU32r, fA32, fAi32,
                                                                          mass=MASS, tol=1e-10, delta=1e-3, maxit=5000),
+            # 16-bit sloppy level (int16 links / clover / directions, built from the fp64 fields in the call)
+            "mixed_h16_delta1e-1": lambda: q.qdp_cg_solve_mixed16(fx, fb, fU, fA, fAi, mass=MASS, tol=1e-10,
+                                                                  delta=0.1, maxit=5000),
+            "mixed_h16_delta1e-2": lambda: q.qdp_cg_solve_mixed16(fx, fb, fU, fA, fAi, mass=MASS, tol=1e-10,
+                                                                  delta=1e-2, maxit=5000),
         }
         tts = {}
         for name, fn in solvers.items():

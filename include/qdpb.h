@@ -37,8 +37,11 @@
  *
  * Streams: every call enqueues its kernels on the context stream (qdp_init / qdp_set_stream)
  * and returns without synchronising, EXCEPT calls that return host values (import, export,
- * norm2, inner_product, cg_solve, clover_build), which synchronise the stream before
- * returning.
+ * norm2, inner_product, cg_solve, clover_build), which return once their values are final:
+ * they synchronise the stream, except norm2 / inner_product on a one-rank context, whose
+ * reduction kernel stores the result and a completion token into mapped host memory in its
+ * final block -- the call polls for the token (a later call is ordered after that kernel on
+ * the stream anyway; a launch failure is then reported by the next synchronising call).
  *
  * Errors: every entry point returns a status; 0 = QDP_OK, > 0 = warning, < 0 = error.
  * On error nothing has been enqueued and the outputs are unchanged, except QDP_ECUDA /
@@ -276,6 +279,17 @@ int qdp_cg_solve_mixed(qdp_field x, const qdp_field b, const qdp_field U, const 
                        const qdp_field Ainv_s, double mass, double tol, double delta, int maxit,
                        int *iters, int *reliable, double *resid_hist, int hist_cap,
                        double *true_resid);
+
+/* qdp_cg_solve_mixed with a 16-bit sloppy level (the half-precision reliable-update solver of
+ * the paper's ref. [2]): the sloppy operator uses U (as reconstruct-12 links, int16 fixed point),
+ * A_oo and A_ee^-1 converted at the start of the call to 16-bit storage (int16 with one float norm
+ * per site for the clover blocks), 16-bit search directions and operator vectors (int16 with a
+ * per-site norm) and fp32 residual and solution, all arithmetic in fp32; fp64 reliable updates
+ * and the convergence test as qdp_cg_solve_mixed.  x, b, U, A, Ainv are QDP_F64 (A, Ainv NULL for
+ * Wilson); the 16-bit copies live in the context's work space. */
+int qdp_cg_solve_mixed16(qdp_field x, const qdp_field b, const qdp_field U, const qdp_field A,
+                         const qdp_field Ainv, double mass, double tol, double delta, int maxit, int *iters,
+                         int *reliable, double *resid_hist, int hist_cap, double *true_resid);
 
 /* ---- site-local expressions: the test functions of PAPER.md Table II (section VI) ----------
  * One fused streaming kernel per expression, evaluated on every site of the output's subset

@@ -8,6 +8,10 @@
 // padded tail of each plane (cb >= Vh) is never read or written.
 #include <string.h>
 
+#include <algorithm>
+#include <atomic>
+#include <functional>
+
 #include "internal.h"
 
 namespace qdpb {
@@ -28,7 +32,8 @@ template <> struct E<float> {
   static __device__ __forceinline__ T put(const float r[4]) { return make_float4(r[0], r[1], r[2], r[3]); }
 };
 
-constexpr int RB = 256;  // reduction block
+constexpr int RB = 256;  // block of the untuned launches
+constexpr int RED_THREADS = 148 * 8 * 256;  // reductions: at most this many threads (grid-stride)
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -65,7 +70,7 @@ __global__ void rank_sum_kernel(const double *g, int nranks, int n, double *res,
 }
 
 template <typename R>
-__global__ void __launch_bounds__(RB) norm2_kernel(const Geom g, const typename E<R>::T *a, int nblk, const __grid_constant__ RedArgs Rd) {
+__global__ void __launch_bounds__(1024) norm2_kernel(const Geom g, const typename E<R>::T *a, int nblk, const __grid_constant__ RedArgs Rd) {
   double acc = 0.0;
   const size_t bs = (size_t)E<R>::NP * g.stride;
   for (int cb = blockIdx.x * blockDim.x + threadIdx.x; cb < g.Vh; cb += gridDim.x * blockDim.x)
@@ -81,7 +86,7 @@ __global__ void __launch_bounds__(RB) norm2_kernel(const Geom g, const typename 
 }
 
 template <typename R>
-__global__ void __launch_bounds__(RB) inner_kernel(const Geom g, const typename E<R>::T *a, const typename E<R>::T *b_,
+__global__ void __launch_bounds__(1024) inner_kernel(const Geom g, const typename E<R>::T *a, const typename E<R>::T *b_,
                                                    int nblk, const __grid_constant__ RedArgs Rd) {
   double re = 0.0, im = 0.0;
   const size_t bs = (size_t)E<R>::NP * g.stride;
@@ -103,7 +108,7 @@ __global__ void __launch_bounds__(RB) inner_kernel(const Geom g, const typename 
 }
 
 template <typename R>
-__global__ void __launch_bounds__(RB) axpy_kernel(const Geom g, R ar, R ai, const typename E<R>::T *x,
+__global__ void __launch_bounds__(1024) axpy_kernel(const Geom g, R ar, R ai, const typename E<R>::T *x,
                                                   typename E<R>::T *y, int nblk) {
   const size_t bs = (size_t)E<R>::NP * g.stride;
   for (int cb = blockIdx.x * blockDim.x + threadIdx.x; cb < g.Vh; cb += gridDim.x * blockDim.x)
@@ -127,7 +132,7 @@ __global__ void __launch_bounds__(RB) axpy_kernel(const Geom g, R ar, R ai, cons
 
 // y = x + a y
 template <typename R>
-__global__ void __launch_bounds__(RB) xpay_kernel(const Geom g, const typename E<R>::T *x, R a, typename E<R>::T *y, int nblk) {
+__global__ void __launch_bounds__(1024) xpay_kernel(const Geom g, const typename E<R>::T *x, R a, typename E<R>::T *y, int nblk) {
   const size_t bs = (size_t)E<R>::NP * g.stride;
   for (int cb = blockIdx.x * blockDim.x + threadIdx.x; cb < g.Vh; cb += gridDim.x * blockDim.x)
     for (int b = 0; b < nblk; b++)
@@ -144,7 +149,7 @@ __global__ void __launch_bounds__(RB) xpay_kernel(const Geom g, const typename E
 }
 
 template <typename R>
-__global__ void __launch_bounds__(RB) scale_copy_kernel(const Geom g, typename E<R>::T *d, const typename E<R>::T *s, R a, int nblk) {
+__global__ void __launch_bounds__(1024) scale_copy_kernel(const Geom g, typename E<R>::T *d, const typename E<R>::T *s, R a, int nblk) {
   const size_t bs = (size_t)E<R>::NP * g.stride;
   for (int cb = blockIdx.x * blockDim.x + threadIdx.x; cb < g.Vh; cb += gridDim.x * blockDim.x)
     for (int b = 0; b < nblk; b++)
@@ -162,7 +167,7 @@ __global__ void __launch_bounds__(RB) scale_copy_kernel(const Geom g, typename E
 // r -= alpha q ; |r|^2 (one launch, reduce.cuh)   with alpha = res[rho] / res[pq]  (CG step 5).
 // Rd.has_cg: iteration Rd.cg.k of the device-side CG (no work once *stop < k; records |r_k|^2).
 template <typename R>
-__global__ void __launch_bounds__(RB) cg_r_kernel(const Geom g, typename E<R>::T *r, const typename E<R>::T *q,
+__global__ void __launch_bounds__(1024) cg_r_kernel(const Geom g, typename E<R>::T *r, const typename E<R>::T *q,
                                                   const double *res, int rho_slot, int pq_slot,
                                                   const __grid_constant__ RedArgs Rd) {
   const bool skip = Rd.has_cg && cg_skip(Rd.cg.stop, Rd.cg.k);
@@ -190,7 +195,7 @@ __global__ void __launch_bounds__(RB) cg_r_kernel(const Geom g, typename E<R>::T
 // x += alpha p ; p = r + beta p (UPD_P), alpha = res[rho] / res[pq], beta = res[rr] / res[rho].
 // stop (device-side CG): no work when *stop < iter; x only when *stop == iter (the last iteration)
 template <typename R, bool UPD_P>
-__global__ void __launch_bounds__(RB) cg_xp_kernel(const Geom g, typename E<R>::T *x, typename E<R>::T *p,
+__global__ void __launch_bounds__(1024) cg_xp_kernel(const Geom g, typename E<R>::T *x, typename E<R>::T *p,
                                                    const typename E<R>::T *r, const double *res, int rho_slot,
                                                    int pq_slot, int rr_slot, const int *stop, int iter) {
   bool upd_p = UPD_P;
@@ -221,7 +226,7 @@ __global__ void __launch_bounds__(RB) cg_xp_kernel(const Geom g, typename E<R>::
 
 // p = r + beta p, beta = res[rr] / res[rho]
 template <typename R>
-__global__ void __launch_bounds__(RB) cg_p_kernel(const Geom g, typename E<R>::T *p, const typename E<R>::T *r,
+__global__ void __launch_bounds__(1024) cg_p_kernel(const Geom g, typename E<R>::T *p, const typename E<R>::T *r,
                                                   const double *res, int rho_slot, int rr_slot) {
   const R beta = (R)(res[rr_slot] / res[rho_slot]);
   for (int cb = blockIdx.x * blockDim.x + threadIdx.x; cb < g.Vh; cb += gridDim.x * blockDim.x)
@@ -239,7 +244,7 @@ __global__ void __launch_bounds__(RB) cg_p_kernel(const Geom g, typename E<R>::T
 
 // Precision conversion of one fermion parity block: fp64 double2[12] <-> fp32 float4[6].
 template <bool TO32>
-__global__ void __launch_bounds__(RB) convert_kernel(const Geom g, double2 *d64, float4 *f32) {
+__global__ void __launch_bounds__(1024) convert_kernel(const Geom g, double2 *d64, float4 *f32) {
   for (int cb = blockIdx.x * blockDim.x + threadIdx.x; cb < g.Vh; cb += gridDim.x * blockDim.x)
 #pragma unroll
     for (int k = 0; k < 6; k++) {
@@ -257,7 +262,7 @@ __global__ void __launch_bounds__(RB) convert_kernel(const Geom g, double2 *d64,
 }
 
 // y64 += x32 (the reliable update's accumulation of the sloppy solution), then x32 = 0
-__global__ void __launch_bounds__(RB) accum_mixed_kernel(const Geom g, double2 *y64, float4 *x32) {
+__global__ void __launch_bounds__(1024) accum_mixed_kernel(const Geom g, double2 *y64, float4 *x32) {
   for (int cb = blockIdx.x * blockDim.x + threadIdx.x; cb < g.Vh; cb += gridDim.x * blockDim.x)
 #pragma unroll
     for (int k = 0; k < 6; k++) {
@@ -273,12 +278,27 @@ __global__ void __launch_bounds__(RB) accum_mixed_kernel(const Geom g, double2 *
 }
 
 // ------------------------------------------------------------------ host wrappers
-static int red_grid(const Geom &g) {
-  int n = grid_for(g.Vh, RB);
-  return n < 148 * 8 ? n : 148 * 8;
-}
 
 template <typename R> using T_ = typename E<R>::T;
+
+// The paper's autotuner (expr.cu tuned_launch) on the launch configuration of
+// every BLAS kernel, per (kernel, precision, number of parity blocks, volume): the block size
+// starts at 1024 and halves on later payload launches until one is 33% slower than the best.
+// `launch(grid, block)` enqueues the kernel; reductions cap the grid (grid-stride loop).
+enum { K_NORM2 = 1, K_INNER, K_AXPY, K_XPAY, K_SCALE, K_COPY, K_CGR, K_CGXP, K_CGXP0, K_CGP, K_CONV32, K_CONV64, K_ACCUM };
+static int blas_launch(qdp_ctx ctx, int kid, int prec, int nblk, bool red,
+                       const std::function<void(int grid, int block)> &launch) {
+  const Geom &g = ctx->geom;
+  const long key = (1L << 60) | ((long)kid << 44) | ((long)prec << 43) | ((long)nblk << 41) | (long)g.Vh;
+  return tuned_launch(ctx, key, [&](int block) -> cudaError_t {
+    int grid = grid_for(g.Vh, block);
+    if (red) grid = std::max(1, std::min(grid, RED_THREADS / block));
+    launch(grid, block);
+    return cudaGetLastError();
+  });
+}
+// largest grid a tuned reduction can use (its partial arrays are sized for it)
+static int red_grid_max(const Geom &g) { return std::max(1, std::min(grid_for(g.Vh, 32), RED_THREADS / 32)); }
 
 int reduce_partials(qdp_ctx ctx, int nparts, int slot) {
   ProfEvent ev;
@@ -300,7 +320,12 @@ int red_setup(qdp_ctx ctx, int nblk, int slot, int n, bool global, bool host, Re
   const bool multi = global && ctx->nranks > 1;
   R->peer = multi && ctx->peer;
   *after = multi && !ctx->peer;  // NCCL: reduce_global after the launch
-  if (host && !*after) R->host = ctx->host_pinned + 32;
+  if (host && !*after) {
+    R->host = ctx->host_pinned + 32;
+    R->host_flag = (unsigned *)(ctx->host_pinned + 36);
+    R->token = ++ctx->red_token;
+    *(volatile unsigned *)R->host_flag = 0u;
+  }
   if (R->peer) {
     R->pa = peer_args(ctx);
     R->seq = peer_next_sum_seq(ctx);
@@ -308,43 +333,59 @@ int red_setup(qdp_ctx ctx, int nblk, int slot, int n, bool global, bool host, Re
   return QDP_OK;
 }
 
+// The final block of the reduction stores the values and then the call's token into mapped host
+// memory: poll for the token (no stream synchronisation -- the kernel's remaining blocks have all
+// finished their share), then read.  Falls back to a synchronisation (which also reports a
+// failed launch) if the token does not show up within ~2 s.
 int read_red_host(qdp_ctx ctx, int n, double *out) {
-  QDP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  const volatile unsigned *flag = (const volatile unsigned *)(ctx->host_pinned + 36);
+  const unsigned token = ctx->red_token;
+  long spins = 0;
+  while (*flag != token) {
+    if (++spins > (1L << 27)) {
+      QDP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+      if (*flag != token) return set_error(ctx, QDP_ECUDA, "reduction result never arrived");
+      break;
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
   for (int i = 0; i < n; i++) out[i] = ((volatile double *)ctx->host_pinned)[32 + i];
   return QDP_OK;
 }
 
 int blas_norm2(qdp_ctx ctx, int prec, const void *a, int nblk, int slot, bool host) {
   const Geom &g = ctx->geom;
-  const int nb = red_grid(g);
   int rc;
   RedArgs R;
   bool after;
-  if ((rc = red_setup(ctx, nb, slot, 1, true, host, &R, &after))) return rc;
+  if ((rc = red_setup(ctx, red_grid_max(g), slot, 1, true, host, &R, &after))) return rc;
   ProfEvent ev;
   prof_begin(ctx, QDP_PK_REDUCE, &ev);
   prof_work(ctx, QDP_PK_REDUCE, 48.0 * g.Vh * nblk, 24.0 * g.Vh * nblk * (prec == QDP_F64 ? 8 : 4));
-  if (prec == QDP_F64) norm2_kernel<double><<<nb, RB, 0, ctx->stream>>>(g, (const T_<double> *)a, nblk, R);
-  else norm2_kernel<float><<<nb, RB, 0, ctx->stream>>>(g, (const T_<float> *)a, nblk, R);
-  if ((rc = prof_end(ctx, &ev))) return rc;
+  rc = blas_launch(ctx, K_NORM2, prec, nblk, true, [&](int nb, int bs) {
+    if (prec == QDP_F64) norm2_kernel<double><<<nb, bs, 0, ctx->stream>>>(g, (const T_<double> *)a, nblk, R);
+    else norm2_kernel<float><<<nb, bs, 0, ctx->stream>>>(g, (const T_<float> *)a, nblk, R);
+  });
+  if (rc || (rc = prof_end(ctx, &ev))) return rc;
   return after ? reduce_global(ctx, slot, 1) : QDP_OK;
 }
 
 int blas_inner(qdp_ctx ctx, int prec, const void *a, const void *b, int nblk, int slot, bool host) {
   const Geom &g = ctx->geom;
-  const int nb = red_grid(g);
   int rc;
   RedArgs R;
   bool after;
-  if ((rc = red_setup(ctx, nb, slot, 2, true, host, &R, &after))) return rc;
+  if ((rc = red_setup(ctx, red_grid_max(g), slot, 2, true, host, &R, &after))) return rc;
   ProfEvent ev;
   prof_begin(ctx, QDP_PK_REDUCE, &ev);
   prof_work(ctx, QDP_PK_REDUCE, 96.0 * g.Vh * nblk, 48.0 * g.Vh * nblk * (prec == QDP_F64 ? 8 : 4));
-  if (prec == QDP_F64)
-    inner_kernel<double><<<nb, RB, 0, ctx->stream>>>(g, (const T_<double> *)a, (const T_<double> *)b, nblk, R);
-  else
-    inner_kernel<float><<<nb, RB, 0, ctx->stream>>>(g, (const T_<float> *)a, (const T_<float> *)b, nblk, R);
-  if ((rc = prof_end(ctx, &ev))) return rc;
+  rc = blas_launch(ctx, K_INNER, prec, nblk, true, [&](int nb, int bs) {
+    if (prec == QDP_F64)
+      inner_kernel<double><<<nb, bs, 0, ctx->stream>>>(g, (const T_<double> *)a, (const T_<double> *)b, nblk, R);
+    else
+      inner_kernel<float><<<nb, bs, 0, ctx->stream>>>(g, (const T_<float> *)a, (const T_<float> *)b, nblk, R);
+  });
+  if (rc || (rc = prof_end(ctx, &ev))) return rc;
   return after ? reduce_global(ctx, slot, 2) : QDP_OK;
 }
 
@@ -366,7 +407,7 @@ __global__ void scalars_kernel(double *dst, const double *src, int n) {
   for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
 }
 template <typename R>
-__global__ void __launch_bounds__(RB) copy_kernel(const Geom g, typename E<R>::T *d, const typename E<R>::T *s, int nblk) {
+__global__ void __launch_bounds__(1024) copy_kernel(const Geom g, typename E<R>::T *d, const typename E<R>::T *s, int nblk) {
   const size_t bs = (size_t)E<R>::NP * g.stride;
   for (int cb = blockIdx.x * blockDim.x + threadIdx.x; cb < g.Vh; cb += gridDim.x * blockDim.x)
     for (int b = 0; b < nblk; b++)
@@ -397,9 +438,11 @@ int copy_blocks(qdp_ctx ctx, int prec, void *dst, const void *src, int nblk) {
   ProfEvent ev;
   prof_begin(ctx, QDP_PK_BLAS, &ev);
   prof_work(ctx, QDP_PK_BLAS, 0.0, 48.0 * g.Vh * nblk * (prec == QDP_F64 ? 8 : 4));
-  const int nb = grid_for(g.Vh, RB);
-  if (prec == QDP_F64) copy_kernel<double><<<nb, RB, 0, ctx->stream>>>(g, (T_<double> *)dst, (const T_<double> *)src, nblk);
-  else copy_kernel<float><<<nb, RB, 0, ctx->stream>>>(g, (T_<float> *)dst, (const T_<float> *)src, nblk);
+  int rc = blas_launch(ctx, K_COPY, prec, nblk, false, [&](int nb, int bs) {
+    if (prec == QDP_F64) copy_kernel<double><<<nb, bs, 0, ctx->stream>>>(g, (T_<double> *)dst, (const T_<double> *)src, nblk);
+    else copy_kernel<float><<<nb, bs, 0, ctx->stream>>>(g, (T_<float> *)dst, (const T_<float> *)src, nblk);
+  });
+  if (rc) return rc;
   return prof_end(ctx, &ev);
 }
 
@@ -408,9 +451,13 @@ int blas_axpy(qdp_ctx ctx, int prec, double ar, double ai, const void *x, void *
   ProfEvent ev;
   prof_begin(ctx, QDP_PK_BLAS, &ev);
   prof_work(ctx, QDP_PK_BLAS, 96.0 * g.Vh * nblk, 72.0 * g.Vh * nblk * (prec == QDP_F64 ? 8 : 4));
-  const int nb = grid_for(g.Vh, RB);
-  if (prec == QDP_F64) axpy_kernel<double><<<nb, RB, 0, ctx->stream>>>(g, ar, ai, (const T_<double> *)x, (T_<double> *)y, nblk);
-  else axpy_kernel<float><<<nb, RB, 0, ctx->stream>>>(g, (float)ar, (float)ai, (const T_<float> *)x, (T_<float> *)y, nblk);
+  int rc = blas_launch(ctx, K_AXPY, prec, nblk, false, [&](int nb, int bs) {
+    if (prec == QDP_F64)
+      axpy_kernel<double><<<nb, bs, 0, ctx->stream>>>(g, ar, ai, (const T_<double> *)x, (T_<double> *)y, nblk);
+    else
+      axpy_kernel<float><<<nb, bs, 0, ctx->stream>>>(g, (float)ar, (float)ai, (const T_<float> *)x, (T_<float> *)y, nblk);
+  });
+  if (rc) return rc;
   return prof_end(ctx, &ev);
 }
 
@@ -419,9 +466,11 @@ int blas_xpay(qdp_ctx ctx, int prec, const void *x, double a, void *y, int nblk)
   ProfEvent ev;
   prof_begin(ctx, QDP_PK_BLAS, &ev);
   prof_work(ctx, QDP_PK_BLAS, 48.0 * g.Vh * nblk, 72.0 * g.Vh * nblk * (prec == QDP_F64 ? 8 : 4));
-  const int nb = grid_for(g.Vh, RB);
-  if (prec == QDP_F64) xpay_kernel<double><<<nb, RB, 0, ctx->stream>>>(g, (const T_<double> *)x, a, (T_<double> *)y, nblk);
-  else xpay_kernel<float><<<nb, RB, 0, ctx->stream>>>(g, (const T_<float> *)x, (float)a, (T_<float> *)y, nblk);
+  int rc = blas_launch(ctx, K_XPAY, prec, nblk, false, [&](int nb, int bs) {
+    if (prec == QDP_F64) xpay_kernel<double><<<nb, bs, 0, ctx->stream>>>(g, (const T_<double> *)x, a, (T_<double> *)y, nblk);
+    else xpay_kernel<float><<<nb, bs, 0, ctx->stream>>>(g, (const T_<float> *)x, (float)a, (T_<float> *)y, nblk);
+  });
+  if (rc) return rc;
   return prof_end(ctx, &ev);
 }
 
@@ -430,20 +479,23 @@ int blas_scale_copy(qdp_ctx ctx, int prec, void *dst, const void *src, double a,
   ProfEvent ev;
   prof_begin(ctx, QDP_PK_BLAS, &ev);
   prof_work(ctx, QDP_PK_BLAS, 24.0 * g.Vh * nblk, 48.0 * g.Vh * nblk * (prec == QDP_F64 ? 8 : 4));
-  const int nb = grid_for(g.Vh, RB);
-  if (prec == QDP_F64) scale_copy_kernel<double><<<nb, RB, 0, ctx->stream>>>(g, (T_<double> *)dst, (const T_<double> *)src, a, nblk);
-  else scale_copy_kernel<float><<<nb, RB, 0, ctx->stream>>>(g, (T_<float> *)dst, (const T_<float> *)src, (float)a, nblk);
+  int rc = blas_launch(ctx, K_SCALE, prec, nblk, false, [&](int nb, int bs) {
+    if (prec == QDP_F64)
+      scale_copy_kernel<double><<<nb, bs, 0, ctx->stream>>>(g, (T_<double> *)dst, (const T_<double> *)src, a, nblk);
+    else
+      scale_copy_kernel<float><<<nb, bs, 0, ctx->stream>>>(g, (T_<float> *)dst, (const T_<float> *)src, (float)a, nblk);
+  });
+  if (rc) return rc;
   return prof_end(ctx, &ev);
 }
 
 int blas_cg_update_r(qdp_ctx ctx, int prec, void *r, const void *q, int rho_slot, int pq_slot, int rr_slot,
                      const CgDev *cg) {
   const Geom &g = ctx->geom;
-  const int nb = red_grid(g);
   int rc;
   RedArgs R;
   bool after;
-  if ((rc = red_setup(ctx, nb, rr_slot, 1, true, false, &R, &after))) return rc;
+  if ((rc = red_setup(ctx, red_grid_max(g), rr_slot, 1, true, false, &R, &after))) return rc;
   if (cg) {
     if (after) return set_error(ctx, QDP_EINVAL, "device-side CG needs the in-kernel global sum");
     R.has_cg = 1;
@@ -452,13 +504,15 @@ int blas_cg_update_r(qdp_ctx ctx, int prec, void *r, const void *q, int rho_slot
   ProfEvent ev;
   prof_begin(ctx, QDP_PK_BLAS, &ev);
   prof_work(ctx, QDP_PK_BLAS, 96.0 * g.Vh, 72.0 * g.Vh * (prec == QDP_F64 ? 8 : 4));
-  if (prec == QDP_F64)
-    cg_r_kernel<double><<<nb, RB, 0, ctx->stream>>>(g, (T_<double> *)r, (const T_<double> *)q, ctx->red_result, rho_slot,
-                                                     pq_slot, R);
-  else
-    cg_r_kernel<float><<<nb, RB, 0, ctx->stream>>>(g, (T_<float> *)r, (const T_<float> *)q, ctx->red_result, rho_slot,
-                                                    pq_slot, R);
-  if ((rc = prof_end(ctx, &ev))) return rc;
+  rc = blas_launch(ctx, K_CGR, prec, 1, true, [&](int nb, int bs) {
+    if (prec == QDP_F64)
+      cg_r_kernel<double><<<nb, bs, 0, ctx->stream>>>(g, (T_<double> *)r, (const T_<double> *)q, ctx->red_result,
+                                                       rho_slot, pq_slot, R);
+    else
+      cg_r_kernel<float><<<nb, bs, 0, ctx->stream>>>(g, (T_<float> *)r, (const T_<float> *)q, ctx->red_result,
+                                                      rho_slot, pq_slot, R);
+  });
+  if (rc || (rc = prof_end(ctx, &ev))) return rc;
   return after ? reduce_global(ctx, rr_slot, 1) : QDP_OK;
 }
 
@@ -469,13 +523,15 @@ int blas_cg_update_xp(qdp_ctx ctx, int prec, void *x, void *p, const void *r, in
   prof_begin(ctx, QDP_PK_BLAS, &ev);
   prof_work(ctx, QDP_PK_BLAS, (update_p ? 96.0 : 48.0) * g.Vh,
             (update_p ? 120.0 : 72.0) * g.Vh * (prec == QDP_F64 ? 8 : 4));
-  const int nb = grid_for(g.Vh, RB);
 #define QDPB_XP(Rt, U)                                                                                              \
-  cg_xp_kernel<Rt, U><<<nb, RB, 0, ctx->stream>>>(g, (T_<Rt> *)x, (T_<Rt> *)p, (const T_<Rt> *)r, ctx->red_result, \
+  cg_xp_kernel<Rt, U><<<nb, bs, 0, ctx->stream>>>(g, (T_<Rt> *)x, (T_<Rt> *)p, (const T_<Rt> *)r, ctx->red_result, \
                                                   rho_slot, pq_slot, rr_slot, stop, iter)
-  if (prec == QDP_F64) { if (update_p) QDPB_XP(double, true); else QDPB_XP(double, false); }
-  else { if (update_p) QDPB_XP(float, true); else QDPB_XP(float, false); }
+  int rc = blas_launch(ctx, update_p ? K_CGXP : K_CGXP0, prec, 1, false, [&](int nb, int bs) {
+    if (prec == QDP_F64) { if (update_p) QDPB_XP(double, true); else QDPB_XP(double, false); }
+    else { if (update_p) QDPB_XP(float, true); else QDPB_XP(float, false); }
+  });
 #undef QDPB_XP
+  if (rc) return rc;
   return prof_end(ctx, &ev);
 }
 
@@ -484,11 +540,13 @@ int blas_cg_update_p(qdp_ctx ctx, int prec, void *p, const void *r, int rho_slot
   ProfEvent ev;
   prof_begin(ctx, QDP_PK_BLAS, &ev);
   prof_work(ctx, QDP_PK_BLAS, 48.0 * g.Vh, 72.0 * g.Vh * (prec == QDP_F64 ? 8 : 4));
-  const int nb = grid_for(g.Vh, RB);
-  if (prec == QDP_F64)
-    cg_p_kernel<double><<<nb, RB, 0, ctx->stream>>>(g, (T_<double> *)p, (const T_<double> *)r, ctx->red_result, rho_slot, rr_slot);
-  else
-    cg_p_kernel<float><<<nb, RB, 0, ctx->stream>>>(g, (T_<float> *)p, (const T_<float> *)r, ctx->red_result, rho_slot, rr_slot);
+  int rc = blas_launch(ctx, K_CGP, prec, 1, false, [&](int nb, int bs) {
+    if (prec == QDP_F64)
+      cg_p_kernel<double><<<nb, bs, 0, ctx->stream>>>(g, (T_<double> *)p, (const T_<double> *)r, ctx->red_result, rho_slot, rr_slot);
+    else
+      cg_p_kernel<float><<<nb, bs, 0, ctx->stream>>>(g, (T_<float> *)p, (const T_<float> *)r, ctx->red_result, rho_slot, rr_slot);
+  });
+  if (rc) return rc;
   return prof_end(ctx, &ev);
 }
 
@@ -497,9 +555,11 @@ int blas_convert(qdp_ctx ctx, void *dst, int dst_prec, const void *src) {
   ProfEvent ev;
   prof_begin(ctx, QDP_PK_BLAS, &ev);
   prof_work(ctx, QDP_PK_BLAS, 0.0, 288.0 * g.Vh);  // 24 reals fp64 + 24 reals fp32 per site
-  const int nb = grid_for(g.Vh, RB);
-  if (dst_prec == QDP_F32) convert_kernel<true><<<nb, RB, 0, ctx->stream>>>(g, (double2 *)src, (float4 *)dst);
-  else convert_kernel<false><<<nb, RB, 0, ctx->stream>>>(g, (double2 *)dst, (float4 *)src);
+  int rc = blas_launch(ctx, dst_prec == QDP_F32 ? K_CONV32 : K_CONV64, 0, 1, false, [&](int nb, int bs) {
+    if (dst_prec == QDP_F32) convert_kernel<true><<<nb, bs, 0, ctx->stream>>>(g, (double2 *)src, (float4 *)dst);
+    else convert_kernel<false><<<nb, bs, 0, ctx->stream>>>(g, (double2 *)dst, (float4 *)src);
+  });
+  if (rc) return rc;
   return prof_end(ctx, &ev);
 }
 
@@ -508,8 +568,10 @@ int blas_accum_mixed(qdp_ctx ctx, void *y64, void *x32) {
   ProfEvent ev;
   prof_begin(ctx, QDP_PK_BLAS, &ev);
   prof_work(ctx, QDP_PK_BLAS, 24.0 * g.Vh, (2.0 * 24 * 8 + 2.0 * 24 * 4) * g.Vh);
-  const int nb = grid_for(g.Vh, RB);
-  accum_mixed_kernel<<<nb, RB, 0, ctx->stream>>>(g, (double2 *)y64, (float4 *)x32);
+  int rc = blas_launch(ctx, K_ACCUM, 0, 1, false, [&](int nb, int bs) {
+    accum_mixed_kernel<<<nb, bs, 0, ctx->stream>>>(g, (double2 *)y64, (float4 *)x32);
+  });
+  if (rc) return rc;
   return prof_end(ctx, &ev);
 }
 

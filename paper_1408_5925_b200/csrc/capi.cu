@@ -789,6 +789,32 @@ extern "C" int qdp_cg_solve_mixed(qdp_field x, const qdp_field b, const qdp_fiel
                         true_resid);
 }
 
+extern "C" int qdp_cg_solve_mixed16(qdp_field x, const qdp_field b, const qdp_field U, const qdp_field A,
+                                    const qdp_field Ainv, double mass, double tol, double delta, int maxit, int *iters,
+                                    int *reliable, double *resid_hist, int hist_cap, double *true_resid) {
+  if (!x || !b || !U) return QDP_EINVAL;
+  qdp_ctx c = x->ctx;
+  int rc;
+  if (x->prec != QDP_F64 || b->prec != QDP_F64) return set_error(c, QDP_EPREC, "cg_mixed16: x, b must be QDP_F64");
+  if (!(delta > 0 && delta < 1)) return set_error(c, QDP_EINVAL, "cg_mixed16: 0 < delta < 1");
+  if ((rc = check_pair(x, b))) return rc;
+  if (U->ctx != c || !is_gauge(U->kind)) return set_error(c, QDP_EINVAL, "cg_mixed16: U must be a gauge field");
+  if (U->prec != QDP_F64) return set_error(c, QDP_EPREC, "cg_mixed16: U must be QDP_F64 (its reliable updates)");
+  if (x->kind != QDP_FERMION || b->kind != QDP_FERMION)
+    return set_error(c, QDP_EINVAL, "cg_mixed16: kinds (fermion, fermion, gauge)");
+  if (x->subset != QDP_ALL || b->subset != QDP_ALL) return set_error(c, QDP_EINVAL, "cg_mixed16: x and b must be QDP_ALL");
+  if (x->data == b->data) return set_error(c, QDP_EALIAS, "cg_mixed16: x aliases b");
+  if ((A == nullptr) != (Ainv == nullptr)) return set_error(c, QDP_EINVAL, "cg_mixed16: give both A and Ainv, or neither");
+  if (A) {
+    if ((rc = check_pair(x, A)) || (rc = check_pair(x, Ainv))) return rc;
+    if (A->kind != QDP_CLOVER || Ainv->kind != QDP_CLOVER || !block_of(A, 1) || !block_of(Ainv, 0))
+      return set_error(c, QDP_EINVAL, "cg_mixed16: A must cover odd, Ainv even sites");
+    if (true_resid && A->subset != QDP_ALL) return set_error(c, QDP_EINVAL, "cg_mixed16: true_resid needs A on all sites");
+  }
+  if (maxit < 0 || !(tol >= 0)) return set_error(c, QDP_EINVAL, "cg_mixed16: bad tol/maxit");
+  return cg_solve_mixed16(x, b, U, A, Ainv, mass, tol, delta, maxit, iters, reliable, resid_hist, hist_cap, true_resid);
+}
+
 // ---------------------------------------------------------------------------- Table II expressions
 extern "C" int qdp_expr(int expr, qdp_field out, const qdp_field a, const qdp_field b, const qdp_field c) {
   if (!out || !a || !b) return QDP_EINVAL;

@@ -16,6 +16,8 @@
 //   EPI_CLOVINV  out = A^{-1} (a x + b [g5] H psi)         (x optional)
 //   EPI_CLOVXPAY out = A x + b [g5] H psi
 // g5_in applies gamma5 to psi as it is loaded (Mhat^dag = g5 Mhat g5).
+#include <type_traits>
+
 #include "internal.h"
 
 namespace qdpb {
@@ -150,7 +152,7 @@ template <typename R, int REC = 18> struct KParams {
   GaugeView<R, REC> U;
   CloverView<R> A;
   int parity;
-  R a, b;
+  Arith_t<R> a, b;  // arithmetic type (fp32 for the 16-bit storage)
   // ghost buffers (exterior): [mu][dir], dir 0 = from -mu (already U^dag P+ psi), 1 = from +mu (P- psi)
   const void *ghost[4][2];
   // pack destinations: [mu][dir], dir 0 = to -mu neighbour, 1 = to +mu neighbour
@@ -158,7 +160,7 @@ template <typename R, int REC = 18> struct KParams {
   // fused Re<dotx, out>: per-block partials
   FermView<R> dotx;
   double *dot_part;
-  R dot_shift;  // with a fused dot: out += dot_shift * dotx first
+  Arith_t<R> dot_shift;  // with a fused dot: out += dot_shift * dotx first
   // peer-to-peer halo (QDP_OPT_P2P; p2p.cu): pack waits war >= seq-2, stores, and its last
   // block release-stores seq into sig; the exterior waits ready >= seq and its last block
   // release-stores seq into ack_to.  pack_counter == nullptr: NCCL / direct halo.
@@ -190,17 +192,18 @@ template <typename R, int REC = 18> struct KParams {
 
 template <typename R, int MU, typename KP>
 __device__ __forceinline__ void hop_dir(const Geom &g, const KP &P, const int c[4], int cb, int p,
-                                        bool G5IN, bool halo, Spinor<R> &acc) {
+                                        bool G5IN, bool halo, Spinor<Arith_t<R>> &acc) {
+  using T = Arith_t<R>;
   // forward: (1 - gamma_mu) U_mu(x) psi(x + mu)
   {
     const bool remote = halo && ((g.part >> MU) & 1) && c[MU] == g.L[MU] - 1;
     if (!remote) {
       int n[4] = {c[0], c[1], c[2], c[3]};
       n[MU] = (c[MU] + 1 == g.L[MU]) ? 0 : c[MU] + 1;
-      Spinor<R> s = P.psi.load(coords_cb(g, n));
+      Spinor<T> s = P.psi.load(coords_cb(g, n));
       if (G5IN) g5(s);
-      Half<R> h = project<MU, -1>(s);
-      Link<R> u = P.U.load(MU, p, cb);
+      Half<T> h = project<MU, -1>(s);
+      Link<T> u = P.U.load(MU, p, cb);
       accum_recon<MU, -1>(acc, mul_link(u, h));
     }
   }
@@ -211,39 +214,40 @@ __device__ __forceinline__ void hop_dir(const Geom &g, const KP &P, const int c[
       int n[4] = {c[0], c[1], c[2], c[3]};
       n[MU] = (c[MU] == 0) ? g.L[MU] - 1 : c[MU] - 1;
       const int ncb = coords_cb(g, n);
-      Spinor<R> s = P.psi.load(ncb);
+      Spinor<T> s = P.psi.load(ncb);
       if (G5IN) g5(s);
-      Half<R> h = project<MU, +1>(s);
-      Link<R> u = P.U.load(MU, 1 - p, ncb);
+      Half<T> h = project<MU, +1>(s);
+      Link<T> u = P.U.load(MU, 1 - p, ncb);
       accum_recon<MU, +1>(acc, mul_link_dag(u, h));
     }
   }
 }
 
 template <typename R, int EPI, typename KP>
-__device__ __forceinline__ Spinor<R> epilogue(const KP &P, int cb, Spinor<R> &acc, bool G5OUT) {
+__device__ __forceinline__ Spinor<Arith_t<R>> epilogue(const KP &P, int cb, Spinor<Arith_t<R>> &acc, bool G5OUT) {
+  using T = Arith_t<R>;
   if (G5OUT) g5(acc);
-  Spinor<R> o;
+  Spinor<T> o;
   if (EPI == EPI_PLAIN) {
 #pragma unroll
     for (int k = 0; k < 12; k++) o.c[k] = P.b * acc.c[k];
   } else if (EPI == EPI_XPAY) {
-    Spinor<R> xv = P.x.load_stream(cb);
+    Spinor<T> xv = P.x.load_stream(cb);
 #pragma unroll
     for (int k = 0; k < 12; k++) o.c[k] = P.a * xv.c[k] + P.b * acc.c[k];
   } else if (EPI == EPI_CLOVINV) {
     if (P.x.p) {
-      Spinor<R> xv = P.x.load_stream(cb);
+      Spinor<T> xv = P.x.load_stream(cb);
 #pragma unroll
       for (int k = 0; k < 12; k++) acc.c[k] = P.a * xv.c[k] + P.b * acc.c[k];
     } else {
 #pragma unroll
       for (int k = 0; k < 12; k++) acc.c[k] = P.b * acc.c[k];
     }
-    o = clover_mul(P.A, cb, acc);
+    o = clover_mul_s(P.A, cb, acc);
   } else {  // EPI_CLOVXPAY
-    Spinor<R> xv = P.x.load_stream(cb);
-    Spinor<R> ax = clover_mul(P.A, cb, xv);
+    Spinor<T> xv = P.x.load_stream(cb);
+    Spinor<T> ax = clover_mul_s(P.A, cb, xv);
 #pragma unroll
     for (int k = 0; k < 12; k++) o.c[k] = ax.c[k] + P.b * acc.c[k];
   }
@@ -293,9 +297,10 @@ __device__ __forceinline__ void pack_site(const Geom &g, const KP &P, int mu, in
   int c[4];
   face_coords(g, mu, fwd ? g.L[mu] - 1 : 0, f, q, c);
   const int cb = coords_cb(g, c);
-  Spinor<R> s = P.psi.load(cb);
+  using T = Arith_t<R>;
+  Spinor<T> s = P.psi.load(cb);
   if (G5IN) g5(s);
-  Half<R> h;
+  Half<T> h;
   if (!fwd) {
     switch (mu) {
       case 0: h = project<0, -1>(s); break;
@@ -303,7 +308,7 @@ __device__ __forceinline__ void pack_site(const Geom &g, const KP &P, int mu, in
       case 2: h = project<2, -1>(s); break;
       default: h = project<3, -1>(s); break;
     }
-    HalfGhost<R>::store(P.dst[mu][0], n, f, h);
+    HalfGhost<T>::store(P.dst[mu][0], n, f, h);
   } else {
     switch (mu) {
       case 0: h = project<0, +1>(s); break;
@@ -311,8 +316,8 @@ __device__ __forceinline__ void pack_site(const Geom &g, const KP &P, int mu, in
       case 2: h = project<2, +1>(s); break;
       default: h = project<3, +1>(s); break;
     }
-    Link<R> u = P.U.load(mu, q, cb);
-    HalfGhost<R>::store(P.dst[mu][1], n, f, mul_link_dag(u, h));
+    Link<T> u = P.U.load(mu, q, cb);
+    HalfGhost<T>::store(P.dst[mu][1], n, f, mul_link_dag(u, h));
   }
 }
 
@@ -353,14 +358,16 @@ __device__ __forceinline__ void fused_signal_last(const Geom &g, unsigned *const
 // (forward: P^- psi(x + mu) from the +mu neighbour, multiplied here by U_mu(x); backward: the
 // neighbour already applied U^dag P^+)
 template <typename R, int MU, typename KP>
-__device__ __forceinline__ void remote_hop(const Geom &g, const KP &P, const int c[4], int cb, int p, Spinor<R> &acc) {
+__device__ __forceinline__ void remote_hop(const Geom &g, const KP &P, const int c[4], int cb, int p,
+                                           Spinor<Arith_t<R>> &acc) {
+  using T = Arith_t<R>;
   if (!((g.part >> MU) & 1)) return;
   const int n = g.faceVh[MU];
   if (c[MU] == g.L[MU] - 1) {
-    const Half<R> h = HalfGhost<R>::load(P.ghost[MU][1], n, face_index(g, MU, c));
+    const Half<T> h = HalfGhost<T>::load(P.ghost[MU][1], n, face_index(g, MU, c));
     accum_recon<MU, -1>(acc, mul_link(P.U.load(MU, p, cb), h));
   }
-  if (c[MU] == 0) accum_recon<MU, +1>(acc, HalfGhost<R>::load(P.ghost[MU][0], n, face_index(g, MU, c)));
+  if (c[MU] == 0) accum_recon<MU, +1>(acc, HalfGhost<T>::load(P.ghost[MU][0], n, face_index(g, MU, c)));
 }
 
 template <typename R, int REC, int EPI, bool G5IN, bool G5OUT, bool HALO, bool DOT>
@@ -424,9 +431,10 @@ __global__ void __launch_bounds__(QDPB_DSLASH_MAXT, (dslash_minb<R, REC>()))
         P.U.prefetch(mu, 1 - p, coords_cb(g, n));
       }
     }
-    Spinor<R> acc;
+    using T = Arith_t<R>;
+    Spinor<T> acc;
 #pragma unroll
-    for (int k = 0; k < 12; k++) acc.c[k] = {R(0), R(0)};
+    for (int k = 0; k < 12; k++) acc.c[k] = {T(0), T(0)};
     hop_dir<R, 0>(g, P, c, cb, p, G5IN, HALO, acc);
     hop_dir<R, 1>(g, P, c, cb, p, G5IN, HALO, acc);
     hop_dir<R, 2>(g, P, c, cb, p, G5IN, HALO, acc);
@@ -437,11 +445,11 @@ __global__ void __launch_bounds__(QDPB_DSLASH_MAXT, (dslash_minb<R, REC>()))
       remote_hop<R, 2>(g, P, c, cb, p, acc);
       remote_hop<R, 3>(g, P, c, cb, p, acc);
     }
-    Spinor<R> o = epilogue<R, EPI>(P, cb, acc, G5OUT);
+    Spinor<T> o = epilogue<R, EPI>(P, cb, acc, G5OUT);
     if (DOT) {
       // fused Re<d, out> (and out += dot_shift d: the base shift of the multi-shift CG)
-      const Spinor<R> d = P.dotx.load_stream(cb);
-      if (P.dot_shift != R(0)) {
+      const Spinor<T> d = P.dotx.load_stream(cb);
+      if (P.dot_shift != T(0)) {
 #pragma unroll
         for (int k = 0; k < 12; k++) o.c[k] = o.c[k] + P.dot_shift * d.c[k];
       }
@@ -478,13 +486,14 @@ __global__ void __launch_bounds__(128) exterior_kernel(const Geom g, const KPara
     int c[4];
     face_coords(g, mu, fwd ? g.L[mu] - 1 : 0, f, p, c);
     const int cb = coords_cb(g, c);
-    Spinor<R> acc;
+    using T = Arith_t<R>;
+    Spinor<T> acc;
 #pragma unroll
-    for (int k = 0; k < 12; k++) acc.c[k] = {R(0), R(0)};
+    for (int k = 0; k < 12; k++) acc.c[k] = {T(0), T(0)};
     if (fwd) {
-      Half<R> h = HalfGhost<R>::load(P.ghost[mu][1], n, f);
-      Link<R> u = P.U.load(mu, p, cb);
-      Half<R> uh = mul_link(u, h);
+      Half<T> h = HalfGhost<T>::load(P.ghost[mu][1], n, f);
+      Link<T> u = P.U.load(mu, p, cb);
+      Half<T> uh = mul_link(u, h);
       switch (mu) {
         case 0: accum_recon<0, -1>(acc, uh); break;
         case 1: accum_recon<1, -1>(acc, uh); break;
@@ -492,7 +501,7 @@ __global__ void __launch_bounds__(128) exterior_kernel(const Geom g, const KPara
         default: accum_recon<3, -1>(acc, uh); break;
       }
     } else {
-      Half<R> uh = HalfGhost<R>::load(P.ghost[mu][0], n, f);
+      Half<T> uh = HalfGhost<T>::load(P.ghost[mu][0], n, f);
       switch (mu) {
         case 0: accum_recon<0, +1>(acc, uh); break;
         case 1: accum_recon<1, +1>(acc, uh); break;
@@ -503,8 +512,8 @@ __global__ void __launch_bounds__(128) exterior_kernel(const Geom g, const KPara
     if (G5OUT) g5(acc);
 #pragma unroll
     for (int k = 0; k < 12; k++) acc.c[k] = P.b * acc.c[k];
-    if (EPI == EPI_CLOVINV) acc = clover_mul(P.A, cb, acc);
-    Spinor<R> o = P.out.load_plain(cb);
+    if (EPI == EPI_CLOVINV) acc = clover_mul_s(P.A, cb, acc);
+    Spinor<T> o = P.out.load_plain(cb);
 #pragma unroll
     for (int k = 0; k < 12; k++) o.c[k] = o.c[k] + acc.c[k];
     P.out.store(cb, o);
@@ -584,6 +593,14 @@ template <typename R, int REC> static GaugeView<R, REC> gview(const void *p, int
 template <typename R> static CloverView<R> cview(const void *p, int stride);
 template <> CloverView<double> cview<double>(const void *p, int stride) { return {(const double2 *)p, stride}; }
 template <> CloverView<float> cview<float>(const void *p, int stride) { return {(const float4 *)p, stride}; }
+// 16-bit storage: [3 int4 planes][float norm plane] / [9 int4 planes][float norm plane]
+template <> FermView<h16> fview<h16>(const void *p, int stride) {
+  return {(int4 *)p, p ? (float *)((char *)p + (size_t)48 * stride) : nullptr, stride};
+}
+template <> CloverView<h16> cview<h16>(const void *p, int stride) {
+  return {(const int4 *)p, p ? (const float *)((const char *)p + (size_t)144 * stride) : nullptr, stride};
+}
+template <typename R> constexpr bool is_h16() { return std::is_same<R, h16>::value; }
 
 template <typename R, int REC, int EPI, bool G5IN, bool G5OUT, bool HALO, bool DOT>
 static void launch_main(qdp_ctx ctx, const KParams<R, REC> &P, int block) {
@@ -594,7 +611,7 @@ static void launch_main(qdp_ctx ctx, const KParams<R, REC> &P, int block) {
 
 template <typename R, int REC, int EPI>
 static void launch_four(qdp_ctx ctx, const KParams<R, REC> &P, bool g5i, bool g5o) {
-  if constexpr (EPI == EPI_PLAIN || EPI == EPI_XPAY) {
+  if constexpr ((EPI == EPI_PLAIN || EPI == EPI_XPAY) && !is_h16<R>()) {
     const int grid = grid_for(ctx->geom.Vh, 32);
 #define QDPB_L4(A, B) dslash4_kernel<R, REC, EPI, A, B><<<grid, 128, 0, ctx->stream>>>(ctx->geom, P)
     if (g5i) { if (g5o) QDPB_L4(true, true); else QDPB_L4(true, false); }
@@ -637,18 +654,21 @@ static void launch_ext(qdp_ctx ctx, const KParams<R, REC> &P, int mu, bool g5o, 
 // site for the hopping term (8 x (12 projection + 132 SU(3) x half spinor) + 7 x 24
 // accumulate) plus the epilogue; compulsory bytes 8 links + input + output (+ x, + clover,
 // + the fused inner product's second vector).
+// 16-bit storage: the bytes the kernel moves (a spinor 52 B, a link 24 B, a clover site 148 B).
 template <typename R, int REC>
 static void dslash_work(qdp_ctx ctx, const DslashArgs &a) {
   double f = 1320, r = 8 * REC + 24 + 24;
+  const double sp = is_h16<R>() ? 52 : 24 * sizeof(R), cl = is_h16<R>() ? 148 : 72 * sizeof(R);
+  double bytes = is_h16<R>() ? 8 * 24 + 2 * sp : r * sizeof(R);
   switch (a.epi) {
     case EPI_PLAIN: f += a.b != 1.0 ? 24 : 0; break;
-    case EPI_XPAY: f += 72; r += 24; break;
-    case EPI_CLOVINV: f += 504 + 24 + (a.x ? 48 : 0); r += 72 + (a.x ? 24 : 0); break;
-    default: f += 504 + 48; r += 72 + 24; break;
+    case EPI_XPAY: f += 72; bytes += sp; break;
+    case EPI_CLOVINV: f += 504 + 24 + (a.x ? 48 : 0); bytes += cl + (a.x ? sp : 0); break;
+    default: f += 504 + 48; bytes += cl + sp; break;
   }
-  if (a.dot_x) { f += 96 + (a.dot_shift != 0.0 ? 48 : 0); r += 24; }
+  if (a.dot_x) { f += 96 + (a.dot_shift != 0.0 ? 48 : 0); bytes += sp; }
   const double vh = ctx->geom.Vh;
-  prof_work(ctx, QDP_PK_DSLASH, f * vh, r * vh * sizeof(R));
+  prof_work(ctx, QDP_PK_DSLASH, f * vh, bytes * vh);
 }
 
 // The paper's autotuner (section VII) on the launch configuration of the
@@ -684,14 +704,14 @@ static int launch_main_epi(qdp_ctx ctx, const DslashArgs &a, const KParams<R, RE
   // tuned: whole lattice, no fused reduction (its partial layout follows the block size), no
   // explicit QDP_OPT_BLOCK
   if (!halo && !dot && ctx->block == 0 && ctx->dslash_variant >= 0) {  // forced (measurements)
-    const int v = variant_count(a.epi, dot) == 3 ? ctx->dslash_variant : std::max(1, ctx->dslash_variant);
+    const int v = (!is_h16<R>() && variant_count(a.epi, dot) == 3) ? ctx->dslash_variant : std::max(1, ctx->dslash_variant);
     const cudaError_t e = go(v);
     const int rc = prof_end(ctx, &ev);
     return e != cudaSuccess ? cuda_check(ctx, e, "dslash launch") : rc;
   }
   if (!halo && !dot && ctx->autotune && ctx->block == 0) {
-    const int nv = variant_count(a.epi, dot);
-    const long key = ((((long)(sizeof(R) == 8) * 2 + (REC == 12)) * 4 + a.epi) << 40) + ctx->geom.Vh;
+    const int nv = is_h16<R>() ? 2 : variant_count(a.epi, dot);
+    const long key = ((((long)(is_h16<R>() ? 2 : sizeof(R) == 8) * 2 + (REC == 12)) * 4 + a.epi) << 40) + ctx->geom.Vh;
     int rc = tuned_variant(ctx, key, nv, [&](int v) { return go(nv == 3 ? v : v + 1); });
     if (rc) {
       prof_end(ctx, &ev);
@@ -744,7 +764,9 @@ static int fuse_order(qdp_ctx ctx, int p, const int **perm, int *nin) {
 template <typename R, int REC>
 static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
   const Geom &g = ctx->geom;
-  const int prec = sizeof(R) == 8 ? QDP_F64 : QDP_F32;
+  const int prec = sizeof(R) == 8 ? QDP_F64 : QDP_F32;  // halo buffers (16-bit storage: fp32 ghosts)
+  using T = Arith_t<R>;
+  constexpr double BPR = is_h16<R>() ? 2.0 : (double)sizeof(R);  // bytes per stored real (accounting)
   KParams<R, REC> P = {};
   P.out = fview<R>(a.out, g.stride);
   P.psi = fview<R>(a.psi, g.stride);
@@ -752,8 +774,8 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
   P.U = gview<R, REC>(a.U, g.stride);
   P.A = cview<R>(a.clov, g.stride);
   P.parity = a.parity;
-  P.a = (R)a.a;
-  P.b = (R)a.b;
+  P.a = (T)a.a;
+  P.b = (T)a.b;
   const int block = ctx->block > 0 ? ctx->block : QDPB_DSLASH_BLOCK;
   const bool halo = g.part != 0;
   const bool dot = a.dot_x != nullptr;
@@ -786,7 +808,7 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
     if ((rc = ensure_reduce(ctx, nparts))) return rc;
     P.dotx = fview<R>(a.dot_x, g.stride);
     P.dot_part = ctx->red_partials;
-    P.dot_shift = (R)a.dot_shift;
+    P.dot_shift = (T)a.dot_shift;
   }
 
   unsigned seq = 0;
@@ -837,7 +859,7 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
         if (!((g.part >> mu) & 1)) continue;
         const bool self = direct_self(ctx, mu);
         any_comm |= !self;
-        face_bytes[mu] = (size_t)g.faceVh[mu] * 12 * sizeof(R);
+        face_bytes[mu] = (size_t)g.faceVh[mu] * 12 * sizeof(T);
         P.dst[mu][0] = self ? ctx->halo_recv[prec][mu][1] : ctx->halo_send[prec][mu][0];
         P.dst[mu][1] = self ? ctx->halo_recv[prec][mu][0] : ctx->halo_send[prec][mu][1];
         P.ghost[mu][0] = ctx->halo_recv[prec][mu][0];
@@ -847,13 +869,13 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
     for (int mu = 0; mu < 4; mu++) {
       if (!((g.part >> mu) & 1)) continue;
       if (fuse) {  // packed by the leading blocks of the main kernel: bytes only, no launch
-        prof_work(ctx, QDP_PK_DSLASH, 0.0, (double)g.faceVh[mu] * (24 + 12 + 24 + REC + 12) * sizeof(R));
+        prof_work(ctx, QDP_PK_DSLASH, 0.0, (double)g.faceVh[mu] * (24 + 12 + 24 + REC + 12) * BPR);
         continue;
       }
       ProfEvent ev;
       prof_begin(ctx, QDP_PK_PACK, &ev);
       // compulsory: psi read on both faces, the forward face's link, the half spinors written
-      prof_work(ctx, QDP_PK_PACK, 0.0, (double)g.faceVh[mu] * (24 + 12 + 24 + REC + 12) * sizeof(R));
+      prof_work(ctx, QDP_PK_PACK, 0.0, (double)g.faceVh[mu] * (24 + 12 + 24 + REC + 12) * BPR);
       const int n = 2 * g.faceVh[mu];
       if (a.g5_in) pack_kernel<R, REC, true><<<grid_for(n, 128), 128, 0, ctx->stream>>>(g, P, mu);
       else pack_kernel<R, REC, false><<<grid_for(n, 128), 128, 0, ctx->stream>>>(g, P, mu);
@@ -885,7 +907,7 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
       // ghost read, forward-face link, output read-modify-write (+ clover on CLOVINV)
       prof_work(ctx, QDP_PK_DSLASH_EXT, 0.0,
                 (double)g.faceVh[mu] * (2 * 12 + REC + 2 * 48 + (a.epi == EPI_CLOVINV ? 2 * 72 : 0) + (dot ? 48 : 0)) *
-                    sizeof(R));
+                    BPR);
       double *dp = dot ? ctx->red_partials + 2 * ext_off[mu] : nullptr;
       if (a.epi == EPI_CLOVINV) launch_ext<R, REC, EPI_CLOVINV>(ctx, P, mu, a.g5_out, nullptr);
       else launch_ext<R, REC, EPI_PLAIN>(ctx, P, mu, a.g5_out, dp);
@@ -908,6 +930,7 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
 }
 
 int dslash(qdp_ctx ctx, int prec, const DslashArgs &a) {
+  if (a.h16) return dslash_t<h16, 12>(ctx, a);
   if (a.rec12) return prec == QDP_F64 ? dslash_t<double, 12>(ctx, a) : dslash_t<float, 12>(ctx, a);
   return prec == QDP_F64 ? dslash_t<double, 18>(ctx, a) : dslash_t<float, 18>(ctx, a);
 }

@@ -234,6 +234,8 @@ void tune_release(qdp_ctx ctx) {
 // the best seen by more than 33%; then the best block is used for good.  Only payload launches.
 // (A launch "fails" when the block exceeds the kernel's maxThreadsPerBlock -- checked up front
 // by `go`, which returns cudaErrorLaunchOutOfResources without launching.)
+// Both tuners below time a candidate on its SECOND payload launch (the first one of a kernel may
+// include its lazy module load and cold caches); every launch is a payload launch.
 int tuned_launch(qdp_ctx ctx, long key, const std::function<cudaError_t(int)> &go) {
   if (!ctx->autotune) {
     cudaError_t err = go(128);
@@ -258,10 +260,12 @@ int tuned_launch(qdp_ctx ctx, long key, const std::function<cudaError_t(int)> &g
       t.block = t.best_block;
     } else {
       t.block /= 2;
+      t.warm = true;
     }
   }
   cudaError_t err = cudaSuccess;
-  if (t.state != 2) QDP_CUDA(ctx, cudaEventRecord(t.a, ctx->stream));
+  const bool timed = t.state != 2 && !t.warm;
+  if (timed) QDP_CUDA(ctx, cudaEventRecord(t.a, ctx->stream));
   for (;;) {
     err = go(t.block);
     if (err == cudaSuccess || t.state != 0 || t.block <= 32) break;
@@ -269,8 +273,11 @@ int tuned_launch(qdp_ctx ctx, long key, const std::function<cudaError_t(int)> &g
   }
   if (err != cudaSuccess) return cuda_check(ctx, err, "tuned launch");
   if (t.state != 2) {
-    QDP_CUDA(ctx, cudaEventRecord(t.b, ctx->stream));
-    t.pending = true;
+    if (timed) {
+      QDP_CUDA(ctx, cudaEventRecord(t.b, ctx->stream));
+      t.pending = true;
+    }
+    t.warm = !timed && t.warm ? false : t.warm;
     t.state = 1;
   }
   return QDP_OK;
@@ -278,9 +285,13 @@ int tuned_launch(qdp_ctx ctx, long key, const std::function<cudaError_t(int)> &g
 
 // The same rule over an ordered list of launch variants (index 0 = the most threads per block):
 // variant 0 first (the next one if it fails to launch), then probe 1, 2, ... on later payload
-// launches until one is 33% slower than the best or the list ends; keep the best.
+// launches until one is 33% slower than the best or the list ends; keep the best.  For kernels
+// whose output does not depend on its old contents (go() may run twice): a probing call launches
+// its candidate twice back to back and times the second launch only -- warm, and with no host
+// launch latency inside the timed interval (a few-microsecond kernel would otherwise be judged
+// by the host's jitter).
 int tuned_variant(qdp_ctx ctx, long key, int nvar, const std::function<cudaError_t(int)> &go) {
-  Tune &t = ctx->tune[key ^ (1L << 62)];
+  Tune &t = ctx->tune[key | (1L << 61)];  // disjoint from expression (< 2^50) and jit (bit 62) keys
   if (!t.a) {
     cudaEventCreate(&t.a);
     cudaEventCreate(&t.b);
@@ -302,7 +313,6 @@ int tuned_variant(qdp_ctx ctx, long key, int nvar, const std::function<cudaError
       t.block++;
     }
   }
-  if (t.state != 2) QDP_CUDA(ctx, cudaEventRecord(t.a, ctx->stream));
   cudaError_t err;
   for (;;) {
     err = go(t.block);
@@ -310,7 +320,9 @@ int tuned_variant(qdp_ctx ctx, long key, int nvar, const std::function<cudaError
     t.block++;  // could not launch (resources): the next variant
   }
   if (err != cudaSuccess) return cuda_check(ctx, err, "tuned launch");
-  if (t.state != 2) {
+  if (t.state != 2) {  // probing: the timed repeat
+    QDP_CUDA(ctx, cudaEventRecord(t.a, ctx->stream));
+    if ((err = go(t.block)) != cudaSuccess) return cuda_check(ctx, err, "tuned launch");
     QDP_CUDA(ctx, cudaEventRecord(t.b, ctx->stream));
     t.pending = true;
     t.state = 1;

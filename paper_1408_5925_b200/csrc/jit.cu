@@ -61,6 +61,7 @@ struct qdpb::JitKernel {
   std::vector<std::array<int, 4>> temp_dp;
   std::vector<qdp_field> temp_field;
   std::vector<std::vector<qdp_field>> temp_steps;
+  std::vector<std::pair<int, int>> leaf_disp_parity;  // (operand, parity flip) of every leaf load
 };
 
 namespace qdpb {
@@ -1153,12 +1154,16 @@ int jit_prepare(qdp_ctx ctx, const char *expr, int out_kind, int subset, int pre
   std::string key = std::string(expr) + "|" + std::to_string(out_kind) + "|" + std::to_string(subset) + "|" +
                     std::to_string(prec) + "|" + std::to_string(g.part);
   for (int k = 0; k < nops; k++) key += "|" + std::to_string(kinds[k]) + "/" + std::to_string(ops[k]->subset);
+  // cache first: a hit skips parsing, type checking and source generation altogether
+  auto it = ctx->jit.find(key);
+  JitKernel *K = it == ctx->jit.end() ? nullptr : it->second;
+  int rc;
   Generated gen;
   std::string err;
-  int rc = generate(expr, out_kind, prec, kinds, nops, g.part, &gen, err);
-  if (rc) return set_error(ctx, rc, "jit: %s", err.c_str());
+  if (!K && (rc = generate(expr, out_kind, prec, kinds, nops, g.part, &gen, err)))
+    return set_error(ctx, rc, "jit: %s", err.c_str());
   // operand subsets: each leaf is read at parity out_parity ^ flip; a one-parity operand must match
-  for (const auto &lp : gen.leaf_disp_parity) {
+  for (const auto &lp : K ? K->leaf_disp_parity : gen.leaf_disp_parity) {
     const qdp_field f = ops[lp.first];
     if (is_gauge(f->kind) && f->subset != QDP_ALL)
       return set_error(ctx, QDP_EINVAL, "jit: gauge operand $%d must cover all sites", lp.first);
@@ -1166,9 +1171,7 @@ int jit_prepare(qdp_ctx ctx, const char *expr, int out_kind, int subset, int pre
     if (subset == QDP_ALL || (subset ^ lp.second) != f->subset)
       return set_error(ctx, QDP_EINVAL, "jit: operand $%d is read on parity it does not hold", lp.first);
   }
-  auto it = ctx->jit.find(key);
-  JitKernel *K;
-  if (it == ctx->jit.end()) {
+  if (!K) {
     const auto t0 = std::chrono::steady_clock::now();
     std::vector<char> cubin;
     if ((rc = compile_cubin(gen.src, &cubin, err))) return set_error(ctx, rc, "jit: %s", err.c_str());
@@ -1188,12 +1191,11 @@ int jit_prepare(qdp_ctx ctx, const char *expr, int out_kind, int subset, int pre
     }
     k->temp_field.assign(gen.temps.size(), nullptr);
     k->temp_steps.assign(gen.temps.size(), {});
+    k->leaf_disp_parity = gen.leaf_disp_parity;
     ctx->jit_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     ctx->jit_compiled++;
     K = k.release();
     ctx->jit[key] = K;
-  } else {
-    K = it->second;
   }
 
   memset(a, 0, sizeof *a);

@@ -87,6 +87,8 @@ struct RedArgs {
   double *res;           // device scalars (red_result)
   int slot, n;           // res[slot .. slot+n), n = 1 or 2
   double *host;          // optional mapped pinned copy of the n values
+  unsigned *host_flag;   // with host: `token` is stored here (mapped) after the values
+  unsigned token;
   int peer;              // 1: global sum over the peer communicator in the final block
   unsigned seq;          //    its call sequence number
   PeerArgs pa;
@@ -185,6 +187,8 @@ static __device__ __noinline__ void red_finish(const RedArgs &R, int nblk, int v
     if (R.host) {
       R.host[0] = v[0];
       if (R.n > 1) R.host[1] = v[1];
+      __threadfence_system();
+      *(volatile unsigned *)R.host_flag = R.token;
     }
     if (R.has_cg && !skip) cg_record(R.cg, v[0]);
   }

@@ -36,6 +36,7 @@ struct Op {
   int prec;
   const void *U;
   bool rec12;          // U is QDP_GAUGE12
+  bool h16 = false;    // U, A, Ainv and every vector in the 16-bit storage (cg_solve_mixed16)
   const void *A_o;     // clover A on odd sites (nullptr: Wilson)
   const void *Ainv_e;  // clover A^-1 on even sites
   double diag;         // 4 + m
@@ -60,6 +61,7 @@ DslashArgs args(const Op &op) {
   DslashArgs a = {};
   a.U = op.U;
   a.rec12 = op.rec12;
+  a.h16 = op.h16;
   return a;
 }
 
@@ -374,6 +376,106 @@ int cg_solve_mixed(qdp_field x, const qdp_field b, const qdp_field U, const qdp_
     if ((rc = blas_convert(ctx, rs, QDP_F32, r))) return rc;
     if ((rc = copy_slot(ctx, S_RR, S_TRUE))) return rc;
     if ((rc = blas_cg_update_p(ctx, QDP_F32, ps, rs, S_RHO, S_RR))) return rc;
+    if ((rc = copy_slot(ctx, S_RHO, S_RR))) return rc;
+  }
+  if (iters_out) *iters_out = k;
+  if (nreliable_out) *nreliable_out = nrel;
+  if ((rc = finish_solve(op, x, b, A, mp, true_resid))) return rc;  // mp | q: a two-block scratch
+  QDP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  if ((rc = p2p_check(ctx))) return rc;
+  return status;
+}
+
+
+// cg_solve_mixed16: cg_solve_mixed with a 16-bit sloppy level -- U (reconstruct-12), A_oo and
+// A_ee^-1 converted to the 16-bit storage at the start of every call (so they can never be stale),
+// the search direction p and the operator's vectors (t, Mhat p, Mhat^dag Mhat p) 16-bit with a
+// per-site norm, the sloppy residual r and solution x fp32; fp64 reliable updates as before.
+int cg_solve_mixed16(qdp_field x, const qdp_field b, const qdp_field U, const qdp_field A, const qdp_field Ainv,
+                     double mass, double tol, double delta, int maxit, int *iters_out, int *nreliable_out,
+                     double *hist, int hist_cap, double *true_resid) {
+  qdp_ctx ctx = x->ctx;
+  const Geom &g = ctx->geom;
+  const size_t b64 = fermion_block_bytes(QDP_F64, g.stride), b32 = fermion_block_bytes(QDP_F32, g.stride);
+  const size_t b16 = h16_fermion_bytes(g.stride), bu = h16_gauge_bytes(g.stride), bc = h16_clover_bytes(g.stride);
+  int rc;
+  // fp64 work: [t | r | c | mp | q | bh] ; fp32: [r | x] ; 16-bit: [t | p | q | mp] ; U16, A16_o, Ainv16_e
+  const size_t need = 6 * b64 + 2 * b32 + 4 * b16 + bu + 2 * bc;
+  if ((rc = ensure_cg_work(ctx, need))) return rc;
+  char *w64 = (char *)ctx->cg_work, *w32 = w64 + 6 * b64, *w16 = w32 + 2 * b32;
+  char *U16 = w16 + 4 * b16, *A16 = U16 + bu, *Ai16 = A16 + bc;
+  const Op op = make_op(ctx, U, A, Ainv, mass, w64);
+  Op ops = op;
+  ops.prec = QDP_F32;
+  ops.h16 = true;
+  ops.rec12 = true;
+  ops.U = U16;
+  ops.t = w16;
+  if (A) {
+    const size_t cbk = parity_block_bytes(KIND_CLOVER, A->prec, g.stride);
+    if ((rc = h16_gauge_from(ctx, U16, U)) ||
+        (rc = h16_clover_from(ctx, A16, (const char *)A->data + (A->subset == QDP_ALL ? cbk : 0), A->prec)) ||
+        (rc = h16_clover_from(ctx, Ai16, Ainv->data, Ainv->prec)))
+      return rc;
+    ops.A_o = A16;
+    ops.Ainv_e = Ai16;
+  } else if ((rc = h16_gauge_from(ctx, U16, U))) {
+    return rc;
+  }
+  void *r = w64 + b64, *c = w64 + 2 * b64, *mp = w64 + 3 * b64, *q = w64 + 4 * b64, *bh = w64 + 5 * b64;
+  void *rs = w32, *xs = w32 + b32;
+  void *ps = w16 + b16, *qs = w16 + 2 * b16, *mps = w16 + 3 * b16;
+  const char *b_e = (const char *)b->data, *b_o = b_e + b64;
+  char *x_o = (char *)x->data + b64;
+  int k = 0, nrel = 0, status = QDP_NOT_CONVERGED;
+  double rho0 = 0.0;
+
+  // c = Mhat^dag bhat (fp64); x_o = 0; r = c; r_s = (float) r; p_s = (16-bit) r_s; x_s = 0
+  if ((rc = prepare_source(op, bh, b_e, b_o))) return rc;
+  if ((rc = apply_mhat(op, c, bh, true))) return rc;
+  QDP_CUDA(ctx, cudaMemsetAsync(x_o, 0, b64, ctx->stream));
+  QDP_CUDA(ctx, cudaMemsetAsync(xs, 0, b32, ctx->stream));
+  if ((rc = copy_blocks(ctx, QDP_F64, r, c, 1))) return rc;
+  if ((rc = blas_norm2(ctx, QDP_F64, r, 1, S_RHO)) || (rc = read_slot(ctx, S_RHO, &rho0))) return rc;
+  if ((rc = blas_convert(ctx, rs, QDP_F32, r)) || (rc = h16_from_f32(ctx, ps, rs))) return rc;
+  if (hist_cap > 0 && hist) hist[0] = 1.0;
+  if (rho0 == 0.0) status = QDP_OK;
+  double maxr = sqrt(rho0);
+
+  while (status == QDP_NOT_CONVERGED && k < maxit) {
+    if ((rc = apply_mhat(ops, mps, ps, false))) return rc;
+    if ((rc = apply_mhat(ops, qs, mps, true, ps, S_PQ))) return rc;
+    if ((rc = h16_cg_r(ctx, rs, qs, S_RHO, S_PQ, S_RR))) return rc;
+    double rr;
+    if ((rc = read_slot(ctx, S_RR, &rr))) return rc;
+    k++;
+    const bool reliable = sqrt(rr) < delta * maxr || rr <= tol * tol * rho0 || k == maxit;
+    if (!reliable) {
+      if (hist && k < hist_cap) hist[k] = sqrt(rr / rho0);
+      if ((rc = h16_cg_xp(ctx, xs, ps, rs, S_RHO, S_PQ, S_RR, true))) return rc;
+      if ((rc = copy_slot(ctx, S_RHO, S_RR))) return rc;
+      continue;
+    }
+    // reliable update: x += x_s (fp64), r = c - Mhat^dag Mhat x (fp64), r_s = (float) r
+    if ((rc = h16_cg_xp(ctx, xs, ps, rs, S_RHO, S_PQ, S_RR, false))) return rc;
+    if ((rc = blas_accum_mixed(ctx, x_o, xs))) return rc;
+    if ((rc = apply_mhat(op, mp, x_o, false)) || (rc = apply_mhat(op, q, mp, true))) return rc;
+    if ((rc = copy_blocks(ctx, QDP_F64, r, c, 1))) return rc;
+    if ((rc = blas_axpy(ctx, QDP_F64, -1.0, 0.0, q, r, 1))) return rc;
+    double rt;
+    if ((rc = blas_norm2(ctx, QDP_F64, r, 1, S_TRUE)) || (rc = read_slot(ctx, S_TRUE, &rt))) return rc;
+    nrel++;
+    if (hist && k < hist_cap) hist[k] = sqrt(rt / rho0);
+    maxr = sqrt(rt);
+    if (rt <= tol * tol * rho0) {
+      status = QDP_OK;
+      break;
+    }
+    if (k == maxit) break;
+    // p_s = r_s + beta p_s with beta = |r|^2 / rho (the fp64 residual norm), rho <- |r|^2
+    if ((rc = blas_convert(ctx, rs, QDP_F32, r))) return rc;
+    if ((rc = copy_slot(ctx, S_RR, S_TRUE))) return rc;
+    if ((rc = h16_cg_p(ctx, ps, rs, S_RHO, S_RR))) return rc;
     if ((rc = copy_slot(ctx, S_RHO, S_RR))) return rc;
   }
   if (iters_out) *iters_out = k;

@@ -70,6 +70,8 @@ _SIGS = {
                      ctypes.c_int, _dp],
     "qdp_cg_solve_mixed": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                            ctypes.c_int, _ip, _ip, _dp, ctypes.c_int, _dp],
+    "qdp_cg_solve_mixed16": [_vp, _vp, _vp, _vp, _vp, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                             ctypes.c_int, _ip, _ip, _dp, ctypes.c_int, _dp],
     "qdp_cg_solve_multishift": [ctypes.POINTER(_vp), ctypes.c_int, _dp, _vp, _vp, _vp, _vp, ctypes.c_double,
                                 ctypes.c_double, ctypes.c_int, _ip, _ip, _dp, ctypes.c_int, _dp],
     "qdp_expr": [ctypes.c_int, _vp, _vp, _vp, _vp],
@@ -383,6 +385,22 @@ def qdp_cg_solve_mixed(x: Field, b: Field, U: Field, A=None, Ainv=None, U_s: Fie
     st = lib().qdp_cg_solve_mixed(x, b, U, A, Ainv, U_s, A_s, Ainv_s, float(mass), float(tol), float(delta),
                                   int(maxit), ctypes.byref(iters), ctypes.byref(rel), hist, int(hist_cap),
                                   ctypes.byref(tr) if true_resid else None)
+    _check(st, x.ctx)
+    n = iters.value
+    return dict(status=st, iters=n, reliable=rel.value, hist=np.array(hist[:min(n + 1, hist_cap)]),
+                true_resid=tr.value if true_resid else None)
+
+
+def qdp_cg_solve_mixed16(x: Field, b: Field, U: Field, A=None, Ainv=None, mass=0.1, tol=1e-10, delta=0.1,
+                         maxit=10000, hist_cap=None, true_resid=True):
+    """Mixed-precision CG with a 16-bit sloppy level built from the fp64 U, A, Ainv (qdpb.h)."""
+    hist_cap = maxit + 1 if hist_cap is None else hist_cap
+    hist = (ctypes.c_double * max(hist_cap, 1))()
+    iters, rel = ctypes.c_int(), ctypes.c_int()
+    tr = ctypes.c_double()
+    st = lib().qdp_cg_solve_mixed16(x, b, U, A, Ainv, float(mass), float(tol), float(delta), int(maxit),
+                                    ctypes.byref(iters), ctypes.byref(rel), hist, int(hist_cap),
+                                    ctypes.byref(tr) if true_resid else None)
     _check(st, x.ctx)
     n = iters.value
     return dict(status=st, iters=n, reliable=rel.value, hist=np.array(hist[:min(n + 1, hist_cap)]),

@@ -65,7 +65,7 @@ def test_expressions_vs_oracle(q, prec, subset):
         om = q.qdp_field_alloc(c, q.QDP_COLORMATRIX, prec, subset)
         osm = q.qdp_field_alloc(c, q.QDP_SPINMATRIX, prec, subset)
         of = q.qdp_field_alloc(c, q.QDP_FERMION, prec, subset)
-        for _ in range(8):  # several payload launches: the autotuner walks through block sizes
+        for _ in range(14):  # several payload launches: the autotuner walks through block sizes (2 each)
             q.qdp_expr(q.QDP_EXPR_LCM, om, fu, fv)
             assert _err(q.qdp_field_export(om).astype(np.float64), oracle.lcm(d["u"], d["v"])[sites]) <= TOL[prec]
             q.qdp_expr(q.QDP_EXPR_UPSI, of, fu, f1)
@@ -101,7 +101,7 @@ def test_autotuner_halves_on_failed_launch(q):
         q.qdp_expr(q.QDP_EXPR_SPMAT, o, fs, ft)
         b0, tuned = q.qdp_expr_block(c, q.QDP_EXPR_SPMAT, 0)
         assert b0 <= 512 and not tuned
-        for _ in range(10):
+        for _ in range(20):  # each probed size: one warm launch, one timed launch
             q.qdp_expr(q.QDP_EXPR_SPMAT, o, fs, ft)
         b1, tuned = q.qdp_expr_block(c, q.QDP_EXPR_SPMAT, 0)
         assert tuned and b1 <= b0

@@ -63,7 +63,8 @@ for L in [(8, 8, 8, 16), (16, 16, 16, 16), (16, 16, 16, 32), (24, 24, 24, 32), (
                   " | ".join(f"{u:8.2f} {f:5.3f}" for u, f in row), flush=True)
     del Ut
 
-print("\n# norm2 (one launch, result in mapped host memory) incl. host readback: wall us per call")
+print("\n# norm2 (one launch, result in mapped host memory) incl. host readback: wall us per call;"
+      " kernel = CUDA-event time of the launch; ctypes = wall time of a no-op library call (qdp_get_option)")
 for L in [(16, 16, 16, 32), (40, 40, 40, 32)]:
     c = q.qdp_init(L, stream=stream)
     f = q.qdp_field_alloc(c, q.QDP_FERMION, q.QDP_F64, q.QDP_ALL)
@@ -80,5 +81,17 @@ for L in [(16, 16, 16, 32), (40, 40, 40, 32)]:
     for _ in range(n):
         q.qdp_norm2(fe)
     te = (time.perf_counter() - t0) / n
-    print(f"{'x'.join(map(str, L)):>14}: full field {t * 1e6:8.2f} us   one parity {te * 1e6:8.2f} us")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    q.qdp_synchronize(c)
+    e0.record(stream)
+    for _ in range(n):
+        q.qdp_norm2(fe)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(n):
+        q.qdp_get_option(c, q.QDP_OPT_OVERLAP)
+    tc = (time.perf_counter() - t0) / n
+    print(f"{'x'.join(map(str, L)):>14}: full field {t * 1e6:8.2f} us   one parity {te * 1e6:8.2f} us   "
+          f"(one parity, stream time per call {e0.elapsed_time(e1) / n * 1e3:6.2f} us; ctypes no-op {tc * 1e6:5.2f} us)")
     q.qdp_finalize(c)

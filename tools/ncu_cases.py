@@ -1,0 +1,62 @@
+"""Small single-GPU workloads for `ncu --set full` captures (tools/gpu_profile_r02.sh):
+  zt     fp64 EO dslash at 40^3x32 with z and t through the peer-to-peer halo path (self-halo,
+         the fused boundary kernel: pack + interior + remote hops in one kernel)
+  t      the same with only t partitioned (the weak-scaling bench's split)
+  h16    a few iterations of qdp_cg_solve_mixed16 (the 16-bit sloppy dslash launches)
+  r12    fp64 reconstruct-12 plain EO dslash
+  blas   norm2 / CG vector updates at 40^3x32
+Each case warms up, then runs the launches to capture (select them with ncu -k / -s / -c)."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch
+
+import fieldgen
+from paper_1408_5925_b200 import qdpb as q
+
+case = sys.argv[1]
+L = (40, 40, 40, 32)
+stream = torch.cuda.Stream()
+torch.cuda.set_stream(stream)
+c = q.qdp_init(L, stream=stream)
+Ut = fieldgen.random_gauge_torch(L, 21)
+
+
+def gauge(kind=q.QDP_GAUGE):
+    f = q.qdp_field_alloc(c, kind, q.QDP_F64, q.QDP_ALL)
+    q.qdp_field_import_device(f, Ut)
+    return f
+
+
+if case in ("zt", "t"):
+    q.qdp_set_option(c, q.QDP_OPT_SELF_HALO, 12 if case == "zt" else 8)
+    q.qdp_set_option(c, q.QDP_OPT_P2P, 1)
+if case in ("zt", "t", "r12"):
+    fU = gauge(q.QDP_GAUGE12 if case == "r12" else q.QDP_GAUGE)
+    fi = q.qdp_field_alloc(c, q.QDP_FERMION, q.QDP_F64, q.QDP_ODD)
+    fo = q.qdp_field_alloc(c, q.QDP_FERMION, q.QDP_F64, q.QDP_EVEN)
+    for _ in range(12):
+        q.qdp_dslash(fo, fU, fi, q.QDP_EVEN)
+    q.qdp_synchronize(c)
+elif case == "h16":
+    fU = gauge()
+    fb = q.qdp_field_alloc(c, q.QDP_FERMION, q.QDP_F64, q.QDP_ALL)
+    q.qdp_field_import_device(fb, fieldgen.random_spinor_torch(L, 22))
+    fx = q.qdp_field_alloc(c, q.QDP_FERMION, q.QDP_F64, q.QDP_ALL)
+    fA = q.qdp_field_alloc(c, q.QDP_CLOVER, q.QDP_F64, q.QDP_ALL)
+    fAi = q.qdp_field_alloc(c, q.QDP_CLOVER, q.QDP_F64, q.QDP_EVEN)
+    q.qdp_clover_build(fA, fAi, fU, 0.1, 1.0)
+    q.qdp_cg_solve_mixed16(fx, fb, fU, fA, fAi, mass=0.1, tol=0.0, delta=0.1, maxit=6)
+elif case == "blas":
+    a = q.qdp_field_alloc(c, q.QDP_FERMION, q.QDP_F64, q.QDP_ALL)
+    q.qdp_field_import_device(a, fieldgen.random_spinor_torch(L, 23))
+    b = q.qdp_field_alloc(c, q.QDP_FERMION, q.QDP_F64, q.QDP_ALL)
+    for _ in range(30):
+        q.qdp_norm2(a)
+        q.qdp_inner_product(a, b)
+        q.qdp_axpy(0.5, 0.0, a, b)
+q.qdp_synchronize(c)
+q.qdp_finalize(c)
+print("done", case)
