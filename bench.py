@@ -387,6 +387,19 @@ def run_native(args, rank, world, local_rank):
     f_dsl, b_dsl = q.qdp_profile_work(ctx, q.QDP_PK_DSLASH)
     f_all, _ = q.qdp_profile_work(ctx, -1)
     n_all, ms_all = q.qdp_profile_query(ctx, -1)
+    breakdown = {}
+    for name, cls in (("dslash", q.QDP_PK_DSLASH), ("dslash_exterior", q.QDP_PK_DSLASH_EXT), ("pack", q.QDP_PK_PACK),
+                      ("blas", q.QDP_PK_BLAS), ("reduce", q.QDP_PK_REDUCE), ("clover", q.QDP_PK_CLOVER),
+                      ("layout", q.QDP_PK_LAYOUT)):
+        n_c, ms_c = q.qdp_profile_query(ctx, cls)
+        if n_c:
+            _, b_c = q.qdp_profile_work(ctx, cls)
+            breakdown[name] = {"launches": n_c, "ms": ms_c, "share_of_step": ms_c / ms,
+                               "gbs": b_c / (ms_c * 1e-3) * 1e-9 if ms_c > 0 else None}
+    breakdown["gaps_and_other"] = {"ms": ms - ms_all, "share_of_step": (ms - ms_all) / ms}
+    _, b_all = q.qdp_profile_work(ctx, -1)
+    breakdown["step_algorithmic_gbs"] = b_all / (ms * 1e-3) * 1e-9
+    breakdown["step_frac_of_measured_hbm"] = breakdown["step_algorithmic_gbs"] / measured_peak()[0]
     q.qdp_set_option(ctx, q.QDP_OPT_PROFILE, 0)
     assert abs(f_all - cg_flops(Vh, args.iters) * args.steps) <= 1e-9 * f_all, (f_all, cg_flops(Vh, args.iters))
     ms_max = b.max_all(ms)
@@ -465,6 +478,7 @@ def run_native(args, rank, world, local_rank):
                      "peak_source": peak_src},
         "e2e": e2e,
         "gpu_launches": n_all,
+        "step_breakdown": breakdown,
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
         "parity": parity,

@@ -144,11 +144,12 @@ int qdp_get_geometry(qdp_ctx ctx, int local_dims[4], int proc_coords[4]);
  *                     buffers -- the NCCL code path of a multi-GPU run, on one GPU. */
  /*  QDP_OPT_P2P        1: dslash halos go peer to peer instead of through NCCL: every rank
  *                     maps its neighbours' ghost buffers (CUDA IPC over NVLink / NVSwitch,
- *                     exchanged collectively at first use).  One kernel per EO dslash: its
- *                     first-started blocks (an atomic start ticket deals out the roles) pack the
- *                     faces straight into the neighbours' ghost slots and release-signal a
- *                     flag; the interior blocks run meanwhile; the blocks holding face sites
- *                     acquire the flags, add the remote hops and acknowledge (two slots per
+ *                     exchanged collectively at first use).  One kernel per EO dslash: the
+ *                     face packing is a work queue taken by its leading blocks -- and by every
+ *                     block about to wait for a ghost, so no wait depends on an unstarted block --
+ *                     which store the faces straight into the neighbours' ghost slots and
+ *                     release-signal a flag; the interior blocks run meanwhile; the blocks holding
+ *                     face sites acquire the flags, add the remote hops and acknowledge (two slots per
  *                     face).  With QDP_OPT_OVERLAP = 0 every block waits for the ghosts first.
  *                     Self-halo dims use the same protocol on this rank.  Changing
  *                     QDP_OPT_SELF_HALO after the first dslash rebuilds the slots when every

@@ -179,11 +179,11 @@ template <typename R, int REC = 18> struct KParams {
   int fuse_nin;     // interior sites: perm[0, nin) interior, perm[nin, Vh) on a partitioned face
   const int *perm;  // visiting order of the output parity's sites (nullptr: only t partitioned)
   int pack_off[5];  // cumulative pack threads per dim (2 faceVh for a partitioned dim, else 0)
-  // block roles are dealt out by an atomic ticket taken when a block starts (not by blockIdx:
-  // CUDA does not promise in-order dispatch), so every packing block is already running before
-  // any block that waits for a ghost; ticket - ticket_base is the block's virtual index
-  unsigned *ticket;
-  unsigned ticket_base;
+  // face packing as a work queue of pack_chunks chunks (blockDim items each): the leading blocks
+  // and every block that is about to wait for a ghost take chunks until none is left, so a wait
+  // never depends on a block that has not started (CUDA does not promise in-order dispatch)
+  unsigned *pack_q;  // set seq & 1: {next chunk, chunks done}; the other set is reset by block 0
+  int pack_chunks;
   int wait_all;     // QDP_OPT_OVERLAP = 0: every block waits for the ghosts (no overlap; Fig. 6)
   // fused inner product finished inside this kernel (reduce.cuh; whole-lattice or fused boundary)
   int red_fin;
@@ -354,6 +354,49 @@ __device__ __forceinline__ void fused_signal_last(const Geom &g, unsigned *const
   }
 }
 
+// Fused boundary: take chunks of the face-packing work until none is left (every thread of the block
+// calls it; roles are uniform per block).  Each chunk is blockDim consecutive pack items (pack_off
+// order); the block publishes its chunks with one system fence and adds them to the done count; the
+// block that completes the last chunk release-stores seq into the receivers' ready flags.
+template <typename R, int REC, bool G5IN, typename KP>
+__device__ __forceinline__ void pack_help(const Geom &g, const KP &P) {
+  __shared__ int s_chunk;
+  unsigned *q = P.pack_q + 2 * (P.seq & 1u);
+  int mine = 0;
+  for (;;) {
+    if (threadIdx.x == 0) s_chunk = (int)atomicAdd(q, 1u);
+    __syncthreads();
+    const int ch = s_chunk;
+    __syncthreads();
+    if (ch >= P.pack_chunks) break;
+    if (!mine) {  // the receivers must have consumed this slot (written two calls ago)
+#pragma unroll
+      for (int mu = 0; mu < 4; mu++)
+        if ((g.part >> mu) & 1) block_wait_flags(P.war[mu][0], P.war[mu][1], P.seq - 2u, P.err);
+    }
+    const int i = ch * (int)blockDim.x + threadIdx.x;
+#pragma unroll
+    for (int mu = 0; mu < 4; mu++)
+      if (i >= P.pack_off[mu] && i < P.pack_off[mu + 1]) pack_site<R, REC, G5IN>(g, P, mu, i - P.pack_off[mu]);
+    mine++;
+  }
+  if (mine) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      const unsigned prev = atomicAdd(q + 1, (unsigned)mine);
+      if (prev + (unsigned)mine == (unsigned)P.pack_chunks) {
+        __threadfence_system();
+        for (int mu = 0; mu < 4; mu++)
+          if ((g.part >> mu) & 1) {
+            st_release_sys(P.sig[mu][0], P.seq);
+            st_release_sys(P.sig[mu][1], P.seq);
+          }
+      }
+    }
+  }
+}
+
 // Fused boundary: the remote hop(s) of dim MU for a site on its faces, from the ghost slots
 // (forward: P^- psi(x + mu) from the +mu neighbour, multiplied here by U_mu(x); backward: the
 // neighbour already applied U^dag P^+)
@@ -374,27 +417,17 @@ template <typename R, int REC, int EPI, bool G5IN, bool G5OUT, bool HALO, bool D
 __global__ void __launch_bounds__(QDPB_DSLASH_MAXT, (dslash_minb<R, REC>()))
     dslash_kernel(const Geom g, const __grid_constant__ KParams<R, REC> P) {
   int cb = blockIdx.x * blockDim.x + threadIdx.x;
-  int vb = blockIdx.x;  // virtual block index (fused boundary: the start ticket)
+  const int vb = blockIdx.x;
   double dot = 0.0;
   bool face = false;  // fused boundary: this block holds sites on a partitioned face
   if (HALO && P.fuse) {
-    __shared__ unsigned s_ticket;
-    if (threadIdx.x == 0) s_ticket = atomicAdd(P.ticket, 1u) - P.ticket_base;
-    __syncthreads();
-    vb = (int)s_ticket;
-    cb = vb * blockDim.x + threadIdx.x;
-    if (vb < P.fuse_npack) {
-      // the first blocks to start: pack the partitioned faces into the neighbours' ghost slots
-      // (as pack_kernel), once the receivers consumed the slot (written two calls ago)
-#pragma unroll
-      for (int mu = 0; mu < 4; mu++)
-        if ((g.part >> mu) & 1) block_wait_flags(P.war[mu][0], P.war[mu][1], P.seq - 2u, P.err);
-      for (int i = cb; i < P.pack_off[4]; i += P.fuse_npack * blockDim.x) {  // grid-stride over face sites
-#pragma unroll
-        for (int mu = 0; mu < 4; mu++)
-          if (i >= P.pack_off[mu] && i < P.pack_off[mu + 1]) pack_site<R, REC, G5IN>(g, P, mu, i - P.pack_off[mu]);
-      }
-      fused_signal_last(g, P.pack_counter, P.fuse_npack, P.sig, P.seq);
+    // the other queue set (used by the previous call, which has completed) is reset for the next one
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      P.pack_q[2 * ((P.seq + 1u) & 1u)] = 0u;
+      P.pack_q[2 * ((P.seq + 1u) & 1u) + 1] = 0u;
+    }
+    if ((int)blockIdx.x < P.fuse_npack) {  // leading blocks: pack (work queue) and leave
+      pack_help<R, REC, G5IN>(g, P);
       if (DOT) {
         if (P.red_fin) red_finish(P.red, gridDim.x, vb, 0.0, 0.0, false);
         else dot_block_partial(0.0, P.dot_part, vb);
@@ -402,8 +435,9 @@ __global__ void __launch_bounds__(QDPB_DSLASH_MAXT, (dslash_minb<R, REC>()))
       return;
     }
     cb -= P.fuse_npack * blockDim.x;
-    face = (vb - P.fuse_npack + 1) * (int)blockDim.x > P.fuse_nin;
+    face = (int)((blockIdx.x - P.fuse_npack + 1) * blockDim.x) > P.fuse_nin;
     if (face || P.wait_all) {
+      pack_help<R, REC, G5IN>(g, P);  // whatever packing is left first: a wait never depends on an unstarted block
 #pragma unroll
       for (int mu = 0; mu < 4; mu++)
         if ((g.part >> mu) & 1) block_wait_flags(P.ready[mu][0], P.ready[mu][1], P.seq, P.err);
@@ -417,6 +451,8 @@ __global__ void __launch_bounds__(QDPB_DSLASH_MAXT, (dslash_minb<R, REC>()))
       }
     }
   }
+  Spinor<Arith_t<R>> o;
+  bool have = false;
   if (cb < g.Vh) {
     const int p = P.parity;
     int c[4];
@@ -445,7 +481,8 @@ __global__ void __launch_bounds__(QDPB_DSLASH_MAXT, (dslash_minb<R, REC>()))
       remote_hop<R, 2>(g, P, c, cb, p, acc);
       remote_hop<R, 3>(g, P, c, cb, p, acc);
     }
-    Spinor<T> o = epilogue<R, EPI>(P, cb, acc, G5OUT);
+    o = epilogue<R, EPI>(P, cb, acc, G5OUT);
+    have = true;
     if (DOT) {
       // fused Re<d, out> (and out += dot_shift d: the base shift of the multi-shift CG)
       const Spinor<T> d = P.dotx.load_stream(cb);
@@ -453,15 +490,16 @@ __global__ void __launch_bounds__(QDPB_DSLASH_MAXT, (dslash_minb<R, REC>()))
 #pragma unroll
         for (int k = 0; k < 12; k++) o.c[k] = o.c[k] + P.dot_shift * d.c[k];
       }
-      P.out.store(cb, o);
       dot = re_dot(d, o);
-    } else {
-      P.out.store(cb, o);
     }
   }
+  // the block's partial of the fused dot goes out BEFORE the output stores (reduce.cuh red_arrive)
+  bool red_last = false;
+  if (DOT && P.red_fin) red_last = red_arrive(P.red, gridDim.x, vb, dot, 0.0);
+  if (have) P.out.store(cb, o);
   if (DOT) {
-    if (P.red_fin) red_finish(P.red, gridDim.x, vb, dot, 0.0, false);
-    else dot_block_partial(dot, P.dot_part, vb);
+    if (!P.red_fin) dot_block_partial(dot, P.dot_part, vb);
+    else if (red_last) red_complete(P.red, gridDim.x, vb, false);
   }
   if (HALO && P.fuse && face) {  // the last face block tells the senders their slots were consumed
     const int first = P.fuse_npack + P.fuse_nin / (int)blockDim.x;
@@ -842,9 +880,8 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
       P.fuse = 1;
       P.fuse_npack = npack;
       for (int k = 0; k < 5; k++) P.pack_off[k] = pack_off[k];
-      P.ticket = L.ticket;
-      P.ticket_base = *L.ticket_base;
-      *L.ticket_base += (unsigned)(grid_for(g.Vh, block) + npack);  // the launch below takes them all
+      P.pack_q = L.pack_q;
+      P.pack_chunks = grid_for(pack_off[4], block);
       P.wait_all = ctx->overlap ? 0 : 1;
     }
   }

@@ -28,7 +28,7 @@ __global__ void __launch_bounds__(HB) gauge_h16_kernel(const Geom g, const Gauge
       int w[6];
 #pragma unroll
       for (int k = 0; k < 6; k++)
-        w[k] = (int)(unsigned short)q16((float)u.m[k].re, s) | ((int)q16((float)u.m[k].im, s) << 16);
+        w[k] = h16_pack((float)u.m[k].re * s, (float)u.m[k].im * s);
       char *b = dst + (size_t)(mu * 2 + par) * 24 * g.stride;
       ((int4 *)b)[cb] = make_int4(w[0], w[1], w[2], w[3]);
       ((int2 *)(b + (size_t)16 * g.stride))[cb] = make_int2(w[4], w[5]);
@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(HB) clover_h16_kernel(const Geom g, const Clov
     int w[4];
 #pragma unroll
     for (int j = 0; j < 4; j++)
-      w[j] = (int)(unsigned short)q16(f[8 * k + 2 * j], inv) | ((int)q16(f[8 * k + 2 * j + 1], inv) << 16);
+      w[j] = h16_pack(f[8 * k + 2 * j] * inv, f[8 * k + 2 * j + 1] * inv);
     dst[(size_t)k * g.stride + cb] = make_int4(w[0], w[1], w[2], w[3]);
   }
   ((float *)(dst + (size_t)9 * g.stride))[cb] = m;

@@ -505,8 +505,17 @@ template <> struct Arith<h16> { using T = float; };
 template <typename S> using Arith_t = typename Arith<S>::T;
 constexpr float H16_SCALE = 32767.0f;
 
-__device__ __forceinline__ short q16(float v, float inv) { return (short)__float2int_rn(v * inv); }
-__device__ __forceinline__ float dq16(int word, int hi) { return (float)(short)(hi ? (word >> 16) : (word & 0xffff)); }
+// int16 <-> fp32 without the quarter-rate I2F / F2I conversions: a 16-bit value q is stored in
+// offset binary u = q + 32768; the float whose bit pattern is 0x4B400000 + u equals 1.5 * 2^23 + u
+// exactly, so one byte permute and one add decode it, and adding 1.5 * 2^23 + 32768 to a value
+// in [-32767.5, 32767.5] leaves round-to-nearest(q) + 32768 in the low 16 bits of the float.
+constexpr float H16_MAGIC = 12615680.0f;  // 1.5 * 2^23 + 32768
+__device__ __forceinline__ float h16_lo(int w) { return __int_as_float(__byte_perm(w, 0x4B400000, 0x7610)) - H16_MAGIC; }
+__device__ __forceinline__ float h16_hi(int w) { return __int_as_float(__byte_perm(w, 0x4B400000, 0x7632)) - H16_MAGIC; }
+// two values already scaled to [-32767, 32767] -> one word (lo in bits 0-15)
+__device__ __forceinline__ int h16_pack(float lo, float hi) {
+  return __byte_perm(__float_as_int(lo + H16_MAGIC), __float_as_int(hi + H16_MAGIC), 0x5410);
+}
 
 template <> struct FermView<h16> {
   int4 *p;      // [3][stride]
@@ -520,7 +529,7 @@ template <> struct FermView<h16> {
       const int4 v = STREAM ? ld_stream(p + (size_t)k * stride + cb) : __ldg(p + (size_t)k * stride + cb);
       const int w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-      for (int j = 0; j < 4; j++) s.c[4 * k + j] = {n * dq16(w[j], 0), n * dq16(w[j], 1)};
+      for (int j = 0; j < 4; j++) s.c[4 * k + j] = {n * h16_lo(w[j]), n * h16_hi(w[j])};
     }
     return s;
   }
@@ -537,7 +546,7 @@ template <> struct FermView<h16> {
       int w[4];
 #pragma unroll
       for (int j = 0; j < 4; j++)
-        w[j] = (int)(unsigned short)q16(s.c[4 * k + j].re, inv) | ((int)q16(s.c[4 * k + j].im, inv) << 16);
+        w[j] = h16_pack(s.c[4 * k + j].re * inv, s.c[4 * k + j].im * inv);
       __stcs(p + (size_t)k * stride + cb, make_int4(w[0], w[1], w[2], w[3]));
     }
     __stcs(norm + cb, m);
@@ -554,7 +563,7 @@ template <> struct GaugeView<h16, 12> {
     constexpr float s = 1.0f / H16_SCALE;
     Link<float> u;
 #pragma unroll
-    for (int k = 0; k < 6; k++) u.m[k] = {s * dq16(w[k], 0), s * dq16(w[k], 1)};
+    for (int k = 0; k < 6; k++) u.m[k] = {s * h16_lo(w[k]), s * h16_hi(w[k])};
     su3_third_row(u);
     return u;
   }
@@ -574,8 +583,8 @@ template <> struct CloverView<h16> {
       const int w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
       for (int j = 0; j < 4; j++) {
-        f[8 * k + 2 * j] = n * dq16(w[j], 0);
-        f[8 * k + 2 * j + 1] = n * dq16(w[j], 1);
+        f[8 * k + 2 * j] = n * h16_lo(w[j]);
+        f[8 * k + 2 * j + 1] = n * h16_hi(w[j]);
       }
     }
     const int o = b ? 4 : 0;  // block 1 starts at entry 36 = plane 4, entry 4
@@ -824,8 +833,7 @@ struct P2PLaunch {
   const unsigned *war[4][2], *ready[4][2];
   unsigned *err;
   unsigned seq;               // this call's sequence number (taken after every set-up step succeeded)
-  unsigned *ticket;           // block-ticket counter of the fused boundary kernel (device)
-  unsigned *ticket_base;      // host mirror: tickets handed out before this launch
+  unsigned *pack_q;           // fused boundary: face-packing work queue, 2 sets x {next, done} (device)
 };
 // set up (collective on first use), then take the next sequence number and fill *out
 int p2p_prepare(qdp_ctx ctx, int prec, P2PLaunch *out);

@@ -26,15 +26,15 @@ enum { F_READY = 0, F_ACK = 1, F_COUNT = 2 };
 constexpr int NFLAGS = 2 * 3 * 4 * 2;
 inline size_t fidx(int prec, int kind, int mu, int d) { return ((size_t)(prec * 3 + kind) * 4 + mu) * 2 + d; }
 
-// words after the flag block: [NFLAGS] error word, [NFLAGS + 1 + prec] block-ticket counter of the
-// fused boundary kernel (local only: never written by a peer)
-constexpr int NWORDS = NFLAGS + 3;
+// words after the flag block: [NFLAGS] error word, [NFLAGS + 1 + 4 prec ..] the face-packing work
+// queue of the fused boundary kernel: two sets (by seq & 1) of {next chunk, chunks done} (local
+// only: never written by a peer)
+constexpr int NWORDS = NFLAGS + 1 + 8;
 
 struct P2P {
-  unsigned *flags = nullptr;  // this rank's flag block (+ error word and ticket counters)
+  unsigned *flags = nullptr;  // this rank's flag block (+ error word and packing work queues)
   size_t slot_bytes[2] = {0, 0};
   int part[2] = {-1, -1};             // partition mask the slots of each precision were set up for
-  unsigned ticket_base[2] = {0, 0};   // tickets handed out so far (host mirror of the counter)
   void *recv[2][4][2] = {};           // this rank's ghost buffers (2 slots each)
   void *peer_recv[2][4][2] = {};      // [prec][mu][d]: ghost slots channel d writes into
   unsigned *peer_flags[4][2] = {};    // flag block of the -mu (d = 0) / +mu (d = 1) neighbour
@@ -89,9 +89,8 @@ static int p2p_setup(qdp_ctx ctx, int prec) {
       }
     const size_t f0 = fidx(prec, 0, 0, 0), nf = fidx(prec + 1, 0, 0, 0) - f0;
     QDP_CUDA(ctx, cudaMemsetAsync(p->flags + f0, 0, sizeof(unsigned) * nf, ctx->stream));
-    QDP_CUDA(ctx, cudaMemsetAsync(p->flags + NFLAGS + 1 + prec, 0, sizeof(unsigned), ctx->stream));
+    QDP_CUDA(ctx, cudaMemsetAsync(p->flags + NFLAGS + 1 + 4 * prec, 0, 4 * sizeof(unsigned), ctx->stream));
     p->seq[prec] = 0;
-    p->ticket_base[prec] = 0;
     p->slot_bytes[prec] = 0;
     p->part[prec] = -1;
   }
@@ -188,8 +187,7 @@ int p2p_prepare(qdp_ctx ctx, int prec, P2PLaunch *L) {
   memset(L, 0, sizeof(*L));
   L->seq = seq;
   L->err = p->flags + NFLAGS;
-  L->ticket = p->flags + NFLAGS + 1 + prec;
-  L->ticket_base = &p->ticket_base[prec];
+  L->pack_q = p->flags + NFLAGS + 1 + 4 * prec;
   for (int mu = 0; mu < 4; mu++) {
     if (!((g.part >> mu) & 1)) continue;
     for (int d = 0; d < 2; d++) {

@@ -133,14 +133,14 @@ __device__ __forceinline__ void cg_record(const CgDev &c, double rr) {
   }
 }
 
-// Called by EVERY thread of EVERY block of the grid (nblk blocks) at its end, with this thread's
-// share (v0, v1); vb = the block's index in the fixed partial order.  skip: the kernel did no
-// work this launch (a CG iteration after convergence); the sum and the peer protocol still run,
-// the CG bookkeeping does not.
-// (out of line, so the main path of the kernels that end with it keeps its registers; pass a
-// __grid_constant__ kernel parameter or any other addressable RedArgs)
-static __device__ __noinline__ void red_finish(const RedArgs &R, int nblk, int vb, double v0, double v1, bool skip) {
-  __shared__ int s_last;
+// First half, called by EVERY thread of EVERY block of the grid (nblk blocks) with this thread's
+// share (v0, v1); vb = the block's index in the fixed partial order.  Stores the block's partial,
+// fences it and counts the block into its group; returns (to every thread) whether this block
+// was the group's last, i.e. must call red_complete.  Kernels that also store a large output call
+// it BEFORE those stores: the fence then only waits for the partial (a fence after the output
+// stores holds each block's SM slot until they are acknowledged -- measured ~16 us per dslash).
+__device__ __forceinline__ bool red_arrive(const RedArgs &R, int nblk, int vb, double v0, double v1) {
+  __shared__ int s_arrive_last;
   block_sum2(v0, v1);
   const int G = blockDim.x;
   const int g = vb / G;
@@ -149,36 +149,51 @@ static __device__ __noinline__ void red_finish(const RedArgs &R, int nblk, int v
     R.part[2 * vb + 1] = v1;
     __threadfence();
     const int ng = min(G, nblk - g * G);
-    s_last = atomicAdd(&R.cnt[1 + g], 1u) == (unsigned)(ng - 1);
+    s_arrive_last = atomicAdd(&R.cnt[1 + g], 1u) == (unsigned)(ng - 1);
   }
   __syncthreads();
-  if (!s_last) return;
+  return s_arrive_last != 0;
+}
+
+// Second half, by every thread of a block for which red_arrive returned true: the group's sum,
+// then (last group) the total, the peer global sum, the results and the CG bookkeeping.  skip:
+// the kernel did no work this launch (a CG iteration after the stopping one): the sum and the peer
+// protocol still run, the CG bookkeeping does not.  Out of line, so the main path of the kernels
+// that end with it keeps its registers (pass a __grid_constant__ kernel parameter or any other
+// addressable RedArgs).
+static __device__ __noinline__ void red_complete(const RedArgs &R, int nblk, int vb, bool skip) {
+  __shared__ int s_last;
+  const int G = blockDim.x;
+  const int g = vb / G;
   __threadfence();
   double a0 = 0.0, a1 = 0.0;
   const int i = g * G + threadIdx.x;
-  if (i < nblk) {
+  if (i < nblk && threadIdx.x < G) {
     a0 = __ldcg(&R.part[2 * i]);
     a1 = __ldcg(&R.part[2 * i + 1]);
   }
   block_sum2(a0, a1);
   const int ngroups = (nblk + G - 1) / G;
+  if (ngroups > 1) {  // (one group: its sum is the total -- no second level, three round trips fewer)
+    if (threadIdx.x == 0) {
+      R.cnt[1 + g] = 0u;
+      R.part2[2 * g] = a0;
+      R.part2[2 * g + 1] = a1;
+      __threadfence();
+      s_last = atomicAdd(&R.cnt[0], 1u) == (unsigned)(ngroups - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    a0 = a1 = 0.0;
+    for (int j = threadIdx.x; j < ngroups; j += G) {
+      a0 += __ldcg(&R.part2[2 * j]);
+      a1 += __ldcg(&R.part2[2 * j + 1]);
+    }
+    block_sum2(a0, a1);
+  }
   if (threadIdx.x == 0) {
     R.cnt[1 + g] = 0u;
-    R.part2[2 * g] = a0;
-    R.part2[2 * g + 1] = a1;
-    __threadfence();
-    s_last = atomicAdd(&R.cnt[0], 1u) == (unsigned)(ngroups - 1);
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  a0 = a1 = 0.0;
-  for (int j = threadIdx.x; j < ngroups; j += G) {
-    a0 += __ldcg(&R.part2[2 * j]);
-    a1 += __ldcg(&R.part2[2 * j + 1]);
-  }
-  block_sum2(a0, a1);
-  if (threadIdx.x == 0) {
     R.cnt[0] = 0u;
     double v[2] = {a0, a1};
     if (R.peer) peer_sum_dev(R.pa, v, R.n, R.seq);
@@ -192,6 +207,11 @@ static __device__ __noinline__ void red_finish(const RedArgs &R, int nblk, int v
     }
     if (R.has_cg && !skip) cg_record(R.cg, v[0]);
   }
+}
+
+// Both halves at the end of a kernel (nothing left to store).
+__device__ __forceinline__ void red_finish(const RedArgs &R, int nblk, int vb, double v0, double v1, bool skip) {
+  if (red_arrive(R, nblk, vb, v0, v1)) red_complete(R, nblk, vb, skip);
 }
 
 // the skip test of a CG kernel of iteration `iter` (stop == nullptr: never skip)

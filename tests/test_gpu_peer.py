@@ -49,3 +49,11 @@ def test_peer_jit(G, P):
 @pytest.mark.parametrize("case", ["cg", "cg_clover", "multishift"])
 def test_peer_cg(case):
     _spawn(case, (4, 4, 4, 8), (1, 1, 1, 2))
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("case", ["cg", "cg_clover"])
+def test_peer_cg_zt(case):
+    """The config-5 decomposition shape (z x t, here 2 x 2 ranks; dist.config5_grid gives 2 x 4 on
+    eight GPUs): fused z x t boundary kernels, one-launch global sums, device-side CG."""
+    _spawn(case, (4, 4, 8, 8), (1, 1, 2, 2))

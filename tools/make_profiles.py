@@ -18,7 +18,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
-PROF = os.path.join(ROOT, "profiles")
+PROF = os.environ.get("PROF_OUT", os.path.join(ROOT, "profiles"))
 tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
 os.makedirs(PROF, exist_ok=True)
 

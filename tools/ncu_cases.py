@@ -17,7 +17,7 @@ import fieldgen
 from paper_1408_5925_b200 import qdpb as q
 
 case = sys.argv[1]
-L = (40, 40, 40, 32)
+L = (16, 16, 16, 32) if case == "blas16" else (40, 40, 40, 32)
 stream = torch.cuda.Stream()
 torch.cuda.set_stream(stream)
 c = q.qdp_init(L, stream=stream)
@@ -49,14 +49,14 @@ elif case == "h16":
     fAi = q.qdp_field_alloc(c, q.QDP_CLOVER, q.QDP_F64, q.QDP_EVEN)
     q.qdp_clover_build(fA, fAi, fU, 0.1, 1.0)
     q.qdp_cg_solve_mixed16(fx, fb, fU, fA, fAi, mass=0.1, tol=0.0, delta=0.1, maxit=6)
-elif case == "blas":
+elif case in ("blas", "blas16"):
     a = q.qdp_field_alloc(c, q.QDP_FERMION, q.QDP_F64, q.QDP_ALL)
     q.qdp_field_import_device(a, fieldgen.random_spinor_torch(L, 23))
     b = q.qdp_field_alloc(c, q.QDP_FERMION, q.QDP_F64, q.QDP_ALL)
     for _ in range(30):
         q.qdp_norm2(a)
         q.qdp_inner_product(a, b)
-        q.qdp_axpy(0.5, 0.0, a, b)
+        q.qdp_axpy(0.5, a, b)
 q.qdp_synchronize(c)
 q.qdp_finalize(c)
 print("done", case)
