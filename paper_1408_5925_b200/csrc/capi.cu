@@ -302,6 +302,7 @@ extern "C" int qdp_finalize(qdp_ctx c) {
   tune_release(c);
   for (int q = 0; q < 2; q++)
     if (c->fuse_perm[q]) cudaFree(c->fuse_perm[q]);
+  if (c->fuse_slabs) cudaFree(c->fuse_slabs);
   p2p_destroy(c);
   peer_destroy(c);
   comm_destroy(c);

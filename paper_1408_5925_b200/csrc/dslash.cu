@@ -177,7 +177,11 @@ template <typename R, int REC = 18> struct KParams {
   int fuse;
   int fuse_npack;   // leading pack blocks
   int fuse_nin;     // interior sites: perm[0, nin) interior, perm[nin, Vh) on a partitioned face
-  const int *perm;  // visiting order of the output parity's sites (nullptr: only t partitioned)
+  const int *perm;  // visiting order of the output parity's sites (nullptr: by arithmetic, below)
+  // z or z x t partitioned: the sites come in (z,t) slabs of S = L0/2 x L1 consecutive cb indices;
+  // interior slabs (z in [sz0, sz0 + nzi), t in [st0, ...)) first, then the face slabs listed here
+  const int *face_slab;
+  int sz0, nzi, st0;
   int pack_off[5];  // cumulative pack threads per dim (2 faceVh for a partitioned dim, else 0)
   // face packing as a work queue of pack_chunks chunks (blockDim items each): the leading blocks
   // and every block that is about to wait for a ghost take chunks until none is left, so a wait
@@ -445,6 +449,15 @@ __global__ void __launch_bounds__(QDPB_DSLASH_MAXT, (dslash_minb<R, REC>()))
     if (cb < g.Vh) {
       if (P.perm) {
         cb = P.perm[cb];
+      } else if (P.face_slab) {  // z or z x t: interior (z,t) slabs by arithmetic, then the face slabs
+        const int S = g.Lh0 * g.L[1];
+        if (cb < P.fuse_nin) {
+          const int sl = cb / S, zi = sl % P.nzi, ti = sl / P.nzi;
+          cb += S * ((zi + P.sz0 + g.L[2] * (ti + P.st0)) - sl);
+        } else {
+          const int k = cb - P.fuse_nin, sl = k / S;
+          cb = k - sl * S + S * __ldg(P.face_slab + sl);
+        }
       } else {  // only t partitioned: interior [F, Vh - F), then the slabs t = 0 and t = L-1, by arithmetic
         const int F = g.faceVh[3];
         cb = cb < P.fuse_nin ? F + cb : (cb - P.fuse_nin < F ? cb - P.fuse_nin : cb);
@@ -762,6 +775,41 @@ static int launch_main_epi(qdp_ctx ctx, const DslashArgs &a, const KParams<R, RE
   return e != cudaSuccess ? cuda_check(ctx, e, "dslash launch") : rc;
 }
 
+struct KParams_slab {
+  const int *face_slab;
+  int sz0, nzi, st0, nin;
+};
+// z or z x t partition (x, y unpartitioned): the face (z,t) slabs, in order, for the fused kernel;
+// the interior slabs are enumerated by arithmetic.  Built once per (context, partition).
+static int fuse_slabs(qdp_ctx ctx, KParams_slab *out) {
+  const Geom &g = ctx->geom;
+  const bool pz = (g.part >> 2) & 1, pt = (g.part >> 3) & 1;
+  if (ctx->fuse_slab_part != g.part) {
+    if (ctx->fuse_slabs) cudaFree(ctx->fuse_slabs);
+    ctx->fuse_slabs = nullptr;
+    std::vector<int> face;
+    int nin = 0;
+    for (int t = 0; t < g.L[3]; t++)
+      for (int z = 0; z < g.L[2]; z++) {
+        const bool onface = (pz && (z == 0 || z == g.L[2] - 1)) || (pt && (t == 0 || t == g.L[3] - 1));
+        if (onface) face.push_back(z + g.L[2] * t);
+        else nin++;
+      }
+    QDP_CUDA(ctx, cudaMalloc((void **)&ctx->fuse_slabs, sizeof(int) * std::max<size_t>(1, face.size())));
+    QDP_CUDA(ctx, cudaMemcpyAsync(ctx->fuse_slabs, face.data(), sizeof(int) * face.size(), cudaMemcpyHostToDevice,
+                                  ctx->stream));
+    QDP_CUDA(ctx, cudaStreamSynchronize(ctx->stream));  // `face` is released on return
+    ctx->fuse_slab_part = g.part;
+    ctx->fuse_nslab_in = nin;
+  }
+  out->face_slab = ctx->fuse_slabs;
+  out->sz0 = pz ? 1 : 0;
+  out->nzi = pz ? g.L[2] - 2 : g.L[2];
+  out->st0 = pt ? 1 : 0;
+  out->nin = ctx->fuse_nslab_in * g.Lh0 * g.L[1];
+  return QDP_OK;
+}
+
 // Visiting order of the fused boundary kernel for output parity p: sites on no partitioned face
 // first (nin of them), then the others; built once per (context, partition, parity), on the host.
 static int fuse_order(qdp_ctx ctx, int p, const int **perm, int *nin) {
@@ -801,6 +849,7 @@ static int fuse_order(qdp_ctx ctx, int p, const int **perm, int *nin) {
 
 template <typename R, int REC>
 static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
+  const bool slab_mode = (ctx->geom.part & 3) == 0 && ctx->geom.part != 8;  // z or z x t
   const Geom &g = ctx->geom;
   const int prec = sizeof(R) == 8 ? QDP_F64 : QDP_F32;  // halo buffers (16-bit storage: fp32 ghosts)
   using T = Arith_t<R>;
@@ -853,7 +902,16 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
   if (halo && ctx->p2p_on) {
     // host-side preparation that can fail comes first; the sequence number is taken last, by
     // p2p_prepare, so a failure never leaves this rank a call behind its neighbours
-    if (fuse && g.part != 8 && (rc = fuse_order(ctx, a.parity, &P.perm, &P.fuse_nin))) return rc;
+    KParams_slab sl = {};
+    if (fuse && slab_mode && (rc = fuse_slabs(ctx, &sl))) return rc;
+    if (fuse && g.part != 8 && !slab_mode && (rc = fuse_order(ctx, a.parity, &P.perm, &P.fuse_nin))) return rc;
+    if (fuse && slab_mode) {
+      P.face_slab = sl.face_slab;
+      P.sz0 = sl.sz0;
+      P.nzi = sl.nzi;
+      P.st0 = sl.st0;
+      P.fuse_nin = sl.nin;
+    }
     // peer-to-peer: pack straight into the neighbours' ghost slots, flags instead of NCCL (p2p.cu)
     P2PLaunch L;
     if ((rc = p2p_prepare(ctx, prec, &L))) return rc;

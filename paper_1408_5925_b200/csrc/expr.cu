@@ -9,6 +9,9 @@
 // Flops and bytes follow Table II's convention (cmul 6, cadd 2; every leaf + the store).
 #include <functional>
 
+#include <stdio.h>
+#include <stdlib.h>
+
 #include "internal.h"
 
 namespace qdpb {
@@ -236,6 +239,11 @@ void tune_release(qdp_ctx ctx) {
 // by `go`, which returns cudaErrorLaunchOutOfResources without launching.)
 // Both tuners below time a candidate on its SECOND payload launch (the first one of a kernel may
 // include its lazy module load and cold caches); every launch is a payload launch.
+static bool tune_log() {  // QDPB_TUNE_LOG=1: report every tuner decision on stderr (measurements)
+  static const bool on = getenv("QDPB_TUNE_LOG") && atoi(getenv("QDPB_TUNE_LOG"));
+  return on;
+}
+
 int tuned_launch(qdp_ctx ctx, long key, const std::function<cudaError_t(int)> &go) {
   if (!ctx->autotune) {
     cudaError_t err = go(128);
@@ -247,8 +255,15 @@ int tuned_launch(qdp_ctx ctx, long key, const std::function<cudaError_t(int)> &g
     cudaEventCreate(&t.b);
   }
   if (t.pending) {  // time of the previous payload launch at t.block
+    // never wait for it: a synchronisation here would leave the GPU idle before the next probe and
+    // put the host's launch latency into its timing; until the events complete, launch untimed
+    const cudaError_t qe = cudaEventQuery(t.b);
+    if (qe == cudaErrorNotReady) {
+      const cudaError_t err = go(t.block);
+      return err != cudaSuccess ? cuda_check(ctx, err, "tuned launch") : QDP_OK;
+    }
+    QDP_CUDA(ctx, qe);
     float ms = 0.f;
-    QDP_CUDA(ctx, cudaEventSynchronize(t.b));
     QDP_CUDA(ctx, cudaEventElapsedTime(&ms, t.a, t.b));
     t.pending = false;
     if (t.best_block == 0 || ms < t.best_ms) {
@@ -258,6 +273,7 @@ int tuned_launch(qdp_ctx ctx, long key, const std::function<cudaError_t(int)> &g
     if (ms > 1.33f * t.best_ms || t.block <= 32) {
       t.state = 2;
       t.block = t.best_block;
+      if (tune_log()) fprintf(stderr, "qdpb tune: key %lx -> block %d (%.2f us)\n", key, t.block, 1e3 * t.best_ms);
     } else {
       t.block /= 2;
       t.warm = true;
@@ -298,8 +314,13 @@ int tuned_variant(qdp_ctx ctx, long key, int nvar, const std::function<cudaError
     t.block = 0;
   }
   if (t.pending) {
+    const cudaError_t qe = cudaEventQuery(t.b);  // never wait (see tuned_launch)
+    if (qe == cudaErrorNotReady) {
+      const cudaError_t err = go(t.block);
+      return err != cudaSuccess ? cuda_check(ctx, err, "tuned launch") : QDP_OK;
+    }
+    QDP_CUDA(ctx, qe);
     float ms = 0.f;
-    QDP_CUDA(ctx, cudaEventSynchronize(t.b));
     QDP_CUDA(ctx, cudaEventElapsedTime(&ms, t.a, t.b));
     t.pending = false;
     if (t.best_ms == 0.f || ms < t.best_ms) {
@@ -309,6 +330,7 @@ int tuned_variant(qdp_ctx ctx, long key, int nvar, const std::function<cudaError
     if (ms > 1.33f * t.best_ms || t.block + 1 >= nvar) {
       t.state = 2;
       t.block = t.best_block;
+      if (tune_log()) fprintf(stderr, "qdpb tune: dslash key %lx -> variant %d (%.2f us)\n", key, t.block, 1e3 * t.best_ms);
     } else {
       t.block++;
     }

@@ -692,6 +692,9 @@ struct qdp_ctx_s {
   int *fuse_perm[2] = {nullptr, nullptr};
   int fuse_nin[2] = {0, 0};
   int fuse_part = -1;
+  // z / z x t partitions: the (z,t) slabs on a partitioned face, after the interior ones (dslash.cu)
+  int *fuse_slabs = nullptr;
+  int fuse_slab_part = -1, fuse_nslab_in = 0;
   // peer-memory communicator (qdp_init_peer; peer.cu): no NCCL; the host allgather callback
   // exchanges IPC handles at set-up time only
   qdpb::PeerComm *peer = nullptr;

@@ -101,8 +101,9 @@ def test_autotuner_halves_on_failed_launch(q):
         q.qdp_expr(q.QDP_EXPR_SPMAT, o, fs, ft)
         b0, tuned = q.qdp_expr_block(c, q.QDP_EXPR_SPMAT, 0)
         assert b0 <= 512 and not tuned
-        for _ in range(20):  # each probed size: one warm launch, one timed launch
+        for _ in range(20):  # each probed size: one warm launch, one timed launch (read without waiting)
             q.qdp_expr(q.QDP_EXPR_SPMAT, o, fs, ft)
+            q.qdp_synchronize(c)
         b1, tuned = q.qdp_expr_block(c, q.QDP_EXPR_SPMAT, 0)
         assert tuned and b1 <= b0
         for _ in range(3):

@@ -35,7 +35,7 @@ def _ctx(q, L, mask):
 @pytest.mark.timeout(120)
 @pytest.mark.parametrize("overlap", [1, 0])
 @pytest.mark.parametrize("prec", [0, 1])
-@pytest.mark.parametrize("mask", [8, 12, 15])
+@pytest.mark.parametrize("mask", [8, 4, 12, 15])
 def test_dslash_p2p_self(q, prec, mask, overlap):
     L = (4, 6, 4, 8)
     U = fieldgen.random_gauge(L, 2101)

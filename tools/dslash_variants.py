@@ -25,9 +25,9 @@ torch.cuda.set_stream(stream)
 def eo_us(c, fU, prec, n=50):
     fi = q.qdp_field_alloc(c, q.QDP_FERMION, prec, q.QDP_ODD)
     fo = q.qdp_field_alloc(c, q.QDP_FERMION, prec, q.QDP_EVEN)
-    for _ in range(8):
+    for _ in range(12):  # the tuner reads its probes' events without waiting: let them complete
         q.qdp_dslash(fo, fU, fi, q.QDP_EVEN)
-    q.qdp_synchronize(c)
+        q.qdp_synchronize(c)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(n):
