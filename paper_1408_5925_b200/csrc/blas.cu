@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(1024) norm2_kernel(const Geom g, const typenam
 #pragma unroll
       for (int k = 0; k < E<R>::NP; k++) {
         R v[E<R>::NR];
-        E<R>::get(a[b * bs + (size_t)k * g.stride + cb], v);
+        E<R>::get(ld_stream(a + b * bs + (size_t)k * g.stride + cb), v);
 #pragma unroll
         for (int j = 0; j < E<R>::NR; j++) acc += (double)v[j] * (double)v[j];
       }
@@ -96,8 +96,8 @@ __global__ void __launch_bounds__(1024) inner_kernel(const Geom g, const typenam
       for (int k = 0; k < E<R>::NP; k++) {
         const size_t i = b * bs + (size_t)k * g.stride + cb;
         R u[E<R>::NR], v[E<R>::NR];
-        E<R>::get(a[i], u);
-        E<R>::get(b_[i], v);
+        E<R>::get(ld_stream(a + i), u);
+        E<R>::get(ld_stream(b_ + i), v);
 #pragma unroll
         for (int j = 0; j < E<R>::NR; j += 2) {
           re += (double)u[j] * v[j] + (double)u[j + 1] * v[j + 1];
@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(1024) axpy_kernel(const Geom g, R ar, R ai, co
       for (int k = 0; k < E<R>::NP; k++) {
         const size_t i = b * bs + (size_t)k * g.stride + cb;
         R u[E<R>::NR], v[E<R>::NR];
-        E<R>::get(x[i], u);
+        E<R>::get(ld_stream(x + i), u);
         E<R>::get(y[i], v);
 #pragma unroll
         for (int j = 0; j < E<R>::NR; j += 2) {
@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(1024) axpy_kernel(const Geom g, R ar, R ai, co
           v[j] = re;
           v[j + 1] = im;
         }
-        y[i] = E<R>::put(v);
+        st_stream(y + i, E<R>::put(v));
       }
 }
 
@@ -140,11 +140,11 @@ __global__ void __launch_bounds__(1024) xpay_kernel(const Geom g, const typename
       for (int k = 0; k < E<R>::NP; k++) {
         const size_t i = b * bs + (size_t)k * g.stride + cb;
         R u[E<R>::NR], v[E<R>::NR];
-        E<R>::get(x[i], u);
+        E<R>::get(ld_stream(x + i), u);
         E<R>::get(y[i], v);
 #pragma unroll
         for (int j = 0; j < E<R>::NR; j++) v[j] = u[j] + a * v[j];
-        y[i] = E<R>::put(v);
+        st_stream(y + i, E<R>::put(v));
       }
 }
 
@@ -157,10 +157,10 @@ __global__ void __launch_bounds__(1024) scale_copy_kernel(const Geom g, typename
       for (int k = 0; k < E<R>::NP; k++) {
         const size_t i = b * bs + (size_t)k * g.stride + cb;
         R u[E<R>::NR];
-        E<R>::get(s[i], u);
+        E<R>::get(ld_stream(s + i), u);
 #pragma unroll
         for (int j = 0; j < E<R>::NR; j++) u[j] *= a;
-        d[i] = E<R>::put(u);
+        st_stream(d + i, E<R>::put(u));
       }
 }
 
@@ -180,13 +180,13 @@ __global__ void __launch_bounds__(1024) cg_r_kernel(const Geom g, typename E<R>:
         const size_t i = (size_t)k * g.stride + cb;
         R rv[E<R>::NR], qv[E<R>::NR];
         E<R>::get(r[i], rv);
-        E<R>::get(q[i], qv);
+        E<R>::get(ld_stream(q + i), qv);
 #pragma unroll
         for (int j = 0; j < E<R>::NR; j++) {
           rv[j] = rv[j] - alpha * qv[j];
           acc += (double)rv[j] * (double)rv[j];
         }
-        r[i] = E<R>::put(rv);
+        st_stream(r + i, E<R>::put(rv));
       }
   }
   red_finish(Rd, gridDim.x, blockIdx.x, acc, 0.0, skip);
@@ -213,14 +213,14 @@ __global__ void __launch_bounds__(1024) cg_xp_kernel(const Geom g, typename E<R>
       R xv[E<R>::NR], pv[E<R>::NR], rv[E<R>::NR];
       E<R>::get(x[i], xv);
       E<R>::get(p[i], pv);
-      if (UPD_P && upd_p) E<R>::get(r[i], rv);
+      if (UPD_P && upd_p) E<R>::get(ld_stream(r + i), rv);
 #pragma unroll
       for (int j = 0; j < E<R>::NR; j++) {
         xv[j] = xv[j] + alpha * pv[j];
         if (UPD_P && upd_p) pv[j] = rv[j] + beta * pv[j];
       }
-      x[i] = E<R>::put(xv);
-      if (UPD_P && upd_p) p[i] = E<R>::put(pv);
+      st_stream(x + i, E<R>::put(xv));
+      if (UPD_P && upd_p) st_stream(p + i, E<R>::put(pv));
     }
 }
 
@@ -235,10 +235,10 @@ __global__ void __launch_bounds__(1024) cg_p_kernel(const Geom g, typename E<R>:
       const size_t i = (size_t)k * g.stride + cb;
       R pv[E<R>::NR], rv[E<R>::NR];
       E<R>::get(p[i], pv);
-      E<R>::get(r[i], rv);
+      E<R>::get(ld_stream(r + i), rv);
 #pragma unroll
       for (int j = 0; j < E<R>::NR; j++) pv[j] = rv[j] + beta * pv[j];
-      p[i] = E<R>::put(pv);
+      st_stream(p + i, E<R>::put(pv));
     }
 }
 
@@ -414,7 +414,7 @@ __global__ void __launch_bounds__(1024) copy_kernel(const Geom g, typename E<R>:
 #pragma unroll
       for (int k = 0; k < E<R>::NP; k++) {
         const size_t i = b * bs + (size_t)k * g.stride + cb;
-        d[i] = s[i];
+        st_stream(d + i, ld_stream(s + i));
       }
 }
 

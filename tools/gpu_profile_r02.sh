@@ -13,9 +13,9 @@ timeout 900 $F -k regex:dslash_kernel -s 12 -c 4 -o gpurun_out/prof_dslash_cg -f
 for c in zt t r12; do
   timeout 600 $F -k regex:dslash_kernel -s 10 -c 1 -o gpurun_out/prof_$c -f python tools/ncu_cases.py $c > gpurun_out/ncu_$c.log 2>&1; echo ${c}_rc=$?
 done
-timeout 600 $F -k "regex:h16" -s 4 -c 4 -o gpurun_out/prof_h16 -f python tools/ncu_cases.py h16 > gpurun_out/ncu_h16.log 2>&1; echo h16_rc=$?
+timeout 600 $F --kernel-name-base demangled -k "regex:dslash_kernel<qdpb::h16" -s 4 -c 4 -o gpurun_out/prof_h16 -f python tools/ncu_cases.py h16 > gpurun_out/ncu_h16.log 2>&1; echo h16_rc=$?
 timeout 600 $F -k "regex:norm2|inner|axpy" -s 30 -c 3 -o gpurun_out/prof_blas -f python tools/ncu_cases.py blas > gpurun_out/ncu_blas.log 2>&1; echo blas_rc=$?
-timeout 600 $F -k "regex:norm2" -s 40 -c 2 -o gpurun_out/prof_blas16 -f python tools/ncu_cases.py blas16 > gpurun_out/ncu_blas16.log 2>&1; echo blas16_rc=$?
+timeout 600 $F -k "regex:norm2" -s 20 -c 2 -o gpurun_out/prof_blas16 -f python tools/ncu_cases.py blas16 > gpurun_out/ncu_blas16.log 2>&1; echo blas16_rc=$?
 ls -la gpurun_out/*.ncu-rep
 # summarise here (gpurun copies back at most 64 MiB): text into gpurun_out/prof_txt, reports removed
 mkdir -p gpurun_out/prof_txt
