@@ -164,7 +164,9 @@ int qdp_get_geometry(qdp_ctx ctx, int local_dims[4], int proc_coords[4]);
  *                     launches, per (precision, gauge storage, epilogue, volume), among:
  *                     0 four threads per site (one per direction, 128-thread blocks; plain
  *                     and xpay epilogues), 1 one thread per site, 64-thread blocks, 2 one thread
- *                     per site, 32-thread blocks.  0, 1, 2 force that variant (measurements). */
+ *                     per site, 32-thread blocks, 3 (fp64) one thread per site with the block's
+ *                     forward links staged into shared memory by the bulk-copy engine.
+ *                     0..3 force that variant where it applies (measurements). */
 enum { QDP_OPT_OVERLAP = 0, QDP_OPT_SELF_HALO = 1, QDP_OPT_PROFILE = 2, QDP_OPT_BLOCK = 3,
        QDP_OPT_DET_REDUCE = 4, QDP_OPT_SELF_NCCL = 5, QDP_OPT_AUTOTUNE = 6 /* see qdp_expr */,
        QDP_OPT_P2P = 7, QDP_OPT_FUSE = 8, QDP_OPT_DSLASH_VARIANT = 9 };

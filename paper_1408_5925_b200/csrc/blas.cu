@@ -33,7 +33,8 @@ template <> struct E<float> {
 };
 
 constexpr int RB = 256;  // block of the untuned launches
-constexpr int RED_THREADS = 148 * 8 * 256;  // reductions: at most this many threads (grid-stride)
+// reductions run one site per thread like the other kernels (a capped grid-stride grid left the
+// last stride a third full at 40^3 x 32; the two-level finish of reduce.cuh takes any block count)
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -284,21 +285,20 @@ template <typename R> using T_ = typename E<R>::T;
 // The paper's autotuner (expr.cu tuned_launch) on the launch configuration of
 // every BLAS kernel, per (kernel, precision, number of parity blocks, volume): the block size
 // starts at 1024 and halves on later payload launches until one is 33% slower than the best.
-// `launch(grid, block)` enqueues the kernel; reductions cap the grid (grid-stride loop).
+// `launch(grid, block)` enqueues the kernel (one site per thread; the kernels keep a grid-stride loop).
 enum { K_NORM2 = 1, K_INNER, K_AXPY, K_XPAY, K_SCALE, K_COPY, K_CGR, K_CGXP, K_CGXP0, K_CGP, K_CONV32, K_CONV64, K_ACCUM };
 static int blas_launch(qdp_ctx ctx, int kid, int prec, int nblk, bool red,
                        const std::function<void(int grid, int block)> &launch) {
   const Geom &g = ctx->geom;
   const long key = (1L << 60) | ((long)kid << 44) | ((long)prec << 43) | ((long)nblk << 41) | (long)g.Vh;
   return tuned_launch(ctx, key, [&](int block) -> cudaError_t {
-    int grid = grid_for(g.Vh, block);
-    if (red) grid = std::max(1, std::min(grid, RED_THREADS / block));
-    launch(grid, block);
+    (void)red;
+    launch(grid_for(g.Vh, block), block);
     return cudaGetLastError();
   });
 }
 // largest grid a tuned reduction can use (its partial arrays are sized for it)
-static int red_grid_max(const Geom &g) { return std::max(1, std::min(grid_for(g.Vh, 32), RED_THREADS / 32)); }
+static int red_grid_max(const Geom &g) { return std::max(1, grid_for(g.Vh, 32)); }
 
 int reduce_partials(qdp_ctx ctx, int nparts, int slot) {
   ProfEvent ev;

@@ -382,7 +382,7 @@ extern "C" int qdp_set_option(qdp_ctx c, int opt, long v) {
     case QDP_OPT_AUTOTUNE: c->autotune = v ? 1 : 0; return QDP_OK;
     case QDP_OPT_FUSE: c->fuse = v ? 1 : 0; return QDP_OK;
     case QDP_OPT_DSLASH_VARIANT:
-      if (v < -1 || v > 2) return set_error(c, QDP_EINVAL, "dslash variant must be -1 (tuned), 0, 1 or 2");
+      if (v < -1 || v > 3) return set_error(c, QDP_EINVAL, "dslash variant must be -1 (tuned), 0, 1, 2 or 3");
       c->dslash_variant = (int)v;
       return QDP_OK;
     case QDP_OPT_P2P:

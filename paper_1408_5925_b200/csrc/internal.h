@@ -815,6 +815,12 @@ struct DslashArgs {
   bool h16;               // every operand in the 16-bit storage (U reconstruct-12)
 };
 int dslash(qdp_ctx ctx, int prec, const DslashArgs &a);
+// the per-(storage, links) translation units behind dslash()
+int dslash_d18(qdp_ctx ctx, const DslashArgs &a);
+int dslash_d12(qdp_ctx ctx, const DslashArgs &a);
+int dslash_f18(qdp_ctx ctx, const DslashArgs &a);
+int dslash_f12(qdp_ctx ctx, const DslashArgs &a);
+int dslash_h16(qdp_ctx ctx, const DslashArgs &a);
 
 // clover.cu
 int clover_build(qdp_ctx ctx, const qdp_field U, void *A, int A_subset, void *Ainv, int Ainv_subset,

@@ -33,6 +33,9 @@ def gauge(kind=q.QDP_GAUGE):
 if case in ("zt", "t"):
     q.qdp_set_option(c, q.QDP_OPT_SELF_HALO, 12 if case == "zt" else 8)
     q.qdp_set_option(c, q.QDP_OPT_P2P, 1)
+if case == "r12tma":  # the fp64 reconstruct-12 dslash with bulk-copy staged forward links
+    q.qdp_set_option(c, q.QDP_OPT_DSLASH_VARIANT, 3)
+    case = "r12"
 if case in ("zt", "t", "r12"):
     fU = gauge(q.QDP_GAUGE12 if case == "r12" else q.QDP_GAUGE)
     fi = q.qdp_field_alloc(c, q.QDP_FERMION, q.QDP_F64, q.QDP_ODD)
