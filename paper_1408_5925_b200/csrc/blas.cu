@@ -171,26 +171,35 @@ template <typename R>
 __global__ void __launch_bounds__(1024) cg_r_kernel(const Geom g, typename E<R>::T *r, const typename E<R>::T *q,
                                                   const double *res, int rho_slot, int pq_slot,
                                                   const __grid_constant__ RedArgs Rd) {
+  // one site per thread (blas_launch sizes the grid); the block's partial of |r|^2 is published
+  // BEFORE the r stores, so its fence does not wait for them (reduce.cuh red_arrive)
   const bool skip = Rd.has_cg && cg_skip(Rd.cg.stop, Rd.cg.k);
+  const int cb = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool have = !skip && cb < g.Vh;
   double acc = 0.0;
-  if (!skip) {
+  typename E<R>::T out[E<R>::NP];
+  if (have) {
     const R alpha = (R)(res[rho_slot] / res[pq_slot]);
-    for (int cb = blockIdx.x * blockDim.x + threadIdx.x; cb < g.Vh; cb += gridDim.x * blockDim.x)
 #pragma unroll
-      for (int k = 0; k < E<R>::NP; k++) {
-        const size_t i = (size_t)k * g.stride + cb;
-        R rv[E<R>::NR], qv[E<R>::NR];
-        E<R>::get(r[i], rv);
-        E<R>::get(ld_stream(q + i), qv);
+    for (int k = 0; k < E<R>::NP; k++) {
+      const size_t i = (size_t)k * g.stride + cb;
+      R rv[E<R>::NR], qv[E<R>::NR];
+      E<R>::get(r[i], rv);
+      E<R>::get(ld_stream(q + i), qv);
 #pragma unroll
-        for (int j = 0; j < E<R>::NR; j++) {
-          rv[j] = rv[j] - alpha * qv[j];
-          acc += (double)rv[j] * (double)rv[j];
-        }
-        st_stream(r + i, E<R>::put(rv));
+      for (int j = 0; j < E<R>::NR; j++) {
+        rv[j] = rv[j] - alpha * qv[j];
+        acc += (double)rv[j] * (double)rv[j];
       }
+      out[k] = E<R>::put(rv);
+    }
   }
-  red_finish(Rd, gridDim.x, blockIdx.x, acc, 0.0, skip);
+  const bool last = red_arrive(Rd, gridDim.x, blockIdx.x, acc, 0.0);
+  if (have) {
+#pragma unroll
+    for (int k = 0; k < E<R>::NP; k++) st_stream(r + (size_t)k * g.stride + cb, out[k]);
+  }
+  if (last) red_complete(Rd, gridDim.x, blockIdx.x, skip);
 }
 
 // x += alpha p ; p = r + beta p (UPD_P), alpha = res[rho] / res[pq], beta = res[rr] / res[rho].
