@@ -168,11 +168,13 @@ __global__ void __launch_bounds__(1024) scale_copy_kernel(const Geom g, typename
 // r -= alpha q ; |r|^2 (one launch, reduce.cuh)   with alpha = res[rho] / res[pq]  (CG step 5).
 // Rd.has_cg: iteration Rd.cg.k of the device-side CG (no work once *stop < k; records |r_k|^2).
 template <typename R>
-__global__ void __launch_bounds__(1024) cg_r_kernel(const Geom g, typename E<R>::T *r, const typename E<R>::T *q,
+__global__ void __launch_bounds__(256) cg_r_kernel(const Geom g, typename E<R>::T *r, const typename E<R>::T *q,
                                                   const double *res, int rho_slot, int pq_slot,
                                                   const __grid_constant__ RedArgs Rd) {
   // one site per thread (blas_launch sizes the grid); the block's partial of |r|^2 is published
-  // BEFORE the r stores, so its fence does not wait for them (reduce.cuh red_arrive)
+  // BEFORE the r stores, so its fence does not wait for them (reduce.cuh red_arrive).  The new r
+  // is held in registers meanwhile: launch bound 256 (1024 would cap it at 64 registers and spill;
+  // the tuner's 1024 and 512 launches fail and it halves)
   const bool skip = Rd.has_cg && cg_skip(Rd.cg.stop, Rd.cg.k);
   const int cb = blockIdx.x * blockDim.x + threadIdx.x;
   const bool have = !skip && cb < g.Vh;
