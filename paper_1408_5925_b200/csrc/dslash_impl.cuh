@@ -1081,6 +1081,10 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
       P.pack_q = L.pack_q;
       P.pack_chunks = grid_for(pack_off[4], block);
       P.wait_all = ctx->overlap ? 0 : 1;
+    } else {
+      // separate kernels: the fused kernel's work-queue sets are not advanced by this call, so a
+      // later fused call must not find the counts a fused call left two sequence numbers ago
+      QDP_CUDA(ctx, cudaMemsetAsync(L.pack_q, 0, 4 * sizeof(unsigned), ctx->stream));
     }
   }
   if (halo) {

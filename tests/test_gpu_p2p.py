@@ -83,10 +83,11 @@ def test_dslash_p2p_separate_kernels(q, mask):
             assert rel_site_err(q.qdp_field_export(fo), ref) <= 1e-13
         n_pack, _ = q.qdp_profile_query(c, q.QDP_PK_PACK)
         assert n_pack == 6 * bin(mask).count("1")
-        q.qdp_set_option(c, q.QDP_OPT_FUSE, 1)  # switching back mid-sequence keeps the protocol
-        q.qdp_dslash(fo, fU, fp, q.QDP_ALL)
-        q.qdp_synchronize(c)
-        assert rel_site_err(q.qdp_field_export(fo), ref) <= 1e-13
+        for fuse in (1, 0, 1, 1, 0, 0, 1):  # switching modes mid-sequence keeps the protocol (both queue sets)
+            q.qdp_set_option(c, q.QDP_OPT_FUSE, fuse)
+            q.qdp_dslash(fo, fU, fp, q.QDP_ALL)
+            q.qdp_synchronize(c)
+            assert rel_site_err(q.qdp_field_export(fo), ref) <= 1e-13
     finally:
         q.qdp_finalize(c)
 
