@@ -370,10 +370,10 @@ def run_native(args, rank, world, local_rank):
     for _ in range(args.warmup):
         step()
 
-    # ---- timed region: K solves, fields resident in HBM
+    # ---- timed region: K solves, fields resident in HBM (no per-launch events: the work counters
+    # are maintained either way, the CUDA-event profile runs in a separate pass below)
     b.sync()
     q.qdp_profile_reset(ctx)
-    q.qdp_set_option(ctx, q.QDP_OPT_PROFILE, 1)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(b.dev, rank) as clk:
         e0.record(stream)
@@ -383,27 +383,40 @@ def run_native(args, rank, world, local_rank):
         torch.cuda.synchronize()
     b.barrier()
     ms = e0.elapsed_time(e1)
+    f_all, b_all = q.qdp_profile_work(ctx, -1)
+    n_all, _ = q.qdp_profile_query(ctx, -1)
+    assert abs(f_all - cg_flops(Vh, args.iters) * args.steps) <= 1e-9 * f_all, (f_all, cg_flops(Vh, args.iters))
+    ms_max = b.max_all(ms)
+    flops_job = b.sum_all(f_all)
+
+    # ---- the same K solves once more with a CUDA-event pair around every launch: the dslash
+    # roofline (live launch durations) and the step breakdown by kernel class
+    b.sync()
+    q.qdp_profile_reset(ctx)
+    q.qdp_set_option(ctx, q.QDP_OPT_PROFILE, 1)
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    for _ in range(args.steps):
+        step()
+    e3.record(stream)
+    torch.cuda.synchronize()
+    ms_p = e2.elapsed_time(e3)
     n_dsl, ms_dsl = q.qdp_profile_query(ctx, q.QDP_PK_DSLASH)
     f_dsl, b_dsl = q.qdp_profile_work(ctx, q.QDP_PK_DSLASH)
-    f_all, _ = q.qdp_profile_work(ctx, -1)
-    n_all, ms_all = q.qdp_profile_query(ctx, -1)
-    breakdown = {}
+    _, ms_all = q.qdp_profile_query(ctx, -1)
+    breakdown = {"pass_ms": ms_p}
     for name, cls in (("dslash", q.QDP_PK_DSLASH), ("dslash_exterior", q.QDP_PK_DSLASH_EXT), ("pack", q.QDP_PK_PACK),
                       ("blas", q.QDP_PK_BLAS), ("reduce", q.QDP_PK_REDUCE), ("clover", q.QDP_PK_CLOVER),
                       ("layout", q.QDP_PK_LAYOUT)):
         n_c, ms_c = q.qdp_profile_query(ctx, cls)
         if n_c:
             _, b_c = q.qdp_profile_work(ctx, cls)
-            breakdown[name] = {"launches": n_c, "ms": ms_c, "share_of_step": ms_c / ms,
+            breakdown[name] = {"launches": n_c, "ms": ms_c, "share_of_pass": ms_c / ms_p,
                                "gbs": b_c / (ms_c * 1e-3) * 1e-9 if ms_c > 0 else None}
-    breakdown["gaps_and_other"] = {"ms": ms - ms_all, "share_of_step": (ms - ms_all) / ms}
-    _, b_all = q.qdp_profile_work(ctx, -1)
-    breakdown["step_algorithmic_gbs"] = b_all / (ms * 1e-3) * 1e-9
+    breakdown["gaps_and_other"] = {"ms": ms_p - ms_all, "share_of_pass": (ms_p - ms_all) / ms_p}
+    breakdown["step_algorithmic_gbs"] = b_all / (ms * 1e-3) * 1e-9  # the timed (unprofiled) region
     breakdown["step_frac_of_measured_hbm"] = breakdown["step_algorithmic_gbs"] / measured_peak()[0]
     q.qdp_set_option(ctx, q.QDP_OPT_PROFILE, 0)
-    assert abs(f_all - cg_flops(Vh, args.iters) * args.steps) <= 1e-9 * f_all, (f_all, cg_flops(Vh, args.iters))
-    ms_max = b.max_all(ms)
-    flops_job = b.sum_all(f_all)
     value = flops_job / (ms_max * 1e-3) * 1e-9
 
     # ---- parity of this exact configuration against the oracle
@@ -471,7 +484,7 @@ def run_native(args, rank, world, local_rank):
         "cg_iters_per_s": args.iters * args.steps / (ms_max * 1e-3),
         "dslash": {"launches": n_dsl, "us_per_launch": us_dsl, "gflops_per_gpu": f_dsl / n_dsl / (us_dsl * 1e-6) * 1e-9,
                    "gbs_compulsory_per_gpu": gbs, "bytes_per_site": (b_dsl / n_dsl) / Vh,
-                   "share_of_step": ms_dsl / ms, "frac_of_8TBs": gbs / 8000.0},
+                   "share_of_step": ms_dsl / ms_p, "frac_of_8TBs": gbs / 8000.0},
         "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
                      "traffic": traffic, "traffic_note": traffic_note,
                      "kernel": "dslash_kernel<double> (fused EO hopping term + clover epilogue)",

@@ -260,6 +260,7 @@ int cg_solve(qdp_field x, const qdp_field b, const qdp_field U, const qdp_field 
   // later iteration do nothing.  The history and the stop are read once per chunk.
   volatile int *stop_host = (volatile int *)(ctx->host_pinned + 40);
   *stop_host = 0x7f7f7f7f;
+  ctx->cg_hist[0] = rho0;  // |r_0|^2: the chunk predictor's first rate uses it
   QDP_CUDA(ctx, cudaMemsetAsync(ctx->cg_stop, 0x7f, sizeof(int), ctx->stream));
   const double tol2 = tol * tol;
   const int rs[2] = {S_RHO, S_RR};
