@@ -302,8 +302,12 @@ static int blas_launch(qdp_ctx ctx, int kid, int prec, int nblk, bool red,
                        const std::function<void(int grid, int block)> &launch) {
   const Geom &g = ctx->geom;
   const long key = (1L << 60) | ((long)kid << 44) | ((long)prec << 43) | ((long)nblk << 41) | (long)g.Vh;
+  // a block above the kernel's launch bound "fails" up front, without a launch (as the expression
+  // kernels do): the tuner halves, and no failed launch reaches the driver
+  const int max_block = kid == K_CGR ? 256 : 1024;
   return tuned_launch(ctx, key, [&](int block) -> cudaError_t {
     (void)red;
+    if (block > max_block) return cudaErrorLaunchOutOfResources;
     launch(grid_for(g.Vh, block), block);
     return cudaGetLastError();
   });
