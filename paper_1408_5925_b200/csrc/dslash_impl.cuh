@@ -115,6 +115,38 @@ __device__ __forceinline__ void accum_recon(Spinor<R> &acc, const Half<R> &h) {
   }
 }
 
+// acc += f x (the reconstruction of accum_recon), with every scaled term one fused multiply-add:
+// the 16-bit dslash applies its operands' scales here instead of to every stored value
+template <int K, typename R>
+__device__ __forceinline__ void add_f(cx<R> &a, cx<R> h, R f) {  // K: 0 +h, 1 -h, 2 +i h, 3 -i h
+  if (K == 0) { a.re = fma(f, h.re, a.re); a.im = fma(f, h.im, a.im); }
+  else if (K == 1) { a.re = fma(-f, h.re, a.re); a.im = fma(-f, h.im, a.im); }
+  else if (K == 2) { a.re = fma(-f, h.im, a.re); a.im = fma(f, h.re, a.im); }
+  else { a.re = fma(f, h.im, a.re); a.im = fma(-f, h.re, a.im); }
+}
+template <int MU, int S, typename R>
+__device__ __forceinline__ void accum_recon_f(Spinor<R> &acc, const Half<R> &h, R f) {
+#pragma unroll
+  for (int c = 0; c < 3; c++) {
+    const cx<R> h0 = h.c[c], h1 = h.c[3 + c];
+    add_f<0>(acc.c[c], h0, f);
+    add_f<0>(acc.c[3 + c], h1, f);
+    if (MU == 0) {        // r2 = -S i h1, r3 = -S i h0
+      add_f<(S > 0 ? 3 : 2)>(acc.c[6 + c], h1, f);
+      add_f<(S > 0 ? 3 : 2)>(acc.c[9 + c], h0, f);
+    } else if (MU == 1) { // r2 = S h1, r3 = -S h0
+      add_f<(S > 0 ? 0 : 1)>(acc.c[6 + c], h1, f);
+      add_f<(S > 0 ? 1 : 0)>(acc.c[9 + c], h0, f);
+    } else if (MU == 2) { // r2 = -S i h0, r3 = S i h1
+      add_f<(S > 0 ? 3 : 2)>(acc.c[6 + c], h0, f);
+      add_f<(S > 0 ? 2 : 3)>(acc.c[9 + c], h1, f);
+    } else {              // r2 = S h0, r3 = S h1
+      add_f<(S > 0 ? 0 : 1)>(acc.c[6 + c], h0, f);
+      add_f<(S > 0 ? 0 : 1)>(acc.c[9 + c], h1, f);
+    }
+  }
+}
+
 template <typename R>
 __device__ __forceinline__ Half<R> mul_link(const Link<R> &u, const Half<R> &h) {  // U h
   Half<R> r;
@@ -208,11 +240,18 @@ __device__ __forceinline__ void hop_dir(const Geom &g, const KP &P, const int c[
     if (!remote) {
       int n[4] = {c[0], c[1], c[2], c[3]};
       n[MU] = (c[MU] + 1 == g.L[MU]) ? 0 : c[MU] + 1;
-      Spinor<T> s = P.psi.load(coords_cb(g, n));
-      if (G5IN) g5(s);
-      Half<T> h = project<MU, -1>(s);
-      Link<T> u = P.U.load(MU, p, cb);
-      accum_recon<MU, -1>(acc, mul_link(u, h));
+      if constexpr (is_h16<R>()) {  // stored integers; both scales applied once, in the accumulation
+        float sc;
+        Spinor<T> s = P.psi.load_raw(coords_cb(g, n), sc);
+        if (G5IN) g5(s);
+        accum_recon_f<MU, -1>(acc, mul_link(P.U.load_raw(MU, p, cb), project<MU, -1>(s)), sc * P.U.raw_scale);
+      } else {
+        Spinor<T> s = P.psi.load(coords_cb(g, n));
+        if (G5IN) g5(s);
+        Half<T> h = project<MU, -1>(s);
+        Link<T> u = P.U.load(MU, p, cb);
+        accum_recon<MU, -1>(acc, mul_link(u, h));
+      }
     }
   }
   // backward: (1 + gamma_mu) U_mu(x - mu)^dag psi(x - mu)
@@ -222,11 +261,19 @@ __device__ __forceinline__ void hop_dir(const Geom &g, const KP &P, const int c[
       int n[4] = {c[0], c[1], c[2], c[3]};
       n[MU] = (c[MU] == 0) ? g.L[MU] - 1 : c[MU] - 1;
       const int ncb = coords_cb(g, n);
-      Spinor<T> s = P.psi.load(ncb);
-      if (G5IN) g5(s);
-      Half<T> h = project<MU, +1>(s);
-      Link<T> u = P.U.load(MU, 1 - p, ncb);
-      accum_recon<MU, +1>(acc, mul_link_dag(u, h));
+      if constexpr (is_h16<R>()) {
+        float sc;
+        Spinor<T> s = P.psi.load_raw(ncb, sc);
+        if (G5IN) g5(s);
+        accum_recon_f<MU, +1>(acc, mul_link_dag(P.U.load_raw(MU, 1 - p, ncb), project<MU, +1>(s)),
+                              sc * P.U.raw_scale);
+      } else {
+        Spinor<T> s = P.psi.load(ncb);
+        if (G5IN) g5(s);
+        Half<T> h = project<MU, +1>(s);
+        Link<T> u = P.U.load(MU, 1 - p, ncb);
+        accum_recon<MU, +1>(acc, mul_link_dag(u, h));
+      }
     }
   }
 }
@@ -767,7 +814,6 @@ template <> FermView<h16> fview<h16>(const void *p, int stride) {
 template <> CloverView<h16> cview<h16>(const void *p, int stride) {
   return {(const int4 *)p, p ? (const float *)((const char *)p + (size_t)144 * stride) : nullptr, stride};
 }
-template <typename R> constexpr bool is_h16() { return std::is_same<R, h16>::value; }
 
 template <typename R, int REC, int EPI, bool G5IN, bool G5OUT, bool HALO, bool DOT>
 static void launch_main(qdp_ctx ctx, const KParams<R, REC> &P, int block) {
