@@ -963,7 +963,9 @@ def measure_tts(b, ctx, fU, fA, fAi, fb, fx, U, bsrc):
     fU32r = q.qdp_field_alloc(ctx, q.QDP_GAUGE12, q.QDP_F32, q.QDP_ALL)
     fA32 = q.qdp_field_alloc(ctx, q.QDP_CLOVER, q.QDP_F32, q.QDP_ODD)
     fAi32 = q.qdp_field_alloc(ctx, q.QDP_CLOVER, q.QDP_F32, q.QDP_EVEN)
+    fU12 = q.qdp_field_alloc(ctx, q.QDP_GAUGE12, q.QDP_F64, q.QDP_ALL)
     try:
+        q.qdp_field_import(fU12, U)
         U32 = U.astype(np.float32)
         q.qdp_field_import(fU32, U32)
         q.qdp_field_import(fU32r, U32)
@@ -985,6 +987,11 @@ def measure_tts(b, ctx, fU, fA, fAi, fb, fx, U, bsrc):
                                                                   delta=0.1, maxit=5000),
             "mixed_h16_delta1e-2": lambda: q.qdp_cg_solve_mixed16(fx, fb, fU, fA, fAi, mass=MASS, tol=1e-10,
                                                                   delta=1e-2, maxit=5000),
+            "mixed_h16_delta1e-3": lambda: q.qdp_cg_solve_mixed16(fx, fb, fU, fA, fAi, mass=MASS, tol=1e-10,
+                                                                  delta=1e-3, maxit=5000),
+            # the same with fp64 reconstruct-12 links for the reliable updates (and the 16-bit copy)
+            "mixed_h16_u12_delta1e-2": lambda: q.qdp_cg_solve_mixed16(fx, fb, fU12, fA, fAi, mass=MASS, tol=1e-10,
+                                                                      delta=1e-2, maxit=5000),
         }
         tts = {}
         for name, fn in solvers.items():
@@ -994,7 +1001,7 @@ def measure_tts(b, ctx, fU, fA, fAi, fb, fx, U, bsrc):
             tts[name] = {"ms": ms, "iters": res["iters"], "true_resid": res["true_resid"],
                          "reliable_updates": res.get("reliable")}
     finally:
-        for f in (fU32, fU32r, fA32, fAi32):
+        for f in (fU32, fU32r, fA32, fAi32, fU12):
             q.qdp_field_free(f)
     return tts
 
