@@ -992,6 +992,8 @@ def measure_tts(b, ctx, fU, fA, fAi, fb, fx, U, bsrc):
             # the same with fp64 reconstruct-12 links for the reliable updates (and the 16-bit copy)
             "mixed_h16_u12_delta1e-2": lambda: q.qdp_cg_solve_mixed16(fx, fb, fU12, fA, fAi, mass=MASS, tol=1e-10,
                                                                       delta=1e-2, maxit=5000),
+            "mixed_h16_u12_delta1e-3": lambda: q.qdp_cg_solve_mixed16(fx, fb, fU12, fA, fAi, mass=MASS, tol=1e-10,
+                                                                      delta=1e-3, maxit=5000),
         }
         tts = {}
         for name, fn in solvers.items():
