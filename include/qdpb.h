@@ -166,10 +166,15 @@ int qdp_get_geometry(qdp_ctx ctx, int local_dims[4], int proc_coords[4]);
  *                     and xpay epilogues), 1 one thread per site, 64-thread blocks, 2 one thread
  *                     per site, 32-thread blocks, 3 (fp64) one thread per site with the block's
  *                     forward links staged into shared memory by the bulk-copy engine.
- *                     0..3 force that variant where it applies (measurements). */
+ *                     0..3 force that variant where it applies (measurements).
+ *  QDP_OPT_PDL        1 (default; environment QDPB_PDL=0 changes the default): the dslash,
+ *                     BLAS and reduction kernels of the solvers are launched with programmatic
+ *                     dependent launch, so each becomes resident while its predecessor drains
+ *                     (it waits for the predecessor's completion before reading anything);
+ *                     0: plain stream order.  Results are identical either way. */
 enum { QDP_OPT_OVERLAP = 0, QDP_OPT_SELF_HALO = 1, QDP_OPT_PROFILE = 2, QDP_OPT_BLOCK = 3,
        QDP_OPT_DET_REDUCE = 4, QDP_OPT_SELF_NCCL = 5, QDP_OPT_AUTOTUNE = 6 /* see qdp_expr */,
-       QDP_OPT_P2P = 7, QDP_OPT_FUSE = 8, QDP_OPT_DSLASH_VARIANT = 9 };
+       QDP_OPT_P2P = 7, QDP_OPT_FUSE = 8, QDP_OPT_DSLASH_VARIANT = 9, QDP_OPT_PDL = 10 };
 int qdp_set_option(qdp_ctx ctx, int option, long value);
 int qdp_get_option(qdp_ctx ctx, int option, long *value);
 

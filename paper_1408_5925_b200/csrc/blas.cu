@@ -72,6 +72,7 @@ __global__ void rank_sum_kernel(const double *g, int nranks, int n, double *res,
 
 template <typename R>
 __global__ void __launch_bounds__(1024) norm2_kernel(const Geom g, const typename E<R>::T *a, int nblk, const __grid_constant__ RedArgs Rd) {
+  pdl_enter();
   double acc = 0.0;
   const size_t bs = (size_t)E<R>::NP * g.stride;
   for (int cb = blockIdx.x * blockDim.x + threadIdx.x; cb < g.Vh; cb += gridDim.x * blockDim.x)
@@ -89,6 +90,7 @@ __global__ void __launch_bounds__(1024) norm2_kernel(const Geom g, const typenam
 template <typename R>
 __global__ void __launch_bounds__(1024) inner_kernel(const Geom g, const typename E<R>::T *a, const typename E<R>::T *b_,
                                                    int nblk, const __grid_constant__ RedArgs Rd) {
+  pdl_enter();
   double re = 0.0, im = 0.0;
   const size_t bs = (size_t)E<R>::NP * g.stride;
   for (int cb = blockIdx.x * blockDim.x + threadIdx.x; cb < g.Vh; cb += gridDim.x * blockDim.x)
@@ -111,6 +113,7 @@ __global__ void __launch_bounds__(1024) inner_kernel(const Geom g, const typenam
 template <typename R>
 __global__ void __launch_bounds__(1024) axpy_kernel(const Geom g, R ar, R ai, const typename E<R>::T *x,
                                                   typename E<R>::T *y, int nblk) {
+  pdl_enter();
   const size_t bs = (size_t)E<R>::NP * g.stride;
   for (int cb = blockIdx.x * blockDim.x + threadIdx.x; cb < g.Vh; cb += gridDim.x * blockDim.x)
     for (int b = 0; b < nblk; b++)
@@ -134,6 +137,7 @@ __global__ void __launch_bounds__(1024) axpy_kernel(const Geom g, R ar, R ai, co
 // y = x + a y
 template <typename R>
 __global__ void __launch_bounds__(1024) xpay_kernel(const Geom g, const typename E<R>::T *x, R a, typename E<R>::T *y, int nblk) {
+  pdl_enter();
   const size_t bs = (size_t)E<R>::NP * g.stride;
   for (int cb = blockIdx.x * blockDim.x + threadIdx.x; cb < g.Vh; cb += gridDim.x * blockDim.x)
     for (int b = 0; b < nblk; b++)
@@ -151,6 +155,7 @@ __global__ void __launch_bounds__(1024) xpay_kernel(const Geom g, const typename
 
 template <typename R>
 __global__ void __launch_bounds__(1024) scale_copy_kernel(const Geom g, typename E<R>::T *d, const typename E<R>::T *s, R a, int nblk) {
+  pdl_enter();
   const size_t bs = (size_t)E<R>::NP * g.stride;
   for (int cb = blockIdx.x * blockDim.x + threadIdx.x; cb < g.Vh; cb += gridDim.x * blockDim.x)
     for (int b = 0; b < nblk; b++)
@@ -171,6 +176,7 @@ template <typename R>
 __global__ void __launch_bounds__(256) cg_r_kernel(const Geom g, typename E<R>::T *r, const typename E<R>::T *q,
                                                   const double *res, int rho_slot, int pq_slot,
                                                   const __grid_constant__ RedArgs Rd) {
+  pdl_enter();
   // one site per thread (blas_launch sizes the grid); the block's partial of |r|^2 is published
   // BEFORE the r stores, so its fence does not wait for them (reduce.cuh red_arrive).  The new r
   // is held in registers meanwhile: launch bound 256 (1024 would cap it at 64 registers and spill;
@@ -210,6 +216,7 @@ template <typename R, bool UPD_P>
 __global__ void __launch_bounds__(1024) cg_xp_kernel(const Geom g, typename E<R>::T *x, typename E<R>::T *p,
                                                    const typename E<R>::T *r, const double *res, int rho_slot,
                                                    int pq_slot, int rr_slot, const int *stop, int iter) {
+  pdl_enter();
   bool upd_p = UPD_P;
   if (stop) {
     const int s = __ldcg(stop);
@@ -240,6 +247,7 @@ __global__ void __launch_bounds__(1024) cg_xp_kernel(const Geom g, typename E<R>
 template <typename R>
 __global__ void __launch_bounds__(1024) cg_p_kernel(const Geom g, typename E<R>::T *p, const typename E<R>::T *r,
                                                   const double *res, int rho_slot, int rr_slot) {
+  pdl_enter();
   const R beta = (R)(res[rr_slot] / res[rho_slot]);
   for (int cb = blockIdx.x * blockDim.x + threadIdx.x; cb < g.Vh; cb += gridDim.x * blockDim.x)
 #pragma unroll
@@ -257,6 +265,7 @@ __global__ void __launch_bounds__(1024) cg_p_kernel(const Geom g, typename E<R>:
 // Precision conversion of one fermion parity block: fp64 double2[12] <-> fp32 float4[6].
 template <bool TO32>
 __global__ void __launch_bounds__(1024) convert_kernel(const Geom g, double2 *d64, float4 *f32) {
+  pdl_enter();
   for (int cb = blockIdx.x * blockDim.x + threadIdx.x; cb < g.Vh; cb += gridDim.x * blockDim.x)
 #pragma unroll
     for (int k = 0; k < 6; k++) {
@@ -275,6 +284,7 @@ __global__ void __launch_bounds__(1024) convert_kernel(const Geom g, double2 *d6
 
 // y64 += x32 (the reliable update's accumulation of the sloppy solution), then x32 = 0
 __global__ void __launch_bounds__(1024) accum_mixed_kernel(const Geom g, double2 *y64, float4 *x32) {
+  pdl_enter();
   for (int cb = blockIdx.x * blockDim.x + threadIdx.x; cb < g.Vh; cb += gridDim.x * blockDim.x)
 #pragma unroll
     for (int k = 0; k < 6; k++) {
@@ -378,8 +388,8 @@ int blas_norm2(qdp_ctx ctx, int prec, const void *a, int nblk, int slot, bool ho
   prof_begin(ctx, QDP_PK_REDUCE, &ev);
   prof_work(ctx, QDP_PK_REDUCE, 48.0 * g.Vh * nblk, 24.0 * g.Vh * nblk * (prec == QDP_F64 ? 8 : 4));
   rc = blas_launch(ctx, K_NORM2, prec, nblk, true, [&](int nb, int bs) {
-    if (prec == QDP_F64) norm2_kernel<double><<<nb, bs, 0, ctx->stream>>>(g, (const T_<double> *)a, nblk, R);
-    else norm2_kernel<float><<<nb, bs, 0, ctx->stream>>>(g, (const T_<float> *)a, nblk, R);
+    if (prec == QDP_F64) launch_k(ctx, norm2_kernel<double>, nb, bs, g, (const T_<double> *)a, nblk, R);
+    else launch_k(ctx, norm2_kernel<float>, nb, bs, g, (const T_<float> *)a, nblk, R);
   });
   if (rc || (rc = prof_end(ctx, &ev))) return rc;
   return after ? reduce_global(ctx, slot, 1) : QDP_OK;
@@ -396,9 +406,9 @@ int blas_inner(qdp_ctx ctx, int prec, const void *a, const void *b, int nblk, in
   prof_work(ctx, QDP_PK_REDUCE, 96.0 * g.Vh * nblk, 48.0 * g.Vh * nblk * (prec == QDP_F64 ? 8 : 4));
   rc = blas_launch(ctx, K_INNER, prec, nblk, true, [&](int nb, int bs) {
     if (prec == QDP_F64)
-      inner_kernel<double><<<nb, bs, 0, ctx->stream>>>(g, (const T_<double> *)a, (const T_<double> *)b, nblk, R);
+      launch_k(ctx, inner_kernel<double>, nb, bs, g, (const T_<double> *)a, (const T_<double> *)b, nblk, R);
     else
-      inner_kernel<float><<<nb, bs, 0, ctx->stream>>>(g, (const T_<float> *)a, (const T_<float> *)b, nblk, R);
+      launch_k(ctx, inner_kernel<float>, nb, bs, g, (const T_<float> *)a, (const T_<float> *)b, nblk, R);
   });
   if (rc || (rc = prof_end(ctx, &ev))) return rc;
   return after ? reduce_global(ctx, slot, 2) : QDP_OK;
@@ -423,6 +433,7 @@ __global__ void scalars_kernel(double *dst, const double *src, int n) {
 }
 template <typename R>
 __global__ void __launch_bounds__(1024) copy_kernel(const Geom g, typename E<R>::T *d, const typename E<R>::T *s, int nblk) {
+  pdl_enter();
   const size_t bs = (size_t)E<R>::NP * g.stride;
   for (int cb = blockIdx.x * blockDim.x + threadIdx.x; cb < g.Vh; cb += gridDim.x * blockDim.x)
     for (int b = 0; b < nblk; b++)
@@ -454,8 +465,8 @@ int copy_blocks(qdp_ctx ctx, int prec, void *dst, const void *src, int nblk) {
   prof_begin(ctx, QDP_PK_BLAS, &ev);
   prof_work(ctx, QDP_PK_BLAS, 0.0, 48.0 * g.Vh * nblk * (prec == QDP_F64 ? 8 : 4));
   int rc = blas_launch(ctx, K_COPY, prec, nblk, false, [&](int nb, int bs) {
-    if (prec == QDP_F64) copy_kernel<double><<<nb, bs, 0, ctx->stream>>>(g, (T_<double> *)dst, (const T_<double> *)src, nblk);
-    else copy_kernel<float><<<nb, bs, 0, ctx->stream>>>(g, (T_<float> *)dst, (const T_<float> *)src, nblk);
+    if (prec == QDP_F64) launch_k(ctx, copy_kernel<double>, nb, bs, g, (T_<double> *)dst, (const T_<double> *)src, nblk);
+    else launch_k(ctx, copy_kernel<float>, nb, bs, g, (T_<float> *)dst, (const T_<float> *)src, nblk);
   });
   if (rc) return rc;
   return prof_end(ctx, &ev);
@@ -468,9 +479,9 @@ int blas_axpy(qdp_ctx ctx, int prec, double ar, double ai, const void *x, void *
   prof_work(ctx, QDP_PK_BLAS, 96.0 * g.Vh * nblk, 72.0 * g.Vh * nblk * (prec == QDP_F64 ? 8 : 4));
   int rc = blas_launch(ctx, K_AXPY, prec, nblk, false, [&](int nb, int bs) {
     if (prec == QDP_F64)
-      axpy_kernel<double><<<nb, bs, 0, ctx->stream>>>(g, ar, ai, (const T_<double> *)x, (T_<double> *)y, nblk);
+      launch_k(ctx, axpy_kernel<double>, nb, bs, g, ar, ai, (const T_<double> *)x, (T_<double> *)y, nblk);
     else
-      axpy_kernel<float><<<nb, bs, 0, ctx->stream>>>(g, (float)ar, (float)ai, (const T_<float> *)x, (T_<float> *)y, nblk);
+      launch_k(ctx, axpy_kernel<float>, nb, bs, g, (float)ar, (float)ai, (const T_<float> *)x, (T_<float> *)y, nblk);
   });
   if (rc) return rc;
   return prof_end(ctx, &ev);
@@ -482,8 +493,8 @@ int blas_xpay(qdp_ctx ctx, int prec, const void *x, double a, void *y, int nblk)
   prof_begin(ctx, QDP_PK_BLAS, &ev);
   prof_work(ctx, QDP_PK_BLAS, 48.0 * g.Vh * nblk, 72.0 * g.Vh * nblk * (prec == QDP_F64 ? 8 : 4));
   int rc = blas_launch(ctx, K_XPAY, prec, nblk, false, [&](int nb, int bs) {
-    if (prec == QDP_F64) xpay_kernel<double><<<nb, bs, 0, ctx->stream>>>(g, (const T_<double> *)x, a, (T_<double> *)y, nblk);
-    else xpay_kernel<float><<<nb, bs, 0, ctx->stream>>>(g, (const T_<float> *)x, (float)a, (T_<float> *)y, nblk);
+    if (prec == QDP_F64) launch_k(ctx, xpay_kernel<double>, nb, bs, g, (const T_<double> *)x, a, (T_<double> *)y, nblk);
+    else launch_k(ctx, xpay_kernel<float>, nb, bs, g, (const T_<float> *)x, (float)a, (T_<float> *)y, nblk);
   });
   if (rc) return rc;
   return prof_end(ctx, &ev);
@@ -496,9 +507,9 @@ int blas_scale_copy(qdp_ctx ctx, int prec, void *dst, const void *src, double a,
   prof_work(ctx, QDP_PK_BLAS, 24.0 * g.Vh * nblk, 48.0 * g.Vh * nblk * (prec == QDP_F64 ? 8 : 4));
   int rc = blas_launch(ctx, K_SCALE, prec, nblk, false, [&](int nb, int bs) {
     if (prec == QDP_F64)
-      scale_copy_kernel<double><<<nb, bs, 0, ctx->stream>>>(g, (T_<double> *)dst, (const T_<double> *)src, a, nblk);
+      launch_k(ctx, scale_copy_kernel<double>, nb, bs, g, (T_<double> *)dst, (const T_<double> *)src, a, nblk);
     else
-      scale_copy_kernel<float><<<nb, bs, 0, ctx->stream>>>(g, (T_<float> *)dst, (const T_<float> *)src, (float)a, nblk);
+      launch_k(ctx, scale_copy_kernel<float>, nb, bs, g, (T_<float> *)dst, (const T_<float> *)src, (float)a, nblk);
   });
   if (rc) return rc;
   return prof_end(ctx, &ev);
@@ -521,10 +532,10 @@ int blas_cg_update_r(qdp_ctx ctx, int prec, void *r, const void *q, int rho_slot
   prof_work(ctx, QDP_PK_BLAS, 96.0 * g.Vh, 72.0 * g.Vh * (prec == QDP_F64 ? 8 : 4));
   rc = blas_launch(ctx, K_CGR, prec, 1, true, [&](int nb, int bs) {
     if (prec == QDP_F64)
-      cg_r_kernel<double><<<nb, bs, 0, ctx->stream>>>(g, (T_<double> *)r, (const T_<double> *)q, ctx->red_result,
+      launch_k(ctx, cg_r_kernel<double>, nb, bs, g, (T_<double> *)r, (const T_<double> *)q, ctx->red_result,
                                                        rho_slot, pq_slot, R);
     else
-      cg_r_kernel<float><<<nb, bs, 0, ctx->stream>>>(g, (T_<float> *)r, (const T_<float> *)q, ctx->red_result,
+      launch_k(ctx, cg_r_kernel<float>, nb, bs, g, (T_<float> *)r, (const T_<float> *)q, ctx->red_result,
                                                       rho_slot, pq_slot, R);
   });
   if (rc || (rc = prof_end(ctx, &ev))) return rc;
@@ -539,7 +550,7 @@ int blas_cg_update_xp(qdp_ctx ctx, int prec, void *x, void *p, const void *r, in
   prof_work(ctx, QDP_PK_BLAS, (update_p ? 96.0 : 48.0) * g.Vh,
             (update_p ? 120.0 : 72.0) * g.Vh * (prec == QDP_F64 ? 8 : 4));
 #define QDPB_XP(Rt, U)                                                                                              \
-  cg_xp_kernel<Rt, U><<<nb, bs, 0, ctx->stream>>>(g, (T_<Rt> *)x, (T_<Rt> *)p, (const T_<Rt> *)r, ctx->red_result, \
+  launch_k(ctx, cg_xp_kernel<Rt, U>, nb, bs, g, (T_<Rt> *)x, (T_<Rt> *)p, (const T_<Rt> *)r, ctx->red_result, \
                                                   rho_slot, pq_slot, rr_slot, stop, iter)
   int rc = blas_launch(ctx, update_p ? K_CGXP : K_CGXP0, prec, 1, false, [&](int nb, int bs) {
     if (prec == QDP_F64) { if (update_p) QDPB_XP(double, true); else QDPB_XP(double, false); }
@@ -557,9 +568,9 @@ int blas_cg_update_p(qdp_ctx ctx, int prec, void *p, const void *r, int rho_slot
   prof_work(ctx, QDP_PK_BLAS, 48.0 * g.Vh, 72.0 * g.Vh * (prec == QDP_F64 ? 8 : 4));
   int rc = blas_launch(ctx, K_CGP, prec, 1, false, [&](int nb, int bs) {
     if (prec == QDP_F64)
-      cg_p_kernel<double><<<nb, bs, 0, ctx->stream>>>(g, (T_<double> *)p, (const T_<double> *)r, ctx->red_result, rho_slot, rr_slot);
+      launch_k(ctx, cg_p_kernel<double>, nb, bs, g, (T_<double> *)p, (const T_<double> *)r, ctx->red_result, rho_slot, rr_slot);
     else
-      cg_p_kernel<float><<<nb, bs, 0, ctx->stream>>>(g, (T_<float> *)p, (const T_<float> *)r, ctx->red_result, rho_slot, rr_slot);
+      launch_k(ctx, cg_p_kernel<float>, nb, bs, g, (T_<float> *)p, (const T_<float> *)r, ctx->red_result, rho_slot, rr_slot);
   });
   if (rc) return rc;
   return prof_end(ctx, &ev);
@@ -571,8 +582,8 @@ int blas_convert(qdp_ctx ctx, void *dst, int dst_prec, const void *src) {
   prof_begin(ctx, QDP_PK_BLAS, &ev);
   prof_work(ctx, QDP_PK_BLAS, 0.0, 288.0 * g.Vh);  // 24 reals fp64 + 24 reals fp32 per site
   int rc = blas_launch(ctx, dst_prec == QDP_F32 ? K_CONV32 : K_CONV64, 0, 1, false, [&](int nb, int bs) {
-    if (dst_prec == QDP_F32) convert_kernel<true><<<nb, bs, 0, ctx->stream>>>(g, (double2 *)src, (float4 *)dst);
-    else convert_kernel<false><<<nb, bs, 0, ctx->stream>>>(g, (double2 *)dst, (float4 *)src);
+    if (dst_prec == QDP_F32) launch_k(ctx, convert_kernel<true>, nb, bs, g, (double2 *)src, (float4 *)dst);
+    else launch_k(ctx, convert_kernel<false>, nb, bs, g, (double2 *)dst, (float4 *)src);
   });
   if (rc) return rc;
   return prof_end(ctx, &ev);
@@ -584,7 +595,7 @@ int blas_accum_mixed(qdp_ctx ctx, void *y64, void *x32) {
   prof_begin(ctx, QDP_PK_BLAS, &ev);
   prof_work(ctx, QDP_PK_BLAS, 24.0 * g.Vh, (2.0 * 24 * 8 + 2.0 * 24 * 4) * g.Vh);
   int rc = blas_launch(ctx, K_ACCUM, 0, 1, false, [&](int nb, int bs) {
-    accum_mixed_kernel<<<nb, bs, 0, ctx->stream>>>(g, (double2 *)y64, (float4 *)x32);
+    launch_k(ctx, accum_mixed_kernel, nb, bs, g, (double2 *)y64, (float4 *)x32);
   });
   if (rc) return rc;
   return prof_end(ctx, &ev);

@@ -228,6 +228,7 @@ static int ctx_create(const int global_dims[4], const int proc_grid[4], int rank
   for (int mu = 0; mu < 4; mu++) g.faceVh[mu] = (int)(V / g.L[mu] / 2);
   update_partition(c);
   if (const char *fe = getenv("QDPB_FUSE")) c->fuse = atoi(fe) ? 1 : 0;
+  if (const char *pe = getenv("QDPB_PDL")) c->pdl = atoi(pe) ? 1 : 0;
 
   int rc = QDP_OK;
   cudaError_t e = cudaGetDevice(&c->device);
@@ -381,8 +382,9 @@ extern "C" int qdp_set_option(qdp_ctx c, int opt, long v) {
     case QDP_OPT_DET_REDUCE: c->det_reduce = v ? 1 : 0; return QDP_OK;
     case QDP_OPT_AUTOTUNE: c->autotune = v ? 1 : 0; return QDP_OK;
     case QDP_OPT_FUSE: c->fuse = v ? 1 : 0; return QDP_OK;
+    case QDP_OPT_PDL: c->pdl = v ? 1 : 0; return QDP_OK;
     case QDP_OPT_DSLASH_VARIANT:
-      if (v < -1 || v > 3) return set_error(c, QDP_EINVAL, "dslash variant must be -1 (tuned), 0, 1, 2 or 3");
+      if (v < -1 || v > 4) return set_error(c, QDP_EINVAL, "dslash variant must be -1 (tuned) or 0 .. 4");
       c->dslash_variant = (int)v;
       return QDP_OK;
     case QDP_OPT_P2P:
@@ -418,6 +420,7 @@ extern "C" int qdp_get_option(qdp_ctx c, int opt, long *v) {
     case QDP_OPT_AUTOTUNE: *v = c->autotune; return QDP_OK;
     case QDP_OPT_P2P: *v = c->p2p_on; return QDP_OK;
     case QDP_OPT_FUSE: *v = c->fuse; return QDP_OK;
+    case QDP_OPT_PDL: *v = c->pdl; return QDP_OK;
     case QDP_OPT_DSLASH_VARIANT: *v = c->dslash_variant; return QDP_OK;
   }
   return set_error(c, QDP_EINVAL, "unknown option %d", opt);

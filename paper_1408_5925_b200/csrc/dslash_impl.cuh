@@ -213,6 +213,9 @@ template <typename R, int REC = 18> struct KParams {
   int fuse;
   int fuse_npack;   // leading pack blocks
   int fuse_nin;     // interior sites: perm[0, nin) interior, perm[nin, Vh) on a partitioned face
+  // the face sites are visited after the first fuse_kin interior sites (a multiple of blockDim;
+  // fuse_nin: after every interior site), then the rest of the interior
+  int fuse_kin;
   const int *perm;  // visiting order of the output parity's sites (nullptr: by arithmetic, below)
   // z or z x t partitioned: the sites come in (z,t) slabs of S = L0/2 x L1 consecutive cb indices;
   // interior slabs (z in [sz0, sz0 + nzi), t in [st0, ...)) first, then the face slabs listed here
@@ -468,9 +471,17 @@ __device__ __forceinline__ void remote_hop(const Geom &g, const KP &P, const int
   if (c[MU] == 0) accum_recon<MU, +1>(acc, HalfGhost<T>::load(P.ghost[MU][0], n, face_index(g, MU, c)));
 }
 
+// Fused boundary: the number of blocks holding face sites (visiting positions [kin, kin + nf))
+template <typename KP>
+__device__ __forceinline__ int fused_face_blocks(const Geom &g, const KP &P) {
+  const int B = (int)blockDim.x, end = P.fuse_kin + g.Vh - P.fuse_nin;
+  return (end + B - 1) / B - P.fuse_kin / B;
+}
+
 template <typename R, int REC, int EPI, bool G5IN, bool G5OUT, bool HALO, bool DOT>
 __global__ void __launch_bounds__(QDPB_DSLASH_MAXT, (dslash_minb<R, REC>()))
     dslash_kernel(const Geom g, const __grid_constant__ KParams<R, REC> P) {
+  pdl_enter();
   int cb = blockIdx.x * blockDim.x + threadIdx.x;
   const int vb = blockIdx.x;
   double dot = 0.0;
@@ -490,7 +501,10 @@ __global__ void __launch_bounds__(QDPB_DSLASH_MAXT, (dslash_minb<R, REC>()))
       return;
     }
     cb -= P.fuse_npack * blockDim.x;
-    face = (int)((blockIdx.x - P.fuse_npack + 1) * blockDim.x) > P.fuse_nin;
+    // visiting position v -> interior sites [0, kin), the face sites, then interior [kin, nin)
+    const int nf = g.Vh - P.fuse_nin, b0 = (int)(blockIdx.x - P.fuse_npack) * (int)blockDim.x;
+    face = b0 + (int)blockDim.x > P.fuse_kin && b0 < P.fuse_kin + nf;
+    if (cb >= P.fuse_kin) cb = cb < P.fuse_kin + nf ? P.fuse_nin + (cb - P.fuse_kin) : cb - nf;
     if (face || P.wait_all) {
       pack_help<R, REC, G5IN>(g, P);  // whatever packing is left first: a wait never depends on an unstarted block
 #pragma unroll
@@ -560,14 +574,13 @@ __global__ void __launch_bounds__(QDPB_DSLASH_MAXT, (dslash_minb<R, REC>()))
   // the block's partial of the fused dot goes out BEFORE the output stores (reduce.cuh red_arrive)
   bool red_last = false;
   if (DOT && P.red_fin) red_last = red_arrive(P.red, gridDim.x, vb, dot, 0.0);
+  // the last face block tells the senders their slots were consumed: the ghosts are in registers
+  // already, so this goes out before the output stores (its fence does not wait for them)
+  if (HALO && P.fuse && face) fused_signal_last(g, P.ext_counter, fused_face_blocks(g, P), P.ack_to, P.seq);
   if (have) P.out.store(cb, o);
   if (DOT) {
     if (!P.red_fin) dot_block_partial(dot, P.dot_part, vb);
     else if (red_last) red_complete(P.red, gridDim.x, vb, false);
-  }
-  if (HALO && P.fuse && face) {  // the last face block tells the senders their slots were consumed
-    const int first = P.fuse_npack + P.fuse_nin / (int)blockDim.x;
-    fused_signal_last(g, P.ext_counter, (int)gridDim.x - first, P.ack_to, P.seq);
   }
 }
 
@@ -797,6 +810,92 @@ __global__ void __launch_bounds__(64, (dslash_minb<R, REC>()))
   }
 }
 
+// ------------------------------------------------------------------ asynchronously pipelined variant
+// Latency hiding without registers (fp64): each thread stages the operands of its next hops -- the
+// neighbour spinor (12 x 16 B) and the link (REC/2 x 16 B) -- into its own slots of a shared-memory
+// ring of NST hop stages with cp.async (LDGSTS), so NST - 1 hops' loads are in flight while it
+// computes the current hop from shared memory.  The bytes in flight are held by the async-copy
+// unit, not by registers, so the register-path kernel's trade (more loads in flight = more registers
+// = fewer warps) does not apply.  Each thread reads only the slots it filled (completion by
+// cp.async.wait_group, no barrier).  Hop order and arithmetic are the main kernel's (fwd, bwd per
+// mu = 0..3), so the output is bit-identical to it.  Whole lattice, any epilogue, no fused dot.
+__device__ __forceinline__ void cp_async16(void *s, const void *gp) {  // L2 only (see the measured note above)
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(s)), "l"(gp) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N> __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int REC> struct PipeHop {
+  static constexpr int NPL = REC / 2, NE = 12 + NPL;  // 16-byte slots per hop and thread
+  // stage hop H (mu = H / 2, forward if H is even) into ring slot `st` (slot [k][thread])
+  template <int H, typename KP>
+  static __device__ __forceinline__ void issue(const Geom &g, const KP &P, const int c[4], int cb, int p, double2 *st) {
+    constexpr int MU = H / 2;
+    int n[4] = {c[0], c[1], c[2], c[3]};
+    if (H % 2 == 0) n[MU] = (c[MU] + 1 == g.L[MU]) ? 0 : c[MU] + 1;
+    else n[MU] = (c[MU] == 0) ? g.L[MU] - 1 : c[MU] - 1;
+    const int ncb = coords_cb(g, n);
+    const double2 *sp = P.psi.p + ncb;
+#pragma unroll
+    for (int k = 0; k < 12; k++) cp_async16(st + k * 64, sp + (size_t)k * g.stride);
+    const double2 *lp = (const double2 *)P.U.p + (size_t)(MU * 2 + (H % 2 == 0 ? p : 1 - p)) * NPL * g.stride +
+                        (H % 2 == 0 ? cb : ncb);
+#pragma unroll
+    for (int k = 0; k < NPL; k++) cp_async16(st + (12 + k) * 64, lp + (size_t)k * g.stride);
+  }
+  template <int H>
+  static __device__ __forceinline__ void compute(const double2 *st, bool G5IN, Spinor<double> &acc) {
+    constexpr int MU = H / 2;
+    Spinor<double> s;
+#pragma unroll
+    for (int k = 0; k < 12; k++) {
+      const double2 v = st[k * 64];
+      s.c[k] = {v.x, v.y};
+    }
+    if (G5IN) g5(s);
+    Link<double> u;
+#pragma unroll
+    for (int k = 0; k < NPL; k++) {
+      const double2 v = st[(12 + k) * 64];
+      u.m[k] = {v.x, v.y};
+    }
+    if (REC == 12) su3_third_row(u);
+    if (H % 2 == 0) accum_recon<MU, -1>(acc, mul_link(u, project<MU, -1>(s)));
+    else accum_recon<MU, +1>(acc, mul_link_dag(u, project<MU, +1>(s)));
+  }
+};
+
+template <int REC, int EPI, bool G5IN, bool G5OUT, int NST>
+__global__ void __launch_bounds__(64) dslash_pipe_kernel(const Geom g, const __grid_constant__ KParams<double, REC> P) {
+  using PH = PipeHop<REC>;
+  extern __shared__ __align__(16) double2 ring[];  // [NST][NE][64]
+  const int cb = blockIdx.x * 64 + threadIdx.x;
+  if (cb >= g.Vh) return;  // whole warps only on the last block: no barrier below
+  const int p = P.parity;
+  int c[4];
+  cb_coords(g, cb, p, c);
+  double2 *base = ring + threadIdx.x;
+#define QDPB_ST(H) (base + ((H) % NST) * PH::NE * 64)
+#define QDPB_ISSUE(H) \
+  if constexpr ((H) < 8) PH::template issue<((H) < 8 ? (H) : 0)>(g, P, c, cb, p, QDPB_ST(H)); \
+  cp_commit();
+#define QDPB_HOP(H)                                  \
+  QDPB_ISSUE((H) + NST - 1)                          \
+  cp_wait<NST - 1>();                                \
+  PH::template compute<H>(QDPB_ST(H), G5IN, acc);
+  QDPB_ISSUE(0)  // prologue: hops 0 .. NST - 2
+  if constexpr (NST > 2) { QDPB_ISSUE(1) }
+  if constexpr (NST > 3) { QDPB_ISSUE(2) }
+  Spinor<double> acc;
+#pragma unroll
+  for (int k = 0; k < 12; k++) acc.c[k] = {0.0, 0.0};
+  QDPB_HOP(0) QDPB_HOP(1) QDPB_HOP(2) QDPB_HOP(3) QDPB_HOP(4) QDPB_HOP(5) QDPB_HOP(6) QDPB_HOP(7)
+#undef QDPB_HOP
+#undef QDPB_ISSUE
+#undef QDPB_ST
+  P.out.store(cb, epilogue<double, EPI>(P, cb, acc, G5OUT));
+}
+
 // ------------------------------------------------------------------ host side
 template <typename R> static FermView<R> fview(const void *p, int stride);
 template <> FermView<double> fview<double>(const void *p, int stride) { return {(double2 *)p, stride}; }
@@ -818,8 +917,12 @@ template <> CloverView<h16> cview<h16>(const void *p, int stride) {
 template <typename R, int REC, int EPI, bool G5IN, bool G5OUT, bool HALO, bool DOT>
 static void launch_main(qdp_ctx ctx, const KParams<R, REC> &P, int block) {
   const Geom &g = ctx->geom;
-  dslash_kernel<R, REC, EPI, G5IN, G5OUT, HALO, DOT>
-      <<<grid_for(g.Vh, block) + P.fuse_npack, block, 0, ctx->stream>>>(g, P);
+  // the fused boundary kernel keeps plain stream order: with PDL its leading (packing) blocks land
+  // on whichever SMs the predecessor frees first, and config 5's z x t rank sub-lattice CG lost 1%
+  // (profiles/r02_pdl.txt); QDPB_PDL_HALO=1 for measurements
+  static const bool pdl_halo = getenv("QDPB_PDL_HALO") && atoi(getenv("QDPB_PDL_HALO"));
+  launch_pdl(ctx->stream, ctx->pdl && (!HALO || pdl_halo), dslash_kernel<R, REC, EPI, G5IN, G5OUT, HALO, DOT>,
+             grid_for(g.Vh, block) + P.fuse_npack, block, g, P);
 }
 
 template <typename R, int REC, int EPI>
@@ -841,6 +944,27 @@ static void launch_tma(qdp_ctx ctx, const KParams<R, REC> &P, bool g5i, bool g5o
     if (g5i) { if (g5o) QDPB_LT(true, true); else QDPB_LT(true, false); }
     else { if (g5o) QDPB_LT(false, true); else QDPB_LT(false, false); }
 #undef QDPB_LT
+  }
+}
+
+template <typename R, int REC, int EPI, int NST>
+static void launch_pipe(qdp_ctx ctx, const KParams<R, REC> &P, bool g5i, bool g5o) {
+  if constexpr (sizeof(R) == 8 && !is_h16<R>()) {
+    const int grid = grid_for(ctx->geom.Vh, 64);
+    const size_t smem = (size_t)NST * PipeHop<REC>::NE * 64 * 16;
+#define QDPB_LP(A, B)                                                                                   \
+  {                                                                                                     \
+    static bool attr = false;                                                                           \
+    if (!attr) {                                                                                        \
+      cudaFuncSetAttribute(dslash_pipe_kernel<REC, EPI, A, B, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           (int)smem);                                                                  \
+      attr = true;                                                                                      \
+    }                                                                                                   \
+    dslash_pipe_kernel<REC, EPI, A, B, NST><<<grid, 64, smem, ctx->stream>>>(ctx->geom, P);       \
+  }
+    if (g5i) { if (g5o) QDPB_LP(true, true) else QDPB_LP(true, false) }
+    else { if (g5o) QDPB_LP(false, true) else QDPB_LP(false, false) }
+#undef QDPB_LP
   }
 }
 
@@ -896,10 +1020,11 @@ static void dslash_work(qdp_ctx ctx, const DslashArgs &a) {
 }
 
 // The paper's autotuner (section VII) on the launch configuration of the
-// whole-lattice EO dslash, on its payload launches: the candidates in decreasing threads per block
-// -- the four-threads-per-site kernel (128), the main kernel with 64 and with 32 threads -- the
-// first launch takes the largest, later launches probe the next ones until one is 33% slower
-// than the best, and the best is kept for the key (precision, gauge storage, epilogue, volume).
+// whole-lattice EO dslash, on its payload launches: the candidates -- the four-threads-per-site
+// kernel (128 threads), the main kernel with 64 threads, the cp.async hop pipeline (fp64), the main
+// kernel with 32 threads, the bulk-copy staged links (fp64 r12) -- the first launch takes the first,
+// later launches probe the next ones until one is 33% slower than the best, and the best is kept
+// for the key (precision, gauge storage, epilogue, volume).
 template <typename R, int REC>
 static int launch_main_epi(qdp_ctx ctx, const DslashArgs &a, const KParams<R, REC> &P, bool halo, int block) {
   ProfEvent ev;
@@ -908,7 +1033,8 @@ static int launch_main_epi(qdp_ctx ctx, const DslashArgs &a, const KParams<R, RE
   const bool dot = a.dot_x != nullptr;
   auto go = [&](int variant) -> cudaError_t {
     // variant: 0 = four threads per site (PLAIN / XPAY only), 1 = main kernel with `block`
-    // threads, 2 = main kernel with 32 threads, 3 = bulk-copy staged forward links (fp64)
+    // threads, 2 = main kernel with 32 threads, 3 = bulk-copy staged forward links (fp64 r12),
+    // 4 = cp.async hop pipeline (fp64)
     if (variant == 0) {
       if (a.epi == EPI_PLAIN) launch_four<R, REC, EPI_PLAIN>(ctx, P, a.g5_in, a.g5_out);
       else launch_four<R, REC, EPI_XPAY>(ctx, P, a.g5_in, a.g5_out);
@@ -923,6 +1049,17 @@ static int launch_main_epi(qdp_ctx ctx, const DslashArgs &a, const KParams<R, RE
       }
       return cudaGetLastError();
     }
+    if (variant == 4) {  // cp.async hop pipeline, two stages (fp64)
+#define QDPB_PIPE(E) launch_pipe<R, REC, E, 2>(ctx, P, a.g5_in, a.g5_out)
+      switch (a.epi) {
+        case EPI_PLAIN: QDPB_PIPE(EPI_PLAIN); break;
+        case EPI_XPAY: QDPB_PIPE(EPI_XPAY); break;
+        case EPI_CLOVINV: QDPB_PIPE(EPI_CLOVINV); break;
+        default: QDPB_PIPE(EPI_CLOVXPAY); break;
+      }
+#undef QDPB_PIPE
+      return cudaGetLastError();
+    }
     const int b = variant == 1 ? block : 32;
     switch (a.epi) {
       case EPI_PLAIN: launch_main_dispatch<R, REC, EPI_PLAIN>(ctx, P, a.g5_in, a.g5_out, halo, false, b); break;
@@ -934,15 +1071,19 @@ static int launch_main_epi(qdp_ctx ctx, const DslashArgs &a, const KParams<R, RE
   };
   // the candidates of this call, in the tuner's order (decreasing threads per block, then the
   // staged variant): whole lattice, no fused reduction (its partials follow the block size)
-  int vids[4], nv = 0;
+  int vids[6], nv = 0;
   if (!is_h16<R>() && (a.epi == EPI_PLAIN || a.epi == EPI_XPAY)) vids[nv++] = 0;
   vids[nv++] = 1;
+  // the hop pipeline right after the main kernel (probed before a slow candidate stops the search);
+  // plain / xpay only: with the clover epilogues it lost inside the CG (profiles/r02_dslash_pipeline.txt)
+  if (sizeof(R) == 8 && !is_h16<R>() && (a.epi == EPI_PLAIN || a.epi == EPI_XPAY)) vids[nv++] = 4;
   vids[nv++] = 2;
   if (sizeof(R) == 8 && REC == 12) vids[nv++] = 3;
   if (!halo && !dot && ctx->block == 0 && ctx->dslash_variant >= 0) {  // forced (measurements)
     int v = 1;
     for (int i = 0; i < nv; i++)
       if (vids[i] == ctx->dslash_variant) v = vids[i];
+    if (sizeof(R) == 8 && !is_h16<R>() && ctx->dslash_variant == 4) v = 4;  // any epilogue (tests)
     const cudaError_t e = go(v);
     const int rc = prof_end(ctx, &ev);
     return e != cudaSuccess ? cuda_check(ctx, e, "dslash launch") : rc;
@@ -1122,6 +1263,14 @@ static int dslash_t(qdp_ctx ctx, const DslashArgs &a) {
         P.fuse_nin = g.Vh - 2 * g.faceVh[3];
       }
       P.fuse = 1;
+      // the face sites halfway through the interior rather than last: they no longer form the
+      // kernel's tail (measured, profiles/r02_fused_face_position.txt: 40^3 x 32 t 260 -> 255 us,
+      // z x t 270 -> 264 us; 48 x 48 x 24 x 24 z x t 183 -> 177 us), and half the interior still
+      // runs before any block waits for a ghost.  QDPB_FACE_AT (fraction of the interior visited
+      // first, >= 1: faces last) for measurements.
+      static const double face_at = getenv("QDPB_FACE_AT") ? atof(getenv("QDPB_FACE_AT")) : 0.5;
+      P.fuse_kin = face_at >= 1.0 ? P.fuse_nin
+                                  : std::max(0, (int)(face_at * P.fuse_nin) / block * block);
       P.fuse_npack = npack;
       for (int k = 0; k < 5; k++) P.pack_off[k] = pack_off[k];
       P.pack_q = L.pack_q;

@@ -74,6 +74,7 @@ __device__ __forceinline__ FermView<float> fview32(void *p, int stride) { return
 
 // p16 = (16-bit) r32
 __global__ void __launch_bounds__(HB) to_h16_kernel(const Geom g, void *p16, const void *r32) {
+  pdl_enter();
   const int cb = blockIdx.x * blockDim.x + threadIdx.x;
   if (cb >= g.Vh) return;
   hview(p16, g.stride).store(cb, fview32(const_cast<void *>(r32), g.stride).load_stream(cb));
@@ -82,6 +83,7 @@ __global__ void __launch_bounds__(HB) to_h16_kernel(const Geom g, void *p16, con
 // r32 -= alpha q16 ; |r|^2 (one launch, reduce.cuh), alpha = res[rho] / res[pq]
 __global__ void __launch_bounds__(HB) cg16_r_kernel(const Geom g, void *r32, const void *q16, const double *res,
                                                     int rho_slot, int pq_slot, const __grid_constant__ RedArgs Rd) {
+  pdl_enter();
   const float alpha = (float)(res[rho_slot] / res[pq_slot]);
   double acc = 0.0;
   const FermView<float> r = fview32(r32, g.stride);
@@ -103,6 +105,7 @@ __global__ void __launch_bounds__(HB) cg16_r_kernel(const Geom g, void *r32, con
 template <bool UPD>
 __global__ void __launch_bounds__(HB) cg16_xp_kernel(const Geom g, void *x32, void *p16, const void *r32,
                                                      const double *res, int rho_slot, int pq_slot, int rr_slot) {
+  pdl_enter();
   const int cb = blockIdx.x * blockDim.x + threadIdx.x;
   if (cb >= g.Vh) return;
   const float alpha = (float)(res[rho_slot] / res[pq_slot]);
@@ -125,6 +128,7 @@ __global__ void __launch_bounds__(HB) cg16_xp_kernel(const Geom g, void *x32, vo
 // p16 = r32 + beta p16, beta = res[rr] / res[rho]
 __global__ void __launch_bounds__(HB) cg16_p_kernel(const Geom g, void *p16, const void *r32, const double *res,
                                                     int rho_slot, int rr_slot) {
+  pdl_enter();
   const int cb = blockIdx.x * blockDim.x + threadIdx.x;
   if (cb >= g.Vh) return;
   const float beta = (float)(res[rr_slot] / res[rho_slot]);
@@ -179,7 +183,7 @@ int h16_from_f32(qdp_ctx ctx, void *p16, const void *r32) {
   ProfEvent ev;
   prof_begin(ctx, QDP_PK_BLAS, &ev);
   prof_work(ctx, QDP_PK_BLAS, 0.0, (96.0 + 52.0) * g.Vh);
-  to_h16_kernel<<<grid_for(g.Vh, HB), HB, 0, ctx->stream>>>(g, p16, r32);
+  launch_k(ctx, to_h16_kernel, grid_for(g.Vh, HB), HB, g, p16, r32);
   return launch_end(ctx, &ev);
 }
 
@@ -193,7 +197,7 @@ int h16_cg_r(qdp_ctx ctx, void *r32, const void *q16, int rho_slot, int pq_slot,
   ProfEvent ev;
   prof_begin(ctx, QDP_PK_BLAS, &ev);
   prof_work(ctx, QDP_PK_BLAS, 96.0 * g.Vh, (2 * 96.0 + 52.0) * g.Vh);
-  cg16_r_kernel<<<nb, HB, 0, ctx->stream>>>(g, r32, q16, ctx->red_result, rho_slot, pq_slot, R);
+  launch_k(ctx, cg16_r_kernel, nb, HB, g, r32, q16, ctx->red_result, rho_slot, pq_slot, R);
   if ((rc = launch_end(ctx, &ev))) return rc;
   return after ? reduce_global(ctx, rr_slot, 1) : QDP_OK;
 }
@@ -204,8 +208,8 @@ int h16_cg_xp(qdp_ctx ctx, void *x32, void *p16, const void *r32, int rho_slot, 
   prof_begin(ctx, QDP_PK_BLAS, &ev);
   prof_work(ctx, QDP_PK_BLAS, (upd ? 96.0 : 48.0) * g.Vh, (upd ? 2 * 96.0 + 2 * 52.0 + 96.0 : 2 * 96.0 + 52.0) * g.Vh);
   const int nb = grid_for(g.Vh, HB);
-  if (upd) cg16_xp_kernel<true><<<nb, HB, 0, ctx->stream>>>(g, x32, p16, r32, ctx->red_result, rho_slot, pq_slot, rr_slot);
-  else cg16_xp_kernel<false><<<nb, HB, 0, ctx->stream>>>(g, x32, p16, r32, ctx->red_result, rho_slot, pq_slot, rr_slot);
+  if (upd) launch_k(ctx, cg16_xp_kernel<true>, nb, HB, g, x32, p16, r32, ctx->red_result, rho_slot, pq_slot, rr_slot);
+  else launch_k(ctx, cg16_xp_kernel<false>, nb, HB, g, x32, p16, r32, ctx->red_result, rho_slot, pq_slot, rr_slot);
   return launch_end(ctx, &ev);
 }
 
@@ -214,7 +218,7 @@ int h16_cg_p(qdp_ctx ctx, void *p16, const void *r32, int rho_slot, int rr_slot)
   ProfEvent ev;
   prof_begin(ctx, QDP_PK_BLAS, &ev);
   prof_work(ctx, QDP_PK_BLAS, 48.0 * g.Vh, (2 * 52.0 + 96.0) * g.Vh);
-  cg16_p_kernel<<<grid_for(g.Vh, HB), HB, 0, ctx->stream>>>(g, p16, r32, ctx->red_result, rho_slot, rr_slot);
+  launch_k(ctx, cg16_p_kernel, grid_for(g.Vh, HB), HB, g, p16, r32, ctx->red_result, rho_slot, rr_slot);
   return launch_end(ctx, &ev);
 }
 

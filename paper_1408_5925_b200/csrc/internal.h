@@ -713,6 +713,7 @@ struct qdp_ctx_s {
   int overlap = 1, self_halo = 0, profiling = 0, block = 0, det_reduce = 1, self_nccl = 0;
   int fuse = 1;  // QDP_OPT_FUSE (default: env QDPB_FUSE, else 1)
   int dslash_variant = -1;  // QDP_OPT_DSLASH_VARIANT: -1 tuned, else the forced launch variant
+  int pdl = 1;  // QDP_OPT_PDL (default: env QDPB_PDL, else 1): solver-chain kernels with programmatic dependent launch
   // scratch (device)
   void *staging = nullptr;
   size_t staging_bytes = 0;
@@ -977,5 +978,37 @@ int comm_ensure_self(qdp_ctx ctx);
 
 inline size_t fermion_block_bytes(int prec, int stride) { return (size_t)stride * (prec == QDP_F64 ? 12 * 16 : 6 * 16); }
 inline int grid_for(long n, int block) { return (int)((n + block - 1) / block); }
+
+// Programmatic dependent launch (QDP_OPT_PDL).  A kernel of the solver chain (dslash, the BLAS and
+// reduction kernels) is launched with programmatic stream serialisation: it may become resident
+// while its predecessor in the stream drains its last blocks, so launch processing and block
+// dispatch overlap that tail instead of following it.  Every such kernel starts with pdl_enter():
+// griddepcontrol.wait blocks until the predecessor grid has completed and its memory is visible
+// (a no-op without the attribute), then launch_dependents lets the successor in once every block
+// of this grid has started -- so a dependent's blocks only take slots this grid's finished blocks
+// free, and waits inside this grid (fused boundary flags, one-launch reductions) never depend on
+// an unstarted block.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+template <typename... KA, typename... A>
+cudaError_t launch_pdl(cudaStream_t stream, bool pdl, void (*kernel)(KA...), int grid, int block, A &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)block);
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(args)...);
+}
+// on the context stream, with PDL as QDP_OPT_PDL says
+template <typename... KA, typename... A>
+cudaError_t launch_k(qdp_ctx ctx, void (*kernel)(KA...), int grid, int block, A &&...args) {
+  return launch_pdl(ctx->stream, ctx->pdl != 0, kernel, grid, block, std::forward<A>(args)...);
+}
 
 }  // namespace qdpb

@@ -38,6 +38,7 @@ struct MsPtrs {
 // One thread; every product / quotient rounded separately (no FMA contraction), evaluated left
 // to right as written in R25, so any plain IEEE implementation takes the same freeze decisions.
 __global__ void ms_coeff_kernel(MsState *st, double *res, int n, int k, double tol2rho0, int last) {
+  pdl_enter();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   const double rho = res[S_RHO], rho_new = res[S_RR];
   const double alpha = __ddiv_rn(rho, res[S_PQ]);
@@ -111,6 +112,7 @@ template <> __device__ __forceinline__ float4 lin_(double a, float4 x, double b,
 template <typename R>
 __global__ void __launch_bounds__(256) ms_update_kernel(const Geom g, const MsPtrs P, const typename MsE<R>::T *r,
                                                         const MsState *st, int n) {
+  pdl_enter();
   using T = typename MsE<R>::T;
   __shared__ double s_ax[MAXS], s_zp[MAXS], s_bp[MAXS];
   __shared__ int s_x[MAXS], s_p[MAXS];
@@ -198,14 +200,14 @@ int cg_solve_multishift(qdp_field *x, int n, const double *sigma, const qdp_fiel
     if ((rc = mhat_apply(ctx, U, A, Ainv, mass, t, q, mp, true, P.p[0], S_PQ, sigma[0]))) return rc;
     if ((rc = blas_cg_update_r(ctx, prec, r, q, S_RHO, S_PQ, S_RR))) return rc;
     k++;
-    ms_coeff_kernel<<<1, 32, 0, ctx->stream>>>(st, ctx->red_result, n, k, tol2rho0, k == maxit ? 1 : 0);
+    launch_k(ctx, ms_coeff_kernel, 1, 32, st, ctx->red_result, n, k, tol2rho0, k == maxit ? 1 : 0);
     QDP_CUDA(ctx, cudaGetLastError());
     ProfEvent ev;
     prof_begin(ctx, QDP_PK_MSHIFT, &ev);
     if (prec == QDP_F64)
-      ms_update_kernel<double><<<grid_for(g.Vh, 256), 256, 0, ctx->stream>>>(g, P, (const double2 *)r, st, n);
+      launch_k(ctx, ms_update_kernel<double>, grid_for(g.Vh, 256), 256, g, P, (const double2 *)r, st, n);
     else
-      ms_update_kernel<float><<<grid_for(g.Vh, 256), 256, 0, ctx->stream>>>(g, P, (const float4 *)r, st, n);
+      launch_k(ctx, ms_update_kernel<float>, grid_for(g.Vh, 256), 256, g, P, (const float4 *)r, st, n);
     if ((rc = prof_end(ctx, &ev))) return rc;
     double s[10];  // slots S_RR .. S_NP
     if ((rc = read_slots(ctx, S_RR, S_NP - S_RR + 1, s))) return rc;

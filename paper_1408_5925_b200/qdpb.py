@@ -26,7 +26,7 @@ QDP_OK, QDP_NOT_CONVERGED = 0, 1
 QDP_EINVAL, QDP_ESHAPE, QDP_EPREC, QDP_EALIAS, QDP_ENOMEM = -1, -2, -3, -4, -5
 QDP_ECUDA, QDP_ENCCL, QDP_ESINGULAR, QDP_EUNSUPPORTED = -6, -7, -8, -9
 (QDP_OPT_OVERLAP, QDP_OPT_SELF_HALO, QDP_OPT_PROFILE, QDP_OPT_BLOCK, QDP_OPT_DET_REDUCE, QDP_OPT_SELF_NCCL,
- QDP_OPT_AUTOTUNE, QDP_OPT_P2P, QDP_OPT_FUSE, QDP_OPT_DSLASH_VARIANT) = range(10)
+ QDP_OPT_AUTOTUNE, QDP_OPT_P2P, QDP_OPT_FUSE, QDP_OPT_DSLASH_VARIANT, QDP_OPT_PDL) = range(11)
 (QDP_PK_DSLASH, QDP_PK_DSLASH_EXT, QDP_PK_PACK, QDP_PK_BLAS, QDP_PK_REDUCE, QDP_PK_CLOVER,
  QDP_PK_SHIFT, QDP_PK_LAYOUT, QDP_PK_MSHIFT, QDP_PK_COUNT) = range(10)
 PK_NAMES = ["dslash", "dslash_ext", "pack", "blas", "reduce", "clover", "shift", "layout", "mshift"]

@@ -91,3 +91,50 @@ def test_cg_chunked_stop_is_exact(q):
         out[ch] = __import__("json").loads(r.stdout.strip().splitlines()[-1])
     assert out["1"][0] == out["16"][0]
     assert np.max(np.abs(np.array(out["1"][1]) - np.array(out["16"][1]))) <= 1e-13
+
+
+@pytest.mark.parametrize("recon", [18, 12])
+@pytest.mark.parametrize("L", [(4, 6, 2, 4), (6, 4, 6, 10), (8, 8, 8, 16)])
+def test_forced_variants_fp64_bit_identical(q, L, recon):
+    """Every fp64 launch variant (QDP_OPT_DSLASH_VARIANT) but the four-threads-per-site one, including
+    the asynchronously pipelined one (4: cp.async hop stages), computes exactly the main kernel's
+    arithmetic in the same order: the plain EO hopping term is the oracle's and bit-identical across variants, and so is a
+    clover CG (its non-fused dslash launches -- the A^-1 and A x + b D epilogues -- take the forced
+    variant): same residual history and solution bits."""
+    U = fieldgen.random_gauge(L, 4103)
+    psi = fieldgen.random_spinor(L, 4203)
+    par = fieldgen.parity(L)
+    ref = oracle.hopping(U, psi, L, -1)
+    c = q.qdp_init(L)
+    try:
+        fU = q.qdp_field_alloc(c, q.QDP_GAUGE12 if recon == 12 else q.QDP_GAUGE, 0, q.QDP_ALL)
+        q.qdp_field_import(fU, U)
+        fA = q.qdp_field_alloc(c, q.QDP_CLOVER, 0, q.QDP_ALL)
+        fAi = q.qdp_field_alloc(c, q.QDP_CLOVER, 0, q.QDP_EVEN)
+        q.qdp_clover_build(fA, fAi, fU, 0.1, 1.0)
+        fi = q.qdp_field_alloc(c, q.QDP_FERMION, 0, q.QDP_ODD)
+        q.qdp_field_import(fi, np.ascontiguousarray(psi[par == 1]))
+        fo = q.qdp_field_alloc(c, q.QDP_FERMION, 0, q.QDP_EVEN)
+        fb = q.qdp_field_alloc(c, q.QDP_FERMION, 0, q.QDP_ALL)
+        q.qdp_field_import(fb, psi)
+        fx = q.qdp_field_alloc(c, q.QDP_FERMION, 0, q.QDP_ALL)
+        q.qdp_set_option(c, q.QDP_OPT_AUTOTUNE, 0)  # fixed reduction launches: identical sums
+        base = None
+        for v in (1, 0, 2, 3, 4):
+            q.qdp_set_option(c, q.QDP_OPT_DSLASH_VARIANT, v)
+            q.qdp_field_zero(fo)
+            q.qdp_dslash(fo, fU, fi, q.QDP_EVEN)
+            got = q.qdp_field_export(fo)
+            r = q.qdp_cg_solve(fx, fb, fU, fA, fAi, mass=0.1, tol=1e-30, maxit=8)
+            now = (got, r["hist"].copy(), q.qdp_field_export(fx))
+            if base is None:
+                base = now
+                assert rel_site_err(got, ref[par == 0]) <= 1e-13
+            elif v == 0:  # four threads per site: the directions' partial sums meet in another order
+                assert rel_site_err(got, base[0]) <= 1e-14
+                assert np.max(np.abs(now[1] - base[1]) / base[1]) <= 1e-12
+            else:
+                for a, b in zip(now, base):
+                    assert np.array_equal(a, b), v
+    finally:
+        q.qdp_finalize(c)

@@ -1,0 +1,42 @@
+# GPU calls of round 2's second session (one `gpurun` call per section; outputs in gpurun_out/, the
+# summaries copied into profiles/ by hand).  Usage: bash tools/gpu_r02b.sh SECTION
+#   check   the GPU suite, smoke, the default bench
+#   fused   fused boundary: face position in the visiting order (QDPB_FACE_AT) x ack before the
+#           output stores; halo tests under the non-default setting  -> profiles/r02_fused_face_position.txt
+#   pdl     programmatic dependent launch off / on (CG it/s), z x t with / without PDL on the fused
+#           kernel (QDPB_PDL_HALO)                                    -> profiles/r02_pdl.txt
+#   pipe    the cp.async hop pipeline: variant sweep, CG with forced variants, ncu --set full of the
+#           fp64 reconstruct-12 dslash as register-path kernel and as pipeline -> profiles/r02_dslash_pipeline.txt
+set -u
+mkdir -p gpurun_out/prof_txt
+case "$1" in
+check)
+  timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/gpu_tests.log 2>&1; echo tests_rc=$?
+  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke_rc=$?
+  timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench_rc=$?
+  tail -3 gpurun_out/gpu_tests.log; cat gpurun_out/smoke.log ;;
+fused)
+  for cfg in "1" "0.5" "0.25" "0.75"; do
+    echo "FACE_AT=$cfg" >> gpurun_out/fused_exp.txt
+    QDPB_FACE_AT=$cfg timeout 300 python tools/fused_sweep.py >> gpurun_out/fused_exp.txt 2>&1
+  done
+  timeout 900 python -m pytest tests/test_gpu_p2p.py tests/test_gpu_peer.py tests/test_gpu_pdl.py -m gpu -q \
+    > gpurun_out/fused_exp_tests.log 2>&1; echo tests_rc=$?
+  cat gpurun_out/fused_exp.txt; tail -3 gpurun_out/fused_exp_tests.log ;;
+pdl)
+  timeout 600 python tools/pdl_cg.py > gpurun_out/pdl_cg.txt 2>&1; echo pdl_rc=$?
+  timeout 600 python tools/pdl_zt.py > gpurun_out/pdl_zt.txt 2>&1
+  QDPB_PDL_HALO=1 timeout 600 python tools/pdl_zt.py >> gpurun_out/pdl_zt.txt 2>&1
+  cat gpurun_out/pdl_cg.txt gpurun_out/pdl_zt.txt ;;
+pipe)
+  timeout 900 python tools/pipe_variants.py > gpurun_out/pipe_variants.txt 2>&1; echo pipe_rc=$?
+  timeout 900 python tools/pipe_cg.py > gpurun_out/pipe_cg.txt 2>&1; echo pipecg_rc=$?
+  timeout 900 python tools/dslash_variants.py > gpurun_out/dslash_variants.txt 2>&1; echo var_rc=$?
+  F="ncu --clock-control none --set full --import-source on"
+  for c in r12main r12pipe; do
+    timeout 600 $F -k regex:dslash -s 10 -c 1 -o gpurun_out/prof_$c -f python tools/ncu_cases.py $c > gpurun_out/ncu_$c.log 2>&1
+    python tools/ncu_summary.py gpurun_out/prof_$c.ncu-rep > gpurun_out/prof_txt/prof_${c}_detail.txt 2>&1
+  done
+  rm -f gpurun_out/*.ncu-rep
+  cat gpurun_out/pipe_variants.txt gpurun_out/pipe_cg.txt ;;
+esac

@@ -3,7 +3,7 @@
          the fused boundary kernel: pack + interior + remote hops in one kernel)
   t      the same with only t partitioned (the weak-scaling bench's split)
   h16    a few iterations of qdp_cg_solve_mixed16 (the 16-bit sloppy dslash launches)
-  r12    fp64 reconstruct-12 plain EO dslash
+  r12    fp64 reconstruct-12 plain EO dslash (tuned; r12main / r12pipe / r12tma: variant 1 / 4 / 3 forced)
   blas   norm2 / CG vector updates at 40^3x32
 Each case warms up, then runs the launches to capture (select them with ncu -k / -s / -c)."""
 import os
@@ -33,8 +33,9 @@ def gauge(kind=q.QDP_GAUGE):
 if case in ("zt", "t"):
     q.qdp_set_option(c, q.QDP_OPT_SELF_HALO, 12 if case == "zt" else 8)
     q.qdp_set_option(c, q.QDP_OPT_P2P, 1)
-if case == "r12tma":  # the fp64 reconstruct-12 dslash with bulk-copy staged forward links
-    q.qdp_set_option(c, q.QDP_OPT_DSLASH_VARIANT, 3)
+if case in ("r12tma", "r12pipe", "r12main"):  # fp64 reconstruct-12 dslash, one forced launch variant:
+    # bulk-copy staged forward links / cp.async hop pipeline / the register-path main kernel
+    q.qdp_set_option(c, q.QDP_OPT_DSLASH_VARIANT, {"r12tma": 3, "r12pipe": 4, "r12main": 1}[case])
     case = "r12"
 if case in ("zt", "t", "r12"):
     fU = gauge(q.QDP_GAUGE12 if case == "r12" else q.QDP_GAUGE)
