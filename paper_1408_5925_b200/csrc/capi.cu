@@ -384,7 +384,7 @@ extern "C" int qdp_set_option(qdp_ctx c, int opt, long v) {
     case QDP_OPT_FUSE: c->fuse = v ? 1 : 0; return QDP_OK;
     case QDP_OPT_PDL: c->pdl = v ? 1 : 0; return QDP_OK;
     case QDP_OPT_DSLASH_VARIANT:
-      if (v < -1 || v > 4) return set_error(c, QDP_EINVAL, "dslash variant must be -1 (tuned) or 0 .. 4");
+      if (v < -1 || v > 5) return set_error(c, QDP_EINVAL, "dslash variant must be -1 (tuned) or 0 .. 5");
       c->dslash_variant = (int)v;
       return QDP_OK;
     case QDP_OPT_P2P:

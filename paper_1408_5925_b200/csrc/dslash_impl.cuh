@@ -22,6 +22,10 @@
 #pragma once
 #include <type_traits>
 
+#ifndef QDPB_TUNE_O8
+#define QDPB_TUNE_O8 1  // offer the 128-register small-volume variant (5) to the tuner
+#endif
+
 #include "internal.h"
 
 namespace qdpb {
@@ -479,8 +483,7 @@ __device__ __forceinline__ int fused_face_blocks(const Geom &g, const KP &P) {
 }
 
 template <typename R, int REC, int EPI, bool G5IN, bool G5OUT, bool HALO, bool DOT>
-__global__ void __launch_bounds__(QDPB_DSLASH_MAXT, (dslash_minb<R, REC>()))
-    dslash_kernel(const Geom g, const __grid_constant__ KParams<R, REC> P) {
+__device__ __forceinline__ void dslash_body(const Geom &g, const KParams<R, REC> &P) {
   pdl_enter();
   int cb = blockIdx.x * blockDim.x + threadIdx.x;
   const int vb = blockIdx.x;
@@ -582,6 +585,21 @@ __global__ void __launch_bounds__(QDPB_DSLASH_MAXT, (dslash_minb<R, REC>()))
     if (!P.red_fin) dot_block_partial(dot, P.dot_part, vb);
     else if (red_last) red_complete(P.red, gridDim.x, vb, false);
   }
+}
+
+template <typename R, int REC, int EPI, bool G5IN, bool G5OUT, bool HALO, bool DOT>
+__global__ void __launch_bounds__(QDPB_DSLASH_MAXT, (dslash_minb<R, REC>()))
+    dslash_kernel(const Geom g, const __grid_constant__ KParams<R, REC> P) {
+  dslash_body<R, REC, EPI, G5IN, G5OUT, HALO, DOT>(g, P);
+}
+
+// Small-volume variant: the same code capped at 128 registers (8 x 64 threads per SM).  Below the
+// bandwidth shoulder the whole lattice is little more than one wave of the 168-register kernel
+// (16^3 x 32: 65536 sites for 56832 resident threads), so its second, nearly empty wave is the
+// tail; at 8 blocks per SM every site is resident at once.  Whole lattice, no fused dot.
+template <typename R, int REC, int EPI, bool G5IN, bool G5OUT>
+__global__ void __launch_bounds__(64, 8) dslash_o8_kernel(const Geom g, const __grid_constant__ KParams<R, REC> P) {
+  dslash_body<R, REC, EPI, G5IN, G5OUT, false, false>(g, P);
 }
 
 // Exterior: add the remote hops of dim mu for the output sites on its two faces.  With DOT,
@@ -947,6 +965,17 @@ static void launch_tma(qdp_ctx ctx, const KParams<R, REC> &P, bool g5i, bool g5o
   }
 }
 
+template <typename R, int REC, int EPI>
+static void launch_o8(qdp_ctx ctx, const KParams<R, REC> &P, bool g5i, bool g5o) {
+  if constexpr (dslash_minb<R, REC>() < 8) {
+    const int grid = grid_for(ctx->geom.Vh, 64);
+#define QDPB_LO(A, B) launch_k(ctx, dslash_o8_kernel<R, REC, EPI, A, B>, grid, 64, ctx->geom, P)
+    if (g5i) { if (g5o) QDPB_LO(true, true); else QDPB_LO(true, false); }
+    else { if (g5o) QDPB_LO(false, true); else QDPB_LO(false, false); }
+#undef QDPB_LO
+  }
+}
+
 template <typename R, int REC, int EPI, int NST>
 static void launch_pipe(qdp_ctx ctx, const KParams<R, REC> &P, bool g5i, bool g5o) {
   if constexpr (sizeof(R) == 8 && !is_h16<R>()) {
@@ -1034,7 +1063,7 @@ static int launch_main_epi(qdp_ctx ctx, const DslashArgs &a, const KParams<R, RE
   auto go = [&](int variant) -> cudaError_t {
     // variant: 0 = four threads per site (PLAIN / XPAY only), 1 = main kernel with `block`
     // threads, 2 = main kernel with 32 threads, 3 = bulk-copy staged forward links (fp64 r12),
-    // 4 = cp.async hop pipeline (fp64)
+    // 4 = cp.async hop pipeline (fp64), 5 = main kernel at 128 registers (8 blocks per SM)
     if (variant == 0) {
       if (a.epi == EPI_PLAIN) launch_four<R, REC, EPI_PLAIN>(ctx, P, a.g5_in, a.g5_out);
       else launch_four<R, REC, EPI_XPAY>(ctx, P, a.g5_in, a.g5_out);
@@ -1046,6 +1075,15 @@ static int launch_main_epi(qdp_ctx ctx, const DslashArgs &a, const KParams<R, RE
         case EPI_XPAY: launch_tma<R, REC, EPI_XPAY>(ctx, P, a.g5_in, a.g5_out); break;
         case EPI_CLOVINV: launch_tma<R, REC, EPI_CLOVINV>(ctx, P, a.g5_in, a.g5_out); break;
         default: launch_tma<R, REC, EPI_CLOVXPAY>(ctx, P, a.g5_in, a.g5_out); break;
+      }
+      return cudaGetLastError();
+    }
+    if (variant == 5) {
+      switch (a.epi) {
+        case EPI_PLAIN: launch_o8<R, REC, EPI_PLAIN>(ctx, P, a.g5_in, a.g5_out); break;
+        case EPI_XPAY: launch_o8<R, REC, EPI_XPAY>(ctx, P, a.g5_in, a.g5_out); break;
+        case EPI_CLOVINV: launch_o8<R, REC, EPI_CLOVINV>(ctx, P, a.g5_in, a.g5_out); break;
+        default: launch_o8<R, REC, EPI_CLOVXPAY>(ctx, P, a.g5_in, a.g5_out); break;
       }
       return cudaGetLastError();
     }
@@ -1071,12 +1109,13 @@ static int launch_main_epi(qdp_ctx ctx, const DslashArgs &a, const KParams<R, RE
   };
   // the candidates of this call, in the tuner's order (decreasing threads per block, then the
   // staged variant): whole lattice, no fused reduction (its partials follow the block size)
-  int vids[6], nv = 0;
+  int vids[7], nv = 0;
   if (!is_h16<R>() && (a.epi == EPI_PLAIN || a.epi == EPI_XPAY)) vids[nv++] = 0;
   vids[nv++] = 1;
   // the hop pipeline right after the main kernel (probed before a slow candidate stops the search);
   // plain / xpay only: with the clover epilogues it lost inside the CG (profiles/r02_dslash_pipeline.txt)
   if (sizeof(R) == 8 && !is_h16<R>() && (a.epi == EPI_PLAIN || a.epi == EPI_XPAY)) vids[nv++] = 4;
+  if (dslash_minb<R, REC>() < 8 && QDPB_TUNE_O8) vids[nv++] = 5;
   vids[nv++] = 2;
   if (sizeof(R) == 8 && REC == 12) vids[nv++] = 3;
   if (!halo && !dot && ctx->block == 0 && ctx->dslash_variant >= 0) {  // forced (measurements)
@@ -1084,6 +1123,7 @@ static int launch_main_epi(qdp_ctx ctx, const DslashArgs &a, const KParams<R, RE
     for (int i = 0; i < nv; i++)
       if (vids[i] == ctx->dslash_variant) v = vids[i];
     if (sizeof(R) == 8 && !is_h16<R>() && ctx->dslash_variant == 4) v = 4;  // any epilogue (tests)
+    if (dslash_minb<R, REC>() < 8 && ctx->dslash_variant == 5) v = 5;
     const cudaError_t e = go(v);
     const int rc = prof_end(ctx, &ev);
     return e != cudaSuccess ? cuda_check(ctx, e, "dslash launch") : rc;

@@ -120,7 +120,7 @@ def test_forced_variants_fp64_bit_identical(q, L, recon):
         fx = q.qdp_field_alloc(c, q.QDP_FERMION, 0, q.QDP_ALL)
         q.qdp_set_option(c, q.QDP_OPT_AUTOTUNE, 0)  # fixed reduction launches: identical sums
         base = None
-        for v in (1, 0, 2, 3, 4):
+        for v in (1, 0, 2, 3, 4, 5):
             q.qdp_set_option(c, q.QDP_OPT_DSLASH_VARIANT, v)
             q.qdp_field_zero(fo)
             q.qdp_dslash(fo, fU, fi, q.QDP_EVEN)

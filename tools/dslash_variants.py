@@ -42,9 +42,10 @@ def eo_us(c, fU, prec, n=50):
 print(f"# EO dslash (PLAIN) us per launch and fraction of measured HBM ({PEAK} GB/s); variants: "
       "0 = four threads per site, 1 = one thread per site / 64-thread blocks, 2 = one / 32, "
       "3 = forward links staged by the bulk-copy engine (fp64 r12 only), 4 = cp.async hop pipeline, two stages (fp64 only); "
-      "rows where a variant does not apply repeat variant 1; tuned = the autotuner")
+      "5 = one thread per site at 128 registers (8 x 64 threads per SM); rows where a variant does not apply repeat variant 1; tuned = the autotuner")
 print(f"{'lattice':>14} {'prec':>4} {'rec':>3} | {'v0 us':>8} {'frac':>5} | {'v1 us':>8} {'frac':>5} | "
-      f"{'v2 us':>8} {'frac':>5} | {'v3 us':>8} {'frac':>5} | {'v4 us':>8} {'frac':>5} | {'tuned':>8} {'frac':>5}")
+      f"{'v2 us':>8} {'frac':>5} | {'v3 us':>8} {'frac':>5} | {'v4 us':>8} {'frac':>5} | {'v5 us':>8} {'frac':>5} | "
+      f"{'tuned':>8} {'frac':>5}")
 for L in [(8, 8, 8, 16), (16, 16, 16, 16), (16, 16, 16, 32), (24, 24, 24, 32), (32, 32, 32, 32), (40, 40, 40, 32)]:
     Vh = L[0] * L[1] * L[2] * L[3] // 2
     Ut = fieldgen.random_gauge_torch(L, 11)
@@ -55,7 +56,7 @@ for L in [(8, 8, 8, 16), (16, 16, 16, 16), (16, 16, 16, 32), (24, 24, 24, 32), (
             q.qdp_field_import_device(fU, Ut if prec == q.QDP_F64 else Ut.float())
             bps = (8 * rec + 48) * (8 if prec == q.QDP_F64 else 4)
             row = []
-            for v in (0, 1, 2, 3, 4, -1):
+            for v in (0, 1, 2, 3, 4, 5, -1):
                 q.qdp_set_option(c, q.QDP_OPT_DSLASH_VARIANT, v)
                 us = eo_us(c, fU, prec)
                 row.append((us, bps * Vh / (us * 1e-6) * 1e-9 / PEAK))

@@ -7,6 +7,10 @@
 #           kernel (QDPB_PDL_HALO)                                    -> profiles/r02_pdl.txt
 #   pipe    the cp.async hop pipeline: variant sweep, CG with forced variants, ncu --set full of the
 #           fp64 reconstruct-12 dslash as register-path kernel and as pipeline -> profiles/r02_dslash_pipeline.txt
+#   c5      config 5's rank sub-lattice CG: per-class times with no halo / t / z x t, and the per-launch
+#           dslash times (ncu) of the CG with and without the z x t halo
+#   small   the launch-variant sweep incl. the 128-register variant, tuner tests, CG it/s PDL off / on
+#                                                                     -> profiles/r02_dslash_variants_pdl.txt
 set -u
 mkdir -p gpurun_out/prof_txt
 case "$1" in
@@ -39,4 +43,17 @@ pipe)
   done
   rm -f gpurun_out/*.ncu-rep
   cat gpurun_out/pipe_variants.txt gpurun_out/pipe_cg.txt ;;
+small)
+  timeout 900 python -m pytest tests/test_gpu_tuner.py -m gpu -q > gpurun_out/o8_tests.log 2>&1; echo tests_rc=$?
+  timeout 900 python tools/dslash_variants.py > gpurun_out/dslash_variants.txt 2>&1; echo var_rc=$?
+  timeout 600 python tools/pdl_cg.py > gpurun_out/pdl_cg.txt 2>&1; echo pdl_rc=$?
+  cat gpurun_out/dslash_variants.txt gpurun_out/pdl_cg.txt; tail -3 gpurun_out/o8_tests.log ;;
+c5)
+  timeout 600 python tools/c5_profile.py > gpurun_out/c5_profile.txt 2>&1; echo c5_rc=$?
+  for c in c5cg c5cg0; do
+    timeout 600 ncu --clock-control none --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
+      -k regex:dslash -s 40 -c 16 --csv --log-file gpurun_out/ncu_$c.csv python tools/ncu_cases.py $c > gpurun_out/ncu_$c.log 2>&1
+    echo ${c}_rc=$?
+  done
+  cat gpurun_out/c5_profile.txt ;;
 esac

@@ -5,6 +5,8 @@
   h16    a few iterations of qdp_cg_solve_mixed16 (the 16-bit sloppy dslash launches)
   r12    fp64 reconstruct-12 plain EO dslash (tuned; r12main / r12pipe / r12tma: variant 1 / 4 / 3 forced)
   blas   norm2 / CG vector updates at 40^3x32
+  c5cg / c5cg0  Wilson CG on config 5's rank sub-lattice 48x48x24x24 with z x t through the fused
+         peer-to-peer halo path (self-halo) / without a halo
 Each case warms up, then runs the launches to capture (select them with ncu -k / -s / -c)."""
 import os
 import sys
@@ -17,7 +19,7 @@ import fieldgen
 from paper_1408_5925_b200 import qdpb as q
 
 case = sys.argv[1]
-L = (16, 16, 16, 32) if case == "blas16" else (40, 40, 40, 32)
+L = (16, 16, 16, 32) if case == "blas16" else (48, 48, 24, 24) if case.startswith("c5cg") else (40, 40, 40, 32)
 stream = torch.cuda.Stream()
 torch.cuda.set_stream(stream)
 c = q.qdp_init(L, stream=stream)
@@ -30,8 +32,8 @@ def gauge(kind=q.QDP_GAUGE):
     return f
 
 
-if case in ("zt", "t"):
-    q.qdp_set_option(c, q.QDP_OPT_SELF_HALO, 12 if case == "zt" else 8)
+if case in ("zt", "t", "c5cg"):
+    q.qdp_set_option(c, q.QDP_OPT_SELF_HALO, 8 if case == "t" else 12)
     q.qdp_set_option(c, q.QDP_OPT_P2P, 1)
 if case in ("r12tma", "r12pipe", "r12main"):  # fp64 reconstruct-12 dslash, one forced launch variant:
     # bulk-copy staged forward links / cp.async hop pipeline / the register-path main kernel
@@ -53,6 +55,13 @@ elif case == "h16":
     fAi = q.qdp_field_alloc(c, q.QDP_CLOVER, q.QDP_F64, q.QDP_EVEN)
     q.qdp_clover_build(fA, fAi, fU, 0.1, 1.0)
     q.qdp_cg_solve_mixed16(fx, fb, fU, fA, fAi, mass=0.1, tol=0.0, delta=0.1, maxit=6)
+elif case in ("c5cg", "c5cg0"):
+    fU = gauge()
+    fb = q.qdp_field_alloc(c, q.QDP_FERMION, q.QDP_F64, q.QDP_ALL)
+    q.qdp_field_import_device(fb, fieldgen.random_spinor_torch(L, 22))
+    fx = q.qdp_field_alloc(c, q.QDP_FERMION, q.QDP_F64, q.QDP_ALL)
+    for _ in range(3):
+        q.qdp_cg_solve(fx, fb, fU, mass=0.1, tol=0.0, maxit=8)
 elif case in ("blas", "blas16"):
     a = q.qdp_field_alloc(c, q.QDP_FERMION, q.QDP_F64, q.QDP_ALL)
     q.qdp_field_import_device(a, fieldgen.random_spinor_torch(L, 23))
