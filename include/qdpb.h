@@ -149,7 +149,8 @@ int qdp_get_geometry(qdp_ctx ctx, int local_dims[4], int proc_coords[4]);
  *                     block about to wait for a ghost, so no wait depends on an unstarted block --
  *                     which store the faces straight into the neighbours' ghost slots and
  *                     release-signal a flag; the interior blocks run meanwhile; the blocks holding
- *                     face sites acquire the flags, add the remote hops and acknowledge (two slots per
+ *                     face sites acquire the flags and add the remote hops; the next call acknowledges
+ *                     the consumed ghosts as it starts (two slots per
  *                     face).  With QDP_OPT_OVERLAP = 0 every block waits for the ghosts first.
  *                     Self-halo dims use the same protocol on this rank.  Changing
  *                     QDP_OPT_SELF_HALO after the first dslash rebuilds the slots when every

@@ -210,10 +210,10 @@ template <typename R, int REC = 18> struct KParams {
   unsigned *err;
   unsigned seq;
   // fused boundary (peer-to-peer): leading blocks pack every partitioned face into the
-  // neighbours' ghost slots; the rest visit the output sites in the order perm -- interior sites
-  // first, sites on a partitioned face last; the blocks holding face sites acquire the ghosts, add
-  // the remote hops themselves (no exterior kernels, no read-modify-write of the output) and the
-  // last of them acknowledges the senders
+  // neighbours' ghost slots; the rest visit the output sites interior first, then the sites on a
+  // partitioned face, then the rest of the interior; the blocks holding face sites acquire the
+  // ghosts and add the remote hops themselves (no exterior kernels, no read-modify-write of the
+  // output); the NEXT call acknowledges the consumed ghosts to the senders as it starts
   int fuse;
   int fuse_npack;   // leading pack blocks
   int fuse_nin;     // interior sites: perm[0, nin) interior, perm[nin, Vh) on a partitioned face
@@ -394,28 +394,6 @@ __global__ void __launch_bounds__(128) pack_kernel(const Geom g, const KParams<R
   if (P.pack_counter[mu]) grid_signal_last(P.pack_counter[mu], P.sig[mu][0], P.sig[mu][1], P.seq);
 }
 
-// Fused boundary: of `nblocks` blocks, the last to arrive release-stores v into both flags of
-// every partitioned dim (counter: that of the first partitioned dim).
-__device__ __forceinline__ void fused_signal_last(const Geom &g, unsigned *const counters[4], int nblocks,
-                                                  unsigned *const flags[4][2], unsigned v) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int m0 = 0;
-    while (!((g.part >> m0) & 1)) m0++;
-    __threadfence_system();
-    const unsigned prev = atomicAdd(counters[m0], 1u);
-    if (prev == (unsigned)nblocks - 1) {
-      *counters[m0] = 0u;
-      __threadfence_system();
-      for (int mu = 0; mu < 4; mu++)
-        if ((g.part >> mu) & 1) {
-          st_release_sys(flags[mu][0], v);
-          st_release_sys(flags[mu][1], v);
-        }
-    }
-  }
-}
-
 // Fused boundary: take chunks of the face-packing work until none is left (every thread of the block
 // calls it; roles are uniform per block).  Each chunk is blockDim consecutive pack items (pack_off
 // order); the block publishes its chunks with one system fence and adds them to the done count; the
@@ -475,13 +453,6 @@ __device__ __forceinline__ void remote_hop(const Geom &g, const KP &P, const int
   if (c[MU] == 0) accum_recon<MU, +1>(acc, HalfGhost<T>::load(P.ghost[MU][0], n, face_index(g, MU, c)));
 }
 
-// Fused boundary: the number of blocks holding face sites (visiting positions [kin, kin + nf))
-template <typename KP>
-__device__ __forceinline__ int fused_face_blocks(const Geom &g, const KP &P) {
-  const int B = (int)blockDim.x, end = P.fuse_kin + g.Vh - P.fuse_nin;
-  return (end + B - 1) / B - P.fuse_kin / B;
-}
-
 template <typename R, int REC, int EPI, bool G5IN, bool G5OUT, bool HALO, bool DOT>
 __device__ __forceinline__ void dslash_body(const Geom &g, const KParams<R, REC> &P) {
   pdl_enter();
@@ -490,10 +461,19 @@ __device__ __forceinline__ void dslash_body(const Geom &g, const KParams<R, REC>
   double dot = 0.0;
   bool face = false;  // fused boundary: this block holds sites on a partitioned face
   if (HALO && P.fuse) {
-    // the other queue set (used by the previous call, which has completed) is reset for the next one
+    // the other queue set (used by the previous call, which has completed) is reset for the next one;
+    // and the previous call's ghosts are consumed -- that grid has completed (this kernel is launched
+    // in plain stream order), so its ghost loads have all returned -- so this call acknowledges them
+    // to the senders (release, system scope): no face block of any call fences or counts itself
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       P.pack_q[2 * ((P.seq + 1u) & 1u)] = 0u;
       P.pack_q[2 * ((P.seq + 1u) & 1u) + 1] = 0u;
+#pragma unroll
+      for (int mu = 0; mu < 4; mu++)
+        if ((g.part >> mu) & 1) {
+          st_release_sys(P.ack_to[mu][0], P.seq - 1u);
+          st_release_sys(P.ack_to[mu][1], P.seq - 1u);
+        }
     }
     if ((int)blockIdx.x < P.fuse_npack) {  // leading blocks: pack (work queue) and leave
       pack_help<R, REC, G5IN>(g, P);
@@ -552,11 +532,14 @@ __device__ __forceinline__ void dslash_body(const Geom &g, const KParams<R, REC>
     Spinor<T> acc;
 #pragma unroll
     for (int k = 0; k < 12; k++) acc.c[k] = {T(0), T(0)};
-    hop_dir<R, 0>(g, P, c, cb, p, G5IN, HALO, acc);
-    hop_dir<R, 1>(g, P, c, cb, p, G5IN, HALO, acc);
-    hop_dir<R, 2>(g, P, c, cb, p, G5IN, HALO, acc);
-    hop_dir<R, 3>(g, P, c, cb, p, G5IN, HALO, acc);
-    if (HALO && P.fuse) {  // remote hops from the ghosts the neighbours stored
+    // fused boundary: a block without face sites has only interior sites (block-uniform: no remote hop
+    // test per site and hop); the separate-kernel interior pass tests every site
+    const bool halo = HALO && (!P.fuse || face);
+    hop_dir<R, 0>(g, P, c, cb, p, G5IN, halo, acc);
+    hop_dir<R, 1>(g, P, c, cb, p, G5IN, halo, acc);
+    hop_dir<R, 2>(g, P, c, cb, p, G5IN, halo, acc);
+    hop_dir<R, 3>(g, P, c, cb, p, G5IN, halo, acc);
+    if (HALO && P.fuse && face) {  // remote hops from the ghosts the neighbours stored
       remote_hop<R, 0>(g, P, c, cb, p, acc);
       remote_hop<R, 1>(g, P, c, cb, p, acc);
       remote_hop<R, 2>(g, P, c, cb, p, acc);
@@ -577,9 +560,6 @@ __device__ __forceinline__ void dslash_body(const Geom &g, const KParams<R, REC>
   // the block's partial of the fused dot goes out BEFORE the output stores (reduce.cuh red_arrive)
   bool red_last = false;
   if (DOT && P.red_fin) red_last = red_arrive(P.red, gridDim.x, vb, dot, 0.0);
-  // the last face block tells the senders their slots were consumed: the ghosts are in registers
-  // already, so this goes out before the output stores (its fence does not wait for them)
-  if (HALO && P.fuse && face) fused_signal_last(g, P.ext_counter, fused_face_blocks(g, P), P.ack_to, P.seq);
   if (have) P.out.store(cb, o);
   if (DOT) {
     if (!P.red_fin) dot_block_partial(dot, P.dot_part, vb);

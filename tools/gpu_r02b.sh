@@ -9,6 +9,10 @@
 #           fp64 reconstruct-12 dslash as register-path kernel and as pipeline -> profiles/r02_dslash_pipeline.txt
 #   c5      config 5's rank sub-lattice CG: per-class times with no halo / t / z x t, and the per-launch
 #           dslash times (ncu) of the CG with and without the z x t halo
+#   zt      ncu --set full (+ SASS source page) of the fused z x t boundary kernel and of the main kernel
+#           on config 5's rank sub-lattice
+#   ack     the fused boundary with the acknowledgement by the next call and block-uniform halo
+#           tests: halo / peer / PDL / mixed tests, fused sweep, config 5's CG
 #   small   the launch-variant sweep incl. the 128-register variant, tuner tests, CG it/s PDL off / on
 #                                                                     -> profiles/r02_dslash_variants_pdl.txt
 set -u
@@ -56,4 +60,20 @@ c5)
     echo ${c}_rc=$?
   done
   cat gpurun_out/c5_profile.txt ;;
+zt)
+  F="ncu --clock-control none --set full --import-source on"
+  for c in c5zt c5whole; do
+    timeout 600 $F -k regex:dslash -s 10 -c 1 -o gpurun_out/prof_$c -f python tools/ncu_cases.py $c > gpurun_out/ncu_$c.log 2>&1; echo ${c}_rc=$?
+    python tools/ncu_summary.py gpurun_out/prof_$c.ncu-rep > gpurun_out/prof_txt/prof_${c}_detail.txt 2>&1
+    ncu -i gpurun_out/prof_$c.ncu-rep --page source --csv --print-source sass > gpurun_out/prof_txt/src_$c.csv 2>&1
+  done
+  rm -f gpurun_out/*.ncu-rep
+  grep -E "gpu__time|dram__bytes|warps_active|long_scoreboard_per|issue_active|l1tex__t_sector_hit|lts__t_sector_hit" gpurun_out/prof_txt/prof_c5*_detail.txt ;;
+ack)
+  timeout 900 python -m pytest tests/test_gpu_p2p.py tests/test_gpu_peer.py tests/test_gpu_pdl.py tests/test_gpu_mixed.py -m gpu -q \
+    > gpurun_out/ack_tests.log 2>&1; echo tests_rc=$?
+  timeout 300 python tools/fused_sweep.py > gpurun_out/ack.txt 2>&1
+  timeout 300 python tools/c5_profile.py >> gpurun_out/ack.txt 2>&1
+  timeout 600 python tools/pdl_zt.py >> gpurun_out/ack.txt 2>&1
+  cat gpurun_out/ack.txt; tail -2 gpurun_out/ack_tests.log ;;
 esac

@@ -5,6 +5,8 @@
   h16    a few iterations of qdp_cg_solve_mixed16 (the 16-bit sloppy dslash launches)
   r12    fp64 reconstruct-12 plain EO dslash (tuned; r12main / r12pipe / r12tma: variant 1 / 4 / 3 forced)
   blas   norm2 / CG vector updates at 40^3x32
+  c5zt / c5whole  plain fp64 EO dslash on config 5's rank sub-lattice 48x48x24x24: the fused z x t
+         boundary kernel (self-halo) / the register-path main kernel without a halo
   c5cg / c5cg0  Wilson CG on config 5's rank sub-lattice 48x48x24x24 with z x t through the fused
          peer-to-peer halo path (self-halo) / without a halo
 Each case warms up, then runs the launches to capture (select them with ncu -k / -s / -c)."""
@@ -19,7 +21,7 @@ import fieldgen
 from paper_1408_5925_b200 import qdpb as q
 
 case = sys.argv[1]
-L = (16, 16, 16, 32) if case == "blas16" else (48, 48, 24, 24) if case.startswith("c5cg") else (40, 40, 40, 32)
+L = (16, 16, 16, 32) if case == "blas16" else (48, 48, 24, 24) if case.startswith("c5") else (40, 40, 40, 32)
 stream = torch.cuda.Stream()
 torch.cuda.set_stream(stream)
 c = q.qdp_init(L, stream=stream)
@@ -32,13 +34,17 @@ def gauge(kind=q.QDP_GAUGE):
     return f
 
 
-if case in ("zt", "t", "c5cg"):
+if case in ("zt", "t", "c5cg", "c5zt"):
     q.qdp_set_option(c, q.QDP_OPT_SELF_HALO, 8 if case == "t" else 12)
     q.qdp_set_option(c, q.QDP_OPT_P2P, 1)
 if case in ("r12tma", "r12pipe", "r12main"):  # fp64 reconstruct-12 dslash, one forced launch variant:
     # bulk-copy staged forward links / cp.async hop pipeline / the register-path main kernel
     q.qdp_set_option(c, q.QDP_OPT_DSLASH_VARIANT, {"r12tma": 3, "r12pipe": 4, "r12main": 1}[case])
     case = "r12"
+if case == "c5whole":  # the register-path main kernel on the same sub-lattice, no halo
+    q.qdp_set_option(c, q.QDP_OPT_DSLASH_VARIANT, 1)
+if case in ("c5zt", "c5whole"):
+    case = "zt"
 if case in ("zt", "t", "r12"):
     fU = gauge(q.QDP_GAUGE12 if case == "r12" else q.QDP_GAUGE)
     fi = q.qdp_field_alloc(c, q.QDP_FERMION, q.QDP_F64, q.QDP_ODD)
