@@ -136,3 +136,37 @@ def test_cg_clover_p2p_self(q):
         assert rel_site_err(q.qdp_field_export(fx), ref["x"]) <= 1e-9
     finally:
         q.qdp_finalize(c)
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("overlap", [1, 0])
+@pytest.mark.parametrize("mask", [8, 12, 15])
+def test_fused_boundary_stress(q, mask, overlap):
+    """Many fused peer-to-peer calls in a row (both slots, both parities, the acknowledgement of each
+    call's ghosts written by the next call, PDL on the reductions in between): every output must be
+    bit-identical to the first, which equals the oracle.  A stale ghost (a slot overwritten before
+    it was consumed, or read before it was written) changes the face sites' bits."""
+    L = (6, 4, 8, 8)
+    U = fieldgen.random_gauge(L, 2111)
+    psi = fieldgen.random_spinor(L, 3111)
+    ref = oracle.hopping(U, psi, L, -1)
+    c = _ctx(q, L, mask)
+    q.qdp_set_option(c, q.QDP_OPT_OVERLAP, overlap)
+    try:
+        fU = _field(q, c, q.QDP_GAUGE, 0, q.QDP_ALL, U)
+        fp = _field(q, c, q.QDP_FERMION, 0, q.QDP_ALL, psi)
+        fo = q.qdp_field_alloc(c, q.QDP_FERMION, 0, q.QDP_ALL)
+        q.qdp_dslash(fo, fU, fp, q.QDP_ALL)
+        first = q.qdp_field_export(fo)
+        assert rel_site_err(first, ref) <= 1e-13
+        n0 = q.qdp_norm2(fo)
+        for i in range(40):
+            q.qdp_field_zero(fo)
+            q.qdp_dslash(fo, fU, fp, q.QDP_ALL)
+            n = q.qdp_norm2(fo)  # a one-launch reduction between the dslash calls
+            assert n == n0, i
+            if i % 8 == 7:
+                assert np.array_equal(q.qdp_field_export(fo), first), i
+        q.qdp_synchronize(c)
+    finally:
+        q.qdp_finalize(c)

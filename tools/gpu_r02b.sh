@@ -1,6 +1,7 @@
 # GPU calls of round 2's second session (one `gpurun` call per section; outputs in gpurun_out/, the
 # summaries copied into profiles/ by hand).  Usage: bash tools/gpu_r02b.sh SECTION
 #   check   the GPU suite, smoke, the default bench
+#   evidence  the bench's ncu launch list, the reference arm, the N = 2 functional run on one GPU
 #   fused   fused boundary: face position in the visiting order (QDPB_FACE_AT) x ack before the
 #           output stores; halo tests under the non-default setting  -> profiles/r02_fused_face_position.txt
 #   pdl     programmatic dependent launch off / on (CG it/s), z x t with / without PDL on the fused
@@ -13,6 +14,7 @@
 #           on config 5's rank sub-lattice
 #   ack     the fused boundary with the acknowledgement by the next call and block-uniform halo
 #           tests: halo / peer / PDL / mixed tests, fused sweep, config 5's CG
+#   cgblas  ncu --set full of the CG's vector updates (cg_r, cg_xp)
 #   small   the launch-variant sweep incl. the 128-register variant, tuner tests, CG it/s PDL off / on
 #                                                                     -> profiles/r02_dslash_variants_pdl.txt
 set -u
@@ -23,6 +25,14 @@ check)
   timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke_rc=$?
   timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench_rc=$?
   tail -3 gpurun_out/gpu_tests.log; cat gpurun_out/smoke.log ;;
+evidence)
+  # the bench's ncu launch list (cold, serialised: shares), the reference arm, the N = 2 path on one GPU
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
+    python bench.py --steps 1 --warmup 3 --iters 8 --no-cpu --no-check --no-tts --ms-shifts 0 --no-strong --no-config5 \
+    > gpurun_out/ncu_launches_bench.log 2>&1; echo launches_rc=$?
+  timeout 900 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo ref_rc=$?
+  QDPB_BENCH_ONE_GPU=1 timeout 900 python bench.py --gpus 2 --steps 3 > gpurun_out/bench_n2.json 2> gpurun_out/bench_n2.err; echo n2_rc=$?
+  tail -c 600 gpurun_out/bench_n2.json ;;
 fused)
   for cfg in "1" "0.5" "0.25" "0.75"; do
     echo "FACE_AT=$cfg" >> gpurun_out/fused_exp.txt
@@ -76,4 +86,10 @@ ack)
   timeout 300 python tools/c5_profile.py >> gpurun_out/ack.txt 2>&1
   timeout 600 python tools/pdl_zt.py >> gpurun_out/ack.txt 2>&1
   cat gpurun_out/ack.txt; tail -2 gpurun_out/ack_tests.log ;;
+cgblas)
+  F="ncu --clock-control none --set full --import-source on"
+  timeout 600 $F -k "regex:cg_r_kernel|cg_xp_kernel" -s 40 -c 2 -o gpurun_out/prof_cgblas -f python tools/ncu_cases.py cgblas > gpurun_out/ncu_cgblas.log 2>&1; echo cgblas_rc=$?
+  python tools/ncu_summary.py gpurun_out/prof_cgblas.ncu-rep > gpurun_out/prof_txt/prof_cgblas_detail.txt 2>&1
+  rm -f gpurun_out/*.ncu-rep
+  grep -E "Kernel Name|gpu__time|dram__bytes|warps_active|long_scoreboard_per|issue_active|registers|block_size|grid_size|barrier_per|membar_per" gpurun_out/prof_txt/prof_cgblas_detail.txt ;;
 esac

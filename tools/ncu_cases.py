@@ -5,6 +5,7 @@
   h16    a few iterations of qdp_cg_solve_mixed16 (the 16-bit sloppy dslash launches)
   r12    fp64 reconstruct-12 plain EO dslash (tuned; r12main / r12pipe / r12tma: variant 1 / 4 / 3 forced)
   blas   norm2 / CG vector updates at 40^3x32
+  cgblas the fp64 clover CG's vector updates at 40^3x32 (cg_r: r -= alpha q with |r|^2; cg_xp)
   c5zt / c5whole  plain fp64 EO dslash on config 5's rank sub-lattice 48x48x24x24: the fused z x t
          boundary kernel (self-halo) / the register-path main kernel without a halo
   c5cg / c5cg0  Wilson CG on config 5's rank sub-lattice 48x48x24x24 with z x t through the fused
@@ -61,6 +62,16 @@ elif case == "h16":
     fAi = q.qdp_field_alloc(c, q.QDP_CLOVER, q.QDP_F64, q.QDP_EVEN)
     q.qdp_clover_build(fA, fAi, fU, 0.1, 1.0)
     q.qdp_cg_solve_mixed16(fx, fb, fU, fA, fAi, mass=0.1, tol=0.0, delta=0.1, maxit=6)
+elif case == "cgblas":
+    fU = gauge()
+    fb = q.qdp_field_alloc(c, q.QDP_FERMION, q.QDP_F64, q.QDP_ALL)
+    q.qdp_field_import_device(fb, fieldgen.random_spinor_torch(L, 22))
+    fx = q.qdp_field_alloc(c, q.QDP_FERMION, q.QDP_F64, q.QDP_ALL)
+    fA = q.qdp_field_alloc(c, q.QDP_CLOVER, q.QDP_F64, q.QDP_ALL)
+    fAi = q.qdp_field_alloc(c, q.QDP_CLOVER, q.QDP_F64, q.QDP_EVEN)
+    q.qdp_clover_build(fA, fAi, fU, 0.1, 1.0)
+    for _ in range(3):
+        q.qdp_cg_solve(fx, fb, fU, fA, fAi, mass=0.1, tol=0.0, maxit=12)
 elif case in ("c5cg", "c5cg0"):
     fU = gauge()
     fb = q.qdp_field_alloc(c, q.QDP_FERMION, q.QDP_F64, q.QDP_ALL)
