@@ -867,6 +867,7 @@ template <int REC, int EPI, bool G5IN, bool G5OUT, int NST>
 __global__ void __launch_bounds__(64) dslash_pipe_kernel(const Geom g, const __grid_constant__ KParams<double, REC> P) {
   using PH = PipeHop<REC>;
   extern __shared__ __align__(16) double2 ring[];  // [NST][NE][64]
+  pdl_enter();
   const int cb = blockIdx.x * 64 + threadIdx.x;
   if (cb >= g.Vh) return;  // whole warps only on the last block: no barrier below
   const int p = P.parity;
@@ -920,7 +921,7 @@ static void launch_main(qdp_ctx ctx, const KParams<R, REC> &P, int block) {
   // (profiles/r02_pdl.txt); QDPB_PDL_HALO=1 for measurements
   static const bool pdl_halo = getenv("QDPB_PDL_HALO") && atoi(getenv("QDPB_PDL_HALO"));
   launch_pdl(ctx->stream, ctx->pdl && (!HALO || pdl_halo), dslash_kernel<R, REC, EPI, G5IN, G5OUT, HALO, DOT>,
-             grid_for(g.Vh, block) + P.fuse_npack, block, g, P);
+             grid_for(g.Vh, block) + P.fuse_npack, block, 0, g, P);
 }
 
 template <typename R, int REC, int EPI>
@@ -960,19 +961,12 @@ template <typename R, int REC, int EPI, int NST>
 static void launch_pipe(qdp_ctx ctx, const KParams<R, REC> &P, bool g5i, bool g5o) {
   if constexpr (sizeof(R) == 8 && !is_h16<R>()) {
     const int grid = grid_for(ctx->geom.Vh, 64);
-    const size_t smem = (size_t)NST * PipeHop<REC>::NE * 64 * 16;
-#define QDPB_LP(A, B)                                                                                   \
-  {                                                                                                     \
-    static bool attr = false;                                                                           \
-    if (!attr) {                                                                                        \
-      cudaFuncSetAttribute(dslash_pipe_kernel<REC, EPI, A, B, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                           (int)smem);                                                                  \
-      attr = true;                                                                                      \
-    }                                                                                                   \
-    dslash_pipe_kernel<REC, EPI, A, B, NST><<<grid, 64, smem, ctx->stream>>>(ctx->geom, P);       \
-  }
-    if (g5i) { if (g5o) QDPB_LP(true, true) else QDPB_LP(true, false) }
-    else { if (g5o) QDPB_LP(false, true) else QDPB_LP(false, false) }
+    // two stages: 36 KB (12-real links) / 42 KB (18) of dynamic shared memory, within the default 48 KB
+    constexpr size_t smem = (size_t)NST * PipeHop<REC>::NE * 64 * 16;
+    static_assert(smem <= 48 * 1024, "the hop ring must fit the default dynamic shared-memory limit");
+#define QDPB_LP(A, B) launch_pdl(ctx->stream, ctx->pdl != 0, dslash_pipe_kernel<REC, EPI, A, B, NST>, grid, 64, smem, ctx->geom, P)
+    if (g5i) { if (g5o) QDPB_LP(true, true); else QDPB_LP(true, false); }
+    else { if (g5o) QDPB_LP(false, true); else QDPB_LP(false, false); }
 #undef QDPB_LP
   }
 }

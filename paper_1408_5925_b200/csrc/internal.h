@@ -993,10 +993,12 @@ __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 template <typename... KA, typename... A>
-cudaError_t launch_pdl(cudaStream_t stream, bool pdl, void (*kernel)(KA...), int grid, int block, A &&...args) {
+cudaError_t launch_pdl(cudaStream_t stream, bool pdl, void (*kernel)(KA...), int grid, int block, size_t smem,
+                       A &&...args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3((unsigned)block);
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1008,7 +1010,7 @@ cudaError_t launch_pdl(cudaStream_t stream, bool pdl, void (*kernel)(KA...), int
 // on the context stream, with PDL as QDP_OPT_PDL says
 template <typename... KA, typename... A>
 cudaError_t launch_k(qdp_ctx ctx, void (*kernel)(KA...), int grid, int block, A &&...args) {
-  return launch_pdl(ctx->stream, ctx->pdl != 0, kernel, grid, block, std::forward<A>(args)...);
+  return launch_pdl(ctx->stream, ctx->pdl != 0, kernel, grid, block, 0, std::forward<A>(args)...);
 }
 
 }  // namespace qdpb
