@@ -368,8 +368,11 @@ def run_native(args, rank, world, local_rank):
     def step():
         return q.qdp_cg_solve(fx, fb, fU, fA, fAi, mass=MASS, tol=0.0, maxit=args.iters)
 
-    for _ in range(args.warmup):
+    for k in range(args.warmup):
+        if k == args.warmup - 1:  # fills the library's CUDA-event pool before the profiled timed region
+            q.qdp_set_option(ctx, q.QDP_OPT_PROFILE, 1)
         step()
+    q.qdp_set_option(ctx, q.QDP_OPT_PROFILE, 0)
 
     # ---- timed region: K solves, fields resident in HBM, a CUDA-event pair around every launch on
     # the launching stream (the roofline's live launch durations and the breakdown by kernel class)
