@@ -22,6 +22,9 @@
 #pragma once
 #include <type_traits>
 
+#ifndef QDPB_H16_F32X2
+#define QDPB_H16_F32X2 1  // 16-bit dslash: SU(3) products and accumulation in packed fp32 pairs (FFMA2)
+#endif
 #ifndef QDPB_TUNE_O8
 #define QDPB_TUNE_O8 1  // offer the 128-register small-volume variant (5) to the tuner
 #endif
@@ -151,6 +154,116 @@ __device__ __forceinline__ void accum_recon_f(Spinor<R> &acc, const Half<R> &h, 
   }
 }
 
+// ---- packed fp32 pairs (FFMA2 / FMUL2, sm_100): the 16-bit dslash is issue-bound,
+// and a complex multiply-add is two packed fused multiply-adds with one operand a broadcast scalar:
+// a * h = a.re (h.re, h.im) + a.im (-h.im, h.re), the second vector i h formed once per h and reused
+// across the three rows of the SU(3) product.  Same products and the same summation order as the
+// scalar code (acc.re: + a.re h.re, then - a.im h.im; acc.im: + a.re h.im, then + a.im h.re).
+typedef unsigned long long f2_t;
+__device__ __forceinline__ f2_t f2pk(float x, float y) {
+  f2_t d;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(x), "f"(y));
+  return d;
+}
+__device__ __forceinline__ f2_t f2pk(cx<float> a) { return f2pk(a.re, a.im); }
+__device__ __forceinline__ cx<float> f2up(f2_t d) {
+  cx<float> r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.re), "=f"(r.im) : "l"(d));
+  return r;
+}
+__device__ __forceinline__ f2_t ffma2(f2_t a, f2_t b, f2_t c) {
+  f2_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f2_t fmul2(f2_t a, f2_t b) {
+  f2_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f2_t splat(float x) { return f2pk(x, x); }
+__device__ __forceinline__ f2_t times_i2(cx<float> h) { return f2pk(-h.im, h.re); }  // i h
+
+__device__ __forceinline__ Half<float> mul_link2(const Link<float> &u, const Half<float> &h) {  // U h
+  Half<float> r;
+#pragma unroll
+  for (int s = 0; s < 2; s++) {
+    f2_t hv[3], ih[3];
+#pragma unroll
+    for (int b = 0; b < 3; b++) {
+      hv[b] = f2pk(h.c[3 * s + b]);
+      ih[b] = times_i2(h.c[3 * s + b]);
+    }
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+      f2_t acc = fmul2(splat(u.m[3 * a].re), hv[0]);
+      acc = ffma2(splat(u.m[3 * a].im), ih[0], acc);
+#pragma unroll
+      for (int b = 1; b < 3; b++) {
+        acc = ffma2(splat(u.m[3 * a + b].re), hv[b], acc);
+        acc = ffma2(splat(u.m[3 * a + b].im), ih[b], acc);
+      }
+      r.c[3 * s + a] = f2up(acc);
+    }
+  }
+  return r;
+}
+__device__ __forceinline__ Half<float> mul_link_dag2(const Link<float> &u, const Half<float> &h) {  // U^dag h
+  Half<float> r;
+#pragma unroll
+  for (int s = 0; s < 2; s++) {
+    f2_t hv[3], ih[3];
+#pragma unroll
+    for (int b = 0; b < 3; b++) {
+      hv[b] = f2pk(h.c[3 * s + b]);
+      ih[b] = times_i2(h.c[3 * s + b]);
+    }
+#pragma unroll
+    for (int a = 0; a < 3; a++) {  // conj(u) h = u.re h - u.im (i h)
+      f2_t acc = fmul2(splat(u.m[a].re), hv[0]);
+      acc = ffma2(splat(-u.m[a].im), ih[0], acc);
+#pragma unroll
+      for (int b = 1; b < 3; b++) {
+        acc = ffma2(splat(u.m[3 * b + a].re), hv[b], acc);
+        acc = ffma2(splat(-u.m[3 * b + a].im), ih[b], acc);
+      }
+      r.c[3 * s + a] = f2up(acc);
+    }
+  }
+  return r;
+}
+// acc += f x (the reconstruction of accum_recon) in packed pairs: +-h by +-f, +-i h by +-f on i h
+template <int K>
+__device__ __forceinline__ void add_f2(cx<float> &a, f2_t h, f2_t ih, float f) {  // K: 0 +h, 1 -h, 2 +i h, 3 -i h
+  if (K == 0) a = f2up(ffma2(splat(f), h, f2pk(a)));
+  else if (K == 1) a = f2up(ffma2(splat(-f), h, f2pk(a)));
+  else if (K == 2) a = f2up(ffma2(splat(f), ih, f2pk(a)));
+  else a = f2up(ffma2(splat(-f), ih, f2pk(a)));
+}
+template <int MU, int S>
+__device__ __forceinline__ void accum_recon_f2(Spinor<float> &acc, const Half<float> &h, float f) {
+#pragma unroll
+  for (int c = 0; c < 3; c++) {
+    const f2_t h0 = f2pk(h.c[c]), h1 = f2pk(h.c[3 + c]);
+    const f2_t i0 = (MU == 0 || MU == 2) ? times_i2(h.c[c]) : h0, i1 = (MU == 0 || MU == 2) ? times_i2(h.c[3 + c]) : h1;
+    add_f2<0>(acc.c[c], h0, i0, f);
+    add_f2<0>(acc.c[3 + c], h1, i1, f);
+    if (MU == 0) {        // r2 = -S i h1, r3 = -S i h0
+      add_f2<(S > 0 ? 3 : 2)>(acc.c[6 + c], h1, i1, f);
+      add_f2<(S > 0 ? 3 : 2)>(acc.c[9 + c], h0, i0, f);
+    } else if (MU == 1) { // r2 = S h1, r3 = -S h0
+      add_f2<(S > 0 ? 0 : 1)>(acc.c[6 + c], h1, i1, f);
+      add_f2<(S > 0 ? 1 : 0)>(acc.c[9 + c], h0, i0, f);
+    } else if (MU == 2) { // r2 = -S i h0, r3 = S i h1
+      add_f2<(S > 0 ? 3 : 2)>(acc.c[6 + c], h0, i0, f);
+      add_f2<(S > 0 ? 2 : 3)>(acc.c[9 + c], h1, i1, f);
+    } else {              // r2 = S h0, r3 = S h1
+      add_f2<(S > 0 ? 0 : 1)>(acc.c[6 + c], h0, i0, f);
+      add_f2<(S > 0 ? 0 : 1)>(acc.c[9 + c], h1, i1, f);
+    }
+  }
+}
+
 template <typename R>
 __device__ __forceinline__ Half<R> mul_link(const Link<R> &u, const Half<R> &h) {  // U h
   Half<R> r;
@@ -251,7 +364,11 @@ __device__ __forceinline__ void hop_dir(const Geom &g, const KP &P, const int c[
         float sc;
         Spinor<T> s = P.psi.load_raw(coords_cb(g, n), sc);
         if (G5IN) g5(s);
+#if QDPB_H16_F32X2
+        accum_recon_f2<MU, -1>(acc, mul_link2(P.U.load_raw(MU, p, cb), project<MU, -1>(s)), sc * P.U.raw_scale);
+#else
         accum_recon_f<MU, -1>(acc, mul_link(P.U.load_raw(MU, p, cb), project<MU, -1>(s)), sc * P.U.raw_scale);
+#endif
       } else {
         Spinor<T> s = P.psi.load(coords_cb(g, n));
         if (G5IN) g5(s);
@@ -272,8 +389,13 @@ __device__ __forceinline__ void hop_dir(const Geom &g, const KP &P, const int c[
         float sc;
         Spinor<T> s = P.psi.load_raw(ncb, sc);
         if (G5IN) g5(s);
+#if QDPB_H16_F32X2
+        accum_recon_f2<MU, +1>(acc, mul_link_dag2(P.U.load_raw(MU, 1 - p, ncb), project<MU, +1>(s)),
+                               sc * P.U.raw_scale);
+#else
         accum_recon_f<MU, +1>(acc, mul_link_dag(P.U.load_raw(MU, 1 - p, ncb), project<MU, +1>(s)),
                               sc * P.U.raw_scale);
+#endif
       } else {
         Spinor<T> s = P.psi.load(ncb);
         if (G5IN) g5(s);

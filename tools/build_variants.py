@@ -12,6 +12,7 @@ from paper_1408_5925_b200 import build as b  # noqa: E402
 VARIANTS = {
     "base": [],
     "pf_off": ["-DQDPB_PF_F12=0"],  # no fp32 reconstruct-12 link prefetch
+    "h16_scalar": ["-DQDPB_H16_F32X2=0"],  # 16-bit dslash with scalar fp32 arithmetic (no FFMA2)
     # occupancy sweeps per (precision, gauge storage): min resident 64-thread blocks per SM
     "occ_a": ["-DQDPB_MINB_D12=7", "-DQDPB_MINB_F18=8", "-DQDPB_MINB_F12=8"],
     "occ_b": ["-DQDPB_MINB_D12=8", "-DQDPB_MINB_F18=10", "-DQDPB_MINB_F12=10"],

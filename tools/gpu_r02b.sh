@@ -15,6 +15,7 @@
 #   ack     the fused boundary with the acknowledgement by the next call and block-uniform halo
 #           tests: halo / peer / PDL / mixed tests, fused sweep, config 5's CG
 #   cgblas  ncu --set full of the CG's vector updates (cg_r, cg_xp)
+#   h16     the 16-bit dslash with packed fp32 arithmetic vs scalar (A/B in one call), mixed-solver tests
 #   small   the launch-variant sweep incl. the 128-register variant, tuner tests, CG it/s PDL off / on
 #                                                                     -> profiles/r02_dslash_variants_pdl.txt
 set -u
@@ -92,4 +93,13 @@ cgblas)
   python tools/ncu_summary.py gpurun_out/prof_cgblas.ncu-rep > gpurun_out/prof_txt/prof_cgblas_detail.txt 2>&1
   rm -f gpurun_out/*.ncu-rep
   grep -E "Kernel Name|gpu__time|dram__bytes|warps_active|long_scoreboard_per|issue_active|registers|block_size|grid_size|barrier_per|membar_per" gpurun_out/prof_txt/prof_cgblas_detail.txt ;;
+h16)
+  # the 16-bit dslash with packed fp32 pairs (FFMA2) vs the scalar build (variants/libqdpb_h16_scalar.so)
+  timeout 900 python -m pytest tests/test_gpu_mixed.py -m gpu -q > gpurun_out/h16_tests.log 2>&1; echo tests_rc=$?
+  for v in scalar f32x2 scalar f32x2; do
+    echo "== $v" >> gpurun_out/h16.txt
+    if [ $v = scalar ]; then QDPB_LIB=variants/libqdpb_h16_scalar.so timeout 600 python tools/mixed_profile.py >> gpurun_out/h16.txt 2>&1
+    else timeout 600 python tools/mixed_profile.py >> gpurun_out/h16.txt 2>&1; fi
+  done
+  cat gpurun_out/h16.txt; tail -2 gpurun_out/h16_tests.log ;;
 esac
