@@ -989,7 +989,6 @@ template <int REC, int EPI, bool G5IN, bool G5OUT, int NST>
 __global__ void __launch_bounds__(64) dslash_pipe_kernel(const Geom g, const __grid_constant__ KParams<double, REC> P) {
   using PH = PipeHop<REC>;
   extern __shared__ __align__(16) double2 ring[];  // [NST][NE][64]
-  pdl_enter();
   const int cb = blockIdx.x * 64 + threadIdx.x;
   if (cb >= g.Vh) return;  // whole warps only on the last block: no barrier below
   const int p = P.parity;
@@ -1086,7 +1085,10 @@ static void launch_pipe(qdp_ctx ctx, const KParams<R, REC> &P, bool g5i, bool g5
     // two stages: 36 KB (12-real links) / 42 KB (18) of dynamic shared memory, within the default 48 KB
     constexpr size_t smem = (size_t)NST * PipeHop<REC>::NE * 64 * 16;
     static_assert(smem <= 48 * 1024, "the hop ring must fit the default dynamic shared-memory limit");
-#define QDPB_LP(A, B) launch_pdl(ctx->stream, ctx->pdl != 0, dslash_pipe_kernel<REC, EPI, A, B, NST>, grid, 64, smem, ctx->geom, P)
+    // plain stream order, no griddepcontrol in the kernel: with PDL a sequence of pipeline launches alone
+    // ran faster, but inside the Wilson CG (mixed with the main kernel and the BLAS kernels) the CG lost
+    // 13-14% (profiles/r02_dslash_pipeline.txt section 7)
+#define QDPB_LP(A, B) launch_pdl(ctx->stream, false, dslash_pipe_kernel<REC, EPI, A, B, NST>, grid, 64, smem, ctx->geom, P)
     if (g5i) { if (g5o) QDPB_LP(true, true); else QDPB_LP(true, false); }
     else { if (g5o) QDPB_LP(false, true); else QDPB_LP(false, false); }
 #undef QDPB_LP
@@ -1208,9 +1210,11 @@ static int launch_main_epi(qdp_ctx ctx, const DslashArgs &a, const KParams<R, RE
   int vids[7], nv = 0;
   if (!is_h16<R>() && (a.epi == EPI_PLAIN || a.epi == EPI_XPAY)) vids[nv++] = 0;
   vids[nv++] = 1;
-  // the hop pipeline right after the main kernel (probed before a slow candidate stops the search);
-  // plain / xpay only: with the clover epilogues it lost inside the CG (profiles/r02_dslash_pipeline.txt)
-  if (sizeof(R) == 8 && !is_h16<R>() && (a.epi == EPI_PLAIN || a.epi == EPI_XPAY)) vids[nv++] = 4;
+  // the hop pipeline right after the main kernel (probed before a slow candidate stops the search):
+  // fp64 reconstruct-12, plain / xpay only.  With the clover epilogues it lost inside the CG; with 18-real
+  // links it only matches the main kernel in isolation and inside the Wilson CG the main kernel, which
+  // overlaps its neighbours under PDL, is 2-4% faster (profiles/r02_dslash_pipeline.txt sections 4, 7)
+  if (sizeof(R) == 8 && !is_h16<R>() && REC == 12 && (a.epi == EPI_PLAIN || a.epi == EPI_XPAY)) vids[nv++] = 4;
   if (dslash_minb<R, REC>() < 8 && QDPB_TUNE_O8) vids[nv++] = 5;
   vids[nv++] = 2;
   if (sizeof(R) == 8 && REC == 12) vids[nv++] = 3;
