@@ -44,10 +44,10 @@ class Timer:
     def __init__(self, stream):
         self.s = stream
 
-    def __call__(self, fn, n, warm=3):
-        for _ in range(warm):
-            fn()
-        torch.cuda.synchronize()
+    def __call__(self, fn, n, warm=12):
+        for _ in range(warm):  # the tuners' probes finish here: they read their events
+            fn()               # only once those completed, so synchronise between the warm-up calls
+            torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(self.s)
         for _ in range(n):
@@ -58,10 +58,14 @@ class Timer:
 
 
 def make_ctx(L, stream, halo_mask=0, nccl=0, overlap=1):
+    """nccl = 1: faces through NCCL send/recv to self (separate pack / interior / exterior kernels);
+    nccl = 0 with a halo mask: the peer-to-peer protocol with the fused boundary kernel (one launch)"""
     c = q.qdp_init(L, stream=stream)
     if halo_mask:
         q.qdp_set_option(c, q.QDP_OPT_SELF_HALO, halo_mask)
         q.qdp_set_option(c, q.QDP_OPT_SELF_NCCL, nccl)
+        if not nccl:
+            q.qdp_set_option(c, q.QDP_OPT_P2P, 1)
         q.qdp_set_option(c, q.QDP_OPT_OVERLAP, overlap)
     return c
 
@@ -233,6 +237,7 @@ def part_configs(stream):
     U = fieldgen.random_gauge(Ls, 1005)
     b = fieldgen.random_spinor(Ls, 2006)
     for tag, mask, nccl in (("rank sub-lattice 48x48x24x24, no halo", 0, 0),
+                            ("same, z+t fused peer-to-peer boundary", 12, 0),
                             ("same, z+t halo path (NCCL to self)", 12, 1)):
         r, ms, fl = cg_run(stream, Ls, U, b, False, 0.0, 50, halo_mask=mask, nccl=nccl)
         out("   " + cg_line(tag + ", 50 it", r, ms, fl))
@@ -243,7 +248,10 @@ def part_fig6(stream):
     out("Fig. 6 analogue: hopping term H on the global volume V (both parities = 2 EO launches + halo kernels),")
     out("GFLOPS at 1320 flop/site.  'halo t' = the code path of a 2-GPU t split on one GPU (pack -> NCCL send/recv")
     out("to self -> exterior); overlap on = interior kernel concurrent with the exchange (PAPER.md:212, 288).")
-    out(f"{'V':>6s} {'prec':>5s} {'whole lattice':>22s} {'halo t, overlap on':>22s} {'halo t, overlap off':>22s}")
+    out("'p2p t' = the fused peer-to-peer boundary kernel (one launch per EO application; overlap off = every block")
+    out("waits for the ghosts first).")
+    out(f"{'V':>6s} {'prec':>5s} {'whole lattice':>22s} {'halo t, overlap on':>22s} {'halo t, overlap off':>22s} "
+        f"{'p2p t, overlap on':>22s} {'p2p t, overlap off':>22s}")
     for n in (8, 12, 16, 20, 24, 32, 40, 48):
         L = (n, n, n, n)
         U = fieldgen.random_gauge(L, 1004)
@@ -252,7 +260,7 @@ def part_fig6(stream):
         for prec in (q.QDP_F32, q.QDP_F64):
             name, dt, _ = PREC[prec]
             cols = []
-            for mask, nccl, ov in ((0, 0, 1), (8, 1, 1), (8, 1, 0)):
+            for mask, nccl, ov in ((0, 0, 1), (8, 1, 1), (8, 1, 0), (8, 0, 1), (8, 0, 0)):
                 c = make_ctx(L, stream, mask, nccl, ov)
                 fU = q.qdp_field_alloc(c, q.QDP_GAUGE, prec, q.QDP_ALL)
                 fp = q.qdp_field_alloc(c, q.QDP_FERMION, prec, q.QDP_ALL)
