@@ -122,6 +122,43 @@ __device__ __forceinline__ void accum_recon(Spinor<R> &acc, const Half<R> &h) {
   }
 }
 
+// Runtime-mu forms of project / accum_recon for the boundary code (face packing, remote hops): one
+// copy of the code for every direction instead of four, so the fused boundary kernel's packing and
+// face-site regions stay small next to the interior's hop code in the instruction cache.  Same
+// arithmetic as the compile-time forms (a unit factor +-1 / +-i is exact), so results are identical.
+template <typename T>
+__device__ __forceinline__ cx<T> mul_unit(cx<T> p, bool im, T sgn) {  // sgn * p or sgn * i p
+  return im ? cx<T>{-sgn * p.im, sgn * p.re} : cx<T>{sgn * p.re, sgn * p.im};
+}
+// rows 0,1 of (1 + S gamma_mu) psi: h0 = p0 + a0 p[k0], h1 = p1 + a1 p[k1] (table of project)
+template <typename T>
+__device__ __forceinline__ Half<T> project_rt(const Spinor<T> &p, int mu, int S) {
+  const bool lo = mu < 2;  // k0 = 3, k1 = 2 (else k0 = 2, k1 = 3); selects, not run-time indices
+  const bool im = (mu & 1) == 0;
+  const T a0 = (T)(mu == 1 ? -S : S), a1 = (T)(mu == 2 ? -S : S);
+  Half<T> h;
+#pragma unroll
+  for (int c = 0; c < 3; c++) {
+    h.c[c] = p.c[c] + mul_unit(lo ? p.c[9 + c] : p.c[6 + c], im, a0);
+    h.c[3 + c] = p.c[3 + c] + mul_unit(lo ? p.c[6 + c] : p.c[9 + c], im, a1);
+  }
+  return h;
+}
+// acc += (1 + S gamma_mu) reconstructed from h: rows 2,3 = b2 h[j2], b3 h[j3] (table of accum_recon)
+template <typename T>
+__device__ __forceinline__ void accum_recon_rt(Spinor<T> &acc, const Half<T> &h, int mu, int S) {
+  const bool im = (mu & 1) == 0;
+  const bool lo = mu < 2;  // rows 2,3 from h1, h0 (else from h0, h1)
+  const T b2 = (T)((mu & 1) == 0 ? -S : S), b3 = (T)(lo ? -S : S);
+#pragma unroll
+  for (int c = 0; c < 3; c++) {
+    acc.c[c] = acc.c[c] + h.c[c];
+    acc.c[3 + c] = acc.c[3 + c] + h.c[3 + c];
+    acc.c[6 + c] = acc.c[6 + c] + mul_unit(lo ? h.c[3 + c] : h.c[c], im, b2);
+    acc.c[9 + c] = acc.c[9 + c] + mul_unit(lo ? h.c[c] : h.c[3 + c], im, b3);
+  }
+}
+
 // acc += f x (the reconstruction of accum_recon), with every scaled term one fused multiply-add:
 // the 16-bit dslash applies its operands' scales here instead of to every stored value
 template <int K, typename R>
@@ -473,33 +510,23 @@ __device__ __forceinline__ void dot_block_partial(double v, double *part, int id
 //   f >= faceVh: my sites at x_mu = L-1    -> U_mu^dag P^+ psi  -> dst[mu][1] (the +mu neighbour's backward ghost)
 template <typename R, int REC, bool G5IN, typename KP>
 __device__ __forceinline__ void pack_site(const Geom &g, const KP &P, int mu, int f) {
-  const int n = g.faceVh[mu];
+  const int n = sel4(g.faceVh, mu);
   if (f >= 2 * n) return;
   const int q = 1 - P.parity;
   const bool fwd = f >= n;
   if (fwd) f -= n;
   int c[4];
-  face_coords(g, mu, fwd ? g.L[mu] - 1 : 0, f, q, c);
+  face_coords(g, mu, fwd ? sel4(g.L, mu) - 1 : 0, f, q, c);
   const int cb = coords_cb(g, c);
   using T = Arith_t<R>;
   Spinor<T> s = P.psi.load(cb);
   if (G5IN) g5(s);
   Half<T> h;
   if (!fwd) {
-    switch (mu) {
-      case 0: h = project<0, -1>(s); break;
-      case 1: h = project<1, -1>(s); break;
-      case 2: h = project<2, -1>(s); break;
-      default: h = project<3, -1>(s); break;
-    }
+    h = project_rt(s, mu, -1);
     HalfGhost<T>::store(P.dst[mu][0], n, f, h);
   } else {
-    switch (mu) {
-      case 0: h = project<0, +1>(s); break;
-      case 1: h = project<1, +1>(s); break;
-      case 2: h = project<2, +1>(s); break;
-      default: h = project<3, +1>(s); break;
-    }
+    h = project_rt(s, mu, +1);
     Link<T> u = P.U.load(mu, q, cb);
     HalfGhost<T>::store(P.dst[mu][1], n, f, mul_link_dag(u, h));
   }
@@ -532,14 +559,18 @@ __device__ __forceinline__ void pack_help(const Geom &g, const KP &P) {
     __syncthreads();
     if (ch >= P.pack_chunks) break;
     if (!mine) {  // the receivers must have consumed this slot (written two calls ago)
-#pragma unroll
+#pragma unroll 1
       for (int mu = 0; mu < 4; mu++)
         if ((g.part >> mu) & 1) block_wait_flags(P.war[mu][0], P.war[mu][1], P.seq - 2u, P.err);
     }
+    // the item's dim found at run time: one copy of the packing code (instruction cache; project_rt)
     const int i = ch * (int)blockDim.x + threadIdx.x;
-#pragma unroll
-    for (int mu = 0; mu < 4; mu++)
-      if (i >= P.pack_off[mu] && i < P.pack_off[mu + 1]) pack_site<R, REC, G5IN>(g, P, mu, i - P.pack_off[mu]);
+    if (i < P.pack_off[4]) {
+      int mu = 0;
+#pragma unroll 1
+      while (i >= P.pack_off[mu + 1]) mu++;
+      pack_site<R, REC, G5IN>(g, P, mu, i - P.pack_off[mu]);
+    }
     mine++;
   }
   if (mine) {
@@ -559,20 +590,23 @@ __device__ __forceinline__ void pack_help(const Geom &g, const KP &P) {
   }
 }
 
-// Fused boundary: the remote hop(s) of dim MU for a site on its faces, from the ghost slots
-// (forward: P^- psi(x + mu) from the +mu neighbour, multiplied here by U_mu(x); backward: the
-// neighbour already applied U^dag P^+)
-template <typename R, int MU, typename KP>
-__device__ __forceinline__ void remote_hop(const Geom &g, const KP &P, const int c[4], int cb, int p,
-                                           Spinor<Arith_t<R>> &acc) {
+// Fused boundary: the remote hops of every partitioned dim for a site on its faces, from the ghost
+// slots (forward: P^- psi(x + mu) from the +mu neighbour, multiplied here by U_mu(x); backward: the
+// neighbour already applied U^dag P^+); runtime mu, one copy of the code (see project_rt)
+template <typename R, typename KP>
+__device__ __forceinline__ void remote_hops(const Geom &g, const KP &P, const int c[4], int cb, int p,
+                                            Spinor<Arith_t<R>> &acc) {
   using T = Arith_t<R>;
-  if (!((g.part >> MU) & 1)) return;
-  const int n = g.faceVh[MU];
-  if (c[MU] == g.L[MU] - 1) {
-    const Half<T> h = HalfGhost<T>::load(P.ghost[MU][1], n, face_index(g, MU, c));
-    accum_recon<MU, -1>(acc, mul_link(P.U.load(MU, p, cb), h));
+#pragma unroll 1
+  for (int mu = 0; mu < 4; mu++) {
+    if (!((g.part >> mu) & 1)) continue;
+    const int n = sel4(g.faceVh, mu), x = sel4(c, mu);
+    if (x == sel4(g.L, mu) - 1) {
+      const Half<T> h = HalfGhost<T>::load(P.ghost[mu][1], n, face_index(g, mu, c));
+      accum_recon_rt(acc, mul_link(P.U.load(mu, p, cb), h), mu, -1);
+    }
+    if (x == 0) accum_recon_rt(acc, HalfGhost<T>::load(P.ghost[mu][0], n, face_index(g, mu, c)), mu, +1);
   }
-  if (c[MU] == 0) accum_recon<MU, +1>(acc, HalfGhost<T>::load(P.ghost[MU][0], n, face_index(g, MU, c)));
 }
 
 template <typename R, int REC, int EPI, bool G5IN, bool G5OUT, bool HALO, bool DOT>
@@ -597,22 +631,24 @@ __device__ __forceinline__ void dslash_body(const Geom &g, const KParams<R, REC>
           st_release_sys(P.ack_to[mu][1], P.seq - 1u);
         }
     }
-    if ((int)blockIdx.x < P.fuse_npack) {  // leading blocks: pack (work queue) and leave
-      pack_help<R, REC, G5IN>(g, P);
+    // leading blocks pack (work queue) and leave; a block about to wait for a ghost takes whatever
+    // packing is left first, so a wait never depends on an unstarted block (one call site: one copy)
+    const bool packer = (int)blockIdx.x < P.fuse_npack;
+    cb -= P.fuse_npack * blockDim.x;
+    // visiting position v -> interior sites [0, kin), the face sites, then interior [kin, nin)
+    const int nf = g.Vh - P.fuse_nin, b0 = (int)(blockIdx.x - P.fuse_npack) * (int)blockDim.x;
+    face = !packer && b0 + (int)blockDim.x > P.fuse_kin && b0 < P.fuse_kin + nf;
+    if (packer || face || P.wait_all) pack_help<R, REC, G5IN>(g, P);
+    if (packer) {
       if (DOT) {
         if (P.red_fin) red_finish(P.red, gridDim.x, vb, 0.0, 0.0, false);
         else dot_block_partial(0.0, P.dot_part, vb);
       }
       return;
     }
-    cb -= P.fuse_npack * blockDim.x;
-    // visiting position v -> interior sites [0, kin), the face sites, then interior [kin, nin)
-    const int nf = g.Vh - P.fuse_nin, b0 = (int)(blockIdx.x - P.fuse_npack) * (int)blockDim.x;
-    face = b0 + (int)blockDim.x > P.fuse_kin && b0 < P.fuse_kin + nf;
     if (cb >= P.fuse_kin) cb = cb < P.fuse_kin + nf ? P.fuse_nin + (cb - P.fuse_kin) : cb - nf;
     if (face || P.wait_all) {
-      pack_help<R, REC, G5IN>(g, P);  // whatever packing is left first: a wait never depends on an unstarted block
-#pragma unroll
+#pragma unroll 1
       for (int mu = 0; mu < 4; mu++)
         if ((g.part >> mu) & 1) block_wait_flags(P.ready[mu][0], P.ready[mu][1], P.seq, P.err);
     }
@@ -661,12 +697,7 @@ __device__ __forceinline__ void dslash_body(const Geom &g, const KParams<R, REC>
     hop_dir<R, 1>(g, P, c, cb, p, G5IN, halo, acc);
     hop_dir<R, 2>(g, P, c, cb, p, G5IN, halo, acc);
     hop_dir<R, 3>(g, P, c, cb, p, G5IN, halo, acc);
-    if (HALO && P.fuse && face) {  // remote hops from the ghosts the neighbours stored
-      remote_hop<R, 0>(g, P, c, cb, p, acc);
-      remote_hop<R, 1>(g, P, c, cb, p, acc);
-      remote_hop<R, 2>(g, P, c, cb, p, acc);
-      remote_hop<R, 3>(g, P, c, cb, p, acc);
-    }
+    if (HALO && P.fuse && face) remote_hops<R>(g, P, c, cb, p, acc);  // from the neighbours' ghosts
     o = epilogue<R, EPI>(P, cb, acc, G5OUT);
     have = true;
     if (DOT) {

@@ -102,21 +102,23 @@ __host__ __device__ inline int face_index(const Geom &g, int mu, const int c[4])
   }
   return lex >> 1;
 }
-// inverse: coordinates of face site f on the face x_mu = xmu with site parity p
+// inverse: coordinates of face site f on the face x_mu = xmu with site parity p.  Written without a
+// run-time index into c[] (mu may be a run-time value: such an index would put c[] in local memory)
 __host__ __device__ inline void face_coords(const Geom &g, int mu, int xmu, int f, int p, int c[4]) {
-  int dims[3], k = 0;
+  // the first two of the other three dims: d0 = (mu == 0 ? 1 : 0), d1 = (mu <= 1 ? 2 : 1)
+  const int A = mu == 0 ? g.L[1] : g.L[0], B = mu <= 1 ? g.L[2] : g.L[1];
+  const int ah = f % (A >> 1), rest = f / (A >> 1), b = rest % B, cc = rest / B;
+  const int x0 = 2 * ah + ((p + xmu + b + cc) & 1);
 #pragma unroll
-  for (int d = 0; d < 4; d++)
-    if (d != mu) dims[k++] = d;
-  int A = g.L[dims[0]], B = g.L[dims[1]];
-  int ah = f % (A >> 1);
-  int rest = f / (A >> 1);
-  int b = rest % B;
-  int cc = rest / B;
-  c[mu] = xmu;
-  c[dims[1]] = b;
-  c[dims[2]] = cc;
-  c[dims[0]] = 2 * ah + ((p + xmu + b + cc) & 1);
+  for (int d = 0; d < 4; d++) {
+    const int k = d - (d > mu ? 1 : 0);  // position among the other dims
+    c[d] = d == mu ? xmu : (k == 0 ? x0 : (k == 1 ? b : cc));
+  }
+}
+// a[mu] for a run-time mu without a run-time index (keeps a local c[] in registers, and a by-value
+// kernel parameter such as Geom out of local memory)
+__host__ __device__ inline int sel4(const int a[4], int mu) {
+  return mu == 0 ? a[0] : mu == 1 ? a[1] : mu == 2 ? a[2] : a[3];
 }
 
 #ifdef __CUDACC__

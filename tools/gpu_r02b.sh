@@ -16,6 +16,7 @@
 #           tests: halo / peer / PDL / mixed tests, fused sweep, config 5's CG
 #   cgblas  ncu --set full of the CG's vector updates (cg_r, cg_xp)
 #   h16     the 16-bit dslash with packed fp32 arithmetic vs scalar (A/B in one call), mixed-solver tests
+#   compact the fused boundary kernel with one copy of its packing / face-site code: tests, sweep, config 5
 #   small   the launch-variant sweep incl. the 128-register variant, tuner tests, CG it/s PDL off / on
 #                                                                     -> profiles/r02_dslash_variants_pdl.txt
 set -u
@@ -102,4 +103,12 @@ h16)
     else timeout 600 python tools/mixed_profile.py >> gpurun_out/h16.txt 2>&1; fi
   done
   cat gpurun_out/h16.txt; tail -2 gpurun_out/h16_tests.log ;;
+compact)
+  # the fused boundary kernel with one copy of its packing / face-site code (run-time mu)
+  timeout 1500 python -m pytest tests/test_gpu_p2p.py tests/test_gpu_peer.py tests/test_gpu_pdl.py tests/test_gpu_parity.py \
+    tests/test_gpu_mixed.py tests/test_gpu_recon12.py tests/test_gpu_comm.py -m gpu -q > gpurun_out/compact_tests.log 2>&1; echo tests_rc=$?
+  timeout 300 python tools/fused_sweep.py > gpurun_out/compact.txt 2>&1
+  timeout 300 python tools/c5_profile.py >> gpurun_out/compact.txt 2>&1
+  timeout 600 python tools/pdl_zt.py >> gpurun_out/compact.txt 2>&1
+  cat gpurun_out/compact.txt; tail -2 gpurun_out/compact_tests.log ;;
 esac
