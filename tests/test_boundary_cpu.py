@@ -63,3 +63,25 @@ def test_oracle_is_not_imported_by_product():
             if f.endswith((".py", ".cu", ".cpp", ".h")):
                 txt = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt and "oracle.c" not in txt, f
+
+
+def test_binding_constants_match_header(q):
+    """Every QDP_OPT_* / QDP_PK_* / status constant of the binding equals the header's enum value."""
+    import re
+    hdr = open(os.path.join(ROOT, "include", "qdpb.h")).read()
+    hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)  # comments mention values too
+    found = 0
+    for body in re.findall(r"enum\s*\{(.*?)\}", hdr, flags=re.S):
+        nxt = 0
+        for item in body.split(","):
+            item = item.strip()
+            if not item:
+                continue
+            name, _, val = item.partition("=")
+            name = name.strip()
+            nxt = int(val.strip(), 0) if val.strip() else nxt
+            if name.startswith("QDP_"):
+                assert getattr(q, name) == nxt, name
+                found += 1
+            nxt += 1
+    assert found >= 30 and q.QDP_OPT_PDL == 10
