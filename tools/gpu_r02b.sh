@@ -66,7 +66,7 @@ small)
   cat gpurun_out/dslash_variants.txt gpurun_out/pdl_cg.txt; tail -3 gpurun_out/o8_tests.log ;;
 c5)
   timeout 600 python tools/c5_profile.py > gpurun_out/c5_profile.txt 2>&1; echo c5_rc=$?
-  for c in c5cg c5cg0; do
+  for c in c5cg c5cg0 t40cg t40cg0; do
     timeout 600 ncu --clock-control none --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
       -k regex:dslash -s 40 -c 16 --csv --log-file gpurun_out/ncu_$c.csv python tools/ncu_cases.py $c > gpurun_out/ncu_$c.log 2>&1
     echo ${c}_rc=$?

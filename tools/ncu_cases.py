@@ -8,6 +8,7 @@
   cgblas the fp64 clover CG's vector updates at 40^3x32 (cg_r: r -= alpha q with |r|^2; cg_xp)
   c5zt / c5whole  plain fp64 EO dslash on config 5's rank sub-lattice 48x48x24x24: the fused z x t
          boundary kernel (self-halo) / the register-path main kernel without a halo
+  t40cg / t40cg0  clover CG at 40^3x32 with t through the fused peer-to-peer halo path / without
   c5cg / c5cg0  Wilson CG on config 5's rank sub-lattice 48x48x24x24 with z x t through the fused
          peer-to-peer halo path (self-halo) / without a halo
 Each case warms up, then runs the launches to capture (select them with ncu -k / -s / -c)."""
@@ -35,8 +36,8 @@ def gauge(kind=q.QDP_GAUGE):
     return f
 
 
-if case in ("zt", "t", "c5cg", "c5zt"):
-    q.qdp_set_option(c, q.QDP_OPT_SELF_HALO, 8 if case == "t" else 12)
+if case in ("zt", "t", "c5cg", "c5zt", "t40cg"):
+    q.qdp_set_option(c, q.QDP_OPT_SELF_HALO, 8 if case in ("t", "t40cg") else 12)
     q.qdp_set_option(c, q.QDP_OPT_P2P, 1)
 if case in ("r12tma", "r12pipe", "r12main"):  # fp64 reconstruct-12 dslash, one forced launch variant:
     # bulk-copy staged forward links / cp.async hop pipeline / the register-path main kernel
@@ -62,6 +63,16 @@ elif case == "h16":
     fAi = q.qdp_field_alloc(c, q.QDP_CLOVER, q.QDP_F64, q.QDP_EVEN)
     q.qdp_clover_build(fA, fAi, fU, 0.1, 1.0)
     q.qdp_cg_solve_mixed16(fx, fb, fU, fA, fAi, mass=0.1, tol=0.0, delta=0.1, maxit=6)
+elif case in ("t40cg", "t40cg0"):
+    fU = gauge()
+    fb = q.qdp_field_alloc(c, q.QDP_FERMION, q.QDP_F64, q.QDP_ALL)
+    q.qdp_field_import_device(fb, fieldgen.random_spinor_torch(L, 22))
+    fx = q.qdp_field_alloc(c, q.QDP_FERMION, q.QDP_F64, q.QDP_ALL)
+    fA = q.qdp_field_alloc(c, q.QDP_CLOVER, q.QDP_F64, q.QDP_ALL)
+    fAi = q.qdp_field_alloc(c, q.QDP_CLOVER, q.QDP_F64, q.QDP_EVEN)
+    q.qdp_clover_build(fA, fAi, fU, 0.1, 1.0)
+    for _ in range(3):
+        q.qdp_cg_solve(fx, fb, fU, fA, fAi, mass=0.1, tol=0.0, maxit=8)
 elif case == "cgblas":
     fU = gauge()
     fb = q.qdp_field_alloc(c, q.QDP_FERMION, q.QDP_F64, q.QDP_ALL)
