@@ -111,4 +111,15 @@ compact)
   timeout 300 python tools/c5_profile.py >> gpurun_out/compact.txt 2>&1
   timeout 600 python tools/pdl_zt.py >> gpurun_out/compact.txt 2>&1
   cat gpurun_out/compact.txt; tail -2 gpurun_out/compact_tests.log ;;
+clovt)
+  # ncu --set full of the clover-xpay dslash of the 40^3x32 clover CG with t through the fused boundary and without
+  F="ncu --clock-control none --set full --import-source on"
+  timeout 600 $F -k "regex:dslash_kernel<double, .int.18, .int.3, .bool.0, .bool.0, .bool.1, .bool.0>" --kernel-name-base demangled -s 2 -c 1 -o gpurun_out/prof_clovt -f python tools/ncu_cases.py t40cg > gpurun_out/ncu_clovt.log 2>&1; echo t_rc=$?
+  timeout 600 $F -k "regex:dslash_kernel<double, .int.18, .int.3, .bool.0, .bool.0, .bool.0, .bool.0>" --kernel-name-base demangled -s 2 -c 1 -o gpurun_out/prof_clov0 -f python tools/ncu_cases.py t40cg0 > gpurun_out/ncu_clov0.log 2>&1; echo w_rc=$?
+  for c in clovt clov0; do
+    python tools/ncu_summary.py gpurun_out/prof_$c.ncu-rep > gpurun_out/prof_txt/prof_${c}_detail.txt 2>&1
+    ncu -i gpurun_out/prof_$c.ncu-rep --page source --csv --print-source sass > gpurun_out/prof_txt/src_$c.csv 2>&1
+  done
+  rm -f gpurun_out/*.ncu-rep
+  grep -E "gpu__time|dram__bytes|no_instruction_per|long_scoreboard_per|membar_per|barrier_per|wait_per|issue_active" gpurun_out/prof_txt/prof_clov*_detail.txt ;;
 esac
