@@ -9,7 +9,8 @@
 #   pipe    the cp.async hop pipeline: variant sweep, CG with forced variants, ncu --set full of the
 #           fp64 reconstruct-12 dslash as register-path kernel and as pipeline -> profiles/r02_dslash_pipeline.txt
 #   c5      config 5's rank sub-lattice CG: per-class times with no halo / t / z x t, and the per-launch
-#           dslash times (ncu) of the CG with and without the z x t halo
+#           dslash times (ncu) of the CG with and without the z x t halo (and of the 40^3x32 clover CG
+#           with and without the t halo)                              -> profiles/r02_halo_cg_cost.txt
 #   zt      ncu --set full (+ SASS source page) of the fused z x t boundary kernel and of the main kernel
 #           on config 5's rank sub-lattice
 #   ack     the fused boundary with the acknowledgement by the next call and block-uniform halo
@@ -19,6 +20,8 @@
 #   compact the fused boundary kernel with one copy of its packing / face-site code: tests, sweep, config 5
 #   small   the launch-variant sweep incl. the 128-register variant, tuner tests, CG it/s PDL off / on
 #                                                                     -> profiles/r02_dslash_variants_pdl.txt
+#   clovt   ncu --set full of the clover-xpay dslash of the 40^3x32 CG with and without the t boundary
+#                                                                     -> profiles/r02_ncu_clover_xpay_t_halo.txt
 set -u
 mkdir -p gpurun_out/prof_txt
 case "$1" in
